@@ -1,0 +1,200 @@
+/*
+ * ORACLE -- TEST INFRASTRUCTURE ONLY.  Plain fp64 loops; shares no code with
+ * the CUDA path (paper_2402_15322_b200/).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline leg may load this library.
+ *
+ * Discrete SE(2) group convolution, PAPER.md subsec:gconv:
+ *     (K b)(g) = sum_h K(h^{-1} g) b(h)
+ * on the lattice of DESIGN.md (cell centres, theta_k = 2 pi k / nt), with the
+ * kernel restricted to the spatial box |ix_g - ix_h| <= R, |iy_g - iy_h| <= R
+ * (all theta offsets) and zero padding outside the window.
+ *
+ * Table layout (the oracle's own): T[(((to * nt) + ti) * S + (dy + R)) * S + (dx + R)]
+ * holds K(h^{-1} g) for g = (x_h + (dx/nx, dy/ny), theta_to), h = (x_h, theta_ti),
+ * i.e. dx = ix_g - ix_h, dy = iy_g - iy_h.  Field layout [theta][y][x].
+ */
+#include <math.h>
+#include <stddef.h>
+
+#define IDX3(t, y, x) (((size_t)(t) * ny + (y)) * nx + (x))
+
+static inline size_t tidx(int nt, int S, int R, int to, int ti, int dy, int dx) {
+    return ((((size_t)to * nt + ti) * S + (dy + R)) * S + (dx + R));
+}
+
+/* y(g) = sum_h K(g,h) v(h)   -- gather form of K (first formula) */
+void oracle_conv_gather(int nx, int ny, int nt, int R, const double* T, const double* v, double* y) {
+    const int S = 2 * R + 1;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int to = 0; to < nt; ++to)
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix) {
+                double acc = 0.0;
+                for (int ti = 0; ti < nt; ++ti)
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = iy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = ix - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            acc += T[tidx(nt, S, R, to, ti, dy, dx)] * v[IDX3(ti, hy, hx)];
+                        }
+                    }
+                y[IDX3(to, iy, ix)] = acc;
+            }
+}
+
+/* y(h) = sum_g K(g,h) a(g)   -- the adjoint K^T (second formula), written as a
+ * SCATTER over g so that K = K^T is tested, not assumed.  Threads own output
+ * channels th, so there is no write race. */
+void oracle_conv_scatter_adjoint(int nx, int ny, int nt, int R, const double* T, const double* a,
+                                 double* y) {
+    const int S = 2 * R + 1;
+    const size_t n = (size_t)nx * ny * nt;
+    for (size_t i = 0; i < n; ++i) y[i] = 0.0;
+#pragma omp parallel for schedule(static)
+    for (int th = 0; th < nt; ++th)
+        for (int tg = 0; tg < nt; ++tg)
+            for (int gy = 0; gy < ny; ++gy)
+                for (int gx = 0; gx < nx; ++gx) {
+                    double ag = a[IDX3(tg, gy, gx)];
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = gy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = gx - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            y[IDX3(th, hy, hx)] += T[tidx(nt, S, R, tg, th, dy, dx)] * ag;
+                        }
+                    }
+                }
+}
+
+/* log-domain gather: ly(g) = log sum_h exp(L(g,h) + lv(h)), exact two-pass LSE
+ * (max, then sum of exp(. - max)).  All-(-inf) inputs give -inf. */
+void oracle_lse_gather(int nx, int ny, int nt, int R, const double* L, const double* lv, double* ly) {
+    const int S = 2 * R + 1;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int to = 0; to < nt; ++to)
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix) {
+                double m = -INFINITY;
+                for (int ti = 0; ti < nt; ++ti)
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = iy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = ix - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            double t = L[tidx(nt, S, R, to, ti, dy, dx)] + lv[IDX3(ti, hy, hx)];
+                            if (t > m) m = t;
+                        }
+                    }
+                if (m == -INFINITY) { ly[IDX3(to, iy, ix)] = -INFINITY; continue; }
+                double s = 0.0;
+                for (int ti = 0; ti < nt; ++ti)
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = iy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = ix - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            s += exp(L[tidx(nt, S, R, to, ti, dy, dx)] + lv[IDX3(ti, hy, hx)] - m);
+                        }
+                    }
+                ly[IDX3(to, iy, ix)] = m + log(s);
+            }
+}
+
+/* log-domain adjoint as a scatter (max pass, then sum pass). */
+void oracle_lse_scatter_adjoint(int nx, int ny, int nt, int R, const double* L, const double* la,
+                                double* ly, double* scratch_max) {
+    const int S = 2 * R + 1;
+    const size_t n = (size_t)nx * ny * nt;
+    for (size_t i = 0; i < n; ++i) { scratch_max[i] = -INFINITY; ly[i] = 0.0; }
+#pragma omp parallel for schedule(static)
+    for (int th = 0; th < nt; ++th)
+        for (int tg = 0; tg < nt; ++tg)
+            for (int gy = 0; gy < ny; ++gy)
+                for (int gx = 0; gx < nx; ++gx) {
+                    double ag = la[IDX3(tg, gy, gx)];
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = gy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = gx - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            double t = L[tidx(nt, S, R, tg, th, dy, dx)] + ag;
+                            if (t > scratch_max[IDX3(th, hy, hx)]) scratch_max[IDX3(th, hy, hx)] = t;
+                        }
+                    }
+                }
+#pragma omp parallel for schedule(static)
+    for (int th = 0; th < nt; ++th)
+        for (int tg = 0; tg < nt; ++tg)
+            for (int gy = 0; gy < ny; ++gy)
+                for (int gx = 0; gx < nx; ++gx) {
+                    double ag = la[IDX3(tg, gy, gx)];
+                    for (int dy = -R; dy <= R; ++dy) {
+                        int hy = gy - dy;
+                        if (hy < 0 || hy >= ny) continue;
+                        for (int dx = -R; dx <= R; ++dx) {
+                            int hx = gx - dx;
+                            if (hx < 0 || hx >= nx) continue;
+                            double m = scratch_max[IDX3(th, hy, hx)];
+                            if (m == -INFINITY) continue;
+                            ly[IDX3(th, hy, hx)] += exp(L[tidx(nt, S, R, tg, th, dy, dx)] + ag - m);
+                        }
+                    }
+                }
+    for (size_t i = 0; i < n; ++i)
+        ly[i] = (scratch_max[i] == -INFINITY) ? -INFINITY : scratch_max[i] + log(ly[i]);
+}
+
+/* Single output sample of the gather conv (for full-size sampled parity). */
+double oracle_conv_point(int nx, int ny, int nt, int R, const double* T, const double* v,
+                         int to, int iy, int ix) {
+    const int S = 2 * R + 1;
+    double acc = 0.0;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int dy = -R; dy <= R; ++dy) {
+            int hy = iy - dy;
+            if (hy < 0 || hy >= ny) continue;
+            for (int dx = -R; dx <= R; ++dx) {
+                int hx = ix - dx;
+                if (hx < 0 || hx >= nx) continue;
+                acc += T[tidx(nt, S, R, to, ti, dy, dx)] * v[IDX3(ti, hy, hx)];
+            }
+        }
+    return acc;
+}
+
+double oracle_lse_point(int nx, int ny, int nt, int R, const double* L, const double* lv,
+                        int to, int iy, int ix) {
+    const int S = 2 * R + 1;
+    double m = -INFINITY;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int dy = -R; dy <= R; ++dy) {
+            int hy = iy - dy;
+            if (hy < 0 || hy >= ny) continue;
+            for (int dx = -R; dx <= R; ++dx) {
+                int hx = ix - dx;
+                if (hx < 0 || hx >= nx) continue;
+                double t = L[tidx(nt, S, R, to, ti, dy, dx)] + lv[IDX3(ti, hy, hx)];
+                if (t > m) m = t;
+            }
+        }
+    if (m == -INFINITY) return -INFINITY;
+    double s = 0.0;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int dy = -R; dy <= R; ++dy) {
+            int hy = iy - dy;
+            if (hy < 0 || hy >= ny) continue;
+            for (int dx = -R; dx <= R; ++dx) {
+                int hx = ix - dx;
+                if (hx < 0 || hx >= nx) continue;
+                s += exp(L[tidx(nt, S, R, to, ti, dy, dx)] + lv[IDX3(ti, hy, hx)] - m);
+            }
+        }
+    return m + log(s);
+}
