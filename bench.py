@@ -1,0 +1,308 @@
+"""Benchmark of the SE(2) entropic-OT hot path (BASELINE.json metric: Sinkhorn iters/s on the SE(2)
+grid + group-conv fraction of roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c4]
+
+Workload (default c4, the largest config, which fits one GPU): the entropic JKO gradient flow on
+the 256x256x64 grid, eps = 0.003, w = (1,3,1), support 31x31x64, tau = 1e-3.  One step = one JKO
+step = 200 inner scaling iterations (2 group convolutions each, fused prox / division / error
+epilogues) + the normalisation of mu_{k+1}.  value = inner Sinkhorn iterations per second summed
+over ranks.  Multi-GPU (torchrun): every rank runs its own JKO flow (independent problems, no
+data-path collective) -> "scaling": "weak".
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the launching
+stream, with an L2 flush (write of a 256 MiB buffer, outside the events) before each step; barrier
++ synchronize around the timed region; the max over ranks is reported.  `e2e` repeats the step
+through the same C-ABI call with the step's input copied from pinned HOST memory and the result
+copied back inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    "c4": "c4: entropic JKO gradient flow on 256x256x64 SE(2) grid ([0,1]^2 x [0,2pi)), eps=0.003, "
+          "w=(1,3,1), support 31x31x64, tau=1e-3, V=|x-c|^2; one step = one JKO step = 200 inner "
+          "scaling iterations (2 group convs each) + normalisation; linear-domain fp32",
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (profiling recipe)."""
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _taps_1d(n, R):
+    """sum over outputs i in [0,n) of #{j in [0,n): |i-j| <= R} (zero padding)."""
+    i = np.arange(n)
+    return int(np.sum(np.minimum(i + R, n - 1) - np.maximum(i - R, 0) + 1))
+
+
+def cpu_oracle_sample(cfg, seconds_hint=15.0):
+    """Time the oracle (as it stands) on a bounded sample of the workload: one group convolution over
+    the first `rows` rows of the grid (its own zero-padded window), scaled to one full inner
+    iteration (2 convs on the full grid) by the exact box-tap ratio.  Returns (iters/s, desc, threads)."""
+    import oracle as O
+    import se2_synth as S
+    rows = 64 if cfg.ny >= 64 else cfg.ny
+    g = O.Grid(cfg.nx, rows, cfg.ntheta)
+    T = O.kernel_table(g, cfg.R, cfg.eps, cfg.w)
+    v = S.random_positive_field((cfg.ntheta, rows, cfg.nx), seed=5).astype(np.float64)
+    t0 = time.perf_counter()
+    O.conv(T, v)
+    dt = time.perf_counter() - t0
+    taps_s = _taps_1d(cfg.nx, cfg.R) * _taps_1d(rows, cfg.R)
+    taps_f = _taps_1d(cfg.nx, cfg.R) * _taps_1d(cfg.ny, cfg.R)
+    t_iter = 2.0 * dt * taps_f / taps_s
+    desc = (f"oracle fp64 conv (C loops, OpenMP) over rows 0-{rows - 1} of the {cfg.nx}x{cfg.ny}x{cfg.ntheta} "
+            f"grid ({dt:.2f} s), scaled by the exact box-tap ratio to one inner iteration (2 convs)")
+    return 1.0 / t_iter, desc, O.oracle_threads(), dt
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import se2_synth as S
+    cfg = S.get_config(args.workload)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, desc, threads, dt = cpu_oracle_sample(cfg)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": "Sinkhorn iters/s on SE(2) grid", "value": value, "unit": "iters/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg.iters / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload]},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import se2_synth as S
+    from paper_2402_15322_b200 import Kernel, make_prox, se2_jko_step, se2_launch_count
+
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = S.get_config(args.workload)
+    d = S.config_inputs(cfg)
+    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1, device=local)
+    st = k.stats()
+    prox = make_prox(k, cfg.tau)
+    mu0 = torch.from_numpy(d["mus"][0]).cuda()
+    mu = mu0.clone()
+    nxt = torch.empty_like(mu)
+    a = torch.empty_like(mu)
+    b = torch.empty_like(mu)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    iters = cfg.iters
+
+    def step():
+        nonlocal mu, nxt
+        se2_jko_step(k, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
+        mu, nxt = nxt, mu
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = se2_launch_count()
+    k.timing_enable(True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))                      # L2 flush (outside the events)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    n_conv, conv_ms, _ = k.timing_get()
+    k.timing_enable(False)
+    launches = se2_launch_count() - l0
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if ws > 1:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = dev_ms / args.steps
+    value = ws * iters * args.steps / (dev_ms / 1000.0)
+
+    # ---- e2e: same step through the C ABI with host buffers, H2D + D2H inside the timed region
+    host_in = torch.from_numpy(d["mus"][0]).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        mu.copy_(host_in, non_blocking=True)
+        se2_jko_step(k, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
+        host_out.copy_(nxt, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = ws * iters * e2e_steps / (e2e_ms / 1000.0)
+    nbytes = mu.numel() * 4
+
+    out = None
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        clocks = clk.summary()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12           # TFLOP/s
+        flop_per_conv = 2.0 * cfg.N * st["nnz_taps"]
+        conv_avg_ms = conv_ms / max(n_conv, 1)
+        achieved = flop_per_conv / (conv_avg_ms / 1000.0) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(f"{args.workload}_conv_linear_bytes_per_launch")
+        out = {
+            "metric": "Sinkhorn iters/s on SE(2) grid", "value": value, "unit": "iters/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload], "inner_iters_per_step": iters,
+                       "l2": "flushed before every timed step (256 MiB write, outside the step events)",
+                       "parallelism": f"replicas x{ws} (independent JKO flows)"},
+            "roofline": {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "achieved": achieved,
+                         "peak": ffma_peak, "unit": "TFLOP/s", "frac": achieved / ffma_peak, "traffic": traffic,
+                         "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (clock from "
+                                        f"MEASURED_PEAKS.json, {peak_src}); FFMA has no measured peak",
+                         "flop_per_launch": flop_per_conv, "conv_launches": n_conv,
+                         "conv_avg_ms": conv_avg_ms, "conv_share_of_step": conv_ms / dev_ms if dev_ms else None,
+                         "peak_at_run_clock": (148 * 128 * 2 * clocks["sm_mhz"] * 1e6 / 1e12)
+                         if clocks.get("sm_mhz") else None},
+            "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "wall_s_timed_region": t_wall,
+        }
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            v, desc, threads, _ = cpu_oracle_sample(cfg)
+            out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc}
+        print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

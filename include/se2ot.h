@@ -1,0 +1,212 @@
+/*
+ * se2ot.h -- C ABI of the B200-native entropic optimal transport hot path on SE(2)
+ *            (arXiv 2402.15322, "Optimal Transport on the Lie Group of Roto-translations").
+ *
+ * Citations: P:n = line n of the paper text, with the equation label.
+ *
+ * The library implements ONE thing: the Sinkhorn / convolutional Wasserstein-barycenter
+ * scaling loop, whose cost is the application of the Gibbs kernel
+ *     K(g) = exp(-rho_b(g)^2 / eps)
+ * as a left-invariant SE(2) group convolution
+ *     (K v)(g) = sum_h K(h^{-1} g) v(h),   and K^T = K
+ * with rho_b the half-angle distance approximation (eq. eq:rhob).
+ *
+ * Conventions (all entry points):
+ *  - Lattice: nx x ny x ntheta on [0,1]^2 x [0,2pi); cell centres x_i = (i+1/2)/nx,
+ *    y_j = (j+1/2)/ny, theta_k = 2 pi k/ntheta (readings R1, R2).
+ *  - Kernel support: spatial box |ix_g-ix_h| <= radius, |iy_g-iy_h| <= radius, all theta
+ *    offsets; zero padding outside the window (R3).
+ *  - Field arrays: fp32, contiguous, layout [batch][ntheta][ny][nx] (x fastest), DEVICE
+ *    pointers on the kernel's device unless stated otherwise.  The caller owns every array.
+ *  - Log-domain state (SE2_LOG_DOMAIN) holds natural logs of the scalings (alpha = log a ...).
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *    Calls that return host scalars / traces synchronise that stream before returning.
+ *  - No exceptions cross the ABI; errors are returned as se2_status, with a thread-local
+ *    message from se2_last_error().  Warnings are >= 100 and leave outputs valid.
+ *  - A kernel object may be used by one stream at a time (it owns scratch buffers).
+ */
+#ifndef SE2OT_H
+#define SE2OT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SE2OT_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SE2_API __attribute__((visibility("default")))
+#else
+#define SE2_API
+#endif
+
+typedef struct CUstream_st* se2_stream; /* == cudaStream_t */
+
+typedef enum {
+    SE2_OK = 0,
+    SE2_EINVAL = 1,       /* bad argument (null pointer, size, eps <= 0, lambdas off simplex ...) */
+    SE2_ENOMEM = 2,       /* device allocation failed                                            */
+    SE2_ECUDA = 3,        /* CUDA runtime error (message has the CUDA error string)              */
+    SE2_ENONFINITE = 5,   /* NaN/Inf produced by the iteration (SPEC NonFiniteIterate)           */
+    SE2_EUNSUPPORTED = 6, /* configuration the kernels do not implement (e.g. radius > 15)       */
+    SE2_WKERNEL_TOO_WIDE = 100 /* warning: support box exceeds the grid (call succeeded)         */
+} se2_status;
+
+/* Flags */
+#define SE2_LOG_DOMAIN 0x1u   /* state/fields are natural logs; conv is log-sum-exp (R7)      */
+#define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1        */
+#define SE2_TRACE_ERR 0x4u    /* compute the marginal error every iteration (fused)           */
+
+typedef struct {
+    int32_t nx, ny, ntheta;
+} se2_grid;
+
+typedef struct {
+    double w1, w2, w3; /* left-invariant metric diag(w1^2, w2^2, w3^2) in the frame A1,A2,A3 */
+} se2_metric;
+
+typedef struct se2_kernel_s* se2_kernel; /* opaque: device tables + scratch */
+
+typedef struct {
+    int64_t box_taps;     /* ntheta * (2r+1)^2: taps per output in the support box                 */
+    int64_t nnz_taps;     /* taps per output whose fp32 value is nonzero (the linear path's work)  */
+    int32_t theta_band;   /* k: fp32-nonzero theta offsets are |theta_o - theta_i| <= k bins       */
+    int32_t radius;
+    double zeta;          /* spatial anisotropy max(w1,w2)/min(w1,w2)                      */
+    size_t table_bytes;   /* device bytes held by the tables                                       */
+} se2_kernel_stats;
+
+/* ------------------------------------------------------------------------------------------
+ * se2_kernel_build -- tabulate the Gibbs kernel once (App. A "K_eps <- exp(-rho_b^2/eps)").
+ *   Tables W[to][ti][dy][dx] = exp(-rho_b((0,0,theta_i)^{-1} (dx/nx, dy/ny, theta_o))^2/eps) (fp32,
+ *   computed in fp64 and rounded) and its log L = -rho_b^2/eps, on device `device`.
+ *   radius: spatial half-width r (support (2r+1)^2), 0 <= r <= 15.
+ *   max_batch: largest batch any later call will use (scratch is sized for it; >= 1).
+ *   Errors: SE2_EINVAL (null out, eps <= 0, w <= 0, sizes <= 0), SE2_EUNSUPPORTED (r > 15),
+ *   SE2_ENOMEM, SE2_ECUDA.  Warning SE2_WKERNEL_TOO_WIDE if 2r+1 > min(nx, ny).
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, double eps, int32_t radius,
+                            int32_t max_batch, int32_t device, se2_kernel* out);
+SE2_API se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* out);
+SE2_API void se2_kernel_destroy(se2_kernel k); /* idempotent on NULL */
+
+/* ------------------------------------------------------------------------------------------
+ * se2_conv -- y = K v (the same operator serves K^T), batch fields at once.
+ *   Linear: out = K in.  SE2_LOG_DOMAIN: out = log(K exp(in)) (exact log-sum-exp).
+ *   in, out: device [batch][N]; in != out.  batch <= max_batch.
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, uint32_t flags,
+                    se2_stream stream);
+
+/* Prox of the second marginal term F2 (eq. equ:scaling_iterations). */
+typedef enum {
+    SE2_PROX_MARGINAL = 0,          /* F2 = indicator{= nu}: prox = nu -> Sinkhorn        */
+    SE2_PROX_ENTROPY_POTENTIAL = 1  /* F2 = tau * (sum s(log s - 1) + sum V s): JKO step; */
+                                    /* b = z^{-tau/(eps+tau)} exp(-tau V/(eps+tau)) (reading R10)     */
+} se2_prox_kind;
+
+typedef struct {
+    int32_t kind;        /* se2_prox_kind                                                           */
+    double tau;          /* JKO time step                                                           */
+    double cx, cy;       /* potential centre in cell units of this (slab) grid                      */
+    double hx, hy;       /* cell sizes: V(i,j) = ((i + 1/2 - cx) hx)^2 + ((j + 1/2 - cy) hy)^2      */
+} se2_prox;
+
+typedef struct {
+    int32_t iters;       /* scaling iterations (fixed count, no early stop; reading R5)             */
+    uint32_t flags;      /* SE2_LOG_DOMAIN | SE2_WARM_START | SE2_TRACE_ERR                          */
+} se2_opts;
+
+/* ------------------------------------------------------------------------------------------
+ * se2_sinkhorn -- scaling iterations:  a = mu / K b ;  b = prox(K^T a) / K^T a,
+ *   starting from b^(0) = 1 (or the given b with SE2_WARM_START).  With prox = NULL or
+ *   SE2_PROX_MARGINAL this is Sinkhorn (nu required); with
+ *   SE2_PROX_ENTROPY_POTENTIAL it is the inner solve of one entropic JKO step (nu ignored).
+ *   batch independent problems are solved at once (mu, nu, a, b: [batch][N]).
+ *   a, b: outputs (scalings, or alpha = log a, beta = log b under SE2_LOG_DOMAIN).
+ *   err_trace_host: nullable host array [iters][batch]; with SE2_TRACE_ERR it receives
+ *   e_l = sum |a * K b - mu| after the l-th b-update (R8).  Divisions are guarded at 1e-30 (R9).
+ *   Errors: SE2_EINVAL, SE2_ECUDA, SE2_ENONFINITE (checked at the end of the solve).
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a, float* b, int32_t batch,
+                        const se2_prox* prox, const se2_opts* opts, double* err_trace_host,
+                        se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
+ * se2_jko_step -- one entropic JKO step = se2_sinkhorn with the entropy+potential
+ *   prox, then mu_next = b * K^T a normalised to mass 1 (R10).  mass_host (nullable) receives
+ *   sum(b * K^T a) before normalisation.  mu_k, mu_next: [N] device (may not alias).
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* a, float* b,
+                        const se2_prox* prox, const se2_opts* opts, double* mass_host,
+                        double* err_trace_host, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
+ * se2_barycenter -- App. A, iterated Bregman projections:
+ *     v_i, w_i <- 1
+ *     for j: mu <- 1; for i: w_i <- mu_i / K v_i ; d_i <- v_i K w_i ; mu <- mu d_i^lambda_i
+ *            for i: v_i <- v_i mu / d_i
+ *   nsolve independent barycenter problems over the SAME n inputs with different weights
+ *   (c1: the 5 interpolation weights t -> (t, 1-t)) run batched (nsolve*n fields per conv).
+ *   mus: device [n][N] input measures.  lambdas: HOST [nsolve][n], each row on the simplex
+ *   within 1e-9 (SE2_EINVAL otherwise); lambda_i = 0 terms are skipped (R6).
+ *   bary: device [nsolve][N] output mu (log mu under SE2_LOG_DOMAIN), as returned by App. A.
+ *   v_state, w_state: nullable device [nsolve][n][N] outputs (v_i, w_i or their logs).
+ *   err_trace_host: nullable host [iters][nsolve]; with SE2_TRACE_ERR receives
+ *   sum_i lambda_i sum|w_i K v_i - mu_i| after each v-update (R8).
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* mus, const double* lambdas,
+                          float* bary, float* v_state, float* w_state, const se2_opts* opts,
+                          double* err_trace_host, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
+ * se2_marginal_error -- err_host[i] = sum_x |a_i(x) (K b_i)(x) - mu_i(x)|  (R8) for
+ *   i < batch.  Under SE2_LOG_DOMAIN a, b are logs.  Deterministic two-stage reduction.
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, const float* mu, int32_t batch,
+                              uint32_t flags, double* err_host, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Step-level entry points (used by the multi-GPU driver, which owns the loop and the collectives).
+ * se2_conv_update: out = target (op) K in, fused in the conv epilogue:
+ *   op = SE2_EPI_DIVIDE:   out = target / max(K in, 1e-30)     | log: out = target - LSE(in)
+ *   op = SE2_EPI_MULTIPLY: out = target * (K in)               | log: out = target + LSE(in)
+ *   op = SE2_EPI_PROX:     out = prox(K in)/K in  (entropy+potential, `prox` required; target unused)
+ * target: device [batch][N] (log targets under SE2_LOG_DOMAIN).
+ * ---------------------------------------------------------------------------------------- */
+#define SE2_EPI_DIVIDE 1
+#define SE2_EPI_MULTIPLY 2
+#define SE2_EPI_PROX 3
+SE2_API se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, float* out, int32_t batch,
+                           int32_t op, const se2_prox* prox, uint32_t flags, se2_stream stream);
+
+/* Barycenter log-mean pieces (App. A, mu <- prod d_i^lambda_i, v_i <- v_i mu / d_i), in logs:
+ *   se2_bary_logmean: lbar[N] = sum_{i<n, lambda_i != 0} lambdas[i] * ld[i][N]   (lambdas HOST)
+ *   se2_bary_update:  lv[i] += lbar - ld[i] for i < n.   Log-domain arrays. */
+SE2_API se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const double* lambdas, float* lbar,
+                            se2_stream stream);
+SE2_API se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar,
+                           se2_stream stream);
+
+/* Sum of a device array (deterministic), result in double on the host. */
+SE2_API se2_status se2_sum(const float* x, int64_t n, double* out_host, se2_stream stream);
+
+/* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
+ * se2_timing_get returns the number of conv launches and their summed device time (ms)
+ * since the last reset (synchronises the events). */
+SE2_API se2_status se2_timing_enable(se2_kernel k, int32_t on);
+SE2_API se2_status se2_timing_get(se2_kernel k, int64_t* n_launches, double* conv_ms, int64_t* all_launches);
+
+/* Number of kernel launches this library has issued in this process (all entry points). */
+SE2_API int64_t se2_launch_count(void);
+
+SE2_API const char* se2_last_error(void);
+SE2_API int32_t se2_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SE2OT_H */

@@ -432,7 +432,8 @@ def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, l
         errs.append(err)
         mu = s / mass
         mus.append(mu)
-    return dict(mus=np.stack(mus), masses=np.array(masses), err=np.array(errs))
+    last = dict(a=a, b=b) if not log_domain else dict(alpha=alpha, beta=beta)
+    return dict(mus=np.stack(mus), masses=np.array(masses), err=np.array(errs), **last)
 
 
 # ----------------------------------------------------------------------------------------------

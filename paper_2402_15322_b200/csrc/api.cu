@@ -1,0 +1,583 @@
+// C ABI of libse2ot (include/se2ot.h): validation, kernel objects, and the scaling-loop drivers
+// (Sinkhorn P:557-560, JKO P:224-234, barycenter App. A).  Host code only orders
+// launches on the caller's stream; every arithmetic step runs in the CUDA kernels.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "se2_internal.cuh"
+
+namespace se2 {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace se2
+
+using namespace se2;
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// grow-only device workspace owned by the kernel object
+struct Workspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+// extra per-kernel state not in the header struct
+struct KernelExtra {
+    Workspace ws;         // fields
+    Workspace trace;      // device error trace
+    Workspace partial;    // conv error partials
+    Workspace misc;       // lambdas, counters, sums
+};
+
+static KernelExtra* extra(se2_kernel_s* k) { return reinterpret_cast<KernelExtra*>(k->extra); }
+
+static se2_status ensure(Workspace& w, size_t bytes) {
+    if (w.bytes >= bytes) return SE2_OK;
+    if (w.ptr) cudaFree(w.ptr);
+    w.ptr = nullptr;
+    w.bytes = 0;
+    cudaError_t e = cudaMalloc(&w.ptr, bytes);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+        return SE2_ENOMEM;
+    }
+    w.bytes = bytes;
+    return SE2_OK;
+}
+
+// ---- conv dispatch with optional event timing ---------------------------------------------------
+static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, bool log_domain, const Epilogue& epi,
+                           cudaStream_t s, int* bpf) {
+    Timing& t = k->timing;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (t.on) {
+        if (t.used == t.events.size()) {
+            cudaEvent_t a, b;
+            SE2_CUDA_TRY(cudaEventCreate(&a));
+            SE2_CUDA_TRY(cudaEventCreate(&b));
+            t.events.push_back({a, b});
+        }
+        e0 = t.events[t.used].first;
+        e1 = t.events[t.used].second;
+        t.used++;
+        SE2_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    cudaError_t e = log_domain ? launch_conv_lse(k, in, batch, epi, s, bpf) : launch_conv_linear(k, in, batch, epi, s, bpf);
+    if (e != cudaSuccess) {
+        set_error(std::string("conv launch: ") + cudaGetErrorString(e));
+        return SE2_ECUDA;
+    }
+    t.all_launches++;
+    if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
+    return SE2_OK;
+}
+
+static se2_status check_kernel(se2_kernel k) {
+    if (!k) {
+        set_error("null kernel");
+        return SE2_EINVAL;
+    }
+    return SE2_OK;
+}
+
+extern "C" {
+
+const char* se2_last_error(void) { return g_last_error.c_str(); }
+int32_t se2_abi_version(void) { return SE2OT_ABI_VERSION; }
+int64_t se2_launch_count(void) { return g_launches.load(); }
+
+se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, double eps, int32_t radius,
+                            int32_t max_batch, int32_t device, se2_kernel* out) {
+    SE2_CHECK_ARG(out != nullptr && grid != nullptr && metric != nullptr, "null argument");
+    *out = nullptr;
+    SE2_CHECK_ARG(grid->nx > 0 && grid->ny > 0 && grid->ntheta > 0, "grid sizes must be positive");
+    SE2_CHECK_ARG(eps > 0 && isfinite(eps), "eps must be > 0");
+    SE2_CHECK_ARG(metric->w1 > 0 && metric->w2 > 0 && metric->w3 > 0, "metric weights must be > 0");
+    SE2_CHECK_ARG(radius >= 0, "radius must be >= 0");
+    SE2_CHECK_ARG(max_batch >= 1, "max_batch must be >= 1");
+    if (radius > kMaxRadius) {
+        set_error("radius > 15 is not supported by the conv engines");
+        return SE2_EUNSUPPORTED;
+    }
+    int ndev = 0;
+    SE2_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    SE2_CHECK_ARG(device >= 0 && device < ndev, "bad device index");
+    DeviceGuard g(device);
+
+    se2_kernel_s* k = new se2_kernel_s();
+    k->device = device;
+    k->nx = grid->nx;
+    k->ny = grid->ny;
+    k->nt = grid->ntheta;
+    k->R = radius;
+    k->S = 2 * radius + 1;
+    k->eps = eps;
+    k->w1 = metric->w1;
+    k->w2 = metric->w2;
+    k->w3 = metric->w3;
+    k->max_batch = max_batch;
+    k->extra = new KernelExtra();
+
+    const int nquads = (k->nt + 3) / 4;
+    const size_t tab = (size_t)nquads * k->nt * k->S * k->S * 4 * sizeof(float);
+    cudaError_t e = cudaMalloc(&k->Wq, tab);
+    if (e == cudaSuccess) e = cudaMalloc(&k->Lq, tab);
+    if (e == cudaSuccess) e = cudaMemset(k->Wq, 0, tab);
+    if (e == cudaSuccess) e = cudaMemset(k->Lq, 0, tab);
+    if (e != cudaSuccess) {
+        set_error(std::string("table allocation: ") + cudaGetErrorString(e));
+        se2_kernel_destroy(k);
+        return SE2_ENOMEM;
+    }
+    k->table_bytes = 2 * tab;
+    e = tabulate(k, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        set_error(std::string("tabulate: ") + cudaGetErrorString(e));
+        se2_kernel_destroy(k);
+        return SE2_ECUDA;
+    }
+    *out = k;
+    if (k->S > std::min(k->nx, k->ny)) {
+        set_error("support box exceeds the grid");
+        return SE2_WKERNEL_TOO_WIDE;
+    }
+    return SE2_OK;
+}
+
+se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* o) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(o != nullptr, "null stats");
+    o->box_taps = (int64_t)k->nt * k->S * k->S;
+    o->nnz_taps = k->nnz_taps;
+    o->theta_band = k->band;
+    o->radius = k->R;
+    o->zeta = std::max(k->w1, k->w2) / std::min(k->w1, k->w2);
+    o->table_bytes = k->table_bytes;
+    return SE2_OK;
+}
+
+void se2_kernel_destroy(se2_kernel k) {
+    if (!k) return;
+    DeviceGuard g(k->device);
+    if (k->Wq) cudaFree(k->Wq);
+    if (k->Lq) cudaFree(k->Lq);
+    KernelExtra* x = extra(k);
+    if (x) {
+        for (Workspace* w : {&x->ws, &x->trace, &x->partial, &x->misc})
+            if (w->ptr) cudaFree(w->ptr);
+        delete x;
+    }
+    for (auto& p : k->timing.events) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    delete k;
+}
+
+se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, uint32_t flags, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(in && out && in != out, "in/out must be distinct non-null device pointers");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    DeviceGuard g(k->device);
+    Epilogue epi;
+    epi.op = EPI_STORE;
+    epi.out = out;
+    return run_conv(k, in, batch, (flags & SE2_LOG_DOMAIN) != 0, epi, (cudaStream_t)stream, nullptr);
+}
+
+static void fill_prox(Epilogue& epi, const se2_kernel_s* k, const se2_prox* prox) {
+    const double p = prox->tau / (k->eps + prox->tau);
+    epi.prox_p = (float)p;
+    epi.prox_q = (float)p;
+    epi.cx = (float)prox->cx;
+    epi.cy = (float)prox->cy;
+    epi.hx = (float)prox->hx;
+    epi.hy = (float)prox->hy;
+}
+
+se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, float* out, int32_t batch,
+                           int32_t op, const se2_prox* prox, uint32_t flags, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(in && out && in != out, "in/out must be distinct non-null device pointers");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    SE2_CHECK_ARG(op == SE2_EPI_DIVIDE || op == SE2_EPI_MULTIPLY || op == SE2_EPI_PROX, "bad epilogue op");
+    SE2_CHECK_ARG(op == SE2_EPI_PROX || target != nullptr, "target required");
+    SE2_CHECK_ARG(op != SE2_EPI_PROX || (prox != nullptr && prox->tau >= 0), "prox required");
+    DeviceGuard g(k->device);
+    Epilogue epi;
+    epi.op = op;
+    epi.target = target;
+    epi.out = out;
+    if (op == SE2_EPI_PROX) fill_prox(epi, k, prox);
+    return run_conv(k, in, batch, (flags & SE2_LOG_DOMAIN) != 0, epi, (cudaStream_t)stream, nullptr);
+}
+
+// ---- Sinkhorn / JKO inner solve -------------------------------------------------------------------
+static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* nu, float* a, float* b, int batch,
+                                const se2_prox* prox, const se2_opts* opts, double* err_trace_host,
+                                float* s_out, cudaStream_t s) {
+    const bool LOG = (opts->flags & SE2_LOG_DOMAIN) != 0;
+    const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
+    const bool jko = prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL;
+    const int64_t N = k->N();
+    const int64_t BN = (int64_t)batch * N;
+    const int iters = opts->iters;
+    KernelExtra* x = extra(k);
+
+    // log targets
+    size_t need = (size_t)(LOG ? 2 : 0) * BN * sizeof(float);
+    se2_status st = ensure(x->ws, std::max<size_t>(need, 16));
+    if (st != SE2_OK) return st;
+    const float* tmu = mu;
+    const float* tnu = nu;
+    if (LOG) {
+        float* lmu = reinterpret_cast<float*>(x->ws.ptr);
+        float* lnu = lmu + BN;
+        SE2_CUDA_TRY(launch_log(mu, lmu, BN, s));
+        tmu = lmu;
+        if (!jko) {
+            SE2_CUDA_TRY(launch_log(nu, lnu, BN, s));
+            tnu = lnu;
+        }
+    }
+    const int bpf = conv_blocks_per_field(k, LOG);
+    if (trace) {
+        st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
+        if (st != SE2_OK) return st;
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * batch * sizeof(double));
+        if (st != SE2_OK) return st;
+    }
+    float* partial = reinterpret_cast<float*>(x->partial.ptr);
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+
+    if (!(opts->flags & SE2_WARM_START)) SE2_CUDA_TRY(launch_fill(b, BN, LOG ? 0.f : 1.f, s));
+
+    for (int l = 0; l < iters; ++l) {
+        // a = mu / K b   (error of the previous iterate fused: sum |a_old K b - mu|)
+        Epilogue e1;
+        e1.op = EPI_DIVIDE;
+        e1.target = tmu;
+        e1.out = a;
+        if (trace && l > 0) {
+            e1.err_a = a;
+            e1.err_mu = mu;
+            e1.err_partial = partial;
+        }
+        st = run_conv(k, b, batch, LOG, e1, s, nullptr);
+        if (st != SE2_OK) return st;
+        if (trace && l > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(l - 1) * batch, s));
+        // b = prox(K^T a) / K^T a    (K^T = K)
+        Epilogue e2;
+        e2.out = b;
+        if (jko) {
+            e2.op = EPI_PROX;
+            fill_prox(e2, k, prox);
+            if (l == iters - 1) e2.out2 = s_out;
+        } else {
+            e2.op = EPI_DIVIDE;
+            e2.target = tnu;
+        }
+        st = run_conv(k, a, batch, LOG, e2, s, nullptr);
+        if (st != SE2_OK) return st;
+    }
+    if (trace && iters > 0) {
+        Epilogue e3;
+        e3.op = EPI_ERRONLY;
+        e3.err_a = a;
+        e3.err_mu = mu;
+        e3.err_partial = partial;
+        st = run_conv(k, b, batch, LOG, e3, s, nullptr);
+        if (st != SE2_OK) return st;
+        SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(iters - 1) * batch, s));
+        SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
+    }
+    return SE2_OK;
+}
+
+static se2_status check_finite(se2_kernel_s* k, const float* const* ptrs, const int64_t* ns, int count,
+                               cudaStream_t s) {
+    KernelExtra* x = extra(k);
+    se2_status st = ensure(x->misc, 4096);
+    if (st != SE2_OK) return st;
+    int* cnt = reinterpret_cast<int*>(x->misc.ptr);
+    SE2_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+    for (int i = 0; i < count; ++i)
+        if (ptrs[i]) SE2_CUDA_TRY(launch_count_nonfinite(ptrs[i], ns[i], cnt, s));
+    int h = 0;
+    SE2_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h != 0) {
+        set_error("non-finite values produced by the iteration (" + std::to_string(h) + " entries)");
+        return SE2_ENONFINITE;
+    }
+    return SE2_OK;
+}
+
+se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a, float* b, int32_t batch,
+                        const se2_prox* prox, const se2_opts* opts, double* err_trace_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required, iters >= 0");
+    SE2_CHECK_ARG(mu && a && b && a != b, "mu, a, b must be non-null distinct device pointers");
+    const bool jko = prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL;
+    SE2_CHECK_ARG(jko || nu != nullptr, "nu required for the marginal prox");
+    SE2_CHECK_ARG(prox == nullptr || prox->kind == SE2_PROX_MARGINAL || (jko && prox->tau >= 0), "bad prox");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    se2_status st = sinkhorn_impl(k, mu, nu, a, b, batch, prox, opts, err_trace_host, nullptr, s);
+    if (st != SE2_OK) return st;
+    const float* ps[2] = {a, b};
+    const int64_t ns[2] = {(int64_t)batch * k->N(), (int64_t)batch * k->N()};
+    return check_finite(k, ps, ns, 2, s);
+}
+
+se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* a, float* b, const se2_prox* prox,
+                        const se2_opts* opts, double* mass_host, double* err_trace_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(opts != nullptr && opts->iters >= 1, "opts required, iters >= 1");
+    SE2_CHECK_ARG(prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL && prox->tau >= 0,
+                  "entropy-potential prox required");
+    SE2_CHECK_ARG(mu_k && mu_next && a && b && mu_k != mu_next, "bad pointers");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    se2_status st = sinkhorn_impl(k, mu_k, nullptr, a, b, 1, prox, opts, err_trace_host, mu_next, s);
+    if (st != SE2_OK) return st;
+    KernelExtra* x = extra(k);
+    st = ensure(x->misc, 4096);
+    if (st != SE2_OK) return st;
+    double* dsum = reinterpret_cast<double*>(reinterpret_cast<char*>(x->misc.ptr) + 64);
+    double* dscr = dsum + 8;
+    const int64_t N = k->N();
+    SE2_CUDA_TRY(launch_sum(mu_next, N, dsum, dscr, s));
+    SE2_CUDA_TRY(launch_scale(mu_next, N, dsum, s));
+    if (mass_host) SE2_CUDA_TRY(cudaMemcpyAsync(mass_host, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
+    const float* ps[3] = {a, b, mu_next};
+    const int64_t ns[3] = {N, N, N};
+    return check_finite(k, ps, ns, 3, s);
+}
+
+// ---- barycenter (App. A) ----------------------------------------------------------------------
+se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* mus, const double* lambdas,
+                          float* bary, float* v_state, float* w_state, const se2_opts* opts,
+                          double* err_trace_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
+    SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n, nsolve >= 1");
+    SE2_CHECK_ARG((int64_t)n * nsolve <= k->max_batch, "n*nsolve exceeds max_batch");
+    SE2_CHECK_ARG(mus && lambdas && bary, "null pointer");
+    for (int sv = 0; sv < nsolve; ++sv) {
+        double sum = 0;
+        for (int i = 0; i < n; ++i) {
+            SE2_CHECK_ARG(lambdas[sv * n + i] >= 0 && isfinite(lambdas[sv * n + i]), "lambda must be >= 0");
+            sum += lambdas[sv * n + i];
+        }
+        SE2_CHECK_ARG(fabs(sum - 1.0) <= 1e-9, "lambdas must lie on the simplex");
+    }
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool LOG = (opts->flags & SE2_LOG_DOMAIN) != 0;
+    const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
+    const int64_t N = k->N();
+    const int F = n * nsolve;
+    const int64_t FN = (int64_t)F * N;
+    const int iters = opts->iters;
+    KernelExtra* x = extra(k);
+    // workspace: mu_rep [F][N] (linear), lmu_rep [F][N], v [F][N], w [F][N], d [F][N]
+    size_t need = (size_t)5 * FN * sizeof(float);
+    se2_status st = ensure(x->ws, need);
+    if (st != SE2_OK) return st;
+    float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
+    float* lmu_rep = mu_rep + FN;
+    float* v = v_state ? v_state : lmu_rep + FN;
+    float* w = w_state ? w_state : lmu_rep + 2 * FN;
+    float* d = lmu_rep + 3 * FN;
+    for (int sv = 0; sv < nsolve; ++sv)
+        SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
+                                     cudaMemcpyDeviceToDevice, s));
+    const float* tmu = mu_rep;
+    if (LOG) {
+        SE2_CUDA_TRY(launch_log(mu_rep, lmu_rep, FN, s));
+        tmu = lmu_rep;
+    }
+    st = ensure(x->misc, 4096 + sizeof(float) * F);
+    if (st != SE2_OK) return st;
+    float* lam_dev = reinterpret_cast<float*>(reinterpret_cast<char*>(x->misc.ptr) + 4096);
+    std::vector<float> lamf(F);
+    for (int i = 0; i < F; ++i) lamf[i] = (float)lambdas[i];
+    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lamf.data(), sizeof(float) * F, cudaMemcpyHostToDevice, s));
+    const int bpf = conv_blocks_per_field(k, LOG);
+    if (trace) {
+        st = ensure(x->partial, (size_t)F * bpf * sizeof(float));
+        if (st != SE2_OK) return st;
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * F * sizeof(double));
+        if (st != SE2_OK) return st;
+    }
+    float* partial = reinterpret_cast<float*>(x->partial.ptr);
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+
+    SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
+    SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
+    for (int j = 0; j < iters; ++j) {
+        // w_i = mu_i / K v_i   (fused: error of the previous v-update, sum |w_i K v_i - mu_i|)
+        Epilogue e1;
+        e1.op = EPI_DIVIDE;
+        e1.target = tmu;
+        e1.out = w;
+        if (trace && j > 0) {
+            e1.err_a = w;
+            e1.err_mu = mu_rep;
+            e1.err_partial = partial;
+        }
+        st = run_conv(k, v, F, LOG, e1, s, nullptr);
+        if (st != SE2_OK) return st;
+        if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
+        // d_i = v_i K w_i
+        Epilogue e2;
+        e2.op = EPI_MULTIPLY;
+        e2.target = v;
+        e2.out = d;
+        st = run_conv(k, w, F, LOG, e2, s, nullptr);
+        if (st != SE2_OK) return st;
+        // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
+        if (LOG) {
+            SE2_CUDA_TRY(launch_bary_logmean(n, nsolve, N, d, lam_dev, bary, s));
+            SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, d, bary, s));
+        } else {
+            SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
+        }
+    }
+    if (trace && iters > 0) {
+        Epilogue e3;
+        e3.op = EPI_ERRONLY;
+        e3.err_a = w;
+        e3.err_mu = mu_rep;
+        e3.err_partial = partial;
+        st = run_conv(k, v, F, LOG, e3, s, nullptr);
+        if (st != SE2_OK) return st;
+        SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
+        std::vector<double> h((size_t)iters * F);
+        SE2_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, sizeof(double) * iters * F, cudaMemcpyDeviceToHost, s));
+        SE2_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int j = 0; j < iters; ++j)
+            for (int sv = 0; sv < nsolve; ++sv) {
+                double e = 0;
+                for (int i = 0; i < n; ++i) e += lambdas[sv * n + i] * h[(size_t)j * F + sv * n + i];
+                err_trace_host[(size_t)j * nsolve + sv] = e;
+            }
+    }
+    const float* ps[3] = {bary, v, w};
+    const int64_t ns[3] = {(int64_t)nsolve * N, FN, FN};
+    return check_finite(k, ps, ns, 3, s);
+}
+
+se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, const float* mu, int32_t batch,
+                              uint32_t flags, double* err_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(a && b && mu && err_host, "null pointer");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool LOG = (flags & SE2_LOG_DOMAIN) != 0;
+    KernelExtra* x = extra(k);
+    const int bpf = conv_blocks_per_field(k, LOG);
+    se2_status st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
+    if (st != SE2_OK) return st;
+    st = ensure(x->trace, (size_t)batch * sizeof(double));
+    if (st != SE2_OK) return st;
+    Epilogue e;
+    e.op = EPI_ERRONLY;
+    e.err_a = a;
+    e.err_mu = mu;
+    e.err_partial = reinterpret_cast<float*>(x->partial.ptr);
+    st = run_conv(k, b, batch, LOG, e, s, nullptr);
+    if (st != SE2_OK) return st;
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    SE2_CUDA_TRY(launch_reduce_partials(e.err_partial, batch, bpf, tr, s));
+    SE2_CUDA_TRY(cudaMemcpyAsync(err_host, tr, sizeof(double) * batch, cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const double* lambdas, float* lbar,
+                            se2_stream stream) {
+    SE2_CHECK_ARG(n >= 1 && N >= 1 && ld && lambdas && lbar, "bad arguments");
+    // lambdas are host values; pass them through a small device copy
+    float* lam_dev = nullptr;
+    SE2_CUDA_TRY(cudaMallocAsync(&lam_dev, sizeof(float) * n, (cudaStream_t)stream));
+    std::vector<float> lf(n);
+    for (int i = 0; i < n; ++i) lf[i] = (float)lambdas[i];
+    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lf.data(), sizeof(float) * n, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    SE2_CUDA_TRY(launch_bary_logmean(n, 1, N, ld, lam_dev, lbar, (cudaStream_t)stream));
+    SE2_CUDA_TRY(cudaFreeAsync(lam_dev, (cudaStream_t)stream));
+    return SE2_OK;
+}
+
+se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar, se2_stream stream) {
+    SE2_CHECK_ARG(n >= 1 && N >= 1 && lv && ld && lbar, "bad arguments");
+    SE2_CUDA_TRY(launch_bary_update_log(n, 1, N, lv, ld, lbar, (cudaStream_t)stream));
+    return SE2_OK;
+}
+
+se2_status se2_sum(const float* xp, int64_t n, double* out_host, se2_stream stream) {
+    SE2_CHECK_ARG(xp && n >= 1 && out_host, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    double* d = nullptr;
+    SE2_CUDA_TRY(cudaMallocAsync(&d, sizeof(double) * 512, s));
+    SE2_CUDA_TRY(launch_sum(xp, n, d, d + 8, s));
+    SE2_CUDA_TRY(cudaMemcpyAsync(out_host, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaFreeAsync(d, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_timing_enable(se2_kernel k, int32_t on) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    k->timing.on = on != 0;
+    k->timing.used = 0;
+    k->timing.all_launches = 0;
+    return SE2_OK;
+}
+
+se2_status se2_timing_get(se2_kernel k, int64_t* n_launches, double* conv_ms, int64_t* all_launches) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    DeviceGuard g(k->device);
+    double tot = 0;
+    for (size_t i = 0; i < k->timing.used; ++i) {
+        SE2_CUDA_TRY(cudaEventSynchronize(k->timing.events[i].second));
+        float ms = 0;
+        SE2_CUDA_TRY(cudaEventElapsedTime(&ms, k->timing.events[i].first, k->timing.events[i].second));
+        tot += ms;
+    }
+    if (n_launches) *n_launches = (int64_t)k->timing.used;
+    if (conv_ms) *conv_ms = tot;
+    if (all_launches) *all_launches = k->timing.all_launches;
+    k->timing.used = 0;
+    k->timing.all_launches = 0;
+    return SE2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// Shared device helpers of the two conv engines (linear FFMA and exact log-sum-exp).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "se2_internal.cuh"
+
+namespace se2 {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 4-byte async copy global -> shared with zero fill when !valid (src-size 0)
+__device__ __forceinline__ void cp_async4(void* dst, const float* src, bool valid) {
+    int sz = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Block-wide deterministic sum of one float per thread; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red /* >= NT/32 floats */) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    float t = 0.f;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) t += red[i];
+    }
+    return t;
+}
+
+// Apply the fused epilogue to one conv output.  y_lin: linear-domain value (linear engine),
+// or ly (natural log) in the log engine.  Returns the marginal-error contribution.
+template <bool LOG>
+__device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, int ix, int iy, float y) {
+    float err = 0.f;
+    if (e.err_a != nullptr) {
+        float a_old = e.err_a[idx];
+        float mu = e.err_mu[idx];
+        float row = LOG ? expf(a_old + y) : a_old * y;
+        err = fabsf(row - mu);
+    }
+    float o;
+    switch (e.op) {
+        case EPI_STORE: o = y; break;
+        case EPI_DIVIDE:
+            if (LOG) {
+                const float t = e.target[idx];
+                o = (t == -INFINITY) ? -INFINITY : t - y;   // log(0 / y) = -inf, as 0 / max(y, floor) = 0
+            } else {
+                o = e.target[idx] / fmaxf(y, kDivFloor);
+            }
+            break;
+        case EPI_MULTIPLY: o = LOG ? (e.target[idx] + y) : (e.target[idx] * y); break;
+        case EPI_PROX: {
+            float dxp = ((float)ix + 0.5f - e.cx) * e.hx, dyp = ((float)iy + 0.5f - e.cy) * e.hy;
+            float V = dxp * dxp + dyp * dyp;
+            if (LOG) {
+                o = -e.prox_p * y - e.prox_q * V;
+                if (e.out2 != nullptr) e.out2[idx] = expf(o + y);
+            } else {
+                float z = fmaxf(y, kDivFloor);
+                o = exp2f(-e.prox_p * log2f(z) - e.prox_q * V * kLog2e);
+                if (e.out2 != nullptr) e.out2[idx] = o * z;
+            }
+            break;
+        }
+        default: return err;  // EPI_ERRONLY
+    }
+    e.out[idx] = o;
+    return err;
+}
+
+}  // namespace se2

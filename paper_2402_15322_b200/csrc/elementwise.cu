@@ -1,0 +1,179 @@
+// Elementwise updates and deterministic reductions of the scaling loop (HBM-bound, tiny next to
+// the convolutions): barycenter geometric mean (App. A), JKO finish (R10), sums.
+#include <math.h>
+
+#include "conv_common.cuh"
+
+namespace se2 {
+
+static inline int grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+__global__ void fill_kernel(float* x, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+cudaError_t launch_fill(float* x, int64_t n, float v, cudaStream_t s) {
+    fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, v);
+    count_launch();
+    return cudaGetLastError();
+}
+
+__global__ void log_kernel(const float* x, float* y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = logf(x[i]);
+}
+cudaError_t launch_log(const float* x, float* y, int64_t n, cudaStream_t s) {
+    log_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// out[b] = sum_{i < nblocks} partial[b][i], fixed order (one block per b) -> deterministic.
+__global__ void reduce_partials_kernel(const float* partial, int nblocks, double* out) {
+    __shared__ double red[256];
+    const int b = blockIdx.x;
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) t += (double)partial[(int64_t)b * nblocks + i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b] = red[0];
+}
+cudaError_t launch_reduce_partials(const float* partial, int batch, int nblocks, double* out, cudaStream_t s) {
+    reduce_partials_kernel<<<batch, 256, 0, s>>>(partial, nblocks, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// lbar[sv][x] = sum_i lam[sv][i] * ld[sv][i][x]  (lambda_i = 0 skipped: d^0 = 1, reading R6)
+__global__ void bary_logmean_kernel(int n, int nsolve, int64_t N, const float* ld, const float* lam,
+                                    float* lbar) {
+    const int64_t total = (int64_t)nsolve * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int sv = (int)(t / N);
+        const int64_t x = t - (int64_t)sv * N;
+        float acc = 0.f;
+        for (int i = 0; i < n; ++i) {
+            float l = lam[sv * n + i];
+            if (l != 0.f) acc += l * ld[((int64_t)sv * n + i) * N + x];
+        }
+        lbar[t] = acc;
+    }
+}
+cudaError_t launch_bary_logmean(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev, float* lbar,
+                                cudaStream_t s) {
+    bary_logmean_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, ld, lam_dev, lbar);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// lv[sv][i] += lbar[sv] - ld[sv][i]   (App. A: v_i <- v_i mu / d_i, in logs)
+__global__ void bary_update_log_kernel(int n, int nsolve, int64_t N, float* lv, const float* ld, const float* lbar) {
+    const int64_t total = (int64_t)nsolve * n * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = t / N;          // field index sv*n + i
+        const int64_t x = t - f * N;
+        const int sv = (int)(f / n);
+        lv[t] = lv[t] + (lbar[(int64_t)sv * N + x] - ld[t]);
+    }
+}
+cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, const float* ld, const float* lbar,
+                                   cudaStream_t s) {
+    bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, ld, lbar);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Linear domain: mu = prod_i d_i^lambda_i ; v_i <- v_i * mu / max(d_i, floor); bary = mu.
+__global__ void bary_update_lin_kernel(int n, int nsolve, int64_t N, float* v, const float* d, const float* lam,
+                                       float* bary) {
+    const int64_t total = (int64_t)nsolve * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int sv = (int)(t / N);
+        const int64_t x = t - (int64_t)sv * N;
+        float mu = 1.f;
+        for (int i = 0; i < n; ++i) {
+            float l = lam[sv * n + i];
+            if (l != 0.f) mu *= powf(d[((int64_t)sv * n + i) * N + x], l);
+        }
+        for (int i = 0; i < n; ++i) {
+            int64_t o = ((int64_t)sv * n + i) * N + x;
+            v[o] = v[o] * mu / fmaxf(d[o], kDivFloor);
+        }
+        bary[t] = mu;
+    }
+}
+cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const float* d, const float* lam_dev,
+                                   float* bary, cudaStream_t s) {
+    bary_update_lin_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, v, d, lam_dev, bary);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Deterministic sum: fixed grid of 296 blocks -> fp64 partials -> one block.
+constexpr int kSumBlocks = 296;
+__global__ void sum_stage1(const float* x, int64_t n, double* part) {
+    __shared__ double red[256];
+    double t = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t += (double)x[i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void sum_stage2(const double* part, int nb, double* out) {
+    __shared__ double red[256];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) t += part[i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = red[0];
+}
+cudaError_t launch_sum(const float* x, int64_t n, double* out_dev, double* scratch, cudaStream_t s) {
+    sum_stage1<<<kSumBlocks, 256, 0, s>>>(x, n, scratch);
+    count_launch();
+    sum_stage2<<<1, 256, 0, s>>>(scratch, kSumBlocks, out_dev);
+    count_launch();
+    return cudaGetLastError();
+}
+
+__global__ void scale_kernel(float* x, int64_t n, const double* sum) {
+    const double inv = 1.0 / sum[0];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = (float)((double)x[i] * inv);
+}
+cudaError_t launch_scale(float* x, int64_t n, const double* sum_dev, cudaStream_t s) {
+    scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, sum_dev);
+    count_launch();
+    return cudaGetLastError();
+}
+
+__global__ void count_nonfinite_kernel(const float* x, int64_t n, int* count) {
+    int c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += (isnan(x[i]) || (isinf(x[i]) && x[i] > 0.f)) ? 1 : 0;   // -inf is a valid log(0)
+    if (c) atomicAdd(count, c);
+}
+cudaError_t launch_count_nonfinite(const float* x, int64_t n, int* count_dev, cudaStream_t s) {
+    count_nonfinite_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, count_dev);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace se2

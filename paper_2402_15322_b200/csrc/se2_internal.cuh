@@ -1,0 +1,118 @@
+// Internal declarations of the se2ot CUDA library (sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "se2ot.h"
+
+namespace se2 {
+
+// thread-local last error message (se2_last_error)
+void set_error(const std::string& msg);
+// process-wide count of kernel launches issued by this library (se2_launch_count)
+void count_launch(int64_t n = 1);
+
+#define SE2_CUDA_TRY(expr)                                                                   \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            ::se2::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));            \
+            return SE2_ECUDA;                                                                \
+        }                                                                                    \
+    } while (0)
+
+#define SE2_CHECK_ARG(cond, msg)                                                             \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            ::se2::set_error(msg);                                                           \
+            return SE2_EINVAL;                                                               \
+        }                                                                                    \
+    } while (0)
+
+constexpr int kMaxRadius = 15;
+constexpr float kDivFloor = 1e-30f;   // division guard (reading R9)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// Epilogue ops of the fused conv (see se2_conv_update in se2ot.h)
+enum EpiOp : int {
+    EPI_STORE = 0,
+    EPI_DIVIDE = 1,     // out = target / max(y, floor)   | log: target - ly
+    EPI_MULTIPLY = 2,   // out = target * y               | log: target + ly
+    EPI_PROX = 3,       // out = max(y,floor)^-p exp(-q V) | log: -p ly - q V
+    EPI_ERRONLY = 4,    // no store; only the marginal-error partial
+};
+
+// Everything an epilogue needs; plain-old-data passed by value to the kernels.
+struct Epilogue {
+    int op = EPI_STORE;
+    const float* target = nullptr;   // [batch][N]
+    float* out = nullptr;            // [batch][N]
+    float* out2 = nullptr;           // EPI_PROX only: s = prox(z) = b * z (or its log-domain form exp(beta + lz))
+    // marginal-error fusion: err += |a_old * y - mu| with a_old = err_a (read before out is written)
+    const float* err_a = nullptr;    // [batch][N] (linear a, or alpha in log domain); null = no error
+    const float* err_mu = nullptr;   // [batch][N] linear mu
+    float* err_partial = nullptr;    // [batch][blocks_per_field]
+    // prox (entropy + potential): p = tau/(eps+tau) exponent, q = tau/(eps+tau) potential factor
+    float prox_p = 0.f, prox_q = 0.f;
+    float cx = 0.f, cy = 0.f, hx = 0.f, hy = 0.f;
+};
+
+struct Timing {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // pool
+    size_t used = 0;
+    int64_t all_launches = 0;
+};
+
+}  // namespace se2
+
+struct se2_kernel_s {
+    int device = 0;
+    int nx = 0, ny = 0, nt = 0, R = 0, S = 0;
+    double eps = 0, w1 = 0, w2 = 0, w3 = 0;
+    int max_batch = 1;
+    int band = 0;           // fp32-nonzero theta half band (bins)
+    int64_t nnz_taps = 0;   // per output
+    // device tables, theta-quad interleaved: [nt/4][nt][S][S][4]  (to = 4*qd + q)
+    float* Wq = nullptr;    // exp(-rho^2/eps)  fp32
+    float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
+    size_t table_bytes = 0;
+    void* extra = nullptr;        // grow-only workspaces (api.cu)
+    se2::Timing timing;
+    int64_t N() const { return (int64_t)nx * ny * nt; }
+};
+
+namespace se2 {
+
+// conv launchers (conv_linear.cu / conv_lse.cu).  in: [batch][N]; epilogue describes the output.
+// returns the number of CTAs per field (for error partial reduction).
+cudaError_t launch_conv_linear(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
+                               cudaStream_t s, int* blocks_per_field);
+cudaError_t launch_conv_lse(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
+                            cudaStream_t s, int* blocks_per_field);
+int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain);
+int conv_blocks_per_field_linear(const se2_kernel_s* k);
+int conv_blocks_per_field_lse(const se2_kernel_s* k);
+
+// tabulation (tabulate.cu)
+cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s);
+
+// elementwise / reductions (elementwise.cu)
+cudaError_t launch_fill(float* x, int64_t n, float v, cudaStream_t s);
+cudaError_t launch_log(const float* x, float* y, int64_t n, cudaStream_t s);
+cudaError_t launch_reduce_partials(const float* partial, int batch, int nblocks, double* out,
+                                   cudaStream_t s);
+cudaError_t launch_bary_logmean(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev,
+                                float* lbar, cudaStream_t s);
+cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, const float* ld,
+                                   const float* lbar, cudaStream_t s);
+cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const float* d,
+                                   const float* lam_dev, float* bary, cudaStream_t s);
+cudaError_t launch_sum(const float* x, int64_t n, double* out_dev, double* scratch, cudaStream_t s);
+cudaError_t launch_scale(float* x, int64_t n, const double* sum_dev, cudaStream_t s);
+cudaError_t launch_count_nonfinite(const float* x, int64_t n, int* count_dev, cudaStream_t s);
+
+}  // namespace se2

@@ -1,0 +1,90 @@
+// K1: Gibbs-kernel tabulation (App. A "K_eps <- exp(-rho_b^2/eps)").
+//
+// For output orientation theta_o = 2 pi to/nt, input orientation theta_i = 2 pi ti/nt and spatial
+// offset (dx, dy) cells (dx = ix_g - ix_h), the relative element is
+//     h^{-1} g = ( R_{-theta_i} (dx/nx, dy/ny),  wrap(theta_o - theta_i) ),   wrap into [-pi, pi)
+// and the half-angle coordinates and rho_b give
+//     W = exp(-rho_b^2/eps),   L2 = -rho_b^2/eps * log2(e).
+// Computed in fp64, stored fp32 in the theta-quad interleaved layout [nt/4][nt][S][S][4]
+// (to = 4*qd + q), so one 16-byte shared-memory broadcast feeds four output orientations.
+#include <math.h>
+
+#include "se2_internal.cuh"
+
+namespace se2 {
+
+__global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
+                                double w3, float* __restrict__ Wq, float* __restrict__ Lq,
+                                int* __restrict__ nnz_pair) {
+    const int S = 2 * R + 1;
+    const int64_t total = (int64_t)nt * nt * S * S;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int dxi = (int)(idx % S);
+        int dyi = (int)((idx / S) % S);
+        int ti = (int)((idx / ((int64_t)S * S)) % nt);
+        int to = (int)(idx / ((int64_t)S * S * nt));
+        const double two_pi = 6.283185307179586476925286766559;
+        double ddx = (double)(dxi - R) / nx;
+        double ddy = (double)(dyi - R) / ny;
+        double thi = two_pi * ti / nt;
+        // R_{-theta_i} applied to the spatial offset
+        double ci = cos(thi), si = sin(thi);
+        double X = ci * ddx + si * ddy;
+        double Y = -si * ddx + ci * ddy;
+        // wrap(theta_o - theta_i) into [-pi, pi): integer bin offset k in [-nt/2, nt/2)
+        int k = ((to - ti) % nt + nt) % nt;
+        if (2 * k >= nt) k -= nt;
+        double Th = two_pi * k / nt;
+        double ch = cos(0.5 * Th), sh = sin(0.5 * Th);
+        double b1 = X * ch + Y * sh;
+        double b2 = -X * sh + Y * ch;
+        double b3 = Th;
+        double rho2 = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2 + w3 * w3 * b3 * b3;
+        double e = -rho2 / eps;
+        float wv = (float)exp(e);
+        int qd = to >> 2, q = to & 3;
+        int64_t o = ((((int64_t)qd * nt + ti) * S + dyi) * S + dxi) * 4 + q;
+        Wq[o] = wv;
+        Lq[o] = (float)(e * 1.4426950408889634073599246810019);
+        if (wv != 0.0f) atomicAdd(&nnz_pair[to * nt + ti], 1);
+    }
+}
+
+cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
+    const int nt = k->nt, S = k->S;
+    const int64_t total = (int64_t)nt * nt * S * S;
+    int* nnz_dev = nullptr;
+    cudaError_t e = cudaMalloc(&nnz_dev, sizeof(int) * nt * nt);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(nnz_dev, 0, sizeof(int) * nt * nt, s);
+    // padding entries of a partial last quad (nt % 4 != 0) stay zero / -inf-like
+    int threads = 256;
+    int blocks = (int)((total + threads - 1) / threads);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    tabulate_kernel<<<blocks, threads, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2, k->w3,
+                                               k->Wq, k->Lq, nnz_dev);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }
+    std::vector<int> nnz(nt * nt);
+    e = cudaMemcpyAsync(nnz.data(), nnz_dev, sizeof(int) * nt * nt, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(nnz_dev);
+    if (e != cudaSuccess) return e;
+    int band = 0;
+    int64_t nnz_total = 0;
+    for (int to = 0; to < nt; ++to)
+        for (int ti = 0; ti < nt; ++ti) {
+            if (nnz[to * nt + ti] == 0) continue;
+            int kk = ((to - ti) % nt + nt) % nt;
+            if (2 * kk >= nt) kk -= nt;
+            if (kk < 0) kk = -kk;
+            if (kk > band) band = kk;
+            nnz_total += nnz[to * nt + ti];
+        }
+    k->band = band;
+    k->nnz_taps = nnz_total / nt;
+    return cudaSuccess;
+}
+
+}  // namespace se2

@@ -204,3 +204,58 @@ def config_inputs(cfg: Config):
     else:
         raise KeyError(cfg.name)
     return out
+
+
+# ------------------------------------------------------------------------------------------------
+# Parity cases (data only): the BASELINE configs at full size (whole runs where the oracle finishes,
+# prefixes where it cannot) and reduced-size analogues with ragged tiles that run to the full
+# iteration count.  tests/golden/make_golden.py computes the expected values with oracle/ only.
+# ------------------------------------------------------------------------------------------------
+
+@dataclasses.dataclass(frozen=True)
+class ParityCase:
+    name: str
+    base: str                  # BASELINE config it derives from
+    nx: int
+    ny: int
+    ntheta: int
+    R: int
+    iters: int
+    jko_steps: int = 0
+    full_fields: bool = True   # store whole fields (else sampled entries)
+
+
+PARITY_CASES: List[ParityCase] = [
+    ParityCase("c0", "c0", 16, 16, 8, 3, 100),
+    ParityCase("c1", "c1", 28, 28, 16, 5, 200),
+    ParityCase("c2p", "c2", 64, 64, 32, 7, 10, full_fields=False),
+    ParityCase("c2m", "c2", 40, 36, 32, 7, 300),
+    ParityCase("c3p", "c3", 128, 128, 32, 10, 2, full_fields=False),
+    ParityCase("c3m", "c3", 44, 40, 32, 10, 40),
+    ParityCase("c4p", "c4", 256, 256, 64, 15, 2, jko_steps=1, full_fields=False),
+    ParityCase("c4m", "c4", 72, 60, 16, 4, 200, jko_steps=3),
+]
+
+
+def get_parity_case(name: str) -> ParityCase:
+    for c in PARITY_CASES:
+        if c.name == name:
+            return c
+    raise KeyError(name)
+
+
+def parity_inputs(pc: ParityCase):
+    """Config of the case (a Config with the case's grid / radius / iteration counts) and its inputs,
+    generated exactly like the base config's (same seeds, same recipe) on the case's grid."""
+    base = get_config(pc.base)
+    cfg = dataclasses.replace(base, name=base.name, nx=pc.nx, ny=pc.ny, ntheta=pc.ntheta,
+                              support=2 * pc.R + 1, iters=pc.iters,
+                              jko_steps=pc.jko_steps if pc.jko_steps else base.jko_steps)
+    return cfg, config_inputs(cfg)
+
+
+def sample_indices(N: int, count: int, seed: int) -> np.ndarray:
+    """Seeded sample of flat field indices (always includes the first and last entries)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    idx = np.unique(np.concatenate([[0, N - 1], rng.choice(N, size=min(count, N), replace=False)]))
+    return idx.astype(np.int64)

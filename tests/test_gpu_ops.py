@@ -1,0 +1,227 @@
+"""GPU parity of the individual hot-path operators against the fp64 oracle (-m gpu).
+
+Kernel tabulation (A1), linear conv (A2), exact LSE conv (A3), the fused scaling-update epilogues
+(A4, A5, A6 pieces) and the marginal-error reduction (A7), on every config grid (full oracle
+field where it finishes in seconds, sampled outputs at the full c3/c4 sizes) plus ragged / odd /
+degenerate shapes.  All calls go through the C ABI (paper_2402_15322_b200 binding).
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import se2_synth as S
+from gpu_util import measure_err, potential_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_CONV = 1e-5     # fp32 sums of positive terms vs fp64 (relative, elementwise)
+TOL_LSE = 1e-5      # |d ly| / max(1, |ly|)
+
+
+def _kernel(nx, ny, nt, eps, w, R, batch=1):
+    from paper_2402_15322_b200 import Kernel
+    return Kernel(nx, ny, nt, eps, w, R, max_batch=batch, device=0)
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+CFG_GRIDS = [(c.name, c.nx, c.ny, c.ntheta, c.eps, c.w, c.R) for c in S.CONFIGS]
+ODD_GRIDS = [
+    ("ragged", 37, 23, 12, 0.02, (1.0, 3.0, 1.0), 5),      # ntheta % 4 != 0, ragged tiles
+    ("thin", 5, 70, 8, 0.05, (1.0, 2.0, 1.5), 3),
+    ("r0", 33, 33, 8, 0.05, (1.0, 3.0, 1.0), 0),           # theta-only convolution
+    ("nt1", 40, 24, 1, 0.01, (1.0, 2.0, 1.0), 6),          # plain anisotropic Gaussian
+    ("wide", 9, 9, 4, 0.5, (1.0, 1.0, 1.0), 7),            # support wider than the grid
+]
+
+
+@pytest.mark.parametrize("case", CFG_GRIDS + ODD_GRIDS, ids=lambda c: c[0])
+def test_kernel_stats(case, cuda_device):
+    name, nx, ny, nt, eps, w, R = case
+    k = _kernel(nx, ny, nt, eps, w, R)
+    st = k.stats()
+    T = O.kernel_table(O.Grid(nx, ny, nt), R, eps, w)
+    T32 = T.astype(np.float32)
+    assert st["box_taps"] == nt * (2 * R + 1) ** 2
+    assert st["nnz_taps"] == int(np.count_nonzero(T32)) // nt
+    band = 0
+    for to in range(nt):
+        for ti in range(nt):
+            if np.any(T32[to, ti] != 0):
+                kk = (to - ti) % nt
+                if 2 * kk >= nt:
+                    kk -= nt
+                band = max(band, abs(kk))
+    assert st["theta_band"] == band
+
+
+def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True):
+    k = _kernel(nx, ny, nt, eps, w, R, batch)
+    g = O.Grid(nx, ny, nt)
+    shape = (batch, nt, ny, nx)
+    if log_domain:
+        rng = np.random.default_rng(zlib.crc32(name.encode()))
+        v = rng.uniform(-100, 100, size=shape).astype(np.float32)     # wide log range
+        Lt = O.log_kernel_table(g, R, eps, w)
+    else:
+        v = S.random_positive_field(shape, seed=zlib.crc32(name.encode()), log_range=30.0)
+        Tt = O.kernel_table(g, R, eps, w)
+    from paper_2402_15322_b200 import se2_conv
+    y = _host(se2_conv(k, _dev(v), log_domain=log_domain))
+    if full:
+        ref = O.lse_conv(Lt, v.astype(np.float64)) if log_domain else O.conv(Tt, v.astype(np.float64))
+        got = y
+    else:
+        N = nx * ny * nt
+        idx = S.sample_indices(N, 400, seed=3)
+        ref, got = [], []
+        for b in range(batch):
+            for f in idx:
+                to, rem = divmod(int(f), nx * ny)
+                iy, ix = divmod(rem, nx)
+                if log_domain:
+                    ref.append(O.lse_conv_point(Lt, v[b].astype(np.float64), to, iy, ix))
+                else:
+                    ref.append(O.conv_point(Tt, v[b].astype(np.float64), to, iy, ix))
+                got.append(y[b, to, iy, ix])
+        ref, got = np.array(ref), np.array(got)
+    if log_domain:
+        e = potential_err(got, ref)
+        assert e < TOL_LSE, (name, e)
+    else:
+        e = float(np.max(np.abs(got - ref) / np.abs(ref)))
+        assert e < TOL_CONV, (name, e)
+
+
+@pytest.mark.parametrize("case", CFG_GRIDS + ODD_GRIDS, ids=lambda c: c[0])
+@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
+def test_conv_parity(case, log_domain, cuda_device):
+    name, nx, ny, nt, eps, w, R = case
+    big = nx * ny * nt > 200000
+    _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=1 if big else 2, full=not big)
+
+
+def test_conv_zero_and_neginf_inputs(cuda_device):
+    from paper_2402_15322_b200 import se2_conv
+    k = _kernel(20, 20, 8, 0.05, (1, 3, 1), 3)
+    z = torch.zeros(8, 20, 20, device="cuda")
+    assert torch.count_nonzero(se2_conv(k, z)).item() == 0
+    ninf = torch.full((8, 20, 20), -float("inf"), device="cuda")
+    out = se2_conv(k, ninf, log_domain=True)
+    assert torch.all(out == -float("inf")).item()
+    # a single finite log value reproduces the log kernel column
+    lv = ninf.clone()
+    lv[2, 10, 10] = 1.5
+    out = _host(se2_conv(k, lv, log_domain=True))
+    L = O.log_kernel_table(O.Grid(20, 20, 8), 3, 0.05, (1, 3, 1))
+    np.testing.assert_allclose(out[:, 7:14, 7:14], L[:, 2] + 1.5, rtol=2e-6, atol=2e-5)
+    assert np.all(out[:, :7, :] == -np.inf)
+
+
+def test_invalid_arguments_raise(cuda_device):
+    from paper_2402_15322_b200 import SE2Error, se2_conv
+    from paper_2402_15322_b200 import Kernel
+    with pytest.raises(SE2Error):
+        Kernel(16, 16, 8, -1.0, (1, 1, 1), 3)
+    with pytest.raises(SE2Error):
+        Kernel(16, 16, 8, 0.1, (1, 1, 1), 16)        # radius > 15 unsupported
+    k = _kernel(16, 16, 8, 0.05, (1, 3, 1), 3, batch=1)
+    x = torch.ones(2, 8, 16, 16, device="cuda")
+    with pytest.raises(SE2Error):
+        se2_conv(k, x)                                 # batch 2 > max_batch 1
+    with pytest.raises(TypeError):
+        se2_conv(k, torch.ones(8, 16, 16))             # host tensor: no CPU fallback
+
+
+@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
+def test_fused_epilogues(log_domain, cuda_device):
+    from paper_2402_15322_b200 import _lib as L, make_prox, se2_conv_update
+    nx, ny, nt, eps, w, R = 40, 36, 16, 0.02, (1.0, 3.0, 1.0), 5
+    k = _kernel(nx, ny, nt, eps, w, R, 2)
+    g = O.Grid(nx, ny, nt)
+    shape = (2, nt, ny, nx)
+    v = S.random_positive_field(shape, seed=21, log_range=20.0).astype(np.float64)
+    tgt = S.random_positive_field(shape, seed=22, lo=1e-6, hi=1e-3).astype(np.float64)
+    Kv = O.conv(O.kernel_table(g, R, eps, w), v)
+    if log_domain:
+        xin, tin = np.log(v), np.log(tgt)
+    else:
+        xin, tin = v, tgt
+    xin32, tin32 = xin.astype(np.float32), tin.astype(np.float32)
+    # reference computed from the fp32-rounded inputs the GPU sees
+    if log_domain:
+        Kv = np.exp(O.lse_conv(O.log_kernel_table(g, R, eps, w), xin32.astype(np.float64)))
+    else:
+        Kv = O.conv(O.kernel_table(g, R, eps, w), xin32.astype(np.float64))
+    t64 = tin32.astype(np.float64)
+    out = torch.empty(shape, device="cuda")
+    se2_conv_update(k, _dev(xin32), _dev(tin32), out, L.SE2_EPI_DIVIDE, log_domain)
+    got = _host(out)
+    if log_domain:
+        assert potential_err(got, t64 - np.log(Kv)) < TOL_LSE
+    else:
+        assert measure_err(got, t64 / Kv) < TOL_CONV
+    se2_conv_update(k, _dev(xin32), _dev(tin32), out, L.SE2_EPI_MULTIPLY, log_domain)
+    got = _host(out)
+    if log_domain:
+        assert potential_err(got, t64 + np.log(Kv)) < TOL_LSE
+    else:
+        assert measure_err(got, t64 * Kv) < TOL_CONV
+    # JKO prox: b = z^{-tau/(eps+tau)} exp(-tau V/(eps+tau)), V = |x - c|^2 (R10)
+    tau = 1e-3
+    prox = make_prox(k, tau)
+    se2_conv_update(k, _dev(xin32), None, out, L.SE2_EPI_PROX, log_domain, prox=prox)
+    got = _host(out)
+    V = O.jko_potential(g)
+    p = tau / (eps + tau)
+    ref_log = -p * np.log(Kv) - p * V
+    if log_domain:
+        assert potential_err(got, ref_log) < TOL_LSE
+    else:
+        assert potential_err(np.log(got), ref_log) < TOL_LSE
+
+
+@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
+def test_marginal_error(log_domain, cuda_device):
+    from paper_2402_15322_b200 import se2_marginal_error
+    nx, ny, nt, eps, w, R = 28, 28, 16, 0.02, (1.0, 3.0, 1.0), 5
+    k = _kernel(nx, ny, nt, eps, w, R, 2)
+    g = O.Grid(nx, ny, nt)
+    shape = (2, nt, ny, nx)
+    a = S.random_positive_field(shape, seed=31, lo=0.5, hi=2.0)
+    b = S.random_positive_field(shape, seed=32, lo=0.5, hi=2.0)
+    mu = S.random_positive_field(shape, seed=33, lo=0.0, hi=1.0)
+    if log_domain:
+        a_in, b_in = np.log(a), np.log(b)
+    else:
+        a_in, b_in = a, b
+    got = se2_marginal_error(k, _dev(a_in), _dev(b_in), _dev(mu), log_domain)
+    Kb = O.conv(O.kernel_table(g, R, eps, w), b.astype(np.float64))
+    ref = [O.marginal_error(a[i].astype(np.float64), Kb[i], mu[i].astype(np.float64)) for i in range(2)]
+    np.testing.assert_allclose(got, ref, rtol=1e-5)
+
+
+def test_bary_pieces(cuda_device):
+    from paper_2402_15322_b200 import se2_bary_logmean, se2_bary_update
+    N = 1000
+    rng = np.random.default_rng(5)
+    ld = rng.normal(size=(3, N)).astype(np.float32)
+    lam = np.array([0.2, 0.0, 0.8])
+    lbar = torch.empty(N, device="cuda")
+    se2_bary_logmean(_dev(ld), lam, N, lbar)
+    ref = lam[0] * ld[0].astype(np.float64) + lam[2] * ld[2]
+    np.testing.assert_allclose(_host(lbar), ref, rtol=1e-6, atol=1e-6)
+    lv = rng.normal(size=(3, N)).astype(np.float32)
+    lv_t = _dev(lv)
+    se2_bary_update(lv_t, _dev(ld), lbar, 3, N)
+    np.testing.assert_allclose(_host(lv_t), lv + (ref[None] - ld), rtol=1e-5, atol=1e-5)

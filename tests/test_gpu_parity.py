@@ -1,0 +1,149 @@
+"""End-to-end GPU parity of the scaling loops against the fp64 oracle (-m gpu).
+
+Expected values come from tests/golden/<case>.npz, written by tests/golden/make_golden.py, which
+calls oracle/ only.  Cases (se2_synth.PARITY_CASES): the BASELINE configs at full size (whole
+runs for c0/c1; prefixes for c2/c3/c4, compared on a seeded sample of entries) and reduced-grid
+analogues with ragged tiles running the configs' full iteration counts.
+
+Tolerances (north_star; reading R12): potentials max|d|/max(1,|ref|) <= 1e-4; transported
+measures max|d|/max(|ref|, 1e-6 max|ref|) <= 1e-4; error traces |d| <= 1e-3 ref + 1e-6.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import se2_synth as S
+from gpu_util import measure_err, potential_err, trace_err
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL_POT = 1e-4
+TOL_MEAS = 1e-4
+TOL_TRACE = 1e-3
+
+
+def _golden(name):
+    p = os.path.join(GOLD, f"{name}.npz")
+    if not os.path.exists(p):
+        pytest.fail(f"missing golden file {p}: run tests/golden/make_golden.py {name}")
+    return dict(np.load(p))
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _sel(arr, gold, full):
+    """Flatten the field axes and pick the golden sample (or everything)."""
+    a = np.asarray(arr).reshape(np.asarray(arr).shape[:-3] + (-1,))
+    return a if full else a[..., gold["sample_idx"]]
+
+
+def _kernel(cfg, batch):
+    from paper_2402_15322_b200 import Kernel
+    return Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=batch, device=0)
+
+
+def _cmp_pot(name, got, ref):
+    e = potential_err(got, ref)
+    assert e <= TOL_POT, f"{name}: potential error {e:.3e}"
+    return e
+
+
+def _cmp_meas(name, got, ref):
+    e = measure_err(got, ref)
+    assert e <= TOL_MEAS, f"{name}: measure error {e:.3e}"
+    return e
+
+
+@pytest.mark.parametrize("case", ["c0"])
+def test_sinkhorn_parity(case, cuda_device):
+    from paper_2402_15322_b200 import se2_conv, se2_sinkhorn
+    pc = S.get_parity_case(case)
+    cfg, d = S.parity_inputs(pc)
+    gold = _golden(case)
+    k = _kernel(cfg, 1)
+    mu, nu = _dev(d["mus"][0]), _dev(d["mus"][1])
+    a = torch.empty_like(mu)
+    b = torch.empty_like(mu)
+    tr = se2_sinkhorn(k, mu, nu, a, b, cfg.iters, cfg.log_domain, trace=True)
+    assert cfg.log_domain
+    _cmp_pot("alpha", _sel(_host(a), gold, pc.full_fields), gold["alpha"].reshape(-1))
+    _cmp_pot("beta", _sel(_host(b), gold, pc.full_fields), gold["beta"].reshape(-1))
+    # transported measures: the plan's marginals a * K b and b * K^T a (K^T = K)
+    row = np.exp(_host(a) + _host(se2_conv(k, b, log_domain=True)))
+    col = np.exp(_host(b) + _host(se2_conv(k, a, log_domain=True)))
+    _cmp_meas("row", row.reshape(-1), gold["row"].reshape(-1))
+    _cmp_meas("col", col.reshape(-1), gold["col"].reshape(-1))
+    assert trace_err(tr[:, 0], gold["err"]) <= TOL_TRACE
+
+
+@pytest.mark.parametrize("case", ["c1", "c2m", "c3m", "c2p", "c3p"])
+def test_barycenter_parity(case, cuda_device):
+    from paper_2402_15322_b200 import se2_barycenter
+    pc = S.get_parity_case(case)
+    cfg, d = S.parity_inputs(pc)
+    gold = _golden(case)
+    lams = gold["lambdas"]
+    n, nsolve = len(d["mus"]), lams.shape[0]
+    k = _kernel(cfg, n * nsolve)
+    mus = _dev(np.stack(d["mus"]))
+    v = torch.empty((nsolve, n) + cfg.shape, device="cuda")
+    w = torch.empty_like(v)
+    bary, tr = se2_barycenter(k, mus, lams, cfg.iters, cfg.log_domain, v_state=v, w_state=w, trace=True)
+    full = pc.full_fields
+    if cfg.log_domain:
+        _cmp_pot("log bary", _sel(_host(bary), gold, full), gold["lbary"].reshape(nsolve, -1))
+        _cmp_meas("bary", np.exp(_sel(_host(bary), gold, full)), gold["bary_lin"].reshape(nsolve, -1))
+        _cmp_pot("lv", _sel(_host(v), gold, full), gold["lv"].reshape(nsolve, n, -1))
+        _cmp_pot("lw", _sel(_host(w), gold, full), gold["lw"].reshape(nsolve, n, -1))
+    else:
+        _cmp_meas("bary", _sel(_host(bary), gold, full), gold["bary"].reshape(nsolve, -1))
+    assert trace_err(tr, gold["err"]) <= TOL_TRACE
+
+
+@pytest.mark.parametrize("case", ["c4m", "c4p"])
+def test_jko_parity(case, cuda_device):
+    from paper_2402_15322_b200 import make_prox, se2_jko_step
+    pc = S.get_parity_case(case)
+    cfg, d = S.parity_inputs(pc)
+    gold = _golden(case)
+    k = _kernel(cfg, 1)
+    prox = make_prox(k, cfg.tau)
+    mu = _dev(d["mus"][0])
+    nxt = torch.empty_like(mu)
+    a = torch.empty_like(mu)
+    b = torch.empty_like(mu)
+    full = pc.full_fields
+    for step in range(cfg.jko_steps):
+        mass, tr = se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, cfg.log_domain, trace=True)
+        assert abs(mass - gold["masses"][step]) <= TOL_MEAS * abs(gold["masses"][step])
+        assert trace_err(tr, gold["err"][step]) <= TOL_TRACE
+        _cmp_meas(f"mu_{step + 1}", _sel(_host(nxt), gold, full), gold["mus"][step + 1].reshape(-1))
+        mu, nxt = nxt, mu
+    # potentials of the last inner solve (linear scalings -> compare logs)
+    _cmp_pot("log a", np.log(_sel(_host(a), gold, full)), np.log(gold["a"].reshape(-1)))
+    _cmp_pot("log b", np.log(_sel(_host(b), gold, full)), np.log(gold["b"].reshape(-1)))
+
+
+def test_determinism(cuda_device):
+    """Two identical solves give bit-identical results (fixed-order reductions, no atomics in the
+    arithmetic)."""
+    from paper_2402_15322_b200 import se2_barycenter
+    pc = S.get_parity_case("c1")
+    cfg, d = S.parity_inputs(pc)
+    k = _kernel(cfg, 10)
+    mus = _dev(np.stack(d["mus"]))
+    lams = np.array([[t, 1 - t] for t in cfg.ts])
+    b1, t1 = se2_barycenter(k, mus, lams, 20, True, trace=True)
+    b2, t2 = se2_barycenter(k, mus, lams, 20, True, trace=True)
+    assert torch.equal(b1, b2)
+    assert np.array_equal(t1, t2)
