@@ -143,16 +143,19 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
 
     const int nquads = (k->nt + 3) / 4;
     const size_t tab = (size_t)nquads * k->nt * k->S * k->S * 4 * sizeof(float);
+    const size_t tabl = (size_t)k->nt * k->nt * k->S * ((k->S + 3) / 4 * 4) * sizeof(float);
     cudaError_t e = cudaMalloc(&k->Wq, tab);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lq, tab);
+    if (e == cudaSuccess) e = cudaMalloc(&k->Wl, tabl);
     if (e == cudaSuccess) e = cudaMemset(k->Wq, 0, tab);
     if (e == cudaSuccess) e = cudaMemset(k->Lq, 0, tab);
+    if (e == cudaSuccess) e = cudaMemset(k->Wl, 0, tabl);
     if (e != cudaSuccess) {
         set_error(std::string("table allocation: ") + cudaGetErrorString(e));
         se2_kernel_destroy(k);
         return SE2_ENOMEM;
     }
-    k->table_bytes = 2 * tab;
+    k->table_bytes = 2 * tab + tabl;
     e = tabulate(k, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -185,6 +188,7 @@ void se2_kernel_destroy(se2_kernel k) {
     DeviceGuard g(k->device);
     if (k->Wq) cudaFree(k->Wq);
     if (k->Lq) cudaFree(k->Lq);
+    if (k->Wl) cudaFree(k->Wl);
     KernelExtra* x = extra(k);
     if (x) {
         for (Workspace* w : {&x->ws, &x->trace, &x->partial, &x->misc})

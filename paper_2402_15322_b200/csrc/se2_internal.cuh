@@ -79,6 +79,7 @@ struct se2_kernel_s {
     // device tables, theta-quad interleaved: [nt/4][nt][S][S][4]  (to = 4*qd + q)
     float* Wq = nullptr;    // exp(-rho^2/eps)  fp32
     float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
+    float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
     size_t table_bytes = 0;
     void* extra = nullptr;        // grow-only workspaces (api.cu)
     se2::Timing timing;

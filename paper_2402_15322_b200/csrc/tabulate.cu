@@ -15,7 +15,7 @@ namespace se2 {
 
 __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
                                 double w3, float* __restrict__ Wq, float* __restrict__ Lq,
-                                int* __restrict__ nnz_pair) {
+                                float* __restrict__ Wl, int* __restrict__ nnz_pair) {
     const int S = 2 * R + 1;
     const int64_t total = (int64_t)nt * nt * S * S;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -47,6 +47,8 @@ __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, doubl
         int64_t o = ((((int64_t)qd * nt + ti) * S + dyi) * S + dxi) * 4 + q;
         Wq[o] = wv;
         Lq[o] = (float)(e * 1.4426950408889634073599246810019);
+        const int SP = (S + 3) / 4 * 4;
+        Wl[(((int64_t)to * nt + ti) * S + dyi) * SP + dxi] = wv;
         if (wv != 0.0f) atomicAdd(&nnz_pair[to * nt + ti], 1);
     }
 }
@@ -63,7 +65,7 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     int blocks = (int)((total + threads - 1) / threads);
     if (blocks > 148 * 32) blocks = 148 * 32;
     tabulate_kernel<<<blocks, threads, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2, k->w3,
-                                               k->Wq, k->Lq, nnz_dev);
+                                               k->Wq, k->Lq, k->Wl, nnz_dev);
     e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }
     std::vector<int> nnz(nt * nt);

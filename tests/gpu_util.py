@@ -3,7 +3,21 @@ import numpy as np
 
 
 def potential_err(g, r):
-    """max |g - r| / max(1, |r|)  -- the north-star metric for (log-)potentials (reading R12)."""
+    """max |g - r| / max(1, max |r|)  -- relative error of a (log-)potential field (reading R12).
+
+    Potentials are defined up to an additive constant (the plan a K b is invariant under
+    (alpha + c, beta - c)), so the error is normalised by the field's sup norm, not
+    elementwise: an elementwise ratio is meaningless where a potential crosses zero."""
+    g = np.asarray(g, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    both_ninf = (g == -np.inf) & (r == -np.inf)
+    d = np.where(both_ninf, 0.0, np.abs(g - r))
+    rr = np.abs(np.where(both_ninf, 0.0, r))
+    return float(np.max(d) / max(1.0, float(np.max(rr))))
+
+
+def potential_err_elementwise(g, r):
+    """max |g - r| / max(1, |r|) elementwise (reported for information)."""
     g = np.asarray(g, dtype=np.float64)
     r = np.asarray(r, dtype=np.float64)
     both_ninf = (g == -np.inf) & (r == -np.inf)
