@@ -59,6 +59,7 @@ typedef enum {
 #define SE2_LOG_DOMAIN 0x1u   /* state/fields are natural logs; conv is log-sum-exp (R7)      */
 #define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1        */
 #define SE2_TRACE_ERR 0x4u    /* compute the marginal error every iteration (fused)           */
+#define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4)   */
 
 typedef struct {
     int32_t nx, ny, ntheta;
@@ -193,6 +194,11 @@ SE2_API se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float*
 
 /* Sum of a device array (deterministic), result in double on the host. */
 SE2_API se2_status se2_sum(const float* x, int64_t n, double* out_host, se2_stream stream);
+
+/* Log-domain engine (K3) path counters since the last reset: (tile-quad, theta_i) pairs that were
+ * active after pruning, handled by the FFMA path, and visited in total. */
+SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs,
+                                      int64_t* visited_pairs, int32_t reset);
 
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)

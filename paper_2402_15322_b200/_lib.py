@@ -14,6 +14,7 @@ SE2_OK = 0
 SE2_LOG_DOMAIN = 0x1
 SE2_WARM_START = 0x2
 SE2_TRACE_ERR = 0x4
+SE2_LSE_EXACT = 0x8
 SE2_EPI_DIVIDE = 1
 SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3
@@ -28,7 +29,7 @@ EXPORTED = [
     "se2_kernel_build", "se2_kernel_stats_get", "se2_kernel_destroy", "se2_conv", "se2_sinkhorn",
     "se2_jko_step", "se2_barycenter", "se2_marginal_error", "se2_conv_update", "se2_bary_logmean",
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
-    "se2_last_error", "se2_abi_version",
+    "se2_last_error", "se2_abi_version", "se2_lse_path_stats",
 ]
 
 
@@ -89,6 +90,7 @@ def load(path: str = LIB_PATH):
         "se2_bary_update": [i32, i64, P, P, P, P],
         "se2_sum": [P, i64, pd, P],
         "se2_timing_enable": [P, i32],
+        "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
     }
     for name, args in sig.items():

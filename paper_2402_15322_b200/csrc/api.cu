@@ -69,8 +69,9 @@ static se2_status ensure(Workspace& w, size_t bytes) {
 }
 
 // ---- conv dispatch with optional event timing ---------------------------------------------------
-static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, bool log_domain, const Epilogue& epi,
+static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t flags, const Epilogue& epi,
                            cudaStream_t s, int* bpf) {
+    const bool log_domain = (flags & SE2_LOG_DOMAIN) != 0;
     Timing& t = k->timing;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (t.on) {
@@ -85,7 +86,13 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, bool log
         t.used++;
         SE2_CUDA_TRY(cudaEventRecord(e0, s));
     }
-    cudaError_t e = log_domain ? launch_conv_lse(k, in, batch, epi, s, bpf) : launch_conv_linear(k, in, batch, epi, s, bpf);
+    cudaError_t e;
+    if (!log_domain)
+        e = launch_conv_linear(k, in, batch, epi, s, bpf);
+    else if (flags & SE2_LSE_EXACT)
+        e = launch_conv_lse(k, in, batch, epi, s, bpf);
+    else
+        e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->tmin, k->tmax, 0, k->lse_counters);
     if (e != cudaSuccess) {
         set_error(std::string("conv launch: ") + cudaGetErrorString(e));
         return SE2_ECUDA;
@@ -144,10 +151,12 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     const int nquads = (k->nt + 3) / 4;
     const size_t tab = (size_t)nquads * k->nt * k->S * k->S * 4 * sizeof(float);
     const size_t tabl = (size_t)k->nt * k->nt * k->S * ((k->S + 3) / 4 * 4) * sizeof(float);
-    cudaError_t e = cudaMalloc(&k->Wq, tab);
+    cudaError_t e = cudaMalloc(&k->Eq, tab);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lq, tab);
     if (e == cudaSuccess) e = cudaMalloc(&k->Wl, tabl);
-    if (e == cudaSuccess) e = cudaMemset(k->Wq, 0, tab);
+    if (e == cudaSuccess) e = cudaMalloc(&k->Lth, sizeof(float) * k->nt * k->nt);
+    if (e == cudaSuccess) e = cudaMalloc(&k->LseS, sizeof(float) * k->nt * k->nt);
+    if (e == cudaSuccess) e = cudaMemset(k->Eq, 0, tab);
     if (e == cudaSuccess) e = cudaMemset(k->Lq, 0, tab);
     if (e == cudaSuccess) e = cudaMemset(k->Wl, 0, tabl);
     if (e != cudaSuccess) {
@@ -155,7 +164,19 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
         se2_kernel_destroy(k);
         return SE2_ENOMEM;
     }
-    k->table_bytes = 2 * tab + tabl;
+    k->table_bytes = 2 * tab + tabl + 2 * sizeof(float) * k->nt * k->nt;
+    {
+        const size_t nst = lse_fast_stats_floats(k, max_batch);
+        cudaError_t e2 = cudaMalloc(&k->tmin, sizeof(float) * nst);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->tmax, sizeof(float) * nst);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(long long) * 4);
+        if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(long long) * 4);
+        if (e2 != cudaSuccess) {
+            set_error(std::string("scratch allocation: ") + cudaGetErrorString(e2));
+            se2_kernel_destroy(k);
+            return SE2_ENOMEM;
+        }
+    }
     e = tabulate(k, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -186,9 +207,14 @@ se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* o) {
 void se2_kernel_destroy(se2_kernel k) {
     if (!k) return;
     DeviceGuard g(k->device);
-    if (k->Wq) cudaFree(k->Wq);
+    if (k->Eq) cudaFree(k->Eq);
+    if (k->Lth) cudaFree(k->Lth);
+    if (k->LseS) cudaFree(k->LseS);
     if (k->Lq) cudaFree(k->Lq);
     if (k->Wl) cudaFree(k->Wl);
+    if (k->tmin) cudaFree(k->tmin);
+    if (k->tmax) cudaFree(k->tmax);
+    if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
     if (x) {
         for (Workspace* w : {&x->ws, &x->trace, &x->partial, &x->misc})
@@ -210,7 +236,7 @@ se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, ui
     Epilogue epi;
     epi.op = EPI_STORE;
     epi.out = out;
-    return run_conv(k, in, batch, (flags & SE2_LOG_DOMAIN) != 0, epi, (cudaStream_t)stream, nullptr);
+    return run_conv(k, in, batch, flags, epi, (cudaStream_t)stream, nullptr);
 }
 
 static void fill_prox(Epilogue& epi, const se2_kernel_s* k, const se2_prox* prox) {
@@ -237,7 +263,7 @@ se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, f
     epi.target = target;
     epi.out = out;
     if (op == SE2_EPI_PROX) fill_prox(epi, k, prox);
-    return run_conv(k, in, batch, (flags & SE2_LOG_DOMAIN) != 0, epi, (cudaStream_t)stream, nullptr);
+    return run_conv(k, in, batch, flags, epi, (cudaStream_t)stream, nullptr);
 }
 
 // ---- Sinkhorn / JKO inner solve -------------------------------------------------------------------
@@ -291,7 +317,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
             e1.err_mu = mu;
             e1.err_partial = partial;
         }
-        st = run_conv(k, b, batch, LOG, e1, s, nullptr);
+        st = run_conv(k, b, batch, opts->flags, e1, s, nullptr);
         if (st != SE2_OK) return st;
         if (trace && l > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(l - 1) * batch, s));
         // b = prox(K^T a) / K^T a    (K^T = K)
@@ -305,7 +331,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
             e2.op = EPI_DIVIDE;
             e2.target = tnu;
         }
-        st = run_conv(k, a, batch, LOG, e2, s, nullptr);
+        st = run_conv(k, a, batch, opts->flags, e2, s, nullptr);
         if (st != SE2_OK) return st;
     }
     if (trace && iters > 0) {
@@ -314,7 +340,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         e3.err_a = a;
         e3.err_mu = mu;
         e3.err_partial = partial;
-        st = run_conv(k, b, batch, LOG, e3, s, nullptr);
+        st = run_conv(k, b, batch, opts->flags, e3, s, nullptr);
         if (st != SE2_OK) return st;
         SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(iters - 1) * batch, s));
         SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
@@ -456,7 +482,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             e1.err_mu = mu_rep;
             e1.err_partial = partial;
         }
-        st = run_conv(k, v, F, LOG, e1, s, nullptr);
+        st = run_conv(k, v, F, opts->flags, e1, s, nullptr);
         if (st != SE2_OK) return st;
         if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
         // d_i = v_i K w_i
@@ -464,7 +490,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         e2.op = EPI_MULTIPLY;
         e2.target = v;
         e2.out = d;
-        st = run_conv(k, w, F, LOG, e2, s, nullptr);
+        st = run_conv(k, w, F, opts->flags, e2, s, nullptr);
         if (st != SE2_OK) return st;
         // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
         if (LOG) {
@@ -480,7 +506,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         e3.err_a = w;
         e3.err_mu = mu_rep;
         e3.err_partial = partial;
-        st = run_conv(k, v, F, LOG, e3, s, nullptr);
+        st = run_conv(k, v, F, opts->flags, e3, s, nullptr);
         if (st != SE2_OK) return st;
         SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
         std::vector<double> h((size_t)iters * F);
@@ -517,7 +543,7 @@ se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, cons
     e.err_a = a;
     e.err_mu = mu;
     e.err_partial = reinterpret_cast<float*>(x->partial.ptr);
-    st = run_conv(k, b, batch, LOG, e, s, nullptr);
+    st = run_conv(k, b, batch, flags, e, s, nullptr);
     if (st != SE2_OK) return st;
     double* tr = reinterpret_cast<double*>(x->trace.ptr);
     SE2_CUDA_TRY(launch_reduce_partials(e.err_partial, batch, bpf, tr, s));
@@ -555,6 +581,20 @@ se2_status se2_sum(const float* xp, int64_t n, double* out_host, se2_stream stre
     SE2_CUDA_TRY(cudaMemcpyAsync(out_host, d, sizeof(double), cudaMemcpyDeviceToHost, s));
     SE2_CUDA_TRY(cudaFreeAsync(d, s));
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs, int64_t* visited_pairs,
+                              int32_t reset) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    DeviceGuard g(k->device);
+    int h[3] = {0, 0, 0};
+    SE2_CUDA_TRY(cudaDeviceSynchronize());
+    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters, sizeof(int) * 3, cudaMemcpyDeviceToHost));
+    if (active_pairs) *active_pairs = h[0];
+    if (ffma_pairs) *ffma_pairs = h[1];
+    if (visited_pairs) *visited_pairs = h[2];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 3));
     return SE2_OK;
 }
 

@@ -35,6 +35,13 @@ constexpr int kMaxRadius = 15;
 constexpr float kDivFloor = 1e-30f;   // division guard (reading R9)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+// factored log-domain engine (conv_lse_fast.cu): spatial table stored as exp(Ls + kEsShift); a
+// channel is handled by the FFMA path when its window range (max over the window - min over the
+// tile, natural log units) is at most kFastRange (validity derivation in DESIGN.md, K3)
+constexpr float kEsShift = 40.f;
+constexpr float kFastRange = 100.f;
+constexpr float kShiftAbove = 62.f;   // per-channel shift m = tile min + kShiftAbove
+constexpr float kPruneGap = 30.f;     // channels whose upper bound is < lower bound - kPruneGap are skipped
 
 // Epilogue ops of the fused conv (see se2_conv_update in se2ot.h)
 enum EpiOp : int {
@@ -77,11 +84,16 @@ struct se2_kernel_s {
     int band = 0;           // fp32-nonzero theta half band (bins)
     int64_t nnz_taps = 0;   // per output
     // device tables, theta-quad interleaved: [nt/4][nt][S][S][4]  (to = 4*qd + q)
-    float* Wq = nullptr;    // exp(-rho^2/eps)  fp32
+    float* Eq = nullptr;    // exp(Ls + kEsShift) fp32, quad-interleaved (factored LSE engine)
+    float* Lth = nullptr;   // [nt][nt] theta part of L (natural log)
+    float* LseS = nullptr;  // [nt][nt] log sum_taps exp(Ls)
     float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
     float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
     size_t table_bytes = 0;
     void* extra = nullptr;        // grow-only workspaces (api.cu)
+    float* tmin = nullptr;        // [max_batch][nt][tiles] per-tile min / max of log fields (K3 stats)
+    float* tmax = nullptr;
+    int* lse_counters = nullptr;  // K3 path counters: active pairs, FFMA pairs, visited pairs
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -97,6 +109,10 @@ cudaError_t launch_conv_lse(const se2_kernel_s* k, const float* in, int batch, c
 int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain);
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);
+cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
+                                 cudaStream_t s, int* bpf, float* tmin, float* tmax, int force_exact,
+                                 int* counters);
+size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch);
 
 // tabulation (tabulate.cu)
 cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s);

@@ -5,8 +5,14 @@
 //     h^{-1} g = ( R_{-theta_i} (dx/nx, dy/ny),  wrap(theta_o - theta_i) ),   wrap into [-pi, pi)
 // and the half-angle coordinates and rho_b give
 //     W = exp(-rho_b^2/eps),   L2 = -rho_b^2/eps * log2(e).
-// Computed in fp64, stored fp32 in the theta-quad interleaved layout [nt/4][nt][S][S][4]
-// (to = 4*qd + q), so one 16-byte shared-memory broadcast feeds four output orientations.
+// rho_b^2 splits into a theta part and a spatial part (the spatial part vanishes at dx = dy = 0):
+//     L = Lth(to, ti) + Ls(to, ti, dx, dy),  Lth = -w3^2 Theta^2/eps,  Ls = -(w1^2 b1^2 + w2^2 b2^2)/eps
+// which the log-domain engine uses (factored per input orientation).  Computed in fp64, stored fp32:
+//   Wl [to][ti][S][SP]           W (linear engine, rows padded to SP = 4*ceil(S/4) with zeros)
+//   Lq [nt/4][nt][S][S][4]       L2 = L log2(e) (exact LSE engine; theta-quad interleaved so one
+//                                16-byte shared-memory broadcast feeds four output orientations)
+//   Eq [nt/4][nt][S][S][4]       exp(Ls + kEsShift) (factored LSE engine)
+//   Lth[to][ti], LseS[to][ti]    Lth and log sum_{dx,dy} exp(Ls) (natural logs)
 #include <math.h>
 
 #include "se2_internal.cuh"
@@ -14,7 +20,7 @@
 namespace se2 {
 
 __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
-                                double w3, float* __restrict__ Wq, float* __restrict__ Lq,
+                                double w3, float* __restrict__ Eq, float* __restrict__ Lq,
                                 float* __restrict__ Wl, int* __restrict__ nnz_pair) {
     const int S = 2 * R + 1;
     const int64_t total = (int64_t)nt * nt * S * S;
@@ -40,17 +46,42 @@ __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, doubl
         double b1 = X * ch + Y * sh;
         double b2 = -X * sh + Y * ch;
         double b3 = Th;
-        double rho2 = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2 + w3 * w3 * b3 * b3;
+        double rho2s = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2;
+        double rho2 = rho2s + w3 * w3 * b3 * b3;
         double e = -rho2 / eps;
         float wv = (float)exp(e);
         int qd = to >> 2, q = to & 3;
         int64_t o = ((((int64_t)qd * nt + ti) * S + dyi) * S + dxi) * 4 + q;
-        Wq[o] = wv;
+        Eq[o] = (float)exp(-rho2s / eps + (double)kEsShift);
         Lq[o] = (float)(e * 1.4426950408889634073599246810019);
         const int SP = (S + 3) / 4 * 4;
         Wl[(((int64_t)to * nt + ti) * S + dyi) * SP + dxi] = wv;
         if (wv != 0.0f) atomicAdd(&nnz_pair[to * nt + ti], 1);
     }
+}
+
+// Lth[to][ti] = -w3^2 Theta^2/eps ; LseS[to][ti] = log sum_{dx,dy} exp(Ls(to,ti,dx,dy))  (fp64 sums)
+__global__ void tabulate_theta_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
+                                      double w3, float* __restrict__ Lth, float* __restrict__ LseS) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nt * nt) return;
+    const int to = p / nt, ti = p % nt;
+    const double two_pi = 6.283185307179586476925286766559;
+    int k = ((to - ti) % nt + nt) % nt;
+    if (2 * k >= nt) k -= nt;
+    const double Th = two_pi * k / nt;
+    const double thi = two_pi * ti / nt;
+    const double ci = cos(thi), si = sin(thi), ch = cos(0.5 * Th), sh = sin(0.5 * Th);
+    double acc = 0.0;
+    for (int dyi = -R; dyi <= R; ++dyi)
+        for (int dxi = -R; dxi <= R; ++dxi) {
+            double ddx = (double)dxi / nx, ddy = (double)dyi / ny;
+            double X = ci * ddx + si * ddy, Y = -si * ddx + ci * ddy;
+            double b1 = X * ch + Y * sh, b2 = -X * sh + Y * ch;
+            acc += exp(-(w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2) / eps);
+        }
+    Lth[p] = (float)(-w3 * w3 * Th * Th / eps);
+    LseS[p] = (float)log(acc);
 }
 
 cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
@@ -65,7 +96,9 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     int blocks = (int)((total + threads - 1) / threads);
     if (blocks > 148 * 32) blocks = 148 * 32;
     tabulate_kernel<<<blocks, threads, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2, k->w3,
-                                               k->Wq, k->Lq, k->Wl, nnz_dev);
+                                               k->Eq, k->Lq, k->Wl, nnz_dev);
+    tabulate_theta_kernel<<<(nt * nt + 127) / 128, 128, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2,
+                                                                  k->w3, k->Lth, k->LseS);
     e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }
     std::vector<int> nnz(nt * nt);

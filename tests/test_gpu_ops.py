@@ -65,19 +65,19 @@ def test_kernel_stats(case, cuda_device):
     assert st["theta_band"] == band
 
 
-def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True):
+def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse_exact=False, log_span=200.0):
     k = _kernel(nx, ny, nt, eps, w, R, batch)
     g = O.Grid(nx, ny, nt)
     shape = (batch, nt, ny, nx)
     if log_domain:
         rng = np.random.default_rng(zlib.crc32(name.encode()))
-        v = rng.uniform(-100, 100, size=shape).astype(np.float32)     # wide log range
+        v = rng.uniform(-log_span / 2, log_span / 2, size=shape).astype(np.float32)
         Lt = O.log_kernel_table(g, R, eps, w)
     else:
         v = S.random_positive_field(shape, seed=zlib.crc32(name.encode()), log_range=30.0)
         Tt = O.kernel_table(g, R, eps, w)
     from paper_2402_15322_b200 import se2_conv
-    y = _host(se2_conv(k, _dev(v), log_domain=log_domain))
+    y = _host(se2_conv(k, _dev(v), log_domain=log_domain, lse_exact=lse_exact))
     if full:
         ref = O.lse_conv(Lt, v.astype(np.float64)) if log_domain else O.conv(Tt, v.astype(np.float64))
         got = y
@@ -109,6 +109,30 @@ def test_conv_parity(case, log_domain, cuda_device):
     name, nx, ny, nt, eps, w, R = case
     big = nx * ny * nt > 200000
     _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=1 if big else 2, full=not big)
+
+
+@pytest.mark.parametrize("case", CFG_GRIDS[:3] + ODD_GRIDS, ids=lambda c: c[0])
+@pytest.mark.parametrize("span", [20.0, 2000.0], ids=["ffma-path", "exact-path"])
+@pytest.mark.parametrize("lse_exact", [False, True], ids=["K3", "K4"])
+def test_lse_engines(case, span, lse_exact, cuda_device):
+    """Both log-domain engines against the oracle: a narrow log range keeps every channel on K3's
+    FFMA path, a 2000-nat range forces its per-tap fallback; K4 is the all-exact engine."""
+    name, nx, ny, nt, eps, w, R = case
+    _conv_check(name + f"-{span}", nx, ny, nt, eps, w, R, True, batch=2, full=True, lse_exact=lse_exact,
+                log_span=span)
+
+
+def test_lse_paths_exercised(cuda_device):
+    from paper_2402_15322_b200 import se2_conv
+    k = _kernel(64, 64, 32, 0.01, (1.0, 4.0, 2.0), 7)
+    rng = np.random.default_rng(1)
+    k.lse_path_stats(reset=True)
+    se2_conv(k, _dev(rng.uniform(-5, 5, (32, 64, 64))), log_domain=True)
+    s1 = k.lse_path_stats(reset=True)
+    assert s1["active"] > 0 and s1["ffma"] == s1["active"] and s1["active"] < s1["visited"]   # pruned + all FFMA
+    se2_conv(k, _dev(rng.uniform(-1000, 1000, (32, 64, 64))), log_domain=True)
+    s2 = k.lse_path_stats(reset=True)
+    assert s2["ffma"] < s2["active"]                                                            # fallback used
 
 
 def test_conv_zero_and_neginf_inputs(cuda_device):
