@@ -63,6 +63,8 @@ typedef enum {
 
 typedef struct {
     int32_t nx, ny, ntheta;
+    double hx, hy;  /* cell sizes in [0,1]^2 units; 0 -> 1/nx, 1/ny.  A slab of a larger grid keeps the
+                       global cell size (R1) while ny counts its own rows (+ halos).            */
 } se2_grid;
 
 typedef struct {
@@ -191,6 +193,13 @@ SE2_API se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const
                             se2_stream stream);
 SE2_API se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar,
                            se2_stream stream);
+
+/* Rows [row0, row0 + rows) of every plane of a [planes][ny][nx] device array (slab decomposition):
+ * deterministic fp64 sum to the host, and in-place scaling by `factor`. */
+SE2_API se2_status se2_sum_rows(const float* x, int32_t planes, int32_t ny, int32_t nx, int32_t row0, int32_t rows,
+                                double* out_host, se2_stream stream);
+SE2_API se2_status se2_scale_rows(float* x, int32_t planes, int32_t ny, int32_t nx, int32_t row0, int32_t rows,
+                                  double factor, se2_stream stream);
 
 /* Sum of a device array (deterministic), result in double on the host. */
 SE2_API se2_status se2_sum(const float* x, int64_t n, double* out_host, se2_stream stream);

@@ -29,7 +29,7 @@ EXPORTED = [
     "se2_kernel_build", "se2_kernel_stats_get", "se2_kernel_destroy", "se2_conv", "se2_sinkhorn",
     "se2_jko_step", "se2_barycenter", "se2_marginal_error", "se2_conv_update", "se2_bary_logmean",
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
-    "se2_last_error", "se2_abi_version", "se2_lse_path_stats",
+    "se2_last_error", "se2_abi_version", "se2_lse_path_stats", "se2_sum_rows", "se2_scale_rows",
 ]
 
 
@@ -40,7 +40,8 @@ class SE2Error(RuntimeError):
 
 
 class se2_grid(ctypes.Structure):
-    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("ntheta", ctypes.c_int32)]
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("ntheta", ctypes.c_int32),
+                ("hx", ctypes.c_double), ("hy", ctypes.c_double)]
 
 
 class se2_metric(ctypes.Structure):
@@ -89,6 +90,8 @@ def load(path: str = LIB_PATH):
         "se2_bary_logmean": [i32, i64, P, pd, P, P],
         "se2_bary_update": [i32, i64, P, P, P, P],
         "se2_sum": [P, i64, pd, P],
+        "se2_sum_rows": [P, i32, i32, i32, i32, i32, pd, P],
+        "se2_scale_rows": [P, i32, i32, i32, i32, i32, dbl, P],
         "se2_timing_enable": [P, i32],
         "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],

@@ -43,14 +43,14 @@ class Kernel:
     """Owns an se2_kernel (device Gibbs-kernel tables + scratch).  se2_kernel_build."""
 
     def __init__(self, nx: int, ny: int, ntheta: int, eps: float, w: Sequence[float], radius: int,
-                 max_batch: int = 1, device: int = 0):
+                 max_batch: int = 1, device: int = 0, hx: float = 0.0, hy: float = 0.0):
         lib = L.load()
         self.nx, self.ny, self.ntheta = int(nx), int(ny), int(ntheta)
         self.eps, self.w, self.radius = float(eps), tuple(float(v) for v in w), int(radius)
         self.max_batch, self.device = int(max_batch), int(device)
         self.N = self.nx * self.ny * self.ntheta
         h = ctypes.c_void_p()
-        g = L.se2_grid(self.nx, self.ny, self.ntheta)
+        g = L.se2_grid(self.nx, self.ny, self.ntheta, float(hx), float(hy))
         m = L.se2_metric(*self.w)
         st = lib.se2_kernel_build(ctypes.byref(g), ctypes.byref(m), self.eps, self.radius, self.max_batch,
                                   self.device, ctypes.byref(h))
@@ -231,6 +231,21 @@ def se2_sum(x: torch.Tensor) -> float:
     out = ctypes.c_double()
     check(L.load().se2_sum(_ptr(x), x.numel(), ctypes.byref(out), _stream(x.device)))
     return out.value
+
+
+def se2_sum_rows(x: torch.Tensor, row0: int, rows: int) -> float:
+    """Sum of rows [row0, row0+rows) of every plane of x ([..., ny, nx], contiguous)."""
+    ny, nx = x.shape[-2], x.shape[-1]
+    planes = x.numel() // (ny * nx)
+    out = ctypes.c_double()
+    check(L.load().se2_sum_rows(_ptr(x), planes, ny, nx, int(row0), int(rows), ctypes.byref(out), _stream(x.device)))
+    return out.value
+
+
+def se2_scale_rows(x: torch.Tensor, row0: int, rows: int, factor: float):
+    ny, nx = x.shape[-2], x.shape[-1]
+    planes = x.numel() // (ny * nx)
+    check(L.load().se2_scale_rows(_ptr(x), planes, ny, nx, int(row0), int(rows), float(factor), _stream(x.device)))
 
 
 def se2_launch_count() -> int:

@@ -146,6 +146,9 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     k->w2 = metric->w2;
     k->w3 = metric->w3;
     k->max_batch = max_batch;
+    SE2_CHECK_ARG(grid->hx >= 0 && grid->hy >= 0, "cell sizes must be >= 0");
+    k->hx = grid->hx > 0 ? grid->hx : 1.0 / grid->nx;
+    k->hy = grid->hy > 0 ? grid->hy : 1.0 / grid->ny;
     k->extra = new KernelExtra();
 
     const int nquads = (k->nt + 3) / 4;
@@ -581,6 +584,27 @@ se2_status se2_sum(const float* xp, int64_t n, double* out_host, se2_stream stre
     SE2_CUDA_TRY(cudaMemcpyAsync(out_host, d, sizeof(double), cudaMemcpyDeviceToHost, s));
     SE2_CUDA_TRY(cudaFreeAsync(d, s));
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_sum_rows(const float* xp, int32_t planes, int32_t ny, int32_t nx, int32_t row0, int32_t rows,
+                        double* out_host, se2_stream stream) {
+    SE2_CHECK_ARG(xp && out_host && planes >= 1 && nx >= 1 && row0 >= 0 && rows >= 0 && row0 + rows <= ny,
+                  "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    double* d = nullptr;
+    SE2_CUDA_TRY(cudaMallocAsync(&d, sizeof(double) * 512, s));
+    SE2_CUDA_TRY(launch_sum_rows(xp, planes, ny, nx, row0, rows, d, d + 8, s));
+    SE2_CUDA_TRY(cudaMemcpyAsync(out_host, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaFreeAsync(d, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_scale_rows(float* xp, int32_t planes, int32_t ny, int32_t nx, int32_t row0, int32_t rows,
+                          double factor, se2_stream stream) {
+    SE2_CHECK_ARG(xp && planes >= 1 && nx >= 1 && row0 >= 0 && rows >= 0 && row0 + rows <= ny, "bad arguments");
+    SE2_CUDA_TRY(launch_scale_rows(xp, planes, ny, nx, row0, rows, factor, (cudaStream_t)stream));
     return SE2_OK;
 }
 

@@ -153,6 +153,49 @@ cudaError_t launch_sum(const float* x, int64_t n, double* out_dev, double* scrat
     return cudaGetLastError();
 }
 
+// rows [row0, row0 + rows) of each of the `planes` planes of a [planes][ny][nx] array
+__global__ void sum_rows_stage1(const float* x, int planes, int ny, int nx, int row0, int rows, double* part) {
+    __shared__ double red[256];
+    const int64_t n = (int64_t)planes * rows * nx;
+    double t = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / ((int64_t)rows * nx);
+        const int64_t rem = i - p * rows * nx;
+        const int r = (int)(rem / nx), c = (int)(rem - (int64_t)r * nx);
+        t += (double)x[(p * ny + row0 + r) * nx + c];
+    }
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+cudaError_t launch_sum_rows(const float* x, int planes, int ny, int nx, int row0, int rows, double* out_dev,
+                            double* scratch, cudaStream_t s) {
+    sum_rows_stage1<<<kSumBlocks, 256, 0, s>>>(x, planes, ny, nx, row0, rows, scratch);
+    count_launch();
+    sum_stage2<<<1, 256, 0, s>>>(scratch, kSumBlocks, out_dev);
+    count_launch();
+    return cudaGetLastError();
+}
+__global__ void scale_rows_kernel(float* x, int planes, int ny, int nx, int row0, int rows, double f) {
+    const int64_t n = (int64_t)planes * rows * nx;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / ((int64_t)rows * nx);
+        const int64_t rem = i - p * rows * nx;
+        const int r = (int)(rem / nx), c = (int)(rem - (int64_t)r * nx);
+        float* e = x + (p * ny + row0 + r) * nx + c;
+        *e = (float)((double)*e * f);
+    }
+}
+cudaError_t launch_scale_rows(float* x, int planes, int ny, int nx, int row0, int rows, double f, cudaStream_t s) {
+    scale_rows_kernel<<<grid_for((int64_t)planes * rows * nx, 256), 256, 0, s>>>(x, planes, ny, nx, row0, rows, f);
+    count_launch();
+    return cudaGetLastError();
+}
+
 __global__ void scale_kernel(float* x, int64_t n, const double* sum) {
     const double inv = 1.0 / sum[0];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -80,6 +80,7 @@ struct se2_kernel_s {
     int device = 0;
     int nx = 0, ny = 0, nt = 0, R = 0, S = 0;
     double eps = 0, w1 = 0, w2 = 0, w3 = 0;
+    double hx = 0, hy = 0;  // cell sizes ([0,1]^2 units)
     int max_batch = 1;
     int band = 0;           // fp32-nonzero theta half band (bins)
     int64_t nnz_taps = 0;   // per output
@@ -130,6 +131,9 @@ cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const
                                    const float* lam_dev, float* bary, cudaStream_t s);
 cudaError_t launch_sum(const float* x, int64_t n, double* out_dev, double* scratch, cudaStream_t s);
 cudaError_t launch_scale(float* x, int64_t n, const double* sum_dev, cudaStream_t s);
+cudaError_t launch_sum_rows(const float* x, int planes, int ny, int nx, int row0, int rows, double* out_dev,
+                            double* scratch, cudaStream_t s);
+cudaError_t launch_scale_rows(float* x, int planes, int ny, int nx, int row0, int rows, double f, cudaStream_t s);
 cudaError_t launch_count_nonfinite(const float* x, int64_t n, int* count_dev, cudaStream_t s);
 
 }  // namespace se2

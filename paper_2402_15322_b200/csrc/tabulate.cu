@@ -19,7 +19,7 @@
 
 namespace se2 {
 
-__global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
+__global__ void tabulate_kernel(double hx, double hy, int nt, int R, double eps, double w1, double w2,
                                 double w3, float* __restrict__ Eq, float* __restrict__ Lq,
                                 float* __restrict__ Wl, int* __restrict__ nnz_pair) {
     const int S = 2 * R + 1;
@@ -31,8 +31,8 @@ __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, doubl
         int ti = (int)((idx / ((int64_t)S * S)) % nt);
         int to = (int)(idx / ((int64_t)S * S * nt));
         const double two_pi = 6.283185307179586476925286766559;
-        double ddx = (double)(dxi - R) / nx;
-        double ddy = (double)(dyi - R) / ny;
+        double ddx = (double)(dxi - R) * hx;
+        double ddy = (double)(dyi - R) * hy;
         double thi = two_pi * ti / nt;
         // R_{-theta_i} applied to the spatial offset
         double ci = cos(thi), si = sin(thi);
@@ -61,7 +61,7 @@ __global__ void tabulate_kernel(int nx, int ny, int nt, int R, double eps, doubl
 }
 
 // Lth[to][ti] = -w3^2 Theta^2/eps ; LseS[to][ti] = log sum_{dx,dy} exp(Ls(to,ti,dx,dy))  (fp64 sums)
-__global__ void tabulate_theta_kernel(int nx, int ny, int nt, int R, double eps, double w1, double w2,
+__global__ void tabulate_theta_kernel(double hx, double hy, int nt, int R, double eps, double w1, double w2,
                                       double w3, float* __restrict__ Lth, float* __restrict__ LseS) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= nt * nt) return;
@@ -75,7 +75,7 @@ __global__ void tabulate_theta_kernel(int nx, int ny, int nt, int R, double eps,
     double acc = 0.0;
     for (int dyi = -R; dyi <= R; ++dyi)
         for (int dxi = -R; dxi <= R; ++dxi) {
-            double ddx = (double)dxi / nx, ddy = (double)dyi / ny;
+            double ddx = (double)dxi * hx, ddy = (double)dyi * hy;
             double X = ci * ddx + si * ddy, Y = -si * ddx + ci * ddy;
             double b1 = X * ch + Y * sh, b2 = -X * sh + Y * ch;
             acc += exp(-(w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2) / eps);
@@ -95,9 +95,9 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     int threads = 256;
     int blocks = (int)((total + threads - 1) / threads);
     if (blocks > 148 * 32) blocks = 148 * 32;
-    tabulate_kernel<<<blocks, threads, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2, k->w3,
+    tabulate_kernel<<<blocks, threads, 0, s>>>(k->hx, k->hy, nt, k->R, k->eps, k->w1, k->w2, k->w3,
                                                k->Eq, k->Lq, k->Wl, nnz_dev);
-    tabulate_theta_kernel<<<(nt * nt + 127) / 128, 128, 0, s>>>(k->nx, k->ny, nt, k->R, k->eps, k->w1, k->w2,
+    tabulate_theta_kernel<<<(nt * nt + 127) / 128, 128, 0, s>>>(k->hx, k->hy, nt, k->R, k->eps, k->w1, k->w2,
                                                                   k->w3, k->Lth, k->LseS);
     e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }

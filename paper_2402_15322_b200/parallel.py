@@ -1,0 +1,177 @@
+"""Multi-GPU drivers of the scaling loop: one process per GPU, torch.distributed for the exchanges.
+
+Two decompositions of the north star (B:north_star "independent barycenter inputs ... go per GPU,
+with an NCCL allreduce over NVLink for the barycenter log-mean, and a single large grid is split
+into spatial slabs with NVLink halo exchange"):
+
+* `ShardedBarycenter` -- App. A with the n inputs distributed over the ranks.  The only
+  exchange per iteration is the allreduce of the partial weighted log-mean
+  `sum_{i on rank} lambda_i log d_i` (NCCL on GPUs).
+* `SlabJKO` -- the entropic JKO step (reading R10) with the grid's rows split into slabs;
+  before every convolution each rank exchanges R boundary rows with its neighbours (send/recv), the
+  conv runs on the slab extended by its halo (zero rows at the global edges), and the plan mass is
+  allreduced once per JKO step.
+
+The per-rank arithmetic goes through an `ops` backend: `CudaOps` (this library's kernels; the
+product path) or, in the CPU tests only, a backend built on the oracle (tests/test_parallel_gloo.py),
+so the decomposition logic is tested with the gloo backend without a GPU.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def partition(n: int, world: int, rank: int):
+    """Contiguous block partition of range(n) over `world` ranks (sizes differ by at most 1)."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class CudaOps:
+    """Per-rank arithmetic on the GPU through the se2ot C ABI."""
+
+    def __init__(self, kernel, log_domain: bool):
+        from . import api
+        self.api = api
+        self.k = kernel
+        self.log = log_domain
+
+    def divide(self, x, target, out):       # out = target / K x   (log: target - LSE x)
+        from ._lib import SE2_EPI_DIVIDE
+        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_DIVIDE, self.log)
+
+    def multiply(self, x, target, out):     # out = target * K x   (log: target + LSE x)
+        from ._lib import SE2_EPI_MULTIPLY
+        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_MULTIPLY, self.log)
+
+    def prox(self, x, out, prox):           # out = prox(K x) / K x   (JKO, R10)
+        from ._lib import SE2_EPI_PROX
+        return self.api.se2_conv_update(self.k, x, None, out, SE2_EPI_PROX, self.log, prox=prox)
+
+    def logmean(self, ld, lambdas, out):    # out = sum_i lambda_i ld_i  (lambda_i = 0 skipped)
+        return self.api.se2_bary_logmean(ld, lambdas, self.k.N, out)
+
+    def bary_update(self, lv, ld, lbar, n):  # lv_i += lbar - ld_i
+        return self.api.se2_bary_update(lv, ld, lbar, n, self.k.N)
+
+    def sum_rows(self, x, row0: int, rows: int) -> float:   # sum over rows [row0, row0+rows) of all planes
+        return self.api.se2_sum_rows(x, row0, rows)
+
+    def scale_rows(self, x, row0: int, rows: int, factor: float):
+        self.api.se2_scale_rows(x, row0, rows, factor)
+
+
+class ShardedBarycenter:
+    """App. A barycenter with inputs sharded over the ranks of the default process group.
+
+    mus_local: [n_local][N] this rank's inputs; lambdas_local: their weights (the full weight vector
+    sums to 1 over all ranks).  Log domain (R7, R13).  After `run`, `lbar` holds log mu on every rank.
+    """
+
+    def __init__(self, ops, mus_local: torch.Tensor, lambdas_local: Sequence[float], group=None):
+        self.ops = ops
+        self.group = group
+        self.n = mus_local.shape[0]
+        self.lam = np.asarray(lambdas_local, dtype=np.float64)
+        self.lmu = torch.log(mus_local)
+        self.lv = torch.zeros_like(mus_local)
+        self.lw = torch.zeros_like(mus_local)
+        self.ld = torch.empty_like(mus_local)
+        self.lbar = torch.empty_like(mus_local[0])
+
+    def iterate(self, iters: int):
+        for _ in range(iters):
+            if self.n > 0:
+                self.ops.divide(self.lv, self.lmu, self.lw)        # w_i = mu_i / K v_i
+                self.ops.multiply(self.lw, self.lv, self.ld)       # d_i = v_i K w_i
+                self.ops.logmean(self.ld, self.lam, self.lbar)     # partial sum_i lambda_i log d_i
+            else:
+                self.lbar.zero_()
+            if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                dist.all_reduce(self.lbar, op=dist.ReduceOp.SUM, group=self.group)   # log mu
+            if self.n > 0:
+                self.ops.bary_update(self.lv, self.ld, self.lbar, self.n)            # v_i <- v_i mu / d_i
+        return self.lbar
+
+
+class SlabJKO:
+    """Entropic JKO steps (R10) with the grid's rows split into slabs over the ranks.
+
+    The local arrays are [nt][rows + 2R][nx]: owned rows are [R, R + rows), the R halo rows on each
+    side hold the neighbours' boundary rows (zero at the global edges = the conv's zero padding).
+    `ops` must wrap a kernel built for the local grid (nx, rows + 2R, nt) and prox factories must shift
+    the potential's centre row by the slab offset.
+    """
+
+    def __init__(self, ops, mu_local_owned: torch.Tensor, R: int, prox, group=None):
+        self.ops = ops
+        self.R = R
+        self.prox = prox
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        nt, rows, nx = mu_local_owned.shape
+        self.rows = rows
+        self.mu = self._ext(mu_local_owned)
+        self.a = torch.zeros_like(self.mu)
+        self.b = torch.zeros_like(self.mu)
+
+    def _ext(self, owned):
+        nt, rows, nx = owned.shape
+        out = torch.zeros((nt, rows + 2 * self.R, nx), dtype=owned.dtype, device=owned.device)
+        out[:, self.R:self.R + rows] = owned
+        return out
+
+    def owned(self, x):
+        return x[:, self.R:self.R + self.rows]
+
+    def halo_exchange(self, x):
+        """Fill x's halo rows from the neighbours' boundary rows (zeros at the global edges)."""
+        R = self.R
+        if R == 0:
+            return
+        if self.world == 1:
+            x[:, :R].zero_()
+            x[:, R + self.rows:].zero_()
+            return
+        up, down = self.rank - 1, self.rank + 1
+        send_up = x[:, R:2 * R].contiguous()                       # my first R owned rows -> rank-1
+        send_down = x[:, self.rows:self.rows + R].contiguous()     # my last R owned rows  -> rank+1
+        recv_up = torch.zeros_like(send_up)                         # rank-1's last rows -> my top halo
+        recv_down = torch.zeros_like(send_down)                     # rank+1's first rows -> my bottom halo
+        ops = []
+        if up >= 0:
+            ops.append(dist.P2POp(dist.isend, send_up, up, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_up, up, self.group))
+        if down < self.world:
+            ops.append(dist.P2POp(dist.isend, send_down, down, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_down, down, self.group))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        x[:, :R] = recv_up
+        x[:, R + self.rows:] = recv_down
+
+    def step(self, iters: int):
+        """One JKO step: b <- 1; iters x (a = mu / K b ; b = prox(K a) / K a); s = b K a; normalise."""
+        self.b.fill_(1.0)
+        for _ in range(iters):
+            self.halo_exchange(self.b)
+            self.ops.divide(self.b, self.mu, self.a)
+            self.halo_exchange(self.a)
+            self.ops.prox(self.a, self.b, self.prox)
+        # s = b * K a (the last prox's input), then mu_{k+1} = s / sum s over all slabs
+        self.ops.multiply(self.a, self.b, self.mu)                  # mu <- b * K a = s (halo rows junk)
+        local = self.ops.sum_rows(self.mu, self.R, self.rows)
+        mass = torch.tensor([local], dtype=torch.float64)
+        if self.world > 1:
+            if dist.get_backend(self.group) == "nccl":
+                mass = mass.cuda()
+            dist.all_reduce(mass, op=dist.ReduceOp.SUM, group=self.group)
+        m = float(mass.item())
+        self.ops.scale_rows(self.mu, self.R, self.rows, 1.0 / m)
+        return m

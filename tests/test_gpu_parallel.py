@@ -1,0 +1,49 @@
+"""The multi-GPU drivers (parallel.py) on one GPU with the CUDA ops backend, against the oracle
+(world size 1: the same code path minus the collectives; the exchanges themselves are covered by
+tests/test_parallel_gloo.py)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import measure_err, potential_err
+
+pytestmark = pytest.mark.gpu
+
+
+def test_sharded_barycenter_single_rank(cuda_device):
+    from paper_2402_15322_b200 import Kernel
+    from paper_2402_15322_b200.parallel import CudaOps, ShardedBarycenter
+    nx, ny, nt, R, eps, w = 40, 36, 16, 5, 0.02, (1.0, 3.0, 1.0)
+    g = O.Grid(nx, ny, nt)
+    rng = np.random.default_rng(0)
+    mus = [(rng.random(g.shape) ** 3 + 1e-3).astype(np.float32) for _ in range(3)]
+    mus = [(m / m.sum()).astype(np.float32) for m in mus]
+    lam = np.array([0.2, 0.5, 0.3])
+    k = Kernel(nx, ny, nt, eps, w, R, max_batch=3)
+    drv = ShardedBarycenter(CudaOps(k, True), torch.from_numpy(np.stack(mus)).cuda(), lam)
+    lbar = drv.iterate(30).cpu().numpy().astype(np.float64)
+    ref = O.barycenter(O.kernel_table(g, R, eps, w), O.log_kernel_table(g, R, eps, w),
+                       [m.astype(np.float64) for m in mus], lam, 30, log_domain=True, trace=False)
+    assert potential_err(lbar, ref["lbary"]) < 1e-4
+    assert measure_err(np.exp(lbar), ref["bary"]) < 1e-4
+
+
+def test_slab_jko_single_rank(cuda_device):
+    from paper_2402_15322_b200 import Kernel, make_prox
+    from paper_2402_15322_b200.parallel import CudaOps, SlabJKO
+    nx, ny, nt, R, eps, tau = 48, 40, 16, 4, 0.003, 1e-3
+    g = O.Grid(nx, ny, nt)
+    rng = np.random.default_rng(1)
+    mu = (rng.random(g.shape) + 0.05)
+    mu = (mu / mu.sum()).astype(np.float32)
+    # slab kernel: the grid plus R halo rows on each side, global cell sizes (R1)
+    k = Kernel(nx, ny + 2 * R, nt, eps, (1, 3, 1), R, hx=1.0 / nx, hy=1.0 / ny)
+    prox = make_prox(k, tau, global_ny=ny, row_offset=-R)
+    drv = SlabJKO(CudaOps(k, False), torch.from_numpy(mu).cuda(), R, prox)
+    masses = [drv.step(50) for _ in range(2)]
+    out = drv.owned(drv.mu).cpu().numpy().astype(np.float64)
+    ref = O.jko(O.kernel_table(g, R, eps, (1, 3, 1)), None, mu.astype(np.float64), g, eps, tau, 2, 50,
+                log_domain=False, trace=False)
+    assert measure_err(out, ref["mus"][2]) < 1e-4
+    np.testing.assert_allclose(masses, ref["masses"], rtol=1e-4)

@@ -1,0 +1,150 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU decompositions in
+paper_2402_15322_b200/parallel.py.  The per-rank arithmetic is supplied by an oracle-backed ops
+object (test-side only), so what is tested here is the decomposition itself: the input partition and
+the log-mean allreduce of the sharded barycenter, and the slab partition, halo exchange, shifted
+potential and mass allreduce of the slab JKO -- against the unsharded oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2402_15322_b200.parallel import ShardedBarycenter, SlabJKO, partition
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleOps:
+    """fp64 CPU arithmetic from the oracle, with the CudaOps interface."""
+
+    def __init__(self, T, L, log, eps=None, global_ny=None, nx=None):
+        self.T, self.L, self.log = T, L, log
+        self.eps, self.gny, self.nx = eps, global_ny, nx
+
+    def _conv(self, x):
+        return O.lse_conv(self.L, x.numpy()) if self.log else O.conv(self.T, x.numpy())
+
+    def divide(self, x, target, out):
+        y = self._conv(x)
+        t = target.numpy()
+        out.copy_(torch.from_numpy(np.where(t == -np.inf, -np.inf, t - y) if self.log
+                                   else t / np.maximum(y, O.DIV_FLOOR)))
+
+    def multiply(self, x, target, out):
+        y = self._conv(x)
+        out.copy_(torch.from_numpy(target.numpy() + y if self.log else target.numpy() * y))
+
+    def prox(self, x, out, prox):
+        tau, row_off = prox
+        z = np.maximum(O.conv(self.T, x.numpy()), O.DIV_FLOOR)
+        nt, ny_loc, nx = z.shape
+        X = (np.arange(nx) + 0.5) / self.nx
+        Y = (np.arange(ny_loc) + row_off + 0.5) / self.gny
+        V = (X[None, None, :] - 0.5) ** 2 + (Y[None, :, None] - 0.5) ** 2
+        p = tau / (self.eps + tau)
+        out.copy_(torch.from_numpy(z ** (-p) * np.exp(-p * V)))
+
+    def logmean(self, ld, lam, out):
+        acc = np.zeros(out.shape)
+        for i, l in enumerate(lam):
+            if l != 0.0:
+                acc = acc + l * ld[i].numpy()
+        out.copy_(torch.from_numpy(acc))
+
+    def bary_update(self, lv, ld, lbar, n):
+        lv += lbar[None] - ld
+
+    def sum_rows(self, x, row0, rows):
+        return float(x[..., row0:row0 + rows, :].sum())
+
+    def scale_rows(self, x, row0, rows, f):
+        x[..., row0:row0 + rows, :] *= f
+
+
+def _bary_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = O.Grid(12, 10, 8)
+        T = O.kernel_table(g, 2, 0.05, (1, 3, 1))
+        L = O.log_kernel_table(g, 2, 0.05, (1, 3, 1))
+        rng = np.random.default_rng(0)
+        mus = [rng.random(g.shape) ** 3 + 1e-3 for _ in range(3)]
+        mus = [m / m.sum() for m in mus]
+        lam = np.array([0.2, 0.5, 0.3])
+        lo, hi = partition(3, world, rank)
+        drv = ShardedBarycenter(OracleOps(T, L, True), torch.from_numpy(np.stack(mus[lo:hi])), lam[lo:hi])
+        lbar = drv.iterate(12).numpy().copy()
+        if rank == 0:
+            ref = O.barycenter(T, L, mus, lam, 12, log_domain=True, trace=False)["lbary"]
+            q.put(float(np.max(np.abs(lbar - ref))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _slab_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny, nt, R, eps, tau = 12, 11, 8, 2, 0.05, 0.02
+        g = O.Grid(nx, ny, nt)
+        T = O.kernel_table(g, R, eps, (1, 3, 1))      # cell sizes of the GLOBAL grid (R1)
+        rng = np.random.default_rng(1)
+        mu = rng.random(g.shape) + 0.05
+        mu /= mu.sum()
+        r0, r1 = partition(ny, world, rank)
+        ops = OracleOps(T, None, False, eps=eps, global_ny=ny, nx=nx)
+        drv = SlabJKO(ops, torch.from_numpy(mu[:, r0:r1].copy()), R, prox=(tau, r0 - R))
+        masses = [drv.step(15) for _ in range(2)]
+        owned = drv.owned(drv.mu).numpy().copy()
+        full = [None] * world
+        dist.all_gather_object(full, (r0, r1, owned))
+        if rank == 0:
+            out = np.zeros(g.shape)
+            for a, b, o in full:
+                out[:, a:b] = o
+            ref = O.jko(T, None, mu, g, eps, tau, 2, 15, log_domain=False, trace=False)
+            q.put((float(np.max(np.abs(out - ref["mus"][2]) / ref["mus"][2])),
+                   float(np.max(np.abs(np.array(masses) - ref["masses"])))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(worker, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    mp.start_processes(worker, args=(world, port, q), nprocs=world, join=True, start_method="spawn")
+    return q.get()
+
+
+def test_partition():
+    for n in (1, 3, 4, 7, 256):
+        for w in (1, 2, 3, 8):
+            parts = [partition(n, w, r) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_sharded_barycenter_gloo():
+    err = _run(_bary_worker)
+    assert err < 1e-10, err
+
+
+def test_slab_jko_gloo():
+    rel, dmass = _run(_slab_worker)
+    assert rel < 1e-10 and dmass < 1e-12, (rel, dmass)
