@@ -160,6 +160,67 @@ def run_reference(args):
     return 0
 
 
+def config_sweep(device: int):
+    """Every BASELINE config solved once end to end on this GPU (after one warm-up solve), timed with
+    CUDA events: iterations/s of the whole config (c1: all five t-values batched), conv time share,
+    and for the log-domain configs the K3 path mix (pruned / FFMA / per-tap fallback pairs)."""
+    import torch
+
+    import se2_synth as S
+    from paper_2402_15322_b200 import Kernel, make_prox, se2_barycenter, se2_jko_step, se2_sinkhorn
+    out = {}
+    for cfg in S.CONFIGS:
+        d = S.config_inputs(cfg)
+        n = len(d["mus"])
+        lams = np.atleast_2d(np.stack(d["lambdas"])) if "lambdas" in d else None
+        batch = n * (lams.shape[0] if lams is not None else 1)
+        k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=max(batch, 1), device=device)
+        mus = torch.from_numpy(np.stack(d["mus"])).cuda()
+
+        def solve():
+            if cfg.problem == "sinkhorn":
+                a = torch.empty_like(mus[0])
+                b = torch.empty_like(mus[0])
+                se2_sinkhorn(k, mus[0].contiguous(), mus[1].contiguous(), a, b, cfg.iters, cfg.log_domain, trace=True)
+                return cfg.iters
+            if cfg.problem == "barycenter":
+                se2_barycenter(k, mus, lams, cfg.iters, cfg.log_domain, trace=True)
+                return cfg.iters
+            prox = make_prox(k, cfg.tau)
+            mu, nxt = mus[0].clone(), torch.empty_like(mus[0])
+            a, b = torch.empty_like(mu), torch.empty_like(mu)
+            se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, cfg.log_domain, trace=True)
+            return cfg.iters
+
+        solve()
+        torch.cuda.synchronize()
+        k.lse_path_stats(reset=True)
+        k.timing_enable(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        it = solve()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        nconv, conv_ms, _ = k.timing_get()
+        k.timing_enable(False)
+        st = k.stats()
+        rec = {"problem": cfg.problem, "grid": f"{cfg.nx}x{cfg.ny}x{cfg.ntheta}", "fields_per_conv": batch,
+               "iters": it, "ms": ms, "iters_per_s": it / (ms / 1000.0), "domain": "log" if cfg.log_domain else "linear",
+               "conv_share": conv_ms / ms if ms else None, "conv_avg_ms": conv_ms / max(nconv, 1)}
+        if not cfg.log_domain:
+            flop = 2.0 * cfg.N * st["nnz_taps"] * (batch if cfg.problem != "jko" else 1)
+            rec["conv_tflops"] = flop / (rec["conv_avg_ms"] / 1000.0) / 1e12
+        else:
+            ps = k.lse_path_stats(reset=True)
+            rec["k3_pairs"] = ps
+            rec["k3_active_frac"] = ps["active"] / max(ps["visited"], 1)
+            rec["k3_ffma_frac_of_active"] = ps["ffma"] / max(ps["active"], 1)
+        out[cfg.name] = rec
+        k.close()
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -283,6 +344,8 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
+        if not args.no_configs:
+            out["configs"] = config_sweep(local)
         if not args.no_cpu_baseline:
             v, desc, threads, _ = cpu_oracle_sample(cfg)
             out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc}
@@ -298,6 +361,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (c0..c4 solves)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
