@@ -60,6 +60,8 @@ typedef enum {
 #define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1        */
 #define SE2_TRACE_ERR 0x4u    /* compute the marginal error every iteration (fused)           */
 #define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4)   */
+#define SE2_LSE_NOTILT 0x10u  /* diagnostics: K3 without its gradient-tilted FFMA path           */
+#define SE2_LSE_K3EXACT 0x20u /* diagnostics: K3 with every active channel on its exact path     */
 
 typedef struct {
     int32_t nx, ny, ntheta;
@@ -205,9 +207,10 @@ SE2_API se2_status se2_scale_rows(float* x, int32_t planes, int32_t ny, int32_t 
 SE2_API se2_status se2_sum(const float* x, int64_t n, double* out_host, se2_stream stream);
 
 /* Log-domain engine (K3) path counters since the last reset: (tile-quad, theta_i) pairs that were
- * active after pruning, handled by the FFMA path, and visited in total. */
+ * active after pruning, handled by an FFMA path (plain or gradient-tilted), visited in total, and
+ * handled by the tilted FFMA path. */
 SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs,
-                                      int64_t* visited_pairs, int32_t reset);
+                                      int64_t* visited_pairs, int64_t* tilted_pairs, int32_t reset);
 
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)

@@ -15,6 +15,8 @@ SE2_LOG_DOMAIN = 0x1
 SE2_WARM_START = 0x2
 SE2_TRACE_ERR = 0x4
 SE2_LSE_EXACT = 0x8
+SE2_LSE_NOTILT = 0x10
+SE2_LSE_K3EXACT = 0x20
 SE2_EPI_DIVIDE = 1
 SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3
@@ -93,7 +95,8 @@ def load(path: str = LIB_PATH):
         "se2_sum_rows": [P, i32, i32, i32, i32, i32, pd, P],
         "se2_scale_rows": [P, i32, i32, i32, i32, i32, dbl, P],
         "se2_timing_enable": [P, i32],
-        "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
+        "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                               ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
     }
     for name, args in sig.items():

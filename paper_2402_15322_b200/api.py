@@ -81,10 +81,10 @@ class Kernel:
     # instrumentation
     def lse_path_stats(self, reset: bool = True) -> dict:
         """K3 counters: (tile-quad, theta_i) pairs active after pruning / on the FFMA path / visited."""
-        a, f, v = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        a, f, v, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         check(L.load().se2_lse_path_stats(self._h, ctypes.byref(a), ctypes.byref(f), ctypes.byref(v),
-                                          1 if reset else 0))
-        return dict(active=a.value, ffma=f.value, visited=v.value)
+                                          ctypes.byref(t), 1 if reset else 0))
+        return dict(active=a.value, ffma=f.value, visited=v.value, tilted=t.value)
 
     def timing_enable(self, on: bool = True):
         check(L.load().se2_timing_enable(self._h, 1 if on else 0))
@@ -107,7 +107,7 @@ def _flags(log_domain: bool, trace: bool = False, warm: bool = False, lse_exact:
 
 
 def se2_conv(k: Kernel, x: torch.Tensor, out: Optional[torch.Tensor] = None, log_domain: bool = False,
-             lse_exact: bool = False) -> torch.Tensor:
+             lse_exact: bool = False, extra_flags: int = 0) -> torch.Tensor:
     """out = K x (or log K exp(x) with log_domain).  lse_exact forces the per-tap
     log-sum-exp engine (K4) instead of the factored one (K3)."""
     _check_field(x, k, "x")
@@ -115,8 +115,8 @@ def se2_conv(k: Kernel, x: torch.Tensor, out: Optional[torch.Tensor] = None, log
     if out is None:
         out = torch.empty_like(x)
     _check_field(out, k, "out", batch)
-    check(L.load().se2_conv(k.handle, _ptr(x), _ptr(out), batch, _flags(log_domain, lse_exact=lse_exact),
-                            _stream(x.device)))
+    check(L.load().se2_conv(k.handle, _ptr(x), _ptr(out), batch,
+                            _flags(log_domain, lse_exact=lse_exact) | int(extra_flags), _stream(x.device)))
     return out
 
 

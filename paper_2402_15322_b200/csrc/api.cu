@@ -92,7 +92,8 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
     else if (flags & SE2_LSE_EXACT)
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
-        e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->tmin, k->tmax, 0, k->lse_counters);
+        e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->lstats,
+                                 (flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0), k->lse_counters);
     if (e != cudaSuccess) {
         set_error(std::string("conv launch: ") + cudaGetErrorString(e));
         return SE2_ECUDA;
@@ -170,8 +171,7 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     k->table_bytes = 2 * tab + tabl + 2 * sizeof(float) * k->nt * k->nt;
     {
         const size_t nst = lse_fast_stats_floats(k, max_batch);
-        cudaError_t e2 = cudaMalloc(&k->tmin, sizeof(float) * nst);
-        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->tmax, sizeof(float) * nst);
+        cudaError_t e2 = cudaMalloc(&k->lstats, sizeof(float) * nst);
         if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(long long) * 4);
         if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(long long) * 4);
         if (e2 != cudaSuccess) {
@@ -215,8 +215,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->LseS) cudaFree(k->LseS);
     if (k->Lq) cudaFree(k->Lq);
     if (k->Wl) cudaFree(k->Wl);
-    if (k->tmin) cudaFree(k->tmin);
-    if (k->tmax) cudaFree(k->tmax);
+    if (k->lstats) cudaFree(k->lstats);
     if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
     if (x) {
@@ -609,16 +608,17 @@ se2_status se2_scale_rows(float* xp, int32_t planes, int32_t ny, int32_t nx, int
 }
 
 se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs, int64_t* visited_pairs,
-                              int32_t reset) {
+                              int64_t* tilted_pairs, int32_t reset) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     DeviceGuard g(k->device);
-    int h[3] = {0, 0, 0};
+    int h[4] = {0, 0, 0, 0};
     SE2_CUDA_TRY(cudaDeviceSynchronize());
-    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters, sizeof(int) * 3, cudaMemcpyDeviceToHost));
+    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters, sizeof(int) * 4, cudaMemcpyDeviceToHost));
     if (active_pairs) *active_pairs = h[0];
     if (ffma_pairs) *ffma_pairs = h[1];
     if (visited_pairs) *visited_pairs = h[2];
-    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 3));
+    if (tilted_pairs) *tilted_pairs = h[3];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 4));
     return SE2_OK;
 }
 

@@ -1,19 +1,26 @@
-// K3: SE(2) group convolution in the log domain -- theta-factored, shifted FFMA log-sum-exp with an
-// exact per-tap fallback and exact-bound channel pruning (reading R7).
+// K3: SE(2) group convolution in the log domain -- theta-factored, shifted FFMA log-sum-exp with a
+// gradient-tilted variant, an exact per-tap fallback and exact-bound channel pruning (reading R7;
+// DESIGN.md "K3").
 //
 //   ly[to, x] = log sum_ti sum_d exp( Lth(to,ti) + Ls(to,ti,d) + lv[ti, x - d] )
 //
-// Per CTA (a 32 x 16 spatial tile T, an output-orientation quad, one field) and per input
-// orientation ti, with mu = min_T lv[ti] and M = max over the window (T + halo) of lv[ti]:
-//   * prune  if  M + Lth + log sum_d e^{Ls}  <  LB - 30  for every to of the quad, where
-//            LB(to) = max_j (Lth(to,j) + mu_j) <= ly(to, x) for all x in T (centre taps);
-//            the skipped mass is < e^{-30} of the output per channel;
-//   * FFMA   if  M - mu <= 100: stage v~ = exp(lv - m), m = mu + 62, and accumulate
-//            S = sum_d exp(Ls + 40) v~ with fp32 FFMA; every term within e^{-25} of the channel's
-//            largest term is a normal fp32 product and the sum cannot overflow (derivation in
-//            DESIGN.md), then fold log S + m - 40 + Lth into the output's running (max, sum);
-//   * exact  otherwise: the two-pass per-tap log-sum-exp of K4 for this channel.
-// Cost of the FFMA path per tap = 1 FFMA (vs 1 MUFU.EX2 + 5 FP32 ops for the exact one).
+// A stats pass fits, per (field, theta, 32 x 16 tile), the plane psi(h) = a + g.(h - c) (least
+// squares, c = tile centre) and records min/max of lv and of the residual r = lv - psi.  Per CTA (a
+// tile T, an output-orientation quad, one field) and per input orientation ti:
+//   * prune   if  M + Lth + log sum_d e^{Ls} < LB - 30 for every to of the quad, where M bounds lv on
+//             the window (T + halo) and LB(to) = max_j (Lth(to,j) + min_T lv_j) <= ly(to, x) on T
+//             (centre taps); the skipped mass is < e^-30 of the output per channel;
+//   * FFMA    if  M - min_T lv <= 100: v~ = exp(lv - m), m = min_T lv + 62, S = sum_d exp(Ls + 40) v~;
+//   * tilted  if the residual range over the window R_hi - R_lo <= 100 (bounded from the 3 x 3 tile
+//     FFMA    neighbourhood's planes and residuals): with T(d) = Ls(d) - g.d and c1 = max_d T(d),
+//             v~ = exp(r - m), m = R_lo + 62, S = sum_d exp(T(d) - c1 + 40) v~, and the channel's
+//             contribution is S exp(psi(x) + c1 - 40 + m + Lth) -- since lv(x-d) = psi(x) - g.d + r(x-d)
+//             the steep part of the potential moves into the (per CTA and channel) tilted kernel;
+//   * exact   otherwise: the two-pass per-tap log-sum-exp of K4 for this channel.
+// In every FFMA variant each term within e^-25 of the channel's largest term is a normal fp32
+// product, the sum cannot overflow and underflowed terms total < 961 e^-25 relative.
+// The channel results are folded into each output's running (max, sum) in log2 units relative to a
+// per-CTA reference, which keeps the fp32 magnitudes small.
 #include "conv_common.cuh"
 
 namespace se2 {
@@ -33,30 +40,38 @@ struct LseFCfg {
     static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * S * 4;
-    static constexpr int MAXNT = 256;
+    static constexpr int MAXNT = 128;
     static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL) * sizeof(float) + 64;
 };
 constexpr int kLseTileY = 32, kLseTileX = 16;
+constexpr int kStat = 8;   // per tile: a, gx, gy, rmin, rmax, vmin, vmax, valid-plane flag
 
-// per (field, theta, tile) min and max of lv over the 32 x 16 tile
+// Per (field, theta, tile): min/max of lv, least-squares plane psi = a + gx (x - cx) + gy (y - cy)
+// about the tile centre (pixel units), and min/max of the residual lv - psi.  One warp per tile.
 __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, int nt, int tiles_x, int tiles_y,
-                                 float* __restrict__ tmin, float* __restrict__ tmax) {
+                                 float* __restrict__ st) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int ntile = tiles_x * tiles_y;
-    const int64_t total = (int64_t)gridDim.y * nt * ntile;   // gridDim.y = batch
     const int b = blockIdx.y;
     if (warp >= nt * ntile) return;
     const int th = warp / ntile, t = warp % ntile;
     const int x0 = (t % tiles_x) * kLseTileX, y0 = (t / tiles_x) * kLseTileY;
+    const int w = min(kLseTileX, nx - x0), h = min(kLseTileY, ny - y0);
+    const float cx = x0 + 0.5f * (w - 1), cy = y0 + 0.5f * (h - 1);
     const float* src = in + ((int64_t)b * nt + th) * nx * ny;
-    float mn = INFINITY, mx = -INFINITY;
-    for (int i = lane; i < kLseTileY * kLseTileX; i += 32) {
-        int y = y0 + i / kLseTileX, x = x0 + i % kLseTileX;
-        if (y < ny && x < nx) {
-            float v = src[(int64_t)y * nx + x];
-            mn = fminf(mn, v);
-            mx = fmaxf(mx, v);
+    constexpr int PER = kLseTileY * kLseTileX / 32;
+    float v[PER];
+    float mn = INFINITY, mx = -INFINITY, s0 = 0.f, sx = 0.f, sy = 0.f;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int i = lane + 32 * k;
+        const int yy = i / kLseTileX, xx = i % kLseTileX;
+        v[k] = 0.f;
+        if (yy < h && xx < w) {
+            v[k] = src[(int64_t)(y0 + yy) * nx + x0 + xx];
+            mn = fminf(mn, v[k]);
+            mx = fmaxf(mx, v[k]);
         }
     }
 #pragma unroll
@@ -64,28 +79,88 @@ __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, i
         mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    if (lane == 0) {
-        int64_t o = ((int64_t)b * nt + th) * ntile + t;
-        tmin[o] = mn;
-        tmax[o] = mx;
+    const bool finite = (mn != -INFINITY) && (mx != INFINITY) && (mn == mn);
+    float a = 0.f, gx = 0.f, gy = 0.f, rmn = mn, rmx = mx;
+    if (finite) {
+        // the valid cells form a w x h rectangle: the centred design is orthogonal
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = lane + 32 * k;
+            const int yy = i / kLseTileX, xx = i % kLseTileX;
+            if (yy < h && xx < w) {
+                const float d = v[k] - mn;      // shift for conditioning
+                s0 += d;
+                sx += d * ((float)(x0 + xx) - cx);
+                sy += d * ((float)(y0 + yy) - cy);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        const float sxx = (float)h * (float)w * ((float)w * w - 1.f) / 12.f;
+        const float syy = (float)w * (float)h * ((float)h * h - 1.f) / 12.f;
+        a = mn + s0 / (float)(w * h);
+        gx = sxx > 0.f ? sx / sxx : 0.f;
+        gy = syy > 0.f ? sy / syy : 0.f;
+        rmn = INFINITY;
+        rmx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = lane + 32 * k;
+            const int yy = i / kLseTileX, xx = i % kLseTileX;
+            if (yy < h && xx < w) {
+                const float r = (v[k] - a) - (gx * ((float)(x0 + xx) - cx) + gy * ((float)(y0 + yy) - cy));
+                rmn = fminf(rmn, r);
+                rmx = fmaxf(rmx, r);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rmn = fminf(rmn, __shfl_xor_sync(0xffffffffu, rmn, o));
+            rmx = fmaxf(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
+        }
     }
-    (void)total;
+    if (lane == 0) {
+        float* o = st + (((int64_t)b * nt + th) * ntile + t) * kStat;
+        o[0] = a; o[1] = gx; o[2] = gy; o[3] = rmn; o[4] = rmx; o[5] = mn; o[6] = mx;
+        o[7] = finite ? 1.f : 0.f;
+    }
+}
+
+// extreme values of (psi_j - psi_0) over the pixel rectangle [xa, xb] x [ya, yb] (an affine function)
+__device__ __forceinline__ void plane_diff_range(float da, float dgx, float dgy, float cxj, float cyj, float cx0,
+                                                 float cy0, float gx0, float gy0, float xa, float xb, float ya,
+                                                 float yb, float& lo, float& hi) {
+    // psi_j(p) - psi_0(p) = da + gxj (x - cxj) + gyj (y - cyj) - gx0 (x - cx0) - gy0 (y - cy0)
+    //                     = const + dgx x + dgy y
+    const float c = da - (dgx + gx0) * cxj - (dgy + gy0) * cyj + gx0 * cx0 + gy0 * cy0;
+    const float v1 = c + dgx * xa + dgy * ya, v2 = c + dgx * xb + dgy * ya;
+    const float v3 = c + dgx * xa + dgy * yb, v4 = c + dgx * xb + dgy * yb;
+    lo = fminf(fminf(v1, v2), fminf(v3, v4));
+    hi = fmaxf(fmaxf(v1, v2), fmaxf(v3, v4));
 }
 
 template <int R>
 __global__ void __launch_bounds__(LseFCfg<R>::NT)
 conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq, const float* __restrict__ Lq,
-                     const float* __restrict__ Lth, const float* __restrict__ LseS,
-                     const float* __restrict__ tmin, const float* __restrict__ tmax, int nx, int ny, int nt,
-                     int tiles_x, int tiles_y, int force_exact, Epilogue epi, int* __restrict__ counters) {
+                     const float* __restrict__ Lth, const float* __restrict__ LseS, const float* __restrict__ st,
+                     int nx, int ny, int nt, int tiles_x, int tiles_y, int force_exact, Epilogue epi,
+                     int* __restrict__ counters) {
     using C = LseFCfg<R>;
     extern __shared__ __align__(16) float smem[];
     float* sWin = smem;
     float* sFil = smem + 2 * C::WIN;
     float* sRed = sFil + 2 * C::FIL;
-    __shared__ float sMu[C::MAXNT], sM[C::MAXNT], sCoef[C::MAXNT][4], sLB[4];
+    __shared__ float sMu[C::MAXNT], sM[C::MAXNT], sLB[4];
+    __shared__ float sA[C::MAXNT], sGx[C::MAXNT], sGy[C::MAXNT], sShift[C::MAXNT];
+    __shared__ float sCoef[C::MAXNT][4];
+    __shared__ float sPart[C::NT / 32][4], sPartD[C::NT / 32][4];
+    __shared__ float sRhi[C::MAXNT];
     __shared__ int sList[C::MAXNT];
-    __shared__ int sNAct, sNFast;
+    __shared__ int sNAct, sNFast, sNTilt;
     __shared__ float sRef;
 
     const int tile = blockIdx.x;
@@ -100,18 +175,42 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     const int wx = threadIdx.x >> 5;
     const float NEG_INF = -INFINITY;
     const float LOW = -1e30f;   // "no term yet" sentinel of the running maxima (finite: no inf - inf)
+    const float cx0 = x0 + 0.5f * (min(C::TX, nx - x0) - 1), cy0 = y0 + 0.5f * (min(C::TY, ny - y0) - 1);
 
-    // ---- per-channel bounds --------------------------------------------------------------------
+    // ---- per-channel bounds from the tile statistics -------------------------------------------
     for (int i = threadIdx.x; i < nt; i += C::NT) {
-        const int64_t base = ((int64_t)b * nt + i) * ntile;
-        sMu[i] = tmin[base + tile];
+        const float* s0 = st + (((int64_t)b * nt + i) * ntile + tile) * kStat;
+        const float mu = s0[5];
         float M = NEG_INF;
+        // tilted bounds of the residual r = lv - psi_0 over the window (3 x 3 tile neighbourhood)
+        const bool plane = s0[7] > 0.5f;
+        const float a0 = s0[0], gx0 = s0[1], gy0 = s0[2];
+        float rlo = INFINITY, rhi = -INFINITY;
+        bool tilt_ok = plane;
         for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx) {
-                int yy = ty + dy, xx = tx + dx;
-                if (yy >= 0 && yy < tiles_y && xx >= 0 && xx < tiles_x) M = fmaxf(M, tmax[base + yy * tiles_x + xx]);
+                const int yy = ty + dy, xx = tx + dx;
+                if (yy < 0 || yy >= tiles_y || xx < 0 || xx >= tiles_x) continue;
+                const float* sj = st + (((int64_t)b * nt + i) * ntile + yy * tiles_x + xx) * kStat;
+                M = fmaxf(M, sj[6]);
+                if (!tilt_ok) continue;
+                if (!(sj[7] > 0.5f)) { tilt_ok = false; continue; }
+                const int xa = xx * C::TX, ya = yy * C::TY;
+                const int xb = min(xa + C::TX, nx) - 1, yb = min(ya + C::TY, ny) - 1;
+                const float cxj = xa + 0.5f * (xb - xa), cyj = ya + 0.5f * (yb - ya);
+                float lo, hi;
+                plane_diff_range(sj[0] - a0, sj[1] - gx0, sj[2] - gy0, cxj, cyj, cx0, cy0, gx0, gy0, (float)xa,
+                                 (float)xb, (float)ya, (float)yb, lo, hi);
+                rlo = fminf(rlo, sj[3] + lo);
+                rhi = fmaxf(rhi, sj[4] + hi);
             }
+        sMu[i] = mu;
         sM[i] = M;
+        sA[i] = a0;
+        sGx[i] = gx0;
+        sGy[i] = gy0;
+        sShift[i] = tilt_ok ? ((rhi - rlo <= kFastRange) ? rlo : NAN) : NAN;   // R_lo when a tilt may be valid
+        sRhi[i] = rhi;
     }
     __syncthreads();
     if (wx < 4) {   // warp q: lower bound LB(to_q) = max_j (Lth(to_q, j) + mu_j)
@@ -135,10 +234,10 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     }
     __syncthreads();
     const float ref = sRef;
-    // status per channel: 0 skip, 1 FFMA path, 2 exact path; coefficient of the FFMA path
+    // status per channel: 0 skip, 1 FFMA, 2 exact, 3 tilted FFMA
     for (int i = threadIdx.x; i < nt; i += C::NT) {
         const float M = sM[i], mu = sMu[i];
-        int st = 0;
+        int stt = 0;
         if (M != NEG_INF) {
             bool active = false;
             for (int q = 0; q < 4; ++q) {
@@ -147,10 +246,15 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 const float ub = M + Lth[to * nt + i] + LseS[to * nt + i];
                 if (!(ub < sLB[q] - kPruneGap)) active = true;
             }
-            if (active) st = (!force_exact && mu != NEG_INF && (M - mu) <= kFastRange) ? 1 : 2;
+            if (active) {
+                if (force_exact == 1) stt = 2;
+                else if (mu != NEG_INF && (M - mu) <= kFastRange) stt = 1;
+                else if (force_exact != 2 && sShift[i] == sShift[i]) stt = 3;   // not NaN: tilt valid
+                else stt = 2;
+            }
         }
-        sList[i] = st;
-        if (st == 1)
+        sList[i] = stt;
+        if (stt == 1)
             for (int q = 0; q < 4; ++q) {
                 const int to = 4 * qd + q;
                 const float lt = (to < nt) ? Lth[to * nt + i] : 0.f;
@@ -160,16 +264,18 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     }
     __syncthreads();
     if (threadIdx.x == 0) {   // compact the active list: entry = channel | (path << 16)
-        int n = 0, nf = 0;
+        int n = 0, nf = 0, ntl = 0;
         for (int i = 0; i < nt; ++i) {
-            int st = sList[i];
-            if (st) {
-                sList[n++] = i | (st << 16);
-                nf += (st == 1);
+            int s = sList[i];
+            if (s) {
+                sList[n++] = i | (s << 16);
+                nf += (s == 1 || s == 3);
+                ntl += (s == 3);
             }
         }
         sNAct = n;
         sNFast = nf;
+        sNTilt = ntl;
     }
     __syncthreads();
     const int nact = sNAct;
@@ -221,23 +327,116 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         } else {
             cp_async_wait<0>();
         }
-        // transform the elements this thread staged (own cp.async copies are complete)
-        {
-            float* dw = sWin + buf * C::WIN;
-            const float shift = (path == 1) ? (sMu[ti] + kShiftAbove) : ref;
+        float* dw = sWin + buf * C::WIN;
+        float* df = sFil + buf * C::FIL;
+        // transform the elements this thread staged (its own cp.async copies are complete)
+        int epath = path;   // effective path of this channel (a tilt candidate may fall back to exact)
+        if (path == 3) {
+            // tilted candidate: T2(d) = (Ls(d) - g.d) log2 e from the staged L table.  c1 = max_d T2 over
+            // the box; c1D = max over the taps valid for every output of the tile (a sub-box, clipped by
+            // the zero padding).  The shift m = R_lo + 62 - dc, dc = max_q (c1 - c1D) (natural), is valid
+            // when R_hi - R_lo + dc <= 100 (K3); otherwise the channel takes the exact path.
+            const float gx = sGx[ti], gy = sGy[ti];
+            const int xt1 = min(x0 + C::TX, nx) - 1, yt1 = min(y0 + C::TY, ny) - 1;
+            const int dxlo = max(-R, xt1 - (nx - 1)), dxhi = min(R, x0);
+            const int dylo = max(-R, yt1 - (ny - 1)), dyhi = min(R, y0);
+            float lt2[4], pmax[4], pmaxD[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int to = 4 * qd + q;
+                lt2[q] = (to < nt ? Lth[to * nt + ti] : 0.f) * kLog2e;
+                pmax[q] = -INFINITY;
+                pmaxD[q] = -INFINITY;
+            }
+            // the filter block was copied in 16-byte chunks (one tap's four q values) by thread
+            // (chunk % NT): read the same chunks (own cp.async writes are visible)
+            const float4* df4 = reinterpret_cast<const float4*>(df);
+            for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) {
+                const int dyi = i / C::S, dxi = i - dyi * C::S;
+                const float gd = (gx * (float)(dxi - R) + gy * (float)(dyi - R)) * kLog2e;
+                const float4 v = df4[i];
+                const float t0 = (v.x - lt2[0]) - gd, t1 = (v.y - lt2[1]) - gd;
+                const float t2 = (v.z - lt2[2]) - gd, t3 = (v.w - lt2[3]) - gd;
+                pmax[0] = fmaxf(pmax[0], t0); pmax[1] = fmaxf(pmax[1], t1);
+                pmax[2] = fmaxf(pmax[2], t2); pmax[3] = fmaxf(pmax[3], t3);
+                if (dxi - R >= dxlo && dxi - R <= dxhi && dyi - R >= dylo && dyi - R <= dyhi) {
+                    pmaxD[0] = fmaxf(pmaxD[0], t0); pmaxD[1] = fmaxf(pmaxD[1], t1);
+                    pmaxD[2] = fmaxf(pmaxD[2], t2); pmaxD[3] = fmaxf(pmaxD[3], t3);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float v = pmax[q], u = pmaxD[q];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                    u = fmaxf(u, __shfl_xor_sync(0xffffffffu, u, o));
+                }
+                if (lane == 0) { sPart[wx][q] = v; sPartD[wx][q] = u; }
+            }
+            __syncthreads();
+            float c1[4], dc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                c1[q] = sPart[0][q];
+                float cD = sPartD[0][q];
+#pragma unroll
+                for (int w2 = 1; w2 < C::NT / 32; ++w2) {
+                    c1[q] = fmaxf(c1[q], sPart[w2][q]);
+                    cD = fmaxf(cD, sPartD[w2][q]);
+                }
+                dc = fmaxf(dc, (c1[q] - cD) * kLn2);        // -inf cD (empty sub-box) -> +inf
+            }
+            const float rlo = sShift[ti], rhi = sRhi[ti];
+            if ((rhi - rlo) + dc <= kFastRange) {
+                const float a0 = sA[ti];
+                const float m = rlo + kShiftAbove - dc;
+                for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
+                    int r = i / C::WIN_W, c = i - r * C::WIN_W;
+                    const float hx = (float)(x0 - R + c) - cx0, hy = (float)(y0 - R + r) - cy0;
+                    float v = dw[r * C::PITCH + c];
+                    dw[r * C::PITCH + c] = ex2_approx(((v - a0) - (gx * hx + gy * hy) - m) * kLog2e);
+                }
+                const float sh = kEsShift * kLog2e;
+                float4* dfw = reinterpret_cast<float4*>(df);
+                for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) {
+                    const int dyi = i / C::S, dxi = i - dyi * C::S;
+                    const float gd = (gx * (float)(dxi - R) + gy * (float)(dyi - R)) * kLog2e;
+                    float4 v = dfw[i];
+                    v.x = ex2_approx(((v.x - lt2[0]) - gd) - c1[0] + sh);
+                    v.y = ex2_approx(((v.y - lt2[1]) - gd) - c1[1] + sh);
+                    v.z = ex2_approx(((v.z - lt2[2]) - gd) - c1[2] + sh);
+                    v.w = ex2_approx(((v.w - lt2[3]) - gd) - c1[3] + sh);
+                    dfw[i] = v;
+                }
+                if (threadIdx.x < 4) {
+                    const int q = threadIdx.x, to = 4 * qd + q;
+                    const float lt = (to < nt) ? Lth[to * nt + ti] : 0.f;
+                    const float c1q = (q == 0) ? c1[0] : (q == 1) ? c1[1] : (q == 2) ? c1[2] : c1[3];
+                    // contribution = S exp(psi(x) + c1 - 40 + m + Lth): relative to ref, natural -> log2
+                    sCoef[ti][q] = (((a0 - ref) + (m - kEsShift) + lt) * kLog2e) + c1q;
+                }
+                if (counters != nullptr && threadIdx.x == 0) atomicAdd(&counters[3], 1);
+            } else {
+                epath = 2;
+                if (counters != nullptr && threadIdx.x == 0) atomicAdd(&counters[1], -1);  // not an FFMA pair
+            }
+        }
+        if (epath == 1 || epath == 2) {
+            const float shift = (epath == 1) ? (sMu[ti] + kShiftAbove) : ref;
             for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
                 int r = i / C::WIN_W, c = i - r * C::WIN_W;
                 float v = dw[r * C::PITCH + c];
                 float u = (v - shift) * kLog2e;
-                dw[r * C::PITCH + c] = (path == 1) ? ex2_approx(u) : u;
+                dw[r * C::PITCH + c] = (epath == 1) ? ex2_approx(u) : u;
             }
         }
         __syncthreads();
-        const float* win = sWin + buf * C::WIN + wx * C::P;
-        const float4* fil = reinterpret_cast<const float4*>(sFil + buf * C::FIL);
+        const float* win = dw + wx * C::P;
+        const float4* fil = reinterpret_cast<const float4*>(df);
         float acc[4][C::P];
-        if (path == 1) {
-            // ---------------- FFMA path: S = sum_d exp(Ls + 40) * exp(lv - m)
+        if (epath != 2) {
+            // ---------------- FFMA paths: S = sum_d Ktilde(d) * v~(x - d)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -265,12 +464,16 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     }
                 }
             }
+            // per-output tilt psi(x) - a (log2 units); zero on the untilted path
+            const float gx2 = (epath == 3) ? sGx[ti] * kLog2e : 0.f, gy2 = (epath == 3) ? sGy[ti] * kLog2e : 0.f;
+            const float ty2 = gy2 * ((float)(y0 + lane) - cy0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float cf = sCoef[ti][q];
+                const float cf = sCoef[ti][q] + ty2;
 #pragma unroll
                 for (int p = 0; p < C::P; ++p) {
-                    const float t = lg2_approx(acc[q][p]) + cf;     // lg2(0) = -inf: no contribution
+                    const float tilt = gx2 * ((float)(x0 + wx * C::P + p) - cx0);
+                    const float t = lg2_approx(acc[q][p]) + (cf + tilt);     // lg2(0) = -inf: no contribution
                     const float mx = fmaxf(Macc[q][p], t);
                     Sacc[q][p] = Sacc[q][p] * ex2_approx(Macc[q][p] - mx) + ex2_approx(t - mx);
                     Macc[q][p] = mx;
@@ -369,8 +572,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
 
 template <int R>
 static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* tmin, float* tmax, int force_exact,
-                                 int* counters) {
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters) {
     using C = LseFCfg<R>;
     const int tiles_x = (k->nx + C::TX - 1) / C::TX;
     const int tiles_y = (k->ny + C::TY - 1) / C::TY;
@@ -378,7 +580,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     {
         const int warps = k->nt * ntile;
         dim3 g((warps * 32 + 255) / 256, batch);
-        lse_stats_kernel<<<g, 256, 0, s>>>(in, k->nx, k->ny, k->nt, tiles_x, tiles_y, tmin, tmax);
+        lse_stats_kernel<<<g, 256, 0, s>>>(in, k->nx, k->ny, k->nt, tiles_x, tiles_y, stats);
         count_launch();
     }
     cudaError_t e = cudaFuncSetAttribute(conv_lse_fast_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -386,9 +588,8 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     if (e != cudaSuccess) return e;
     dim3 grid(ntile, (k->nt + 3) / 4, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->Lth, k->LseS, tmin, tmax, k->nx,
-                                                          k->ny, k->nt, tiles_x, tiles_y, force_exact, epi,
-                                                          counters);
+    conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->Lth, k->LseS, stats, k->nx, k->ny,
+                                                          k->nt, tiles_x, tiles_y, force_exact, epi, counters);
     count_launch();
     return cudaGetLastError();
 }
@@ -396,7 +597,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
 size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch) {
     const int tiles_x = (k->nx + kLseTileX - 1) / kLseTileX;
     const int tiles_y = (k->ny + kLseTileY - 1) / kLseTileY;
-    return (size_t)batch * k->nt * tiles_x * tiles_y;
+    return (size_t)batch * k->nt * tiles_x * tiles_y * kStat;
 }
 
 int conv_blocks_per_field_lse_fast(const se2_kernel_s* k) {
@@ -406,12 +607,11 @@ int conv_blocks_per_field_lse_fast(const se2_kernel_s* k) {
 }
 
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* tmin, float* tmax, int force_exact,
-                                 int* counters) {
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters) {
     if (k->nt > LseFCfg<1>::MAXNT) return cudaErrorInvalidValue;
     switch (k->R) {
 #define SE2_CASE(r) \
-    case r: return launch_lsef_r<r>(k, in, batch, epi, s, bpf, tmin, tmax, force_exact, counters);
+    case r: return launch_lsef_r<r>(k, in, batch, epi, s, bpf, stats, force_exact, counters);
         SE2_CASE(0) SE2_CASE(1) SE2_CASE(2) SE2_CASE(3) SE2_CASE(4) SE2_CASE(5) SE2_CASE(6) SE2_CASE(7)
         SE2_CASE(8) SE2_CASE(9) SE2_CASE(10) SE2_CASE(11) SE2_CASE(12) SE2_CASE(13) SE2_CASE(14) SE2_CASE(15)
 #undef SE2_CASE

@@ -92,9 +92,8 @@ struct se2_kernel_s {
     float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
     size_t table_bytes = 0;
     void* extra = nullptr;        // grow-only workspaces (api.cu)
-    float* tmin = nullptr;        // [max_batch][nt][tiles] per-tile min / max of log fields (K3 stats)
-    float* tmax = nullptr;
-    int* lse_counters = nullptr;  // K3 path counters: active pairs, FFMA pairs, visited pairs
+    float* lstats = nullptr;      // [max_batch][nt][tiles][8] per-tile plane fit + ranges of log fields (K3)
+    int* lse_counters = nullptr;  // K3 path counters: active, FFMA (incl. tilted), visited, tilted pairs
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -111,8 +110,7 @@ int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain);
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* tmin, float* tmax, int force_exact,
-                                 int* counters);
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters);
 size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch);
 
 // tabulation (tabulate.cu)

@@ -135,6 +135,30 @@ def test_lse_paths_exercised(cuda_device):
     assert s2["ffma"] < s2["active"]                                                            # fallback used
 
 
+@pytest.mark.parametrize("grid", [(64, 64, 32, 0.01, (1.0, 4.0, 2.0), 7), (37, 45, 12, 0.005, (1.0, 3.0, 1.0), 10)],
+                         ids=["c2grid", "ragged"])
+def test_lse_tilted_path(grid, cuda_device):
+    """Steep but smooth log fields (20-40 nats per pixel plus curvature and noise) overflow the plain
+    shifted path's 100-nat window range; K3's gradient-tilted FFMA path must take them, exactly."""
+    from paper_2402_15322_b200 import se2_conv
+    nx, ny, nt, eps, w, R = grid
+    k = _kernel(nx, ny, nt, eps, w, R, 2)
+    rng = np.random.default_rng(7)
+    X, Y = np.meshgrid(np.arange(nx), np.arange(ny), indexing="xy")
+    lv = np.empty((2, nt, ny, nx))
+    for b in range(2):
+        for t in range(nt):
+            gx, gy = rng.uniform(-40, 40, 2)
+            lv[b, t] = gx * X + gy * Y + 0.02 * (X - nx / 2) ** 2 + rng.uniform(-3, 3, (ny, nx)) + 50 * t
+    lv = lv.astype(np.float32)
+    k.lse_path_stats(reset=True)
+    y = _host(se2_conv(k, _dev(lv), log_domain=True))
+    ps = k.lse_path_stats(reset=True)
+    assert ps["tilted"] > 0, ps
+    ref = O.lse_conv(O.log_kernel_table(O.Grid(nx, ny, nt), R, eps, w), lv.astype(np.float64))
+    assert potential_err(y, ref) < TOL_LSE
+
+
 def test_conv_zero_and_neginf_inputs(cuda_device):
     from paper_2402_15322_b200 import se2_conv
     k = _kernel(20, 20, 8, 0.05, (1, 3, 1), 3)
