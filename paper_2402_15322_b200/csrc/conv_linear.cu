@@ -17,34 +17,42 @@
 
 namespace se2 {
 
-template <int R, int WX>
+template <int R, int WX, bool TMA = false>
 struct LinCfg {
     static constexpr int S = 2 * R + 1;
     static constexpr int SP = (S + 3) / 4 * 4;  // filter row pitch (LDS.128 of 4 taps)
     static constexpr int P = 16;   // columns per thread
     static constexpr int NT = 32 * WX;
     static constexpr int TY = 32, TX = P * WX;
+    // left halo of the staged window: R (cp.async path) or R rounded up to a multiple of 4 (TMA
+    // boxes must start on a 16-byte boundary in x); smem column c <-> global column x0 - A + c
+    static constexpr int A = TMA ? (R + 3) / 4 * 4 : R;
     static constexpr int WIN_H = TY + 2 * R;
-    static constexpr int WIN_W = TX + 2 * R;
-    static constexpr int RL = ((P + 2 * R) + 3) / 4 * 4;  // register row length (floats)
+    static constexpr int WIN_W = TX + R + A;
+    static constexpr int RL = ((P + R + A) + 3) / 4 * 4;  // register row length (floats)
     static constexpr int NEED = ((WX - 1) * P + RL) > WIN_W ? ((WX - 1) * P + RL) : WIN_W;
     static constexpr int P0 = (NEED + 3) / 4 * 4;
     static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;  // pitch/4 odd -> no conflicts
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * SP;
     static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL) * sizeof(float) + 64;
+    // TMA variant: window buffers padded to 128 B (TMA destination alignment) + 2 mbarriers
+    static constexpr int WINA = (WIN * 4 + 127) / 128 * 32;
+    static constexpr size_t SMEM_TMA = (size_t)(2 * WINA + 2 * FIL) * sizeof(float) + 64 + 128;
 };
 
 // W table layout used here: Wl[to][ti][S][SP] (dx padded with zeros to SP)
-template <int R, int WX>
+template <int R, int WX, bool TMA>
 __global__ void __launch_bounds__(LinCfg<R, WX>::NT)
 conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, int nx, int ny, int nt,
-                   int band, int tiles_x, Epilogue epi) {
-    using C = LinCfg<R, WX>;
-    extern __shared__ __align__(16) float smem[];
-    float* sWin = smem;                 // [2][WIN]
-    float* sFil = smem + 2 * C::WIN;    // [2][FIL]
-    float* sRed = sFil + 2 * C::FIL;    // reduction scratch (16 floats)
+                   int band, int tiles_x, Epilogue epi, const __grid_constant__ CUtensorMap tmap) {
+    using C = LinCfg<R, WX, TMA>;
+    extern __shared__ __align__(128) float smem[];
+    constexpr int WSTRIDE = TMA ? C::WINA : C::WIN;   // floats between the two window buffers
+    float* sWin = smem;                     // [2][WSTRIDE]
+    float* sFil = smem + 2 * WSTRIDE;       // [2][FIL]
+    float* sRed = sFil + 2 * C::FIL;        // reduction scratch (16 floats)
+    uint64_t* sBar = reinterpret_cast<uint64_t*>(sRed + 16);   // 2 mbarriers (TMA variant)
 
     const int tile = blockIdx.x;
     const int to = blockIdx.y;
@@ -61,27 +69,51 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
     int ti0 = to - band;
     if (nti >= nt) { nti = nt; ti0 = 0; }
 
-    // zero the pitch padding columns once (never used in arithmetic; keeps initcheck clean)
-    for (int i = threadIdx.x; i < 2 * C::WIN_H; i += C::NT) {
-        float* row = sWin + (i / C::WIN_H) * C::WIN + (i % C::WIN_H) * C::PITCH;
-        for (int c = C::WIN_W; c < C::PITCH; ++c) row[c] = 0.f;
+    // address of the __grid_constant__ tensor map taken here (param space); a lambda capture of the
+    // parameter itself would copy it to local memory, which TMA cannot read
+    const CUtensorMap* tmp = &tmap;
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&sBar[0], 1);
+            mbar_init(&sBar[1], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    } else {
+        // zero the pitch padding columns once (never used in arithmetic; keeps initcheck clean)
+        for (int i = threadIdx.x; i < 2 * C::WIN_H; i += C::NT) {
+            float* row = sWin + (i / C::WIN_H) * WSTRIDE + (i % C::WIN_H) * C::PITCH;
+            for (int c = C::WIN_W; c < C::PITCH; ++c) row[c] = 0.f;
+        }
     }
 
+    // stage the window of input orientation ti (with its halo; zeros outside the grid) and the filter
+    // slice W[to][ti].  TMA variant: one thread issues a 3-D tensor copy of the PITCH x WIN_H box at
+    // (x0 - R, y0 - R, b*nt + ti) (out-of-bounds -> zero fill) plus a 1-D bulk copy of the filter.
     auto stage = [&](int it, int buf) {
         int ti = ti0 + it;
         ti = ((ti % nt) + nt) % nt;
-        const float* src = vin + (int64_t)ti * nx * ny;
-        float* dw = sWin + buf * C::WIN;
-        for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
-            int r = i / C::WIN_W, c = i - r * C::WIN_W;
-            int gy = y0 - R + r, gx = x0 - R + c;
-            bool ok = (gy >= 0) && (gy < ny) && (gx >= 0) && (gx < nx);
-            cp_async4(dw + r * C::PITCH + c, ok ? (src + (int64_t)gy * nx + gx) : vin, ok);
-        }
         const float* fsrc = Wl + ((int64_t)to * nt + ti) * C::FIL;
+        float* dw = sWin + buf * WSTRIDE;
         float* df = sFil + buf * C::FIL;
-        for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) cp_async16(df + 4 * i, fsrc + 4 * i);
-        cp_async_commit();
+        if (TMA) {
+            if (threadIdx.x == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&sBar[buf], (uint32_t)((C::WIN_H * C::PITCH + C::FIL) * sizeof(float)));
+                tma_load_3d(dw, tmp, &sBar[buf], x0 - C::A, y0 - R, b * nt + ti);
+                bulk_load(df, fsrc, (uint32_t)(C::FIL * sizeof(float)), &sBar[buf]);
+            }
+        } else {
+            const float* src = vin + (int64_t)ti * nx * ny;
+            for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
+                int r = i / C::WIN_W, c = i - r * C::WIN_W;
+                int gy = y0 - R + r, gx = x0 - C::A + c;
+                bool ok = (gy >= 0) && (gy < ny) && (gx >= 0) && (gx < nx);
+                cp_async4(dw + r * C::PITCH + c, ok ? (src + (int64_t)gy * nx + gx) : vin, ok);
+            }
+            for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) cp_async16(df + 4 * i, fsrc + 4 * i);
+            cp_async_commit();
+        }
     };
 
     float acc[C::P];
@@ -91,14 +123,15 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
     stage(0, 0);
     for (int it = 0; it < nti; ++it) {
         const int buf = it & 1;
-        if (it + 1 < nti) {
-            stage(it + 1, buf ^ 1);
-            cp_async_wait<1>();
+        if (it + 1 < nti) stage(it + 1, buf ^ 1);
+        if (TMA) {
+            mbar_wait(&sBar[buf], (uint32_t)((it >> 1) & 1));
         } else {
-            cp_async_wait<0>();
+            if (it + 1 < nti) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncthreads();
         }
-        __syncthreads();
-        const float* win = sWin + buf * C::WIN + wx * C::P;
+        const float* win = sWin + buf * WSTRIDE + wx * C::P;
         const float* fil = sFil + buf * C::FIL;
 #pragma unroll 1
         for (int dy = 0; dy < C::S; ++dy) {
@@ -119,7 +152,7 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
                     const int dx = 4 * d4 + e;
                     if (dx < C::S) {
 #pragma unroll
-                        for (int p = 0; p < C::P; ++p) acc[p] = fmaf(wv[e], r[p - dx + 2 * R], acc[p]);
+                        for (int p = 0; p < C::P; ++p) acc[p] = fmaf(wv[e], r[p - dx + R + C::A], acc[p]);
                     }
                 }
             }
@@ -153,22 +186,34 @@ constexpr int kLinWX = 2;
 template <int R>
 static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
                                 cudaStream_t s, int* bpf) {
-    using C = LinCfg<R, kLinWX>;
-    cudaError_t e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
+    using C = LinCfg<R, kLinWX, false>;
+    using CT = LinCfg<R, kLinWX, true>;
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
     int tiles_y = (k->ny + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, k->nt, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_linear_kernel<R, kLinWX><<<grid, C::NT, C::SMEM, s>>>(in, k->Wl, k->nx, k->ny, k->nt, k->band,
-                                                                 tiles_x, epi);
+    CUtensorMap tmap;
+    const bool tma = make_field_tmap(&tmap, in, k->nx, k->ny, k->nt * batch, CT::PITCH, CT::WIN_H);
+    cudaError_t e;
+    if (tma) {
+        e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)CT::SMEM_TMA);
+        if (e != cudaSuccess) return e;
+        conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, CT::SMEM_TMA, s>>>(in, k->Wl, k->nx, k->ny, k->nt, k->band,
+                                                                            tiles_x, epi, tmap);
+    } else {
+        e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        conv_linear_kernel<R, kLinWX, false><<<grid, C::NT, C::SMEM, s>>>(in, k->Wl, k->nx, k->ny, k->nt, k->band,
+                                                                         tiles_x, epi, tmap);
+    }
     count_launch();
     return cudaGetLastError();
 }
 
 int conv_blocks_per_field_linear(const se2_kernel_s* k) {
-    using C = LinCfg<1, kLinWX>;   // all radii share the tile geometry
+    using C = LinCfg<1, kLinWX, false>;   // all radii and variants share the tile geometry
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
     int tiles_y = (k->ny + C::TY - 1) / C::TY;
     return tiles_x * tiles_y * k->nt;
