@@ -109,8 +109,12 @@ SE2_API se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t b
 /* Prox of the second marginal term F2 (eq. equ:scaling_iterations). */
 typedef enum {
     SE2_PROX_MARGINAL = 0,          /* F2 = indicator{= nu}: prox = nu -> Sinkhorn        */
-    SE2_PROX_ENTROPY_POTENTIAL = 1  /* F2 = tau * (sum s(log s - 1) + sum V s): JKO step; */
+    SE2_PROX_ENTROPY_POTENTIAL = 1, /* F2 = tau * (sum s(log s - 1) + sum V s): JKO step; */
                                     /* b = z^{-tau/(eps+tau)} exp(-tau V/(eps+tau)) (reading R10)     */
+    SE2_PROX_POROUS = 2             /* F2 = tau/(m-1) int rho^m dH, the porous-medium energy of the    */
+                                    /* paper's gradient flow, rho = s/cell the density on   */
+                                    /* cells of Haar measure dx dy dtheta: s = prox(z) solves per site   */
+                                    /* (tau m/(eps(m-1))) (s/cell)^{m-1} + log(s/z) = 0 (Newton in log s)*/
 } se2_prox_kind;
 
 typedef struct {
@@ -118,6 +122,7 @@ typedef struct {
     double tau;          /* JKO time step                                                           */
     double cx, cy;       /* potential centre in cell units of this (slab) grid                      */
     double hx, hy;       /* cell sizes: V(i,j) = ((i + 1/2 - cx) hx)^2 + ((j + 1/2 - cy) hy)^2      */
+    double m;            /* porous-medium exponent m > 1 (SE2_PROX_POROUS only)                      */
 } se2_prox;
 
 typedef struct {
@@ -141,8 +146,8 @@ SE2_API se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, 
                         se2_stream stream);
 
 /* ------------------------------------------------------------------------------------------
- * se2_jko_step -- one entropic JKO step = se2_sinkhorn with the entropy+potential
- *   prox, then mu_next = b * K^T a normalised to mass 1 (R10).  mass_host (nullable) receives
+ * se2_jko_step -- one entropic JKO step = se2_sinkhorn with the entropy+potential or
+ *   porous-medium prox, then mu_next = b * K^T a normalised to mass 1 (R10).  mass_host (nullable) receives
  *   sum(b * K^T a) before normalisation.  mu_k, mu_next: [N] device (may not alias).
  * ---------------------------------------------------------------------------------------- */
 SE2_API se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* a, float* b,
@@ -175,11 +180,20 @@ SE2_API se2_status se2_marginal_error(se2_kernel k, const float* a, const float*
                               uint32_t flags, double* err_host, se2_stream stream);
 
 /* ------------------------------------------------------------------------------------------
+ * se2_transport_cost -- cost_host[i] = <pi_i, c> = sum_{x,y} a_i(x) K(x,y) rho_b(x,y)^2 b_i(y) for the plan
+ *   pi = a K b of a scaling solution (R11; the transport term of the entropic W_2^2, P:186-195,
+ *   SURVEY NEXT #2) without materialising pi: one conv of b with the cost table K rho^2.  Under
+ *   SE2_LOG_DOMAIN a, b are logs.  Cost tables are built on the first call.
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_transport_cost(se2_kernel k, const float* a, const float* b, int32_t batch, uint32_t flags,
+                                      double* cost_host, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
  * Step-level entry points (used by the multi-GPU driver, which owns the loop and the collectives).
  * se2_conv_update: out = target (op) K in, fused in the conv epilogue:
  *   op = SE2_EPI_DIVIDE:   out = target / max(K in, 1e-30)     | log: out = target - LSE(in)
  *   op = SE2_EPI_MULTIPLY: out = target * (K in)               | log: out = target + LSE(in)
- *   op = SE2_EPI_PROX:     out = prox(K in)/K in  (entropy+potential, `prox` required; target unused)
+ *   op = SE2_EPI_PROX:     out = prox(K in)/K in  (JKO proxes, `prox` required; target unused)
  * target: device [batch][N] (log targets under SE2_LOG_DOMAIN).
  * ---------------------------------------------------------------------------------------- */
 #define SE2_EPI_DIVIDE 1

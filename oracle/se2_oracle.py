@@ -20,7 +20,7 @@ __all__ = [
     "Grid", "kernel_table", "log_kernel_table", "dense_kernel_matrix",
     "conv", "conv_adjoint", "lse_conv", "lse_conv_adjoint", "conv_point", "lse_conv_point",
     "conv_numpy", "sinkhorn", "barycenter", "jko", "jko_potential", "marginal_error",
-    "quarter_turn", "oracle_threads", "DIV_FLOOR",
+    "quarter_turn", "oracle_threads", "DIV_FLOOR", "porous_prox", "haar_cell", "cost_table", "transport_cost",
 ]
 
 DIV_FLOOR = 1e-30      # division guard (reading R9)
@@ -127,6 +127,18 @@ def kernel_table(grid: Grid, R: int, eps: float, w) -> np.ndarray:
 def log_kernel_table(grid: Grid, R: int, eps: float, w) -> np.ndarray:
     """L = -rho_b^2 / eps (log of kernel_table, evaluated directly, never via log(exp))."""
     return -_relative_rho2(grid, R, w) / eps
+
+
+def cost_table(grid: Grid, R: int, eps: float, w) -> np.ndarray:
+    """Tc = K * c with c = rho_b^2 (P:186-195 with d := rho_b, p = 2): the kernel of the transport cost."""
+    r2 = _relative_rho2(grid, R, w)
+    return np.exp(-r2 / eps) * r2
+
+
+def transport_cost(Tc, a, b) -> float:
+    """<pi, c> = sum_{g,h} a(g) K(g,h) c(g,h) b(h) for the plan pi = a K b (R11), i.e.
+    sum_g a(g) (Tc * b)(g) -- the plan is never materialised."""
+    return float(np.sum(np.asarray(a, dtype=np.float64) * conv(Tc, b)))
 
 
 def dense_kernel_matrix(grid: Grid, R: int, eps: float, w) -> np.ndarray:
@@ -391,8 +403,46 @@ def jko_potential(grid: Grid) -> np.ndarray:
     return np.broadcast_to(V, grid.shape).copy()
 
 
+def haar_cell(grid: Grid) -> float:
+    """Haar measure of one lattice cell, dx dy dtheta with the [0,1]^2 x [0,2pi) window (R1)."""
+    return (1.0 / grid.nx) * (1.0 / grid.ny) * (TWO_PI / grid.ntheta)
+
+
+def porous_prox(z, eps: float, tau: float, m: float, cell: float):
+    """KL-prox of the porous-medium energy F(mu) = 1/(m-1) int mu^m dH, mu a density w.r.t.
+    the Haar measure, discretised with masses s on cells of measure `cell` (density s/cell):
+        s = argmin_s (tau/eps) F(s) + KL(s | z),   F(s) = cell/(m-1) sum (s/cell)^m.
+    Stationarity per site: (tau m / (eps (m-1))) (s/cell)^{m-1} + log(s/z) = 0.  With u = log s:
+        g(u) = C e^{(m-1) u} + u - log z = 0,  C = tau m / (eps (m-1)) cell^{1-m},
+    g convex and increasing, root <= log z: Newton from u = log z (monotone), bisection fallback on
+    [log z - 50, log z].  s = 0 where z = 0."""
+    z = np.asarray(z, dtype=np.float64)
+    C = tau * m / (eps * (m - 1.0)) * cell ** (1.0 - m)
+    out = np.zeros_like(z)
+    pos = z > 0
+    lz = np.log(z[pos])
+    u = lz.copy()
+    for _ in range(200):
+        ex = C * np.exp((m - 1.0) * u)
+        du = (ex + u - lz) / ((m - 1.0) * ex + 1.0)
+        u = u - du
+        if np.all(np.abs(du) <= 1e-15 * (1.0 + np.abs(u))):
+            break
+    bad = ~np.isfinite(u) | (np.abs(C * np.exp((m - 1.0) * u) + u - lz) > 1e-12 * (1 + np.abs(lz)))
+    if np.any(bad):
+        lo, hi = lz[bad] - 50.0, lz[bad].copy()
+        for _ in range(200):
+            mid = 0.5 * (lo + hi)
+            gm = C * np.exp((m - 1.0) * mid) + mid - lz[bad]
+            hi = np.where(gm > 0, mid, hi)
+            lo = np.where(gm > 0, lo, mid)
+        u[bad] = 0.5 * (lo + hi)
+    out[pos] = np.exp(u)
+    return out
+
+
 def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, log_domain: bool,
-        trace: bool = True) -> Dict:
+        trace: bool = True, energy: str = "entropy_potential", m: float = 5.0) -> Dict:
     """Entropic JKO time-marching (eq. equ:GF_JKO) solved with the scaling iterations
     (eq. equ:scaling_iterations): F1 = marginal constraint mu_k (prox = mu_k),
     F2 = tau F with F(s) = sum s (log s - 1) + sum V s (entropy + linear potential, BASELINE
@@ -404,6 +454,8 @@ def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, l
     V = jko_potential(grid)
     p = tau / (eps + tau)
     q = tau / (eps + tau)
+    cell = haar_cell(grid)
+    porous = energy == "porous"
     mu = np.asarray(mu0, dtype=np.float64)
     masses, errs, mus = [], [], [mu]
     for _k in range(steps):
@@ -413,7 +465,10 @@ def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, l
             for _l in range(iters):
                 a = mu / np.maximum(conv(T, b), DIV_FLOOR)
                 z = np.maximum(conv_adjoint(T, a), DIV_FLOOR)
-                b = z ** (-p) * np.exp(-q * V)
+                if porous:
+                    b = porous_prox(z, eps, tau, m, cell) / z            # b = prox(z)/z
+                else:
+                    b = z ** (-p) * np.exp(-q * V)
                 if trace:
                     err.append(marginal_error(a, conv(T, b), mu))
             s = b * z
@@ -423,7 +478,10 @@ def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, l
             for _l in range(iters):
                 alpha = _ldiv(lmu, lse_conv(L, beta))
                 lz = lse_conv_adjoint(L, alpha)
-                beta = -p * lz - q * V
+                if porous:
+                    beta = np.log(porous_prox(np.exp(lz), eps, tau, m, cell)) - lz
+                else:
+                    beta = -p * lz - q * V
                 if trace:
                     err.append(float(np.sum(np.abs(np.exp(alpha + lse_conv(L, beta)) - mu))))
             s = np.exp(beta + lz)

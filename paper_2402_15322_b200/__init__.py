@@ -4,11 +4,12 @@ in include/se2ot.h, with this thin Python binding on top (argument marshalling o
 
     from paper_2402_15322_b200 import Kernel, se2_conv, se2_sinkhorn, se2_barycenter, ...
 """
-from .api import (Kernel, make_prox, se2_bary_logmean, se2_bary_update, se2_barycenter, se2_conv,
+from .api import (Kernel, make_porous_prox, make_prox, se2_bary_logmean, se2_bary_update, se2_barycenter, se2_conv,
                   se2_conv_update, se2_jko_step, se2_kernel_build, se2_launch_count, se2_marginal_error,
-                  se2_scale_rows, se2_sinkhorn, se2_sum, se2_sum_rows)
+                  se2_scale_rows, se2_sinkhorn, se2_sum, se2_sum_rows, se2_transport_cost)
 from ._lib import SE2Error, LIB_PATH
 
-__all__ = ["Kernel", "make_prox", "se2_bary_logmean", "se2_bary_update", "se2_barycenter", "se2_conv",
+__all__ = ["Kernel", "make_porous_prox", "make_prox", "se2_bary_logmean", "se2_bary_update", "se2_barycenter", "se2_conv",
            "se2_conv_update", "se2_jko_step", "se2_kernel_build", "se2_launch_count", "se2_marginal_error",
-           "se2_sinkhorn", "se2_sum", "se2_sum_rows", "se2_scale_rows", "SE2Error", "LIB_PATH"]
+           "se2_sinkhorn", "se2_sum", "se2_sum_rows", "se2_scale_rows", "se2_transport_cost", "SE2Error",
+           "LIB_PATH"]

@@ -22,6 +22,7 @@ SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3
 SE2_PROX_MARGINAL = 0
 SE2_PROX_ENTROPY_POTENTIAL = 1
+SE2_PROX_POROUS = 2
 
 STATUS_NAMES = {0: "SE2_OK", 1: "SE2_EINVAL", 2: "SE2_ENOMEM", 3: "SE2_ECUDA", 5: "SE2_ENONFINITE",
                 6: "SE2_EUNSUPPORTED", 100: "SE2_WKERNEL_TOO_WIDE"}
@@ -32,6 +33,7 @@ EXPORTED = [
     "se2_jko_step", "se2_barycenter", "se2_marginal_error", "se2_conv_update", "se2_bary_logmean",
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
     "se2_last_error", "se2_abi_version", "se2_lse_path_stats", "se2_sum_rows", "se2_scale_rows",
+    "se2_transport_cost",
 ]
 
 
@@ -57,7 +59,8 @@ class se2_kernel_stats(ctypes.Structure):
 
 class se2_prox(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("tau", ctypes.c_double), ("cx", ctypes.c_double),
-                ("cy", ctypes.c_double), ("hx", ctypes.c_double), ("hy", ctypes.c_double)]
+                ("cy", ctypes.c_double), ("hx", ctypes.c_double), ("hy", ctypes.c_double),
+                ("m", ctypes.c_double)]
 
 
 class se2_opts(ctypes.Structure):
@@ -88,6 +91,7 @@ def load(path: str = LIB_PATH):
         "se2_jko_step": [P, P, P, P, P, ctypes.POINTER(se2_prox), ctypes.POINTER(se2_opts), pd, pd, P],
         "se2_barycenter": [P, i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],
         "se2_marginal_error": [P, P, P, P, i32, u32, pd, P],
+        "se2_transport_cost": [P, P, P, i32, u32, pd, P],
         "se2_conv_update": [P, P, P, P, i32, i32, ctypes.POINTER(se2_prox), u32, P],
         "se2_bary_logmean": [i32, i64, P, pd, P, P],
         "se2_bary_update": [i32, i64, P, P, P, P],

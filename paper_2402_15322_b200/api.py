@@ -126,7 +126,14 @@ def make_prox(k: Kernel, tau: float, global_ny: Optional[int] = None, row_offset
     the centre row shifts by -row_offset (cells)."""
     gny = k.ny if global_ny is None else int(global_ny)
     return L.se2_prox(L.SE2_PROX_ENTROPY_POTENTIAL, float(tau), k.nx / 2.0, gny / 2.0 - row_offset,
-                      1.0 / k.nx, 1.0 / gny)
+                      1.0 / k.nx, 1.0 / gny, 0.0)
+
+
+def make_porous_prox(tau: float, m: float) -> L.se2_prox:
+    """Porous-medium prox of the paper's gradient flow, F = 1/(m-1) sum s^m."""
+    if not m > 1.0:
+        raise ValueError("porous-medium exponent m must be > 1")
+    return L.se2_prox(L.SE2_PROX_POROUS, float(tau), 0.0, 0.0, 0.0, 0.0, float(m))
 
 
 def se2_sinkhorn(k: Kernel, mu: torch.Tensor, nu: Optional[torch.Tensor], a: torch.Tensor, b: torch.Tensor,
@@ -198,6 +205,17 @@ def se2_marginal_error(k: Kernel, a: torch.Tensor, b: torch.Tensor, mu: torch.Te
     out = np.zeros(batch, dtype=np.float64)
     check(L.load().se2_marginal_error(k.handle, _ptr(a), _ptr(b), _ptr(mu), batch, _flags(log_domain),
                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(mu.device)))
+    return out
+
+
+def se2_transport_cost(k: Kernel, a: torch.Tensor, b: torch.Tensor, log_domain: bool) -> np.ndarray:
+    """<pi, rho_b^2> of the plan pi = a K b (one conv with the cost table; NEXT #2)."""
+    _check_field(a, k, "a")
+    batch = a.numel() // k.N
+    _check_field(b, k, "b", batch)
+    out = np.zeros(batch, dtype=np.float64)
+    check(L.load().se2_transport_cost(k.handle, _ptr(a), _ptr(b), batch, _flags(log_domain),
+                                      out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(a.device)))
     return out
 
 

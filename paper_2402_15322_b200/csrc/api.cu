@@ -215,6 +215,8 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->LseS) cudaFree(k->LseS);
     if (k->Lq) cudaFree(k->Lq);
     if (k->Wl) cudaFree(k->Wl);
+    if (k->Wcl) cudaFree(k->Wcl);
+    if (k->Lcq) cudaFree(k->Lcq);
     if (k->lstats) cudaFree(k->lstats);
     if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
@@ -242,6 +244,13 @@ se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, ui
 }
 
 static void fill_prox(Epilogue& epi, const se2_kernel_s* k, const se2_prox* prox) {
+    epi.prox_kind = prox->kind;
+    if (prox->kind == SE2_PROX_POROUS) {
+        // C = tau m / (eps (m-1)) cell^{1-m}: the energy acts on the density s / cell, cell = dx dy dtheta
+        const double cell = k->hx * k->hy * (6.283185307179586476925286766559 / k->nt);
+        epi.prox_c = (float)(prox->tau * prox->m / (k->eps * (prox->m - 1.0)) * pow(cell, 1.0 - prox->m));
+        epi.prox_m1 = (float)(prox->m - 1.0);
+    }
     const double p = prox->tau / (k->eps + prox->tau);
     epi.prox_p = (float)p;
     epi.prox_q = (float)p;
@@ -258,7 +267,10 @@ se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, f
     SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
     SE2_CHECK_ARG(op == SE2_EPI_DIVIDE || op == SE2_EPI_MULTIPLY || op == SE2_EPI_PROX, "bad epilogue op");
     SE2_CHECK_ARG(op == SE2_EPI_PROX || target != nullptr, "target required");
-    SE2_CHECK_ARG(op != SE2_EPI_PROX || (prox != nullptr && prox->tau >= 0), "prox required");
+    SE2_CHECK_ARG(op != SE2_EPI_PROX || (prox != nullptr && prox->tau >= 0 &&
+                                         (prox->kind == SE2_PROX_ENTROPY_POTENTIAL ||
+                                          (prox->kind == SE2_PROX_POROUS && prox->m > 1.0))),
+                  "JKO prox required (entropy+potential, or porous with m > 1)");
     DeviceGuard g(k->device);
     Epilogue epi;
     epi.op = op;
@@ -274,7 +286,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
                                 float* s_out, cudaStream_t s) {
     const bool LOG = (opts->flags & SE2_LOG_DOMAIN) != 0;
     const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
-    const bool jko = prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL;
+    const bool jko = prox != nullptr && (prox->kind == SE2_PROX_ENTROPY_POTENTIAL || prox->kind == SE2_PROX_POROUS);
     const int64_t N = k->N();
     const int64_t BN = (int64_t)batch * N;
     const int iters = opts->iters;
@@ -374,9 +386,11 @@ se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required, iters >= 0");
     SE2_CHECK_ARG(mu && a && b && a != b, "mu, a, b must be non-null distinct device pointers");
-    const bool jko = prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL;
+    const bool jko = prox != nullptr && (prox->kind == SE2_PROX_ENTROPY_POTENTIAL || prox->kind == SE2_PROX_POROUS);
     SE2_CHECK_ARG(jko || nu != nullptr, "nu required for the marginal prox");
-    SE2_CHECK_ARG(prox == nullptr || prox->kind == SE2_PROX_MARGINAL || (jko && prox->tau >= 0), "bad prox");
+    SE2_CHECK_ARG(prox == nullptr || prox->kind == SE2_PROX_MARGINAL ||
+                      (jko && prox->tau >= 0 && (prox->kind != SE2_PROX_POROUS || prox->m > 1.0)),
+                  "bad prox");
     SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
@@ -391,8 +405,9 @@ se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* 
                         const se2_opts* opts, double* mass_host, double* err_trace_host, se2_stream stream) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 1, "opts required, iters >= 1");
-    SE2_CHECK_ARG(prox != nullptr && prox->kind == SE2_PROX_ENTROPY_POTENTIAL && prox->tau >= 0,
-                  "entropy-potential prox required");
+    SE2_CHECK_ARG(prox != nullptr && prox->tau >= 0 &&
+                      (prox->kind == SE2_PROX_ENTROPY_POTENTIAL || (prox->kind == SE2_PROX_POROUS && prox->m > 1.0)),
+                  "JKO prox required (entropy+potential, or porous with m > 1)");
     SE2_CHECK_ARG(mu_k && mu_next && a && b && mu_k != mu_next, "bad pointers");
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
@@ -550,6 +565,59 @@ se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, cons
     double* tr = reinterpret_cast<double*>(x->trace.ptr);
     SE2_CUDA_TRY(launch_reduce_partials(e.err_partial, batch, bpf, tr, s));
     SE2_CUDA_TRY(cudaMemcpyAsync(err_host, tr, sizeof(double) * batch, cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    return SE2_OK;
+}
+
+se2_status se2_transport_cost(se2_kernel k, const float* a, const float* b, int32_t batch, uint32_t flags,
+                              double* cost_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(a && b && cost_host, "null pointer");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool LOG = (flags & SE2_LOG_DOMAIN) != 0;
+    if (k->Wcl == nullptr) {
+        const size_t tabl = (size_t)k->nt * k->nt * k->S * ((k->S + 3) / 4 * 4) * sizeof(float);
+        const size_t tab = (size_t)((k->nt + 3) / 4) * k->nt * k->S * k->S * 4 * sizeof(float);
+        cudaError_t e = cudaMalloc(&k->Wcl, tabl);
+        if (e == cudaSuccess) e = cudaMalloc(&k->Lcq, tab);
+        if (e == cudaSuccess) e = cudaMemsetAsync(k->Wcl, 0, tabl, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(k->Lcq, 0xff, tab, s);   // NaN pattern; overwritten below
+        if (e == cudaSuccess) e = tabulate_cost(k, s);
+        if (e != cudaSuccess) {
+            set_error(std::string("cost tables: ") + cudaGetErrorString(e));
+            return SE2_ENOMEM;
+        }
+        // quad padding (to >= nt) must not produce NaN in the log engine: set it to -inf
+        if (k->nt % 4 != 0) {
+            std::vector<float> h(tab / sizeof(float));
+            SE2_CUDA_TRY(cudaMemcpyAsync(h.data(), k->Lcq, tab, cudaMemcpyDeviceToHost, s));
+            SE2_CUDA_TRY(cudaStreamSynchronize(s));
+            for (float& v : h)
+                if (v != v) v = -INFINITY;
+            SE2_CUDA_TRY(cudaMemcpyAsync(k->Lcq, h.data(), tab, cudaMemcpyHostToDevice, s));
+        }
+        k->table_bytes += tabl + tab;
+    }
+    KernelExtra* x = extra(k);
+    const int bpf = LOG ? conv_blocks_per_field_lse(k) : conv_blocks_per_field_linear(k);
+    se2_status st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
+    if (st != SE2_OK) return st;
+    st = ensure(x->trace, (size_t)batch * sizeof(double));
+    if (st != SE2_OK) return st;
+    Epilogue e;
+    e.op = EPI_DOT;
+    e.table = LOG ? k->Lcq : k->Wcl;
+    e.err_a = a;
+    e.err_partial = reinterpret_cast<float*>(x->partial.ptr);
+    // cost = sum_x a(x) sum_y K(x,y) rho^2(x,y) b(y): one conv of b with the cost table (the log domain
+    // uses the exact per-tap engine: the cost table has no theta-factored form)
+    st = run_conv(k, b, batch, LOG ? (flags | SE2_LSE_EXACT) : flags, e, s, nullptr);
+    if (st != SE2_OK) return st;
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    SE2_CUDA_TRY(launch_reduce_partials(e.err_partial, batch, bpf, tr, s));
+    SE2_CUDA_TRY(cudaMemcpyAsync(cost_host, tr, sizeof(double) * batch, cudaMemcpyDeviceToHost, s));
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
     return SE2_OK;
 }

@@ -93,6 +93,7 @@ __device__ __forceinline__ float block_sum(float v, float* red /* >= NT/32 float
 template <bool LOG>
 __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, int ix, int iy, float y) {
     float err = 0.f;
+    if (e.op == EPI_DOT) return LOG ? expf(e.err_a[idx] + y) : e.err_a[idx] * y;
     if (e.err_a != nullptr) {
         float a_old = e.err_a[idx];
         float mu = e.err_mu[idx];
@@ -112,6 +113,23 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
             break;
         case EPI_MULTIPLY: o = LOG ? (e.target[idx] + y) : (e.target[idx] * y); break;
         case EPI_PROX: {
+            if (e.prox_kind == 2) {
+                // porous medium: u = log s solves c e^{(m-1) u} + u - log z = 0; Newton from
+                // u = log z (the root is <= log z; g is convex increasing, so the iterates decrease
+                // monotonically to it)
+                const float lz = LOG ? y : logf(fmaxf(y, kDivFloor));
+                float u = lz;
+                for (int it = 0; it < 60; ++it) {
+                    const float ex = e.prox_c * expf(e.prox_m1 * u);
+                    const float g = ex + u - lz;
+                    const float du = g / (e.prox_m1 * ex + 1.f);
+                    u -= du;
+                    if (fabsf(du) <= 1e-7f * (1.f + fabsf(u))) break;
+                }
+                o = LOG ? (u - lz) : expf(u - lz);
+                if (e.out2 != nullptr) e.out2[idx] = expf(u);
+                break;
+            }
             float dxp = ((float)ix + 0.5f - e.cx) * e.hx, dyp = ((float)iy + 0.5f - e.cy) * e.hy;
             float V = dxp * dxp + dyp * dyp;
             if (LOG) {

@@ -199,13 +199,13 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
         e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)CT::SMEM_TMA);
         if (e != cudaSuccess) return e;
-        conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, CT::SMEM_TMA, s>>>(in, k->Wl, k->nx, k->ny, k->nt, k->band,
+        conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, CT::SMEM_TMA, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
                                                                             tiles_x, epi, tmap);
     } else {
         e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        conv_linear_kernel<R, kLinWX, false><<<grid, C::NT, C::SMEM, s>>>(in, k->Wl, k->nx, k->ny, k->nt, k->band,
+        conv_linear_kernel<R, kLinWX, false><<<grid, C::NT, C::SMEM, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
                                                                          tiles_x, epi, tmap);
     }
     count_launch();

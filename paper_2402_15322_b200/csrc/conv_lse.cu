@@ -208,7 +208,7 @@ static cudaError_t launch_lse_r(const se2_kernel_s* k, const float* in, int batc
     int tiles_y = (k->ny + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, (k->nt + 3) / 4, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_lse_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Lq, k->nx, k->ny, k->nt, tiles_x, epi);
+    conv_lse_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, epi.table ? epi.table : k->Lq, k->nx, k->ny, k->nt, tiles_x, epi);
     count_launch();
     return cudaGetLastError();
 }

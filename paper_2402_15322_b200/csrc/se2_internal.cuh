@@ -50,11 +50,13 @@ enum EpiOp : int {
     EPI_MULTIPLY = 2,   // out = target * y               | log: target + ly
     EPI_PROX = 3,       // out = max(y,floor)^-p exp(-q V) | log: -p ly - q V
     EPI_ERRONLY = 4,    // no store; only the marginal-error partial
+    EPI_DOT = 5,        // no store; partial += a * y (log: exp(alpha + ly)) -- transport cost
 };
 
 // Everything an epilogue needs; plain-old-data passed by value to the kernels.
 struct Epilogue {
     int op = EPI_STORE;
+    const float* table = nullptr;    // table override (cost tables); null = the kernel's Gibbs tables
     const float* target = nullptr;   // [batch][N]
     float* out = nullptr;            // [batch][N]
     float* out2 = nullptr;           // EPI_PROX only: s = prox(z) = b * z (or its log-domain form exp(beta + lz))
@@ -63,7 +65,9 @@ struct Epilogue {
     const float* err_mu = nullptr;   // [batch][N] linear mu
     float* err_partial = nullptr;    // [batch][blocks_per_field]
     // prox (entropy + potential): p = tau/(eps+tau) exponent, q = tau/(eps+tau) potential factor
+    int prox_kind = 1;               // 1 entropy + potential, 2 porous medium
     float prox_p = 0.f, prox_q = 0.f;
+    float prox_c = 0.f, prox_m1 = 0.f; // porous: c = tau m / (eps (m-1)), m1 = m - 1
     float cx = 0.f, cy = 0.f, hx = 0.f, hy = 0.f;
 };
 
@@ -90,6 +94,8 @@ struct se2_kernel_s {
     float* LseS = nullptr;  // [nt][nt] log sum_taps exp(Ls)
     float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
     float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
+    float* Wcl = nullptr;   // cost tables (built on first se2_transport_cost): rho^2 exp(-rho^2/eps), Wl layout
+    float* Lcq = nullptr;   //   and log2(rho^2) + L2, Lq layout
     size_t table_bytes = 0;
     void* extra = nullptr;        // grow-only workspaces (api.cu)
     float* lstats = nullptr;      // [max_batch][nt][tiles][8] per-tile plane fit + ranges of log fields (K3)
@@ -115,6 +121,7 @@ size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch);
 
 // tabulation (tabulate.cu)
 cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s);
+cudaError_t tabulate_cost(se2_kernel_s* k, cudaStream_t s);
 
 // elementwise / reductions (elementwise.cu)
 cudaError_t launch_fill(float* x, int64_t n, float v, cudaStream_t s);

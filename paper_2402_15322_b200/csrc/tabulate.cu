@@ -84,6 +84,47 @@ __global__ void tabulate_theta_kernel(double hx, double hy, int nt, int R, doubl
     LseS[p] = (float)log(acc);
 }
 
+// cost-weighted tables for the transport cost <pi, rho^2>: Wc = rho^2 exp(-rho^2/eps)
+// (linear layout) and Lc2 = (log(rho^2) - rho^2/eps) log2(e) (quad layout; -inf where rho = 0)
+__global__ void tabulate_cost_kernel(double hx, double hy, int nt, int R, double eps, double w1, double w2, double w3,
+                                     float* __restrict__ Wcl, float* __restrict__ Lcq) {
+    const int S = 2 * R + 1;
+    const int SP = (S + 3) / 4 * 4;
+    const int64_t total = (int64_t)nt * nt * S * S;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int dxi = (int)(idx % S);
+        int dyi = (int)((idx / S) % S);
+        int ti = (int)((idx / ((int64_t)S * S)) % nt);
+        int to = (int)(idx / ((int64_t)S * S * nt));
+        const double two_pi = 6.283185307179586476925286766559;
+        double ddx = (double)(dxi - R) * hx, ddy = (double)(dyi - R) * hy;
+        double thi = two_pi * ti / nt;
+        double ci = cos(thi), si = sin(thi);
+        double X = ci * ddx + si * ddy, Y = -si * ddx + ci * ddy;
+        int kk = ((to - ti) % nt + nt) % nt;
+        if (2 * kk >= nt) kk -= nt;
+        double Th = two_pi * kk / nt;
+        double ch = cos(0.5 * Th), sh = sin(0.5 * Th);
+        double b1 = X * ch + Y * sh, b2 = -X * sh + Y * ch;
+        double rho2 = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2 + w3 * w3 * Th * Th;
+        Wcl[(((int64_t)to * nt + ti) * S + dyi) * SP + dxi] = (float)(rho2 * exp(-rho2 / eps));
+        int qd = to >> 2, q = to & 3;
+        int64_t o = ((((int64_t)qd * nt + ti) * S + dyi) * S + dxi) * 4 + q;
+        Lcq[o] = rho2 > 0.0 ? (float)((log(rho2) - rho2 / eps) * 1.4426950408889634073599246810019) : -INFINITY;
+    }
+}
+
+cudaError_t tabulate_cost(se2_kernel_s* k, cudaStream_t s) {
+    const int64_t total = (int64_t)k->nt * k->nt * k->S * k->S;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    tabulate_cost_kernel<<<blocks, 256, 0, s>>>(k->hx, k->hy, k->nt, k->R, k->eps, k->w1, k->w2, k->w3, k->Wcl,
+                                                 k->Lcq);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     const int nt = k->nt, S = k->S;
     const int64_t total = (int64_t)nt * nt * S * S;

@@ -223,6 +223,9 @@ class ParityCase:
     iters: int
     jko_steps: int = 0
     full_fields: bool = True   # store whole fields (else sampled entries)
+    energy: str = "entropy_potential"   # JKO energy: BASELINE configs[4], or the paper's porous medium
+    m: float = 5.0                      # porous-medium exponent
+    w: Optional[Tuple[float, float, float]] = None   # metric override
 
 
 PARITY_CASES: List[ParityCase] = [
@@ -234,6 +237,9 @@ PARITY_CASES: List[ParityCase] = [
     ParityCase("c3m", "c3", 44, 40, 32, 10, 40),
     ParityCase("c4p", "c4", 256, 256, 64, 15, 2, jko_steps=1, full_fields=False),
     ParityCase("c4m", "c4", 72, 60, 16, 4, 200, jko_steps=3),
+    # NEXT #1: the paper's own gradient flow -- porous medium m = 5, w = (1, sqrt 10, sqrt 2)
+    ParityCase("c5m", "c4", 64, 56, 16, 4, 100, jko_steps=2, energy="porous", m=5.0,
+               w=(1.0, math.sqrt(10.0), math.sqrt(2.0))),
 ]
 
 
@@ -250,7 +256,8 @@ def parity_inputs(pc: ParityCase):
     base = get_config(pc.base)
     cfg = dataclasses.replace(base, name=base.name, nx=pc.nx, ny=pc.ny, ntheta=pc.ntheta,
                               support=2 * pc.R + 1, iters=pc.iters,
-                              jko_steps=pc.jko_steps if pc.jko_steps else base.jko_steps)
+                              jko_steps=pc.jko_steps if pc.jko_steps else base.jko_steps,
+                              w=pc.w if pc.w is not None else base.w)
     return cfg, config_inputs(cfg)
 
 

@@ -57,7 +57,8 @@ def make(pc):
         out["err"] = np.stack([r["err"] for r in res], axis=1)          # [iters][nsolve]
         out["errs"] = np.stack([r["errs"] for r in res], axis=1)        # [iters][nsolve][n]
     elif cfg.problem == "jko":
-        r = O.jko(T, L, mus[0], g, cfg.eps, cfg.tau, cfg.jko_steps, cfg.iters, cfg.log_domain)
+        r = O.jko(T, L, mus[0], g, cfg.eps, cfg.tau, cfg.jko_steps, cfg.iters, cfg.log_domain,
+                  energy=pc.energy, m=pc.m)
         _store(out, "mus", r["mus"], pc, idx)
         out["masses"] = r["masses"]
         out["err"] = r["err"]

@@ -273,3 +273,21 @@ def test_bary_pieces(cuda_device):
     lv_t = _dev(lv)
     se2_bary_update(lv_t, _dev(ld), lbar, 3, N)
     np.testing.assert_allclose(_host(lv_t), lv + (ref[None] - ld), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
+@pytest.mark.parametrize("grid", [(28, 28, 16, 0.02, (1.0, 3.0, 1.0), 5), (37, 23, 12, 0.02, (1.0, 3.0, 1.0), 5)],
+                         ids=["c1grid", "ragged"])
+def test_transport_cost(grid, log_domain, cuda_device):
+    from paper_2402_15322_b200 import se2_transport_cost
+    nx, ny, nt, eps, w, R = grid
+    k = _kernel(nx, ny, nt, eps, w, R, 2)
+    g = O.Grid(nx, ny, nt)
+    shape = (2, nt, ny, nx)
+    a = S.random_positive_field(shape, seed=41, log_range=10.0)
+    b = S.random_positive_field(shape, seed=42, log_range=10.0)
+    ain, bin_ = (np.log(a), np.log(b)) if log_domain else (a, b)
+    got = se2_transport_cost(k, _dev(ain), _dev(bin_), log_domain)
+    Tc = O.cost_table(g, R, eps, w)
+    ref = [O.transport_cost(Tc, a[i].astype(np.float64), b[i].astype(np.float64)) for i in range(2)]
+    np.testing.assert_allclose(got, ref, rtol=2e-5)

@@ -110,14 +110,14 @@ def test_barycenter_parity(case, cuda_device):
     assert trace_err(tr, gold["err"]) <= TOL_TRACE
 
 
-@pytest.mark.parametrize("case", ["c4m", "c4p"])
+@pytest.mark.parametrize("case", ["c4m", "c4p", "c5m"])
 def test_jko_parity(case, cuda_device):
-    from paper_2402_15322_b200 import make_prox, se2_jko_step
+    from paper_2402_15322_b200 import make_porous_prox, make_prox, se2_jko_step
     pc = S.get_parity_case(case)
     cfg, d = S.parity_inputs(pc)
     gold = _golden(case)
     k = _kernel(cfg, 1)
-    prox = make_prox(k, cfg.tau)
+    prox = make_porous_prox(cfg.tau, pc.m) if pc.energy == "porous" else make_prox(k, cfg.tau)
     mu = _dev(d["mus"][0])
     nxt = torch.empty_like(mu)
     a = torch.empty_like(mu)

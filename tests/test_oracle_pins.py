@@ -408,3 +408,76 @@ def test_jko_prox_stationarity_mass_equivariance():
     np.testing.assert_allclose(rl["mus"], rn["mus"], rtol=1e-10)
     rq = O.jko(T, L, O.quarter_turn(mu), g, eps=eps, tau=tau, steps=2, iters=40, log_domain=False)
     np.testing.assert_allclose(rq["mus"][2], O.quarter_turn(rn["mus"][2]), rtol=1e-10)
+
+
+# ---------------------------------------------------------------- porous-medium prox --
+def test_porous_prox_stationarity_and_brute_force():
+    """KL-prox of F = cell/(m-1) sum (s/cell)^m: the stationarity residual vanishes, it agrees with a
+    direct scalar minimisation of the per-site objective, tau -> 0 gives s = z, z = 0 gives s = 0."""
+    from scipy.optimize import minimize_scalar
+    eps, tau, m, cell = 0.003, 1e-3, 5.0, 1e-3
+    rng = np.random.default_rng(13)
+    z = np.concatenate([[0.0, 1e-8, 1e-4], rng.uniform(1e-5, 0.5, 20)])
+    s = O.porous_prox(z, eps, tau, m, cell)
+    assert s[0] == 0.0
+    pos = z > 0
+    C = tau * m / (eps * (m - 1)) * cell ** (1 - m)
+    res = C * s[pos] ** (m - 1) + np.log(s[pos] / z[pos])
+    assert np.abs(res).max() < 1e-12
+    assert np.all(s[pos] <= z[pos])
+    for zi, si in zip(z[pos][:8], s[pos][:8]):
+        f = lambda x: (tau / eps) * cell / (m - 1) * (x / cell) ** m + x * np.log(x / zi) - x + zi
+        r = minimize_scalar(f, bounds=(1e-300, zi), method="bounded", options={"xatol": 1e-18})
+        assert abs(r.x - si) <= 1e-6 * si
+    np.testing.assert_allclose(O.porous_prox(z, eps, 1e-24, m, cell), z, rtol=1e-9)   # tau -> 0
+    # monotone in z
+    zz = np.linspace(1e-6, 1, 200)
+    assert np.all(np.diff(O.porous_prox(zz, eps, tau, m, cell)) > 0)
+
+
+def test_jko_porous_mass_equivariance():
+    g = O.Grid(8, 8, 8)
+    eps, tau = 0.05, 0.02
+    T = O.kernel_table(g, 2, eps, (1, np.sqrt(10), np.sqrt(2)))
+    L = O.log_kernel_table(g, 2, eps, (1, np.sqrt(10), np.sqrt(2)))
+    rng = np.random.default_rng(14)
+    mu = rng.random(g.shape) ** 3 + 0.01
+    mu /= mu.sum()
+    r = O.jko(T, L, mu, g, eps, tau, 1, 300, False, energy="porous", m=5.0)
+    assert r["err"][0][-1] < 1e-9
+    assert abs(r["masses"][0] - 1.0) < 1e-8
+    rl = O.jko(T, L, mu, g, eps, tau, 2, 30, True, energy="porous", m=5.0, trace=False)
+    rn = O.jko(T, L, mu, g, eps, tau, 2, 30, False, energy="porous", m=5.0, trace=False)
+    np.testing.assert_allclose(rl["mus"], rn["mus"], rtol=1e-10)
+    rq = O.jko(T, L, O.quarter_turn(mu), g, eps, tau, 2, 30, False, energy="porous", m=5.0, trace=False)
+    np.testing.assert_allclose(rq["mus"][2], O.quarter_turn(rn["mus"][2]), rtol=1e-10)
+    r0 = O.jko(T, L, mu, g, eps, 0.0, 1, 3, False, energy="porous", m=5.0, trace=False)
+    blur = O.conv(T, mu / O.conv(T, np.ones(g.shape)))
+    np.testing.assert_allclose(r0["mus"][1], blur / blur.sum(), rtol=1e-12)
+
+
+# ---------------------------------------------------------------- transport cost (P:186-195) -------
+def test_transport_cost_two_diracs_and_dense():
+    """Two Diracs: the only coupling is delta x delta, so <pi, c> = rho_b(h^{-1} g)^2 exactly (group law);
+    random scalings: equals the dense double sum a K c b."""
+    g = O.Grid(8, 8, 8)
+    R, eps, w = 3, 0.05, (1, 3, 1)
+    T = O.kernel_table(g, R, eps, w)
+    L = O.log_kernel_table(g, R, eps, w)
+    Tc = O.cost_table(g, R, eps, w)
+    mu = np.zeros(g.shape)
+    mu[1, 3, 2] = 1
+    nu = np.zeros(g.shape)
+    nu[2, 5, 4] = 1
+    r = O.sinkhorn(T, L, mu, nu, 3, log_domain=False, trace=False)
+    ge, he = g.element(1, 3, 2), g.element(2, 5, 4)
+    expect = O.rho_b(O.se2_mul(O.se2_inv(he), ge), w) ** 2
+    assert abs(O.transport_cost(Tc, r["a"], r["b"]) - expect) < 1e-12 * expect
+    K = O.dense_kernel_matrix(g, R, eps, w)
+    N = K.shape[0]
+    E = g.element(*np.meshgrid(np.arange(8), np.arange(8), np.arange(8), indexing="ij")).reshape(-1, 3)
+    C = O.rho_b(O.se2_mul(O.se2_inv(E[None, :, :]), E[:, None, :]), w) ** 2
+    rng = np.random.default_rng(15)
+    a, b = rng.random(g.shape), rng.random(g.shape)
+    dense = a.reshape(-1) @ ((K * C) @ b.reshape(-1))
+    assert abs(O.transport_cost(Tc, a, b) - dense) < 1e-12 * dense
