@@ -93,7 +93,8 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
         e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->lstats,
-                                 (flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0), k->lse_counters);
+                                 (flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0), k->lse_counters,
+                                 k->split, k->split_floats);
     if (e != cudaSuccess) {
         set_error(std::string("conv launch: ") + cudaGetErrorString(e));
         return SE2_ECUDA;
@@ -174,6 +175,14 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
         cudaError_t e2 = cudaMalloc(&k->lstats, sizeof(float) * nst);
         if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(long long) * 4);
         if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(long long) * 4);
+        // theta_i-split scratch for grids that give fewer than 2 CTAs per SM (at most 8 groups, 64 MB)
+        {
+            const int64_t N = k->N();
+            size_t want = (size_t)max_batch * N * 8;
+            if (want * sizeof(float) > ((size_t)64 << 20)) want = ((size_t)64 << 20) / sizeof(float);
+            if (e2 == cudaSuccess) e2 = cudaMalloc(&k->split, sizeof(float) * want);
+            k->split_floats = want;
+        }
         if (e2 != cudaSuccess) {
             set_error(std::string("scratch allocation: ") + cudaGetErrorString(e2));
             se2_kernel_destroy(k);
@@ -218,6 +227,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->Wcl) cudaFree(k->Wcl);
     if (k->Lcq) cudaFree(k->Lcq);
     if (k->lstats) cudaFree(k->lstats);
+    if (k->split) cudaFree(k->split);
     if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
     if (x) {
@@ -454,7 +464,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     const int iters = opts->iters;
     KernelExtra* x = extra(k);
     // workspace: mu_rep [F][N] (linear), lmu_rep [F][N], v [F][N], w [F][N], d [F][N]
-    size_t need = (size_t)5 * FN * sizeof(float);
+    size_t need = (size_t)6 * FN * sizeof(float);
     se2_status st = ensure(x->ws, need);
     if (st != SE2_OK) return st;
     float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
@@ -462,6 +472,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     float* v = v_state ? v_state : lmu_rep + FN;
     float* w = w_state ? w_state : lmu_rep + 2 * FN;
     float* d = lmu_rep + 3 * FN;
+    float* v_lo = lmu_rep + 4 * FN;   // compensation of the running sum log v (log domain)
     for (int sv = 0; sv < nsolve; ++sv)
         SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
                                      cudaMemcpyDeviceToDevice, s));
@@ -487,6 +498,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     double* tr = reinterpret_cast<double*>(x->trace.ptr);
 
     SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
+    SE2_CUDA_TRY(launch_fill(v_lo, FN, 0.f, s));
     SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
     for (int j = 0; j < iters; ++j) {
         // w_i = mu_i / K v_i   (fused: error of the previous v-update, sum |w_i K v_i - mu_i|)
@@ -512,7 +524,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
         if (LOG) {
             SE2_CUDA_TRY(launch_bary_logmean(n, nsolve, N, d, lam_dev, bary, s));
-            SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, d, bary, s));
+            SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, v_lo, d, bary, s));
         } else {
             SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
         }
@@ -638,7 +650,7 @@ se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const double*
 
 se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar, se2_stream stream) {
     SE2_CHECK_ARG(n >= 1 && N >= 1 && lv && ld && lbar, "bad arguments");
-    SE2_CUDA_TRY(launch_bary_update_log(n, 1, N, lv, ld, lbar, (cudaStream_t)stream));
+    SE2_CUDA_TRY(launch_bary_update_log(n, 1, N, lv, nullptr, ld, lbar, (cudaStream_t)stream));
     return SE2_OK;
 }
 

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(LseFCfg<R>::NT)
 conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq, const float* __restrict__ Lq,
                      const float* __restrict__ Lth, const float* __restrict__ LseS, const float* __restrict__ st,
                      int nx, int ny, int nt, int tiles_x, int tiles_y, int force_exact, Epilogue epi,
-                     int* __restrict__ counters) {
+                     int* __restrict__ counters, int ngroups, float* __restrict__ split_out) {
     using C = LseFCfg<R>;
     extern __shared__ __align__(16) float smem[];
     float* sWin = smem;
@@ -164,7 +164,10 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     __shared__ float sRef;
 
     const int tile = blockIdx.x;
-    const int qd = blockIdx.y;
+    // theta_i split (small grids): blockIdx.y = qd * ngroups + group; the CTA handles the input
+    // orientations ti with ti % ngroups == group and writes its partial log-sum to split_out
+    const int qd = blockIdx.y / ngroups;
+    const int grp = blockIdx.y - qd * ngroups;
     const int b = blockIdx.z;
     const int ntile = tiles_x * tiles_y;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -267,7 +270,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         int n = 0, nf = 0, ntl = 0;
         for (int i = 0; i < nt; ++i) {
             int s = sList[i];
-            if (s) {
+            if (s && (i % ngroups) == grp) {
                 sList[n++] = i | (s << 16);
                 nf += (s == 1 || s == 3);
                 ntl += (s == 3);
@@ -282,7 +285,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     if (counters != nullptr && threadIdx.x == 0) {
         atomicAdd(&counters[0], nact);
         atomicAdd(&counters[1], sNFast);
-        atomicAdd(&counters[2], nt);
+        atomicAdd(&counters[2], grp == 0 ? nt : 0);   // visited pairs: once per (tile, quad)
     }
 
     for (int i = threadIdx.x; i < 2 * C::WIN_H; i += C::NT) {
@@ -558,8 +561,54 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                                    ? NEG_INF
                                    : ref + (Macc[q][p] + log2f(Sacc[q][p])) * kLn2;
                     int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
-                    err += apply_epilogue<true>(epi, idx, gx, gy, ly);
+                    if (ngroups > 1)
+                        split_out[(int64_t)grp * gridDim.z * N + idx] = ly;   // partial: combined later
+                    else
+                        err += apply_epilogue<true>(epi, idx, gx, gy, ly);
                 }
+            }
+        }
+    }
+    if (ngroups == 1 && epi.err_partial != nullptr) {
+        float t = block_sum<C::NT>(err, sRed);
+        if (threadIdx.x == 0)
+            epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
+// Same (tile, quad) blocks and thread -> output mapping as the main kernel, so the error partials have
+// the unsplit layout.
+template <int R>
+__global__ void __launch_bounds__(LseFCfg<R>::NT)
+lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x,
+                         Epilogue epi) {
+    using C = LseFCfg<R>;
+    __shared__ float sRed[C::NT / 32];
+    const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
+    const int x0 = (tile % tiles_x) * C::TX, y0 = (tile / tiles_x) * C::TY;
+    const int64_t N = (int64_t)nx * ny * nt;
+    const int64_t GN = (int64_t)gridDim.z * N;
+    const int lane = threadIdx.x & 31, wx = threadIdx.x >> 5;
+    float err = 0.f;
+    const int gy = y0 + lane;
+    if (gy < ny) {
+        for (int q = 0; q < 4; ++q) {
+            const int to = 4 * qd + q;
+            if (to >= nt) continue;
+            for (int p = 0; p < C::P; ++p) {
+                const int gx = x0 + wx * C::P + p;
+                if (gx >= nx) continue;
+                const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
+                float m = -INFINITY;
+                for (int g = 0; g < ngroups; ++g) m = fmaxf(m, part[g * GN + idx]);
+                float ly = m;
+                if (m != -INFINITY) {
+                    float s = 0.f;
+                    for (int g = 0; g < ngroups; ++g) s += expf(part[g * GN + idx] - m);
+                    ly = m + logf(s);
+                }
+                err += apply_epilogue<true>(epi, idx, gx, gy, ly);
             }
         }
     }
@@ -572,7 +621,8 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
 
 template <int R>
 static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters) {
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters,
+                                 float* split_scratch, size_t split_floats) {
     using C = LseFCfg<R>;
     const int tiles_x = (k->nx + C::TX - 1) / C::TX;
     const int tiles_y = (k->ny + C::TY - 1) / C::TY;
@@ -586,11 +636,25 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     cudaError_t e = cudaFuncSetAttribute(conv_lse_fast_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    dim3 grid(ntile, (k->nt + 3) / 4, batch);
-    if (bpf) *bpf = (int)(grid.x * grid.y);
+    const int nquad = (k->nt + 3) / 4;
+    // small grids: split the input orientations over `groups` CTAs per (tile, quad) so that at least
+    // ~2 CTAs per SM exist (the per-channel loop of one CTA is latency-bound), then combine
+    const int base_ctas = ntile * nquad * batch;
+    int groups = 1;
+    if (base_ctas < 2 * 148) groups = (2 * 148 + base_ctas - 1) / base_ctas;
+    if (groups > k->nt) groups = k->nt;
+    if (groups > 1 && (size_t)groups * batch * k->N() > split_floats) groups = 1;
+    if (bpf) *bpf = ntile * nquad;
+    dim3 grid(ntile, nquad * groups, batch);
     conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->Lth, k->LseS, stats, k->nx, k->ny,
-                                                          k->nt, tiles_x, tiles_y, force_exact, epi, counters);
+                                                          k->nt, tiles_x, tiles_y, force_exact, epi, counters,
+                                                          groups, split_scratch);
     count_launch();
+    if (groups > 1) {
+        dim3 g2(ntile, nquad, batch);
+        lse_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi);
+        count_launch();
+    }
     return cudaGetLastError();
 }
 
@@ -607,11 +671,12 @@ int conv_blocks_per_field_lse_fast(const se2_kernel_s* k) {
 }
 
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters) {
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters,
+                                 float* split_scratch, size_t split_floats) {
     if (k->nt > LseFCfg<1>::MAXNT) return cudaErrorInvalidValue;
     switch (k->R) {
 #define SE2_CASE(r) \
-    case r: return launch_lsef_r<r>(k, in, batch, epi, s, bpf, stats, force_exact, counters);
+    case r: return launch_lsef_r<r>(k, in, batch, epi, s, bpf, stats, force_exact, counters, split_scratch, split_floats);
         SE2_CASE(0) SE2_CASE(1) SE2_CASE(2) SE2_CASE(3) SE2_CASE(4) SE2_CASE(5) SE2_CASE(6) SE2_CASE(7)
         SE2_CASE(8) SE2_CASE(9) SE2_CASE(10) SE2_CASE(11) SE2_CASE(12) SE2_CASE(13) SE2_CASE(14) SE2_CASE(15)
 #undef SE2_CASE

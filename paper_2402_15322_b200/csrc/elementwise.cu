@@ -75,19 +75,34 @@ cudaError_t launch_bary_logmean(int n, int nsolve, int64_t N, const float* ld, c
     return cudaGetLastError();
 }
 
-// lv[sv][i] += lbar[sv] - ld[sv][i]   (App. A: v_i <- v_i mu / d_i, in logs)
-__global__ void bary_update_log_kernel(int n, int nsolve, int64_t N, float* lv, const float* ld, const float* lbar) {
+// lv[sv][i] += lbar[sv] - ld[sv][i]   (App. A: v_i <- v_i mu / d_i, in logs).  log v_i is a running
+// sum over the iterations; with lv_lo != null it is carried as an unevaluated fp32 pair (hi, lo)
+// (two-sum compensation), so the rounding of a 100-1000 nat potential to fp32 does not accumulate
+// into a drift of the gauge; lv (hi) is what the convolutions read.
+__global__ void bary_update_log_kernel(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
+                                       const float* lbar) {
     const int64_t total = (int64_t)nsolve * n * N;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t f = t / N;          // field index sv*n + i
         const int64_t x = t - f * N;
         const int sv = (int)(f / n);
-        lv[t] = lv[t] + (lbar[(int64_t)sv * N + x] - ld[t]);
+        const float dlt = lbar[(int64_t)sv * N + x] - ld[t];
+        if (lv_lo == nullptr) {
+            lv[t] = lv[t] + dlt;
+        } else {
+            const float hi = lv[t];
+            const float y = dlt + lv_lo[t];
+            const float s = hi + y;                        // two-sum (Knuth): s + e == hi + y exactly
+            const float bb = s - hi;
+            const float e = (hi - (s - bb)) + (y - bb);
+            lv[t] = s;
+            lv_lo[t] = (s == s && fabsf(s) != INFINITY) ? e : 0.f;
+        }
     }
 }
-cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, const float* ld, const float* lbar,
-                                   cudaStream_t s) {
-    bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, ld, lbar);
+cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
+                                   const float* lbar, cudaStream_t s) {
+    bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, lv_lo, ld, lbar);
     count_launch();
     return cudaGetLastError();
 }

@@ -100,6 +100,8 @@ struct se2_kernel_s {
     void* extra = nullptr;        // grow-only workspaces (api.cu)
     float* lstats = nullptr;      // [max_batch][nt][tiles][8] per-tile plane fit + ranges of log fields (K3)
     int* lse_counters = nullptr;  // K3 path counters: active, FFMA (incl. tilted), visited, tilted pairs
+    float* split = nullptr;       // K3 theta_i-split partials (small grids): [groups][max_batch][N]
+    size_t split_floats = 0;
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -116,7 +118,8 @@ int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain);
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
-                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters);
+                                 cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters,
+                                 float* split_scratch, size_t split_floats);
 size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch);
 
 // tabulation (tabulate.cu)
@@ -130,7 +133,7 @@ cudaError_t launch_reduce_partials(const float* partial, int batch, int nblocks,
                                    cudaStream_t s);
 cudaError_t launch_bary_logmean(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev,
                                 float* lbar, cudaStream_t s);
-cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, const float* ld,
+cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
                                    const float* lbar, cudaStream_t s);
 cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const float* d,
                                    const float* lam_dev, float* bary, cudaStream_t s);

@@ -21,3 +21,13 @@ for s in range(ns):
         gv = gold["lv"].reshape(ns, n, -1)[s, i]; gw = gold["lw"].reshape(ns, n, -1)[s, i]
         dv = V[s, i] - gv; dw = W[s, i] - gw
         print(f"   input {i}: lv range [{gv.min():.1f},{gv.max():.1f}] err {potential_err(V[s,i], gv):.2e} mean diff {dv.mean():+.3e} std {dv.std():.2e} | lw err {potential_err(W[s,i], gw):.2e} mean {dw.mean():+.3e}")
+import sys as _s
+sys.path.insert(0, "tests")
+from gpu_util import measure_err
+G = gold["bary_lin"].reshape(ns, -1)
+for s in range(ns):
+    g = np.exp(B[s]); r = G[s]
+    for fl in (1e-6, 1e-5, 1e-4):
+        print(f"solve {s} measure err floor {fl:g}: {measure_err(g, r, fl):.3e}")
+    rel = np.abs(g - r) / np.maximum(r, 1e-6 * r.max())
+    i = np.argmax(rel); print("   worst at", i, "ref", r[i], "max ref", r.max(), "got", g[i])
