@@ -21,6 +21,8 @@ void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed
 
 using namespace se2;
 
+extern "C" int64_t se2_launch_count(void);
+
 namespace {
 
 struct DeviceGuard {
@@ -44,18 +46,34 @@ struct Workspace {
 
 }  // namespace
 
+// a captured solve (CUDA graph) keyed by everything its launches depend on
+struct GraphEntry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t nlaunch = 0;
+};
+
 // extra per-kernel state not in the header struct
 struct KernelExtra {
     Workspace ws;         // fields
     Workspace trace;      // device error trace
     Workspace partial;    // conv error partials
     Workspace misc;       // lambdas, counters, sums
+    std::vector<GraphEntry> graphs;   // small-problem solves replayed as CUDA graphs
+    cudaStream_t cap = nullptr;       // private stream for capture / replay
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    void clear_graphs() {
+        for (auto& gph : graphs)
+            if (gph.exec) cudaGraphExecDestroy(gph.exec);
+        graphs.clear();
+    }
 };
 
 static KernelExtra* extra(se2_kernel_s* k) { return reinterpret_cast<KernelExtra*>(k->extra); }
 
-static se2_status ensure(Workspace& w, size_t bytes) {
+static se2_status ensure(Workspace& w, size_t bytes, KernelExtra* owner = nullptr) {
     if (w.bytes >= bytes) return SE2_OK;
+    if (owner) owner->clear_graphs();   // captured graphs reference the old buffers
     if (w.ptr) cudaFree(w.ptr);
     w.ptr = nullptr;
     w.bytes = 0;
@@ -103,6 +121,72 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
     if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
     return SE2_OK;
 }
+
+// Replay `enqueue` (a launch sequence on a given stream) as a CUDA graph for small problems, where the
+// ~10 launches per scaling iteration are latency-bound; the graph is captured on first use and cached
+// under `key`.  Work is ordered after / before the caller's stream with events.  `use` = false runs
+// the sequence directly on the caller's stream (large problems, timing instrumentation on).
+template <class F>
+static se2_status run_graph(se2_kernel_s* k, cudaStream_t s, std::vector<uint64_t> key, bool use, F&& enqueue) {
+    static const bool disabled = getenv("SE2_NO_GRAPH") != nullptr;
+    if (!use || disabled || k->timing.on) return enqueue(s);
+    KernelExtra* x = extra(k);
+    if (!x->cap) {
+        SE2_CUDA_TRY(cudaStreamCreateWithFlags(&x->cap, cudaStreamNonBlocking));
+        SE2_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming));
+        SE2_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
+    }
+    GraphEntry* hit = nullptr;
+    for (auto& gph : x->graphs)
+        if (gph.key == key) hit = &gph;
+    SE2_CUDA_TRY(cudaEventRecord(x->ev_in, s));
+    SE2_CUDA_TRY(cudaStreamWaitEvent(x->cap, x->ev_in, 0));
+    if (!hit) {
+        if (x->graphs.size() >= 8) {   // small cache: drop the oldest
+            if (x->graphs.front().exec) cudaGraphExecDestroy(x->graphs.front().exec);
+            x->graphs.erase(x->graphs.begin());
+        }
+        SE2_CUDA_TRY(cudaStreamBeginCapture(x->cap, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = se2_launch_count();
+        se2_status st = enqueue(x->cap);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(x->cap, &graph);
+        if (st != SE2_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) {
+            set_error(std::string("graph capture: ") + cudaGetErrorString(e));
+            return SE2_ECUDA;
+        }
+        GraphEntry ge;
+        ge.key = std::move(key);
+        ge.nlaunch = se2_launch_count() - l0;
+        e = cudaGraphInstantiate(&ge.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            set_error(std::string("graph instantiate: ") + cudaGetErrorString(e));
+            return SE2_ECUDA;
+        }
+        x->graphs.push_back(ge);
+        hit = &x->graphs.back();
+        SE2_CUDA_TRY(cudaGraphLaunch(hit->exec, x->cap));   // the capture itself executed nothing
+    } else {
+        SE2_CUDA_TRY(cudaGraphLaunch(hit->exec, x->cap));
+        count_launch(hit->nlaunch);
+    }
+    SE2_CUDA_TRY(cudaEventRecord(x->ev_out, x->cap));
+    SE2_CUDA_TRY(cudaStreamWaitEvent(s, x->ev_out, 0));
+    return SE2_OK;
+}
+
+static uint64_t as_key(const void* p) { return (uint64_t)(uintptr_t)p; }
+static uint64_t as_key(double v) {
+    uint64_t u;
+    memcpy(&u, &v, sizeof(u));
+    return u;
+}
+constexpr int64_t kGraphMaxElems = (int64_t)1 << 21;   // batch * N at or below which solves use graphs
 
 static se2_status check_kernel(se2_kernel k) {
     if (!k) {
@@ -231,6 +315,10 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
     if (x) {
+        x->clear_graphs();
+        if (x->cap) cudaStreamDestroy(x->cap);
+        if (x->ev_in) cudaEventDestroy(x->ev_in);
+        if (x->ev_out) cudaEventDestroy(x->ev_out);
         for (Workspace* w : {&x->ws, &x->trace, &x->partial, &x->misc})
             if (w->ptr) cudaFree(w->ptr);
         delete x;
@@ -302,10 +390,28 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     const int iters = opts->iters;
     KernelExtra* x = extra(k);
 
-    // log targets
+    // workspaces first (allocation invalidates captured graphs), then the launch sequence
     size_t need = (size_t)(LOG ? 2 : 0) * BN * sizeof(float);
-    se2_status st = ensure(x->ws, std::max<size_t>(need, 16));
+    se2_status st = ensure(x->ws, std::max<size_t>(need, 16), x);
     if (st != SE2_OK) return st;
+    const int bpf = conv_blocks_per_field(k, LOG);
+    if (trace) {
+        st = ensure(x->partial, (size_t)batch * bpf * sizeof(float), x);
+        if (st != SE2_OK) return st;
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * batch * sizeof(double), x);
+        if (st != SE2_OK) return st;
+    }
+    float* partial = reinterpret_cast<float*>(x->partial.ptr);
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    std::vector<uint64_t> key = {1, as_key(mu), as_key(nu), as_key(a), as_key(b), (uint64_t)batch, (uint64_t)iters,
+                                 (uint64_t)opts->flags, (uint64_t)trace, as_key(s_out), as_key(x->ws.ptr),
+                                 as_key(partial), as_key(tr)};
+    if (prox) {
+        key.push_back((uint64_t)prox->kind);
+        for (double v : {prox->tau, prox->cx, prox->cy, prox->hx, prox->hy, prox->m}) key.push_back(as_key(v));
+    }
+    auto enqueue = [&](cudaStream_t s) -> se2_status {
+    se2_status st = SE2_OK;
     const float* tmu = mu;
     const float* tnu = nu;
     if (LOG) {
@@ -318,16 +424,6 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
             tnu = lnu;
         }
     }
-    const int bpf = conv_blocks_per_field(k, LOG);
-    if (trace) {
-        st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
-        if (st != SE2_OK) return st;
-        st = ensure(x->trace, (size_t)std::max(iters, 1) * batch * sizeof(double));
-        if (st != SE2_OK) return st;
-    }
-    float* partial = reinterpret_cast<float*>(x->partial.ptr);
-    double* tr = reinterpret_cast<double*>(x->trace.ptr);
-
     if (!(opts->flags & SE2_WARM_START)) SE2_CUDA_TRY(launch_fill(b, BN, LOG ? 0.f : 1.f, s));
 
     for (int l = 0; l < iters; ++l) {
@@ -367,8 +463,13 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         st = run_conv(k, b, batch, opts->flags, e3, s, nullptr);
         if (st != SE2_OK) return st;
         SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(iters - 1) * batch, s));
-        SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
     }
+    return SE2_OK;
+    };
+    st = run_graph(k, s, std::move(key), (int64_t)batch * N <= kGraphMaxElems, enqueue);
+    if (st != SE2_OK) return st;
+    if (trace && iters > 0)
+        SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
     return SE2_OK;
 }
 
@@ -465,7 +566,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     KernelExtra* x = extra(k);
     // workspace: mu_rep [F][N] (linear), lmu_rep [F][N], v [F][N], w [F][N], d [F][N]
     size_t need = (size_t)6 * FN * sizeof(float);
-    se2_status st = ensure(x->ws, need);
+    se2_status st = ensure(x->ws, need, x);
     if (st != SE2_OK) return st;
     float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
     float* lmu_rep = mu_rep + FN;
@@ -473,71 +574,83 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     float* w = w_state ? w_state : lmu_rep + 2 * FN;
     float* d = lmu_rep + 3 * FN;
     float* v_lo = lmu_rep + 4 * FN;   // compensation of the running sum log v (log domain)
-    for (int sv = 0; sv < nsolve; ++sv)
-        SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
-                                     cudaMemcpyDeviceToDevice, s));
-    const float* tmu = mu_rep;
-    if (LOG) {
-        SE2_CUDA_TRY(launch_log(mu_rep, lmu_rep, FN, s));
-        tmu = lmu_rep;
-    }
-    st = ensure(x->misc, 4096 + sizeof(float) * F);
+    st = ensure(x->misc, 4096 + sizeof(float) * F, x);
     if (st != SE2_OK) return st;
-    float* lam_dev = reinterpret_cast<float*>(reinterpret_cast<char*>(x->misc.ptr) + 4096);
-    std::vector<float> lamf(F);
-    for (int i = 0; i < F; ++i) lamf[i] = (float)lambdas[i];
-    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lamf.data(), sizeof(float) * F, cudaMemcpyHostToDevice, s));
     const int bpf = conv_blocks_per_field(k, LOG);
     if (trace) {
-        st = ensure(x->partial, (size_t)F * bpf * sizeof(float));
+        st = ensure(x->partial, (size_t)F * bpf * sizeof(float), x);
         if (st != SE2_OK) return st;
-        st = ensure(x->trace, (size_t)std::max(iters, 1) * F * sizeof(double));
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * F * sizeof(double), x);
         if (st != SE2_OK) return st;
     }
     float* partial = reinterpret_cast<float*>(x->partial.ptr);
     double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    float* lam_dev = reinterpret_cast<float*>(reinterpret_cast<char*>(x->misc.ptr) + 4096);
+    std::vector<float> lamf(F);
+    for (int i = 0; i < F; ++i) lamf[i] = (float)lambdas[i];
+    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lamf.data(), sizeof(float) * F, cudaMemcpyHostToDevice, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));   // lamf lives on this stack frame
 
-    SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
-    SE2_CUDA_TRY(launch_fill(v_lo, FN, 0.f, s));
-    SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
-    for (int j = 0; j < iters; ++j) {
-        // w_i = mu_i / K v_i   (fused: error of the previous v-update, sum |w_i K v_i - mu_i|)
-        Epilogue e1;
-        e1.op = EPI_DIVIDE;
-        e1.target = tmu;
-        e1.out = w;
-        if (trace && j > 0) {
-            e1.err_a = w;
-            e1.err_mu = mu_rep;
-            e1.err_partial = partial;
-        }
-        st = run_conv(k, v, F, opts->flags, e1, s, nullptr);
-        if (st != SE2_OK) return st;
-        if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
-        // d_i = v_i K w_i
-        Epilogue e2;
-        e2.op = EPI_MULTIPLY;
-        e2.target = v;
-        e2.out = d;
-        st = run_conv(k, w, F, opts->flags, e2, s, nullptr);
-        if (st != SE2_OK) return st;
-        // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
+    std::vector<uint64_t> key = {2, as_key(mus), as_key(bary), as_key(v), as_key(w), (uint64_t)n, (uint64_t)nsolve,
+                                 (uint64_t)iters, (uint64_t)opts->flags, (uint64_t)trace, as_key(x->ws.ptr),
+                                 as_key(x->misc.ptr), as_key(partial), as_key(tr)};
+    auto enqueue = [&](cudaStream_t s) -> se2_status {
+        se2_status st = SE2_OK;
+        for (int sv = 0; sv < nsolve; ++sv)
+            SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
+                                         cudaMemcpyDeviceToDevice, s));
+        const float* tmu = mu_rep;
         if (LOG) {
-            SE2_CUDA_TRY(launch_bary_logmean(n, nsolve, N, d, lam_dev, bary, s));
-            SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, v_lo, d, bary, s));
-        } else {
-            SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
+            SE2_CUDA_TRY(launch_log(mu_rep, lmu_rep, FN, s));
+            tmu = lmu_rep;
         }
-    }
+        SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
+        SE2_CUDA_TRY(launch_fill(v_lo, FN, 0.f, s));
+        SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
+        for (int j = 0; j < iters; ++j) {
+            // w_i = mu_i / K v_i   (fused: error of the previous v-update, sum |w_i K v_i - mu_i|)
+            Epilogue e1;
+            e1.op = EPI_DIVIDE;
+            e1.target = tmu;
+            e1.out = w;
+            if (trace && j > 0) {
+                e1.err_a = w;
+                e1.err_mu = mu_rep;
+                e1.err_partial = partial;
+            }
+            st = run_conv(k, v, F, opts->flags, e1, s, nullptr);
+            if (st != SE2_OK) return st;
+            if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
+            // d_i = v_i K w_i
+            Epilogue e2;
+            e2.op = EPI_MULTIPLY;
+            e2.target = v;
+            e2.out = d;
+            st = run_conv(k, w, F, opts->flags, e2, s, nullptr);
+            if (st != SE2_OK) return st;
+            // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
+            if (LOG) {
+                SE2_CUDA_TRY(launch_bary_logmean(n, nsolve, N, d, lam_dev, bary, s));
+                SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, v_lo, d, bary, s));
+            } else {
+                SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
+            }
+        }
+        if (trace && iters > 0) {
+            Epilogue e3;
+            e3.op = EPI_ERRONLY;
+            e3.err_a = w;
+            e3.err_mu = mu_rep;
+            e3.err_partial = partial;
+            st = run_conv(k, v, F, opts->flags, e3, s, nullptr);
+            if (st != SE2_OK) return st;
+            SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
+        }
+        return SE2_OK;
+    };
+    st = run_graph(k, s, std::move(key), FN <= kGraphMaxElems, enqueue);
+    if (st != SE2_OK) return st;
     if (trace && iters > 0) {
-        Epilogue e3;
-        e3.op = EPI_ERRONLY;
-        e3.err_a = w;
-        e3.err_mu = mu_rep;
-        e3.err_partial = partial;
-        st = run_conv(k, v, F, opts->flags, e3, s, nullptr);
-        if (st != SE2_OK) return st;
-        SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
         std::vector<double> h((size_t)iters * F);
         SE2_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, sizeof(double) * iters * F, cudaMemcpyDeviceToHost, s));
         SE2_CUDA_TRY(cudaStreamSynchronize(s));
