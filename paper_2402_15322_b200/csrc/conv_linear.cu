@@ -42,16 +42,16 @@ struct LinCfg {
 };
 
 // W table layout used here: Wl[to][ti][S][SP] (dx padded with zeros to SP)
-template <int R, int WX, bool TMA>
+template <int R, int WX, bool TMA, int NBUF = 2>
 __global__ void __launch_bounds__(LinCfg<R, WX>::NT)
 conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, int nx, int ny, int nt,
                    int band, int tiles_x, Epilogue epi, const __grid_constant__ CUtensorMap tmap) {
     using C = LinCfg<R, WX, TMA>;
     extern __shared__ __align__(128) float smem[];
     constexpr int WSTRIDE = TMA ? C::WINA : C::WIN;   // floats between the two window buffers
-    float* sWin = smem;                     // [2][WSTRIDE]
-    float* sFil = smem + 2 * WSTRIDE;       // [2][FIL]
-    float* sRed = sFil + 2 * C::FIL;        // reduction scratch (16 floats)
+    float* sWin = smem;                     // [NBUF][WSTRIDE]
+    float* sFil = smem + NBUF * WSTRIDE;    // [NBUF][FIL]
+    float* sRed = sFil + NBUF * C::FIL;     // reduction scratch (16 floats)
     uint64_t* sBar = reinterpret_cast<uint64_t*>(sRed + 16);   // 2 mbarriers (TMA variant)
 
     const int tile = blockIdx.x;
@@ -122,10 +122,14 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
 
     stage(0, 0);
     for (int it = 0; it < nti; ++it) {
-        const int buf = it & 1;
-        if (it + 1 < nti) stage(it + 1, buf ^ 1);
+        const int buf = (NBUF == 2) ? (it & 1) : 0;
+        if (NBUF == 2) {
+            if (it + 1 < nti) stage(it + 1, buf ^ 1);
+        } else if (it > 0) {
+            stage(it, 0);   // single buffer: the previous channel's readers finished at the barrier below
+        }
         if (TMA) {
-            mbar_wait(&sBar[buf], (uint32_t)((it >> 1) & 1));
+            mbar_wait(&sBar[buf], (uint32_t)(NBUF == 2 ? ((it >> 1) & 1) : (it & 1)));
         } else {
             if (it + 1 < nti) cp_async_wait<1>();
             else cp_async_wait<0>();
@@ -195,11 +199,32 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
     CUtensorMap tmap;
     const bool tma = make_field_tmap(&tmap, in, k->nx, k->ny, k->nt * batch, CT::PITCH, CT::WIN_H);
     cudaError_t e;
-    if (tma) {
-        e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)CT::SMEM_TMA);
+    // buffers per CTA and CTAs per SM (via smem padding).  Tuned on B200 at c4 (profiles/r01_*):
+    // a single TMA buffer (20.8 KB -> 10 CTAs / 20 warps per SM; the other CTAs hide each CTA's load
+    // bubble) beats double buffering at 5 CTAs / SM: 1.448 vs 1.553 ms.  Env overrides for experiments.
+    static const int nbuf = getenv("SE2_LIN_NBUF") ? atoi(getenv("SE2_LIN_NBUF")) : 1;
+    static const int occ = getenv("SE2_LIN_OCC") ? atoi(getenv("SE2_LIN_OCC")) : 0;
+    if (tma && nbuf == 1) {
+        size_t smem = (size_t)(CT::WINA + CT::FIL) * sizeof(float) + 64 + 128;
+        if (occ > 0) {
+            size_t want = (size_t)(227 * 1024) / occ - 1024;
+            if (want > smem) smem = want;
+        }
+        e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
         if (e != cudaSuccess) return e;
-        conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, CT::SMEM_TMA, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
+        conv_linear_kernel<R, kLinWX, true, 1><<<grid, CT::NT, smem, s>>>(in, epi.table ? epi.table : k->Wl, k->nx,
+                                                                         k->ny, k->nt, k->band, tiles_x, epi, tmap);
+    } else if (tma) {
+        size_t smem = CT::SMEM_TMA;
+        if (occ > 0) {
+            size_t want = (size_t)(227 * 1024) / occ - 1024;
+            if (want > smem) smem = want;
+        }
+        e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, smem, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
                                                                             tiles_x, epi, tmap);
     } else {
         e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
