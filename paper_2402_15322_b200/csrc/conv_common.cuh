@@ -66,6 +66,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^x for x <= 0 on the FMA pipe (frees the MUFU pipe, which bounds the exact log-sum-exp): x is
+// clamped at -125 (2^-125 is far below any retained term), n = rint(x) by the 1.5*2^23 trick,
+// 2^f = e^{f ln 2} for |f| <= 1/2 by its degree-6 Taylor polynomial (relative error < 1.3e-7, the
+// accuracy of ex2.approx), scaled by adding n to the exponent bits.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.f);
+    const float t = x + 12582912.f;
+    const float n = t - 12582912.f;
+    const float f = x - n;
+    float p = 1.5403530393381608e-4f;          // ln2^6 / 720
+    p = fmaf(p, f, 1.3333558146428443e-3f);    // ln2^5 / 120
+    p = fmaf(p, f, 9.6181291076284772e-3f);    // ln2^4 / 24
+    p = fmaf(p, f, 5.5504108664821580e-2f);    // ln2^3 / 6
+    p = fmaf(p, f, 2.4022650695910071e-1f);    // ln2^2 / 2
+    p = fmaf(p, f, 6.9314718055994531e-1f);    // ln2
+    p = fmaf(p, f, 1.f);
+    const int ni = __float_as_int(t) - 0x4B400000;
+    return __int_as_float(__float_as_int(p) + (ni << 23));
+}
+
 __device__ __forceinline__ float lg2_approx(float x) {
     float y;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

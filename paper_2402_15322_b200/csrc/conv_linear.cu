@@ -17,11 +17,11 @@
 
 namespace se2 {
 
-template <int R, int WX, bool TMA = false>
+template <int R, int WX, bool TMA = false, int PP = 16>
 struct LinCfg {
     static constexpr int S = 2 * R + 1;
     static constexpr int SP = (S + 3) / 4 * 4;  // filter row pitch (LDS.128 of 4 taps)
-    static constexpr int P = 16;   // columns per thread
+    static constexpr int P = PP;   // columns per thread
     static constexpr int NT = 32 * WX;
     static constexpr int TY = 32, TX = P * WX;
     // left halo of the staged window: R (cp.async path) or R rounded up to a multiple of 4 (TMA
@@ -42,11 +42,11 @@ struct LinCfg {
 };
 
 // W table layout used here: Wl[to][ti][S][SP] (dx padded with zeros to SP)
-template <int R, int WX, bool TMA, int NBUF = 2>
+template <int R, int WX, bool TMA, int NBUF = 2, int PP = 16>
 __global__ void __launch_bounds__(LinCfg<R, WX>::NT)
 conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, int nx, int ny, int nt,
                    int band, int tiles_x, Epilogue epi, const __grid_constant__ CUtensorMap tmap) {
-    using C = LinCfg<R, WX, TMA>;
+    using C = LinCfg<R, WX, TMA, PP>;
     extern __shared__ __align__(128) float smem[];
     constexpr int WSTRIDE = TMA ? C::WINA : C::WIN;   // floats between the two window buffers
     float* sWin = smem;                     // [NBUF][WSTRIDE]
@@ -201,7 +201,8 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
     cudaError_t e;
     // buffers per CTA and CTAs per SM (via smem padding).  Tuned on B200 at c4 (profiles/r01_*):
     // a single TMA buffer (20.8 KB -> 10 CTAs / 20 warps per SM; the other CTAs hide each CTA's load
-    // bubble) beats double buffering at 5 CTAs / SM: 1.448 vs 1.553 ms.  Env overrides for experiments.
+    // bubble) beats double buffering at 5 CTAs / SM: 1.448 vs 1.553 ms; 32 columns per thread (one
+    // warp per CTA) measured 1.516 ms.  Env overrides for experiments.
     static const int nbuf = getenv("SE2_LIN_NBUF") ? atoi(getenv("SE2_LIN_NBUF")) : 1;
     static const int occ = getenv("SE2_LIN_OCC") ? atoi(getenv("SE2_LIN_OCC")) : 0;
     if (tma && nbuf == 1) {
