@@ -82,7 +82,7 @@ class ShardedBarycenter:
         self.lv = torch.zeros_like(mus_local)
         self.lw = torch.zeros_like(mus_local)
         self.ld = torch.empty_like(mus_local)
-        self.lbar = torch.empty_like(mus_local[0])
+        self.lbar = torch.empty(tuple(mus_local.shape[1:]), dtype=mus_local.dtype, device=mus_local.device)
 
     def iterate(self, iters: int):
         for _ in range(iters):

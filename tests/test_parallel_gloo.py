@@ -148,3 +148,34 @@ def test_sharded_barycenter_gloo():
 def test_slab_jko_gloo():
     rel, dmass = _run(_slab_worker)
     assert rel < 1e-10 and dmass < 1e-12, (rel, dmass)
+
+
+def _empty_rank_worker(rank, world, port, q):
+    """3 ranks, 2 inputs: rank 2 owns none and still takes part in the allreduce."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = O.Grid(10, 8, 4)
+        T = O.kernel_table(g, 2, 0.1, (1, 2, 1))
+        L = O.log_kernel_table(g, 2, 0.1, (1, 2, 1))
+        rng = np.random.default_rng(3)
+        mus = [rng.random(g.shape) + 0.05 for _ in range(2)]
+        mus = [m / m.sum() for m in mus]
+        lam = np.array([0.6, 0.4])
+        lo, hi = partition(2, world, rank)
+        local = torch.from_numpy(np.stack(mus[lo:hi])) if hi > lo else torch.zeros((0,) + g.shape, dtype=torch.float64)
+        drv = ShardedBarycenter(OracleOps(T, L, True), local, lam[lo:hi])
+        lbar = drv.iterate(6).numpy().copy()
+        ref = O.barycenter(T, L, mus, lam, 6, log_domain=True, trace=False)["lbary"]
+        err = float(np.max(np.abs(lbar - ref)))
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if rank == 0:
+            q.put(max(errs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_barycenter_rank_without_inputs_gloo():
+    assert _run(_empty_rank_worker, world=3) < 1e-10
