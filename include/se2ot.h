@@ -221,10 +221,11 @@ SE2_API se2_status se2_scale_rows(float* x, int32_t planes, int32_t ny, int32_t 
 SE2_API se2_status se2_sum(const float* x, int64_t n, double* out_host, se2_stream stream);
 
 /* Log-domain engine (K3) path counters since the last reset: (tile-quad, theta_i) pairs that were
- * active after pruning, handled by an FFMA path (plain or gradient-tilted), visited in total, and
- * handled by the tilted FFMA path. */
+ * active after pruning, handled by an FFMA path (plain or gradient-tilted), visited in total, handled
+ * by the tilted FFMA path, and CTAs whose hinted exact-path shift failed verification (redone). */
 SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs,
-                                      int64_t* visited_pairs, int64_t* tilted_pairs, int32_t reset);
+                                      int64_t* visited_pairs, int64_t* tilted_pairs, int64_t* hint_redos,
+                                      int32_t reset);
 
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)

@@ -100,7 +100,7 @@ def load(path: str = LIB_PATH):
         "se2_scale_rows": [P, i32, i32, i32, i32, i32, dbl, P],
         "se2_timing_enable": [P, i32],
         "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
-                               ctypes.POINTER(i64), i32],
+                               ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
     }
     for name, args in sig.items():

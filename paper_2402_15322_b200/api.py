@@ -81,10 +81,10 @@ class Kernel:
     # instrumentation
     def lse_path_stats(self, reset: bool = True) -> dict:
         """K3 counters: (tile-quad, theta_i) pairs active after pruning / on the FFMA path / visited."""
-        a, f, v, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        a, f, v, t, h = (ctypes.c_int64() for _ in range(5))
         check(L.load().se2_lse_path_stats(self._h, ctypes.byref(a), ctypes.byref(f), ctypes.byref(v),
-                                          ctypes.byref(t), 1 if reset else 0))
-        return dict(active=a.value, ffma=f.value, visited=v.value, tilted=t.value)
+                                          ctypes.byref(t), ctypes.byref(h), 1 if reset else 0))
+        return dict(active=a.value, ffma=f.value, visited=v.value, tilted=t.value, hint_redos=h.value)
 
     def timing_enable(self, on: bool = True):
         check(L.load().se2_timing_enable(self._h, 1 if on else 0))

@@ -257,8 +257,8 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     {
         const size_t nst = lse_fast_stats_floats(k, max_batch);
         cudaError_t e2 = cudaMalloc(&k->lstats, sizeof(float) * nst);
-        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(long long) * 4);
-        if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(long long) * 4);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(int) * 8);
+        if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(int) * 8);
         // theta_i-split scratch for grids that give fewer than 2 CTAs per SM (at most 8 groups, 64 MB)
         {
             const int64_t N = k->N();
@@ -391,7 +391,8 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     KernelExtra* x = extra(k);
 
     // workspaces first (allocation invalidates captured graphs), then the launch sequence
-    size_t need = (size_t)(LOG ? 2 : 0) * BN * sizeof(float);
+    // log targets (2 BN) + shift hints of the two convolutions (2 BN)
+    size_t need = (size_t)(LOG ? 4 : 0) * BN * sizeof(float);
     se2_status st = ensure(x->ws, std::max<size_t>(need, 16), x);
     if (st != SE2_OK) return st;
     const int bpf = conv_blocks_per_field(k, LOG);
@@ -426,12 +427,16 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     }
     if (!(opts->flags & SE2_WARM_START)) SE2_CUDA_TRY(launch_fill(b, BN, LOG ? 0.f : 1.f, s));
 
+    float* hint1 = LOG ? reinterpret_cast<float*>(x->ws.ptr) + 2 * BN : nullptr;   // K b
+    float* hint2 = LOG ? hint1 + BN : nullptr;                                      // K a
     for (int l = 0; l < iters; ++l) {
         // a = mu / K b   (error of the previous iterate fused: sum |a_old K b - mu|)
         Epilogue e1;
         e1.op = EPI_DIVIDE;
         e1.target = tmu;
         e1.out = a;
+        e1.hint_in = (l > 0) ? hint1 : nullptr;
+        e1.hint_out = hint1;
         if (trace && l > 0) {
             e1.err_a = a;
             e1.err_mu = mu;
@@ -443,6 +448,8 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         // b = prox(K^T a) / K^T a    (K^T = K)
         Epilogue e2;
         e2.out = b;
+        e2.hint_in = (l > 0) ? hint2 : nullptr;
+        e2.hint_out = hint2;
         if (jko) {
             e2.op = EPI_PROX;
             fill_prox(e2, k, prox);
@@ -460,6 +467,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         e3.err_a = a;
         e3.err_mu = mu;
         e3.err_partial = partial;
+        e3.hint_in = hint1;
         st = run_conv(k, b, batch, opts->flags, e3, s, nullptr);
         if (st != SE2_OK) return st;
         SE2_CUDA_TRY(launch_reduce_partials(partial, batch, bpf, tr + (int64_t)(iters - 1) * batch, s));
@@ -565,7 +573,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     const int iters = opts->iters;
     KernelExtra* x = extra(k);
     // workspace: mu_rep [F][N] (linear), lmu_rep [F][N], v [F][N], w [F][N], d [F][N]
-    size_t need = (size_t)6 * FN * sizeof(float);
+    size_t need = (size_t)8 * FN * sizeof(float);
     se2_status st = ensure(x->ws, need, x);
     if (st != SE2_OK) return st;
     float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
@@ -574,6 +582,8 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     float* w = w_state ? w_state : lmu_rep + 2 * FN;
     float* d = lmu_rep + 3 * FN;
     float* v_lo = lmu_rep + 4 * FN;   // compensation of the running sum log v (log domain)
+    float* hint1 = LOG ? lmu_rep + 5 * FN : nullptr;   // shift hints of K v and K w (log domain)
+    float* hint2 = LOG ? lmu_rep + 6 * FN : nullptr;
     st = ensure(x->misc, 4096 + sizeof(float) * F, x);
     if (st != SE2_OK) return st;
     const int bpf = conv_blocks_per_field(k, LOG);
@@ -613,6 +623,8 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             e1.op = EPI_DIVIDE;
             e1.target = tmu;
             e1.out = w;
+            e1.hint_in = (j > 0) ? hint1 : nullptr;
+            e1.hint_out = hint1;
             if (trace && j > 0) {
                 e1.err_a = w;
                 e1.err_mu = mu_rep;
@@ -626,6 +638,8 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             e2.op = EPI_MULTIPLY;
             e2.target = v;
             e2.out = d;
+            e2.hint_in = (j > 0) ? hint2 : nullptr;
+            e2.hint_out = hint2;
             st = run_conv(k, w, F, opts->flags, e2, s, nullptr);
             if (st != SE2_OK) return st;
             // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
@@ -642,6 +656,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             e3.err_a = w;
             e3.err_mu = mu_rep;
             e3.err_partial = partial;
+            e3.hint_in = hint1;
             st = run_conv(k, v, F, opts->flags, e3, s, nullptr);
             if (st != SE2_OK) return st;
             SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
@@ -801,17 +816,18 @@ se2_status se2_scale_rows(float* xp, int32_t planes, int32_t ny, int32_t nx, int
 }
 
 se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma_pairs, int64_t* visited_pairs,
-                              int64_t* tilted_pairs, int32_t reset) {
+                              int64_t* tilted_pairs, int64_t* hint_redos, int32_t reset) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     DeviceGuard g(k->device);
-    int h[4] = {0, 0, 0, 0};
+    int h[5] = {0, 0, 0, 0, 0};
     SE2_CUDA_TRY(cudaDeviceSynchronize());
-    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters, sizeof(int) * 4, cudaMemcpyDeviceToHost));
+    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters, sizeof(int) * 5, cudaMemcpyDeviceToHost));
     if (active_pairs) *active_pairs = h[0];
     if (ffma_pairs) *ffma_pairs = h[1];
     if (visited_pairs) *visited_pairs = h[2];
     if (tilted_pairs) *tilted_pairs = h[3];
-    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 4));
+    if (hint_redos) *hint_redos = h[4];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 5));
     return SE2_OK;
 }
 

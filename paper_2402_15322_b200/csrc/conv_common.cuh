@@ -120,6 +120,7 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
         float row = LOG ? expf(a_old + y) : a_old * y;
         err = fabsf(row - mu);
     }
+    if (LOG && e.hint_out != nullptr) e.hint_out[idx] = y;
     float o;
     switch (e.op) {
         case EPI_STORE: o = y; break;

@@ -314,10 +314,24 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     };
 
     float Macc[4][C::P], Sacc[4][C::P];
+    const bool have_hint = (epi.hint_in != nullptr) && (ngroups == 1);
+    for (int attempt = have_hint ? 0 : 1; attempt < 2; ++attempt) {
+    const bool use_hint = (attempt == 0);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int p = 0; p < C::P; ++p) { Macc[q][p] = LOW; Sacc[q][p] = 0.f; }
+        for (int p = 0; p < C::P; ++p) {
+            Macc[q][p] = LOW;
+            Sacc[q][p] = 0.f;
+            if (use_hint) {
+                // shift = previous output + 20 nats, relative to ref, log2 units
+                const int to = 4 * qd + q, gy = y0 + lane, gx = x0 + wx * C::P + p;
+                if (to < nt && gy < ny && gx < nx) {
+                    const float h = epi.hint_in[(int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx];
+                    if (h > -1e30f && h < 1e30f) Macc[q][p] = ((h - ref) + 20.f) * kLog2e;
+                }
+            }
+        }
 
     if (nact > 0) stage(0, 0);
     for (int a = 0; a < nact; ++a) {
@@ -483,13 +497,14 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 }
             }
         } else {
-            // ---------------- exact path: two passes over the taps of this channel
+            // ---------------- exact path: two passes over the taps of this channel (pass A, the
+            // per-output maximum, is skipped when the output shift comes from a verified hint)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
                 for (int p = 0; p < C::P; ++p) acc[q][p] = Macc[q][p];
 #pragma unroll 1
-            for (int dy = 0; dy < C::S; ++dy) {
+            for (int dy = 0; dy < (use_hint ? 0 : C::S); ++dy) {
                 const float4* rowp = reinterpret_cast<const float4*>(win + (lane - dy + 2 * R) * C::PITCH);
                 float r[C::RL];
 #pragma unroll
@@ -511,14 +526,16 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     }
                 }
             }
+            if (!use_hint) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int p = 0; p < C::P; ++p) {
-                    const float mn = acc[q][p];      // >= Macc (LOW sentinel when nothing finite yet)
-                    Sacc[q][p] *= ex2_approx(Macc[q][p] - mn);
-                    Macc[q][p] = mn;
-                }
+                    for (int p = 0; p < C::P; ++p) {
+                        const float mn = acc[q][p];      // >= Macc (LOW sentinel when nothing finite yet)
+                        Sacc[q][p] *= ex2_approx(Macc[q][p] - mn);
+                        Macc[q][p] = mn;
+                    }
+            }
 #pragma unroll 1
             for (int dy = 0; dy < C::S; ++dy) {
                 const float4* rowp = reinterpret_cast<const float4*>(win + (lane - dy + 2 * R) * C::PITCH);
@@ -546,6 +563,23 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             }
         }
         __syncthreads();
+    }
+    if (!use_hint) break;
+    // verify the hinted shifts: every stored output must have a finite, non-overflowing sum whose largest
+    // terms were not flushed (sum >= 2^-60 relative to the shift); otherwise the CTA redoes two-pass
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < C::P; ++p) {
+            const int to = 4 * qd + q, gyy = y0 + lane, gxx = x0 + wx * C::P + p;
+            if (to < nt && gyy < ny && gxx < nx) {
+                const float sv = Sacc[q][p];
+                if (!(sv >= 8.67361738e-19f && sv <= 1.2676506e30f)) bad = true;   // [2^-60, 2^100]
+            }
+        }
+    if (!__syncthreads_or(bad)) break;
+    if (counters != nullptr && threadIdx.x == 0) atomicAdd(&counters[4], 1);   // hint redo
     }
 
     float err = 0.f;

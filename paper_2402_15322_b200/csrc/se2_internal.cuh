@@ -57,6 +57,11 @@ enum EpiOp : int {
 struct Epilogue {
     int op = EPI_STORE;
     const float* table = nullptr;    // table override (cost tables); null = the kernel's Gibbs tables
+    // log domain (K3): the previous iteration's output of the same operator, used as the per-output
+    // shift of the exact path (skips its max pass; verified, with a two-pass redo); ly is written to
+    // hint_out (may alias hint_in: same thread, same index)
+    const float* hint_in = nullptr;
+    float* hint_out = nullptr;
     const float* target = nullptr;   // [batch][N]
     float* out = nullptr;            // [batch][N]
     float* out2 = nullptr;           // EPI_PROX only: s = prox(z) = b * z (or its log-domain form exp(beta + lz))
