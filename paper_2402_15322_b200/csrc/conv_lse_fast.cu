@@ -268,9 +268,10 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     __syncthreads();
     if (threadIdx.x == 0) {   // compact the active list: entry = channel | (path << 16)
         int n = 0, nf = 0, ntl = 0;
+        int seen = 0;   // active channels are dealt round-robin over the split groups (balanced)
         for (int i = 0; i < nt; ++i) {
             int s = sList[i];
-            if (s && (i % ngroups) == grp) {
+            if (s && ((seen++) % ngroups) == grp) {
                 sList[n++] = i | (s << 16);
                 nf += (s == 1 || s == 3);
                 ntl += (s == 3);
@@ -314,7 +315,9 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     };
 
     float Macc[4][C::P], Sacc[4][C::P];
-    const bool have_hint = (epi.hint_in != nullptr) && (ngroups == 1);
+    // hinted shifts: verified here (whole-CTA redo) when unsplit; in a theta_i split the partial sums
+    // cannot be judged alone, so the combine kernel verifies the total and recomputes bad outputs
+    const bool have_hint = (epi.hint_in != nullptr);
     for (int attempt = have_hint ? 0 : 1; attempt < 2; ++attempt) {
     const bool use_hint = (attempt == 0);
 #pragma unroll
@@ -564,7 +567,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         }
         __syncthreads();
     }
-    if (!use_hint) break;
+    if (!use_hint || ngroups > 1) break;
     // verify the hinted shifts: every stored output must have a finite, non-overflowing sum whose largest
     // terms were not flushed (sum >= 2^-60 relative to the shift); otherwise the CTA redoes two-pass
     bool bad = false;
@@ -615,10 +618,46 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
 // Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
 // Same (tile, quad) blocks and thread -> output mapping as the main kernel, so the error partials have
 // the unsplit layout.
+// exact log-sum-exp of one output over every input orientation and tap (two passes, the definition):
+// the combine kernel's fallback when a hinted shift failed (expected never; correct always)
+__device__ __noinline__ float exact_lse_point(const float* __restrict__ vin, const float* __restrict__ Lq, int nx, int ny, int nt,
+                                 int R, int to, int y, int x) {
+    const int S = 2 * R + 1, qd = to >> 2, q = to & 3;
+    float m = -INFINITY;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int dy = -R; dy <= R; ++dy) {
+            const int hy = y - dy;
+            if (hy < 0 || hy >= ny) continue;
+            for (int dx = -R; dx <= R; ++dx) {
+                const int hx = x - dx;
+                if (hx < 0 || hx >= nx) continue;
+                const float t = vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
+                                Lq[((((int64_t)qd * nt + ti) * S + dy + R) * S + dx + R) * 4 + q];
+                m = fmaxf(m, t);
+            }
+        }
+    if (m == -INFINITY) return -INFINITY;
+    float sacc = 0.f;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int dy = -R; dy <= R; ++dy) {
+            const int hy = y - dy;
+            if (hy < 0 || hy >= ny) continue;
+            for (int dx = -R; dx <= R; ++dx) {
+                const int hx = x - dx;
+                if (hx < 0 || hx >= nx) continue;
+                const float t = vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
+                                Lq[((((int64_t)qd * nt + ti) * S + dy + R) * S + dx + R) * 4 + q];
+                sacc += ex2_approx(t - m);
+            }
+        }
+    return (m + log2f(sacc)) * kLn2;
+}
+
 template <int R>
 __global__ void __launch_bounds__(LseFCfg<R>::NT)
 lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x,
-                         Epilogue epi) {
+                         Epilogue epi, const float* __restrict__ in, const float* __restrict__ Lq,
+                         int* __restrict__ counters) {
     using C = LseFCfg<R>;
     __shared__ float sRed[C::NT / 32];
     const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
@@ -643,6 +682,15 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
                     float s = 0.f;
                     for (int g = 0; g < ngroups; ++g) s += expf(part[g * GN + idx] - m);
                     ly = m + logf(s);
+                }
+                if (epi.hint_in != nullptr) {
+                    // the partials used shift = hint + 20 nats: valid iff no overflow (finite) and the
+                    // total is at most 40 nats below the hint (largest terms stayed normal fp32)
+                    const float h = epi.hint_in[idx];
+                    if (!(ly < 1e30f && ly >= h - 40.f)) {
+                        ly = exact_lse_point(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, gy, gx);
+                        if (counters != nullptr) atomicAdd(&counters[4], 1);
+                    }
                 }
                 err += apply_epilogue<true>(epi, idx, gx, gy, ly);
             }
@@ -677,7 +725,8 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     // ~2 CTAs per SM exist (the per-channel loop of one CTA is latency-bound), then combine
     const int base_ctas = ntile * nquad * batch;
     int groups = 1;
-    if (base_ctas < 2 * 148) groups = (2 * 148 + base_ctas - 1) / base_ctas;
+    static const int split_min = getenv("SE2_K3_SPLIT_MIN") ? atoi(getenv("SE2_K3_SPLIT_MIN")) : 2 * 148;
+    if (base_ctas < split_min) groups = (2 * 148 + base_ctas - 1) / base_ctas;
     if (groups > k->nt) groups = k->nt;
     if (groups > 1 && (size_t)groups * batch * k->N() > split_floats) groups = 1;
     if (bpf) *bpf = ntile * nquad;
@@ -688,7 +737,8 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     count_launch();
     if (groups > 1) {
         dim3 g2(ntile, nquad, batch);
-        lse_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi);
+        lse_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi, in,
+                                                         k->Lq, counters);
         count_launch();
     }
     return cudaGetLastError();
