@@ -62,6 +62,7 @@ typedef enum {
 #define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4)   */
 #define SE2_LSE_NOTILT 0x10u  /* diagnostics: K3 without its gradient-tilted FFMA path           */
 #define SE2_LSE_K3EXACT 0x20u /* diagnostics: K3 with every active channel on its exact path     */
+#define SE2_NO_GRAPH 0x40u    /* solvers: launch directly instead of replaying a CUDA graph       */
 
 typedef struct {
     int32_t nx, ny, ntheta;

@@ -101,9 +101,10 @@ def se2_kernel_build(nx, ny, ntheta, eps, w, radius, max_batch=1, device=0) -> K
     return Kernel(nx, ny, ntheta, eps, w, radius, max_batch, device)
 
 
-def _flags(log_domain: bool, trace: bool = False, warm: bool = False, lse_exact: bool = False) -> int:
+def _flags(log_domain: bool, trace: bool = False, warm: bool = False, lse_exact: bool = False,
+           no_graph: bool = False) -> int:
     return (L.SE2_LOG_DOMAIN if log_domain else 0) | (L.SE2_TRACE_ERR if trace else 0) | (
-        L.SE2_WARM_START if warm else 0) | (L.SE2_LSE_EXACT if lse_exact else 0)
+        L.SE2_WARM_START if warm else 0) | (L.SE2_LSE_EXACT if lse_exact else 0) | (L.SE2_NO_GRAPH if no_graph else 0)
 
 
 def se2_conv(k: Kernel, x: torch.Tensor, out: Optional[torch.Tensor] = None, log_domain: bool = False,
@@ -138,7 +139,7 @@ def make_porous_prox(tau: float, m: float) -> L.se2_prox:
 
 def se2_sinkhorn(k: Kernel, mu: torch.Tensor, nu: Optional[torch.Tensor], a: torch.Tensor, b: torch.Tensor,
                  iters: int, log_domain: bool, prox: Optional[L.se2_prox] = None, trace: bool = False,
-                 warm_start: bool = False, lse_exact: bool = False) -> Optional[np.ndarray]:
+                 warm_start: bool = False, lse_exact: bool = False, no_graph: bool = False) -> Optional[np.ndarray]:
     """Scaling iterations a = mu / K b, b = prox(K^T a)/K^T a.  Returns the marginal
     error trace [iters][batch] when trace=True."""
     _check_field(mu, k, "mu")
@@ -147,7 +148,7 @@ def se2_sinkhorn(k: Kernel, mu: torch.Tensor, nu: Optional[torch.Tensor], a: tor
         _check_field(t, k, name, batch)
     if nu is not None:
         _check_field(nu, k, "nu", batch)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace, warm_start, lse_exact))
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace, warm_start, lse_exact, no_graph))
     tr = np.zeros((max(iters, 1), batch), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None
     check(L.load().se2_sinkhorn(k.handle, _ptr(mu), _ptr(nu), _ptr(a), _ptr(b), batch,
@@ -172,7 +173,8 @@ def se2_jko_step(k: Kernel, mu_k: torch.Tensor, mu_next: torch.Tensor, a: torch.
 
 def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain: bool,
                    bary: Optional[torch.Tensor] = None, v_state: Optional[torch.Tensor] = None,
-                   w_state: Optional[torch.Tensor] = None, trace: bool = False, lse_exact: bool = False):
+                   w_state: Optional[torch.Tensor] = None, trace: bool = False, lse_exact: bool = False,
+                   no_graph: bool = False):
     """App. A barycenter.  mus: [n][N]; lambdas: [nsolve][n] (host).  Returns
     (bary [nsolve][N] -- log mu under log_domain --, err trace [iters][nsolve] or None)."""
     _check_field(mus, k, "mus")
@@ -187,7 +189,7 @@ def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain
     for name, t in (("v_state", v_state), ("w_state", w_state)):
         if t is not None:
             _check_field(t, k, name, nsolve * n)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace, lse_exact=lse_exact))
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace, lse_exact=lse_exact, no_graph=no_graph))
     tr = np.zeros((max(iters, 1), nsolve), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None
     check(L.load().se2_barycenter(k.handle, n, nsolve, _ptr(mus), lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

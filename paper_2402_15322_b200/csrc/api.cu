@@ -477,7 +477,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     }
     return SE2_OK;
     };
-    st = run_graph(k, s, std::move(key), (int64_t)batch * N <= kGraphMaxElems, enqueue);
+    st = run_graph(k, s, std::move(key), (int64_t)batch * N <= kGraphMaxElems && !(opts->flags & SE2_NO_GRAPH), enqueue);
     if (st != SE2_OK) return st;
     if (trace && iters > 0)
         SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
@@ -667,7 +667,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         }
         return SE2_OK;
     };
-    st = run_graph(k, s, std::move(key), FN <= kGraphMaxElems, enqueue);
+    st = run_graph(k, s, std::move(key), FN <= kGraphMaxElems && !(opts->flags & SE2_NO_GRAPH), enqueue);
     if (st != SE2_OK) return st;
     if (trace && iters > 0) {
         std::vector<double> h((size_t)iters * F);

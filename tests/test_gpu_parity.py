@@ -147,3 +147,43 @@ def test_determinism(cuda_device):
     b2, t2 = se2_barycenter(k, mus, lams, 20, True, trace=True)
     assert torch.equal(b1, b2)
     assert np.array_equal(t1, t2)
+
+
+def test_graph_replay_equals_direct_launches(cuda_device):
+    """The CUDA-graph replay of a small solve is bit-identical to launching its kernels directly, on
+    the first (capturing) and on a cached replay."""
+    from paper_2402_15322_b200 import se2_barycenter, se2_sinkhorn
+    pc = S.get_parity_case("c1")
+    cfg, d = S.parity_inputs(pc)
+    k = _kernel(cfg, 10)
+    mus = _dev(np.stack(d["mus"]))
+    lams = np.array([[t, 1 - t] for t in cfg.ts])
+    ref, tref = se2_barycenter(k, mus, lams, 15, True, trace=True, no_graph=True)
+    for _ in range(2):
+        b, t = se2_barycenter(k, mus, lams, 15, True, trace=True)
+        assert torch.equal(b, ref) and np.array_equal(t, tref)
+    pc0 = S.get_parity_case("c0")
+    cfg0, d0 = S.parity_inputs(pc0)
+    k0 = _kernel(cfg0, 1)
+    mu, nu = _dev(d0["mus"][0]), _dev(d0["mus"][1])
+    a1, b1, a2, b2 = (torch.empty_like(mu) for _ in range(4))
+    t1 = se2_sinkhorn(k0, mu, nu, a1, b1, 20, True, trace=True, no_graph=True)
+    for _ in range(2):
+        t2 = se2_sinkhorn(k0, mu, nu, a2, b2, 20, True, trace=True)
+        assert torch.equal(a1, a2) and torch.equal(b1, b2) and np.array_equal(t1, t2)
+
+
+def test_sinkhorn_jko_determinism(cuda_device):
+    from paper_2402_15322_b200 import make_prox, se2_jko_step
+    pc = S.get_parity_case("c4m")
+    cfg, d = S.parity_inputs(pc)
+    k = _kernel(cfg, 1)
+    prox = make_prox(k, cfg.tau)
+    outs = []
+    for _ in range(2):
+        mu = _dev(d["mus"][0])
+        nxt, a, b = torch.empty_like(mu), torch.empty_like(mu), torch.empty_like(mu)
+        mass, tr = se2_jko_step(k, mu, nxt, a, b, 30, prox, False, trace=True)
+        outs.append((nxt.clone(), mass, tr))
+    assert torch.equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][2], outs[1][2])
