@@ -195,6 +195,7 @@ def config_sweep(device: int):
         solve()                      # warm-up (captures the CUDA graph of small solves)
         torch.cuda.synchronize()
         k.lse_path_stats(reset=True)
+        k.lse_row_stats(reset=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         it = solve()                 # timed: as a user runs it (graph replay for small problems)
@@ -202,6 +203,7 @@ def config_sweep(device: int):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         ps = k.lse_path_stats(reset=True)
+        rs = k.lse_row_stats(reset=True)
         k.timing_enable(True)        # instrumented re-run (direct launches) for the conv time share
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -223,6 +225,7 @@ def config_sweep(device: int):
             rec["k3_pairs"] = ps
             rec["k3_active_frac"] = ps["active"] / max(ps["visited"], 1)
             rec["k3_ffma_frac_of_active"] = ps["ffma"] / max(ps["active"], 1)
+            rec["k3_exact_rows_live_frac"] = rs["live"] / max(rs["visited"], 1)
         out[cfg.name] = rec
         k.close()
     return out

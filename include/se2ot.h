@@ -228,6 +228,11 @@ SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64
                                       int64_t* visited_pairs, int64_t* tilted_pairs, int64_t* hint_redos,
                                       int32_t reset);
 
+/* K3 exact-path row pruning counters since the last reset (synchronises the device): rows of taps
+ * (warp, input orientation, dy) evaluated / visited.  A row is skipped when its largest possible term
+ * lies more than 25 nats below a lower bound of every output of the warp (K3). */
+SE2_API se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_visited, int32_t reset);
+
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)
  * since the last reset (synchronises the events). */

@@ -34,7 +34,7 @@ EXPORTED = [
     "se2_jko_step", "se2_barycenter", "se2_marginal_error", "se2_conv_update", "se2_bary_logmean",
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
     "se2_last_error", "se2_abi_version", "se2_lse_path_stats", "se2_sum_rows", "se2_scale_rows",
-    "se2_transport_cost",
+    "se2_transport_cost", "se2_lse_row_stats",
 ]
 
 
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
         "se2_lse_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                                ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
+        "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

@@ -86,6 +86,12 @@ class Kernel:
                                           ctypes.byref(t), ctypes.byref(h), 1 if reset else 0))
         return dict(active=a.value, ffma=f.value, visited=v.value, tilted=t.value, hint_redos=h.value)
 
+    def lse_row_stats(self, reset: bool = True) -> dict:
+        """K3 exact-path rows of taps (warp, theta_i, dy) evaluated / visited after row pruning."""
+        live, vis = ctypes.c_int64(), ctypes.c_int64()
+        check(L.load().se2_lse_row_stats(self._h, ctypes.byref(live), ctypes.byref(vis), 1 if reset else 0))
+        return dict(live=live.value, visited=vis.value)
+
     def timing_enable(self, on: bool = True):
         check(L.load().se2_timing_enable(self._h, 1 if on else 0))
 

@@ -242,6 +242,7 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     const size_t tabl = (size_t)k->nt * k->nt * k->S * ((k->S + 3) / 4 * 4) * sizeof(float);
     cudaError_t e = cudaMalloc(&k->Eq, tab);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lq, tab);
+    if (e == cudaSuccess) e = cudaMalloc(&k->LqRow, (size_t)nquads * k->nt * k->S * 4 * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&k->Wl, tabl);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lth, sizeof(float) * k->nt * k->nt);
     if (e == cudaSuccess) e = cudaMalloc(&k->LseS, sizeof(float) * k->nt * k->nt);
@@ -257,8 +258,8 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     {
         const size_t nst = lse_fast_stats_floats(k, max_batch);
         cudaError_t e2 = cudaMalloc(&k->lstats, sizeof(float) * nst);
-        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(int) * 8);
-        if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(int) * 8);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(int) * 16);
+        if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(int) * 16);
         // theta_i-split scratch for grids that give fewer than 2 CTAs per SM (at most 8 groups, 64 MB)
         {
             const int64_t N = k->N();
@@ -307,6 +308,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->Lth) cudaFree(k->Lth);
     if (k->LseS) cudaFree(k->LseS);
     if (k->Lq) cudaFree(k->Lq);
+    if (k->LqRow) cudaFree(k->LqRow);
     if (k->Wl) cudaFree(k->Wl);
     if (k->Wcl) cudaFree(k->Wcl);
     if (k->Lcq) cudaFree(k->Lcq);
@@ -832,6 +834,18 @@ se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma
     if (tilted_pairs) *tilted_pairs = h[3];
     if (hint_redos) *hint_redos = h[4];
     if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 5));
+    return SE2_OK;
+}
+
+se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_visited, int32_t reset) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    DeviceGuard g(k->device);
+    unsigned long long h[2] = {0, 0};
+    SE2_CUDA_TRY(cudaDeviceSynchronize());
+    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters + 8, sizeof(h), cudaMemcpyDeviceToHost));
+    if (rows_live) *rows_live = (int64_t)h[0];
+    if (rows_visited) *rows_visited = (int64_t)h[1];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters + 8, 0, sizeof(h)));
     return SE2_OK;
 }
 

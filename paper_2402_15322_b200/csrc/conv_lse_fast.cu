@@ -40,8 +40,9 @@ struct LseFCfg {
     static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * S * 4;
+    static constexpr int RMX = S * 4;            // per tap row: max over dx of the L2 table (4 q)
     static constexpr int MAXNT = 128;
-    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL) * sizeof(float) + 64;
+    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL + 2 * RMX) * sizeof(float) + 64;
 };
 constexpr int kLseTileY = 32, kLseTileX = 16;
 constexpr int kStat = 8;   // per tile: a, gx, gy, rmin, rmax, vmin, vmax, valid-plane flag
@@ -146,6 +147,7 @@ __device__ __forceinline__ void plane_diff_range(float da, float dgx, float dgy,
 template <int R>
 __global__ void __launch_bounds__(LseFCfg<R>::NT)
 conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq, const float* __restrict__ Lq,
+                     const float* __restrict__ LqRow,
                      const float* __restrict__ Lth, const float* __restrict__ LseS, const float* __restrict__ st,
                      int nx, int ny, int nt, int tiles_x, int tiles_y, int force_exact, Epilogue epi,
                      int* __restrict__ counters, int ngroups, float* __restrict__ split_out) {
@@ -153,7 +155,8 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     extern __shared__ __align__(16) float smem[];
     float* sWin = smem;
     float* sFil = smem + 2 * C::WIN;
-    float* sRed = sFil + 2 * C::FIL;
+    float* sRmx = sFil + 2 * C::FIL;
+    float* sRed = sRmx + 2 * C::RMX;
     __shared__ float sMu[C::MAXNT], sM[C::MAXNT], sLB[4];
     __shared__ float sA[C::MAXNT], sGx[C::MAXNT], sGy[C::MAXNT], sShift[C::MAXNT];
     __shared__ float sCoef[C::MAXNT][4];
@@ -311,10 +314,20 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         const float* fsrc = (path == 1 ? Eq : Lq) + ((int64_t)qd * nt + ti) * C::FIL;
         float* df = sFil + buf * C::FIL;
         for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) cp_async16(df + 4 * i, fsrc + 4 * i);
+        const float* rsrc = LqRow + ((int64_t)qd * nt + ti) * C::RMX;
+        float* dr = sRmx + buf * C::RMX;
+        for (int i = threadIdx.x; i < C::RMX / 4; i += C::NT) cp_async16(dr + 4 * i, rsrc + 4 * i);
         cp_async_commit();
     };
 
     float Macc[4][C::P], Sacc[4][C::P];
+    unsigned vmask = 0;   // outputs of this thread inside the grid (bit 4q + p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < C::P; ++p)
+            if (4 * qd + q < nt && y0 + lane < ny && x0 + wx * C::P + p < nx) vmask |= 1u << (4 * q + p);
+    unsigned rows_live = 0, rows_seen = 0;
     // hinted shifts: verified here (whole-CTA redo) when unsplit; in a theta_i split the partial sums
     // cannot be judged alone, so the combine kernel verifies the total and recomputes bad outputs
     const bool have_hint = (epi.hint_in != nullptr);
@@ -331,7 +344,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 const int to = 4 * qd + q, gy = y0 + lane, gx = x0 + wx * C::P + p;
                 if (to < nt && gy < ny && gx < nx) {
                     const float h = epi.hint_in[(int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx];
-                    if (h > -1e30f && h < 1e30f) Macc[q][p] = ((h - ref) + 20.f) * kLog2e;
+                    if (h > -1e30f && h < 1e30f) Macc[q][p] = ((h - ref) + kHintAbove) * kLog2e;
                 }
             }
         }
@@ -501,7 +514,34 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             }
         } else {
             // ---------------- exact path: two passes over the taps of this channel (pass A, the
-            // per-output maximum, is skipped when the output shift comes from a verified hint)
+            // per-output maximum, is skipped when the output shift comes from a verified hint).
+            // Row pruning: the row dy of taps is skipped by the whole warp when, for every output of
+            // every lane, its largest possible term  max_dx L2(dy, .) + max(row segment of lv)  is below
+            // thr = (lower bound of the output) - gap, in pass B: the running max (<= ly) - kRowGap, or
+            // with a hint the verified floor h - kHintDrop - kRowGap; the skipped terms then total
+            // < S^2 nt e^-25 of the output.  (Pruning pass A as well costs 87 registers; pass A only
+            // runs without a hint.)
+            const float4* rmx = reinterpret_cast<const float4*>(sRmx + buf * C::RMX);
+            float thr[4];
+            auto set_thr = [&](float drop2) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float t = INFINITY;
+#pragma unroll
+                    for (int p = 0; p < C::P; ++p)
+                        if (vmask & (1u << (4 * q + p))) t = fminf(t, Macc[q][p]);
+                    thr[q] = t - drop2;
+                }
+            };
+            auto row_live = [&](const float* r, int dy) -> bool {
+                float sm = r[0];
+#pragma unroll
+                for (int j = 1; j < C::P + 2 * R; ++j) sm = fmaxf(sm, r[j]);
+                const float4 m4 = rmx[dy];
+                const bool live = (sm + m4.x >= thr[0]) || (sm + m4.y >= thr[1]) || (sm + m4.z >= thr[2]) ||
+                                  (sm + m4.w >= thr[3]);
+                return __any_sync(0xffffffffu, live);
+            };
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -539,6 +579,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                         Macc[q][p] = mn;
                     }
             }
+            set_thr((use_hint ? (kHintAbove + kHintDrop + kRowGap) : kRowGap) * kLog2e);
 #pragma unroll 1
             for (int dy = 0; dy < C::S; ++dy) {
                 const float4* rowp = reinterpret_cast<const float4*>(win + (lane - dy + 2 * R) * C::PITCH);
@@ -548,6 +589,9 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     float4 t = rowp[j];
                     r[4 * j + 0] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
                 }
+                ++rows_seen;
+                if (!row_live(r, dy)) continue;
+                ++rows_live;
                 const float4* frow = fil + dy * C::S;
 #pragma unroll
                 for (int dx = 0; dx < C::S; ++dx) {
@@ -568,8 +612,9 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         __syncthreads();
     }
     if (!use_hint || ngroups > 1) break;
-    // verify the hinted shifts: every stored output must have a finite, non-overflowing sum whose largest
-    // terms were not flushed (sum >= 2^-60 relative to the shift); otherwise the CTA redoes two-pass
+    // verify the hinted shifts: every stored output must have a finite, non-overflowing sum and lie at
+    // least at h - kHintDrop (sum >= e^-(kHintAbove + kHintDrop) relative to the shift h + kHintAbove: the
+    // floor the row pruning assumed); otherwise the CTA redoes two-pass
     bool bad = false;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -578,13 +623,18 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             const int to = 4 * qd + q, gyy = y0 + lane, gxx = x0 + wx * C::P + p;
             if (to < nt && gyy < ny && gxx < nx) {
                 const float sv = Sacc[q][p];
-                if (!(sv >= 8.67361738e-19f && sv <= 1.2676506e30f)) bad = true;   // [2^-60, 2^100]
+                if (!(sv >= 9.3576230e-14f && sv <= 1.2676506e30f)) bad = true;   // [e^-30, 2^100]
             }
         }
     if (!__syncthreads_or(bad)) break;
     if (counters != nullptr && threadIdx.x == 0) atomicAdd(&counters[4], 1);   // hint redo
     }
 
+    if (counters != nullptr && lane == 0 && rows_seen > 0) {
+        unsigned long long* rc = reinterpret_cast<unsigned long long*>(counters + 8);
+        atomicAdd(&rc[0], (unsigned long long)rows_live);
+        atomicAdd(&rc[1], (unsigned long long)rows_seen);
+    }
     float err = 0.f;
     const int gy = y0 + lane;
     if (gy < ny) {
@@ -684,10 +734,10 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
                     ly = m + logf(s);
                 }
                 if (epi.hint_in != nullptr) {
-                    // the partials used shift = hint + 20 nats: valid iff no overflow (finite) and the
-                    // total is at most 40 nats below the hint (largest terms stayed normal fp32)
+                    // the partials used shift = hint + kHintAbove and rows pruned against the floor
+                    // h - kHintDrop: valid iff no overflow (finite) and the total reached that floor
                     const float h = epi.hint_in[idx];
-                    if (!(ly < 1e30f && ly >= h - 40.f)) {
+                    if (!(ly < 1e30f && ly >= h - kHintDrop)) {
                         ly = exact_lse_point(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, gy, gx);
                         if (counters != nullptr) atomicAdd(&counters[4], 1);
                     }
@@ -731,7 +781,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     if (groups > 1 && (size_t)groups * batch * k->N() > split_floats) groups = 1;
     if (bpf) *bpf = ntile * nquad;
     dim3 grid(ntile, nquad * groups, batch);
-    conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->Lth, k->LseS, stats, k->nx, k->ny,
+    conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->LqRow, k->Lth, k->LseS, stats, k->nx, k->ny,
                                                           k->nt, tiles_x, tiles_y, force_exact, epi, counters,
                                                           groups, split_scratch);
     count_launch();

@@ -42,6 +42,12 @@ constexpr float kEsShift = 40.f;
 constexpr float kFastRange = 100.f;
 constexpr float kShiftAbove = 62.f;   // per-channel shift m = tile min + kShiftAbove
 constexpr float kPruneGap = 30.f;     // channels whose upper bound is < lower bound - kPruneGap are skipped
+// exact path row pruning (K3): a row of taps is skipped for a warp when its largest possible term is
+// more than kRowGap nats below a lower bound of every output of the warp; with a hint h (previous
+// output) the shift is h + kHintAbove and the result is accepted only if ly >= h - kHintDrop
+constexpr float kRowGap = 25.f;
+constexpr float kHintAbove = 20.f;
+constexpr float kHintDrop = 10.f;
 
 // Epilogue ops of the fused conv (see se2_conv_update in se2ot.h)
 enum EpiOp : int {
@@ -98,13 +104,15 @@ struct se2_kernel_s {
     float* Lth = nullptr;   // [nt][nt] theta part of L (natural log)
     float* LseS = nullptr;  // [nt][nt] log sum_taps exp(Ls)
     float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
+    float* LqRow = nullptr; // [nt/4][nt][S][4] max over dx of Lq (row bounds of the exact path)
     float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
     float* Wcl = nullptr;   // cost tables (built on first se2_transport_cost): rho^2 exp(-rho^2/eps), Wl layout
     float* Lcq = nullptr;   //   and log2(rho^2) + L2, Lq layout
     size_t table_bytes = 0;
     void* extra = nullptr;        // grow-only workspaces (api.cu)
     float* lstats = nullptr;      // [max_batch][nt][tiles][8] per-tile plane fit + ranges of log fields (K3)
-    int* lse_counters = nullptr;  // K3 path counters: active, FFMA (incl. tilted), visited, tilted pairs
+    int* lse_counters = nullptr;  // K3 path counters: active, FFMA (incl. tilted), visited, tilted pairs,
+                                  // hint redos; [8..11] = two uint64: exact-path rows live / visited
     float* split = nullptr;       // K3 theta_i-split partials (small grids): [groups][max_batch][N]
     size_t split_floats = 0;
     se2::Timing timing;

@@ -13,6 +13,7 @@
 //                                16-byte shared-memory broadcast feeds four output orientations)
 //   Eq [nt/4][nt][S][S][4]       exp(Ls + kEsShift) (factored LSE engine)
 //   Lth[to][ti], LseS[to][ti]    Lth and log sum_{dx,dy} exp(Ls) (natural logs)
+//   LqRow [nt/4][nt][S][4]       max over dx of Lq (per tap row: the exact path's row bounds)
 #include <math.h>
 
 #include "se2_internal.cuh"
@@ -115,6 +116,19 @@ __global__ void tabulate_cost_kernel(double hx, double hy, int nt, int R, double
     }
 }
 
+// LqRow[qd][ti][dy][q] = max_dx Lq[qd][ti][dy][dx][q] (after tabulate_kernel; padding quads stay 0)
+__global__ void tabulate_rowmax_kernel(int nquads, int nt, int S, const float* __restrict__ Lq,
+                                       float* __restrict__ LqRow) {
+    const int64_t total = (int64_t)nquads * nt * S * 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(i & 3);
+        const int64_t row = i >> 2;   // (qd, ti, dy)
+        float m = -INFINITY;
+        for (int dx = 0; dx < S; ++dx) m = fmaxf(m, Lq[(row * S + dx) * 4 + q]);
+        LqRow[i] = m;
+    }
+}
+
 cudaError_t tabulate_cost(se2_kernel_s* k, cudaStream_t s) {
     const int64_t total = (int64_t)k->nt * k->nt * k->S * k->S;
     int blocks = (int)((total + 255) / 256);
@@ -140,6 +154,11 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
                                                k->Eq, k->Lq, k->Wl, nnz_dev);
     tabulate_theta_kernel<<<(nt * nt + 127) / 128, 128, 0, s>>>(k->hx, k->hy, nt, k->R, k->eps, k->w1, k->w2,
                                                                   k->w3, k->Lth, k->LseS);
+    {
+        const int nquads = (nt + 3) / 4;
+        const int64_t rows = (int64_t)nquads * nt * S * 4;
+        tabulate_rowmax_kernel<<<(int)((rows + 255) / 256), 256, 0, s>>>(nquads, nt, S, k->Lq, k->LqRow);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }
     std::vector<int> nnz(nt * nt);

@@ -35,6 +35,7 @@ y = torch.empty_like(v)
 se2_conv(k, v, y, log_domain=True, lse_exact=a.exact)
 torch.cuda.synchronize()
 k.lse_path_stats(reset=True)
+k.lse_row_stats(reset=True)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(a.reps):
@@ -43,7 +44,9 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
 ps = k.lse_path_stats(reset=True)
+rs = k.lse_row_stats(reset=True)
 vv = v.cpu().numpy()
 print(f"{a.cfg} state after {a.iters} iters: lv range [{vv.min():.1f}, {vv.max():.1f}]; "
       f"{'K4' if a.exact else 'K3'} conv over {F} fields: {ms:.3f} ms; pairs {ps}, "
-      f"active {ps['active'] / max(ps['visited'], 1):.3f}, ffma/active {ps['ffma'] / max(ps['active'], 1):.3f}")
+      f"active {ps['active'] / max(ps['visited'], 1):.3f}, ffma/active {ps['ffma'] / max(ps['active'], 1):.3f}, "
+      f"exact rows live {rs['live'] / max(rs['visited'], 1):.3f}")
