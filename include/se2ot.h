@@ -63,6 +63,7 @@ typedef enum {
 #define SE2_LSE_NOTILT 0x10u  /* diagnostics: K3 without its gradient-tilted FFMA path           */
 #define SE2_LSE_K3EXACT 0x20u /* diagnostics: K3 with every active channel on its exact path     */
 #define SE2_NO_GRAPH 0x40u    /* solvers: launch directly instead of replaying a CUDA graph       */
+#define SE2_NO_PERSISTENT 0x80u /* se2_sinkhorn: never use the one-launch cluster solver (K9)     */
 
 typedef struct {
     int32_t nx, ny, ntheta;

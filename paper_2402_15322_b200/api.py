@@ -145,16 +145,19 @@ def make_porous_prox(tau: float, m: float) -> L.se2_prox:
 
 def se2_sinkhorn(k: Kernel, mu: torch.Tensor, nu: Optional[torch.Tensor], a: torch.Tensor, b: torch.Tensor,
                  iters: int, log_domain: bool, prox: Optional[L.se2_prox] = None, trace: bool = False,
-                 warm_start: bool = False, lse_exact: bool = False, no_graph: bool = False) -> Optional[np.ndarray]:
+                 warm_start: bool = False, lse_exact: bool = False, no_graph: bool = False,
+                 persistent: bool = True) -> Optional[np.ndarray]:
     """Scaling iterations a = mu / K b, b = prox(K^T a)/K^T a.  Returns the marginal
-    error trace [iters][batch] when trace=True."""
+    error trace [iters][batch] when trace=True.  persistent=False disables the one-launch cluster
+    solver (K9) that small log-domain problems use otherwise."""
     _check_field(mu, k, "mu")
     batch = mu.numel() // k.N
     for name, t in (("a", a), ("b", b)):
         _check_field(t, k, name, batch)
     if nu is not None:
         _check_field(nu, k, "nu", batch)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace, warm_start, lse_exact, no_graph))
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace, warm_start, lse_exact, no_graph)
+                      | (0 if persistent else L.SE2_NO_PERSISTENT))
     tr = np.zeros((max(iters, 1), batch), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None
     check(L.load().se2_sinkhorn(k.handle, _ptr(mu), _ptr(nu), _ptr(a), _ptr(b), batch,

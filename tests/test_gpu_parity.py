@@ -64,9 +64,12 @@ def _cmp_meas(name, got, ref):
     return e
 
 
+@pytest.mark.parametrize("persistent", [True, False], ids=["K9", "K3"])
 @pytest.mark.parametrize("case", ["c0"])
-def test_sinkhorn_parity(case, cuda_device):
-    from paper_2402_15322_b200 import se2_conv, se2_sinkhorn
+def test_sinkhorn_parity(case, persistent, cuda_device):
+    """c0 through the one-launch cluster solver (K9, the default for this size) and through the
+    per-conv K3 path."""
+    from paper_2402_15322_b200 import se2_conv, se2_launch_count, se2_sinkhorn
     pc = S.get_parity_case(case)
     cfg, d = S.parity_inputs(pc)
     gold = _golden(case)
@@ -74,7 +77,13 @@ def test_sinkhorn_parity(case, cuda_device):
     mu, nu = _dev(d["mus"][0]), _dev(d["mus"][1])
     a = torch.empty_like(mu)
     b = torch.empty_like(mu)
-    tr = se2_sinkhorn(k, mu, nu, a, b, cfg.iters, cfg.log_domain, trace=True)
+    n0 = se2_launch_count()
+    tr = se2_sinkhorn(k, mu, nu, a, b, cfg.iters, cfg.log_domain, trace=True, persistent=persistent)
+    launches = se2_launch_count() - n0
+    if persistent:
+        assert launches <= 3, launches          # K9 + the two non-finite checks
+    else:
+        assert launches > cfg.iters, launches
     assert cfg.log_domain
     _cmp_pot("alpha", _sel(_host(a), gold, pc.full_fields), gold["alpha"].reshape(-1))
     _cmp_pot("beta", _sel(_host(b), gold, pc.full_fields), gold["beta"].reshape(-1))
@@ -167,9 +176,9 @@ def test_graph_replay_equals_direct_launches(cuda_device):
     k0 = _kernel(cfg0, 1)
     mu, nu = _dev(d0["mus"][0]), _dev(d0["mus"][1])
     a1, b1, a2, b2 = (torch.empty_like(mu) for _ in range(4))
-    t1 = se2_sinkhorn(k0, mu, nu, a1, b1, 20, True, trace=True, no_graph=True)
+    t1 = se2_sinkhorn(k0, mu, nu, a1, b1, 20, True, trace=True, no_graph=True, persistent=False)
     for _ in range(2):
-        t2 = se2_sinkhorn(k0, mu, nu, a2, b2, 20, True, trace=True)
+        t2 = se2_sinkhorn(k0, mu, nu, a2, b2, 20, True, trace=True, persistent=False)
         assert torch.equal(a1, a2) and torch.equal(b1, b2) and np.array_equal(t1, t2)
 
 
@@ -187,3 +196,62 @@ def test_sinkhorn_jko_determinism(cuda_device):
         outs.append((nxt.clone(), mass, tr))
     assert torch.equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
     assert np.array_equal(outs[0][2], outs[1][2])
+
+
+@pytest.mark.parametrize("shape", [(12, 10, 8, 2, False), (9, 7, 4, 1, True), (16, 16, 8, 3, True), (20, 18, 12, 4, False)],
+                         ids=["12x10x8", "9x7x4-warm", "16x16x8-warm", "20x18x12"])
+def test_sinkhorn_k9_ragged(shape, cuda_device):
+    """K9 (one cluster launch) on ragged grids (N not a multiple of 16 -> smaller clusters), with and
+    without a warm start, against the fp64 oracle's log-domain Sinkhorn run on the same inputs."""
+    import oracle as O
+    from paper_2402_15322_b200 import Kernel, se2_launch_count, se2_sinkhorn
+    nx, ny, nt, R, warm = shape
+    g = O.Grid(nx, ny, nt)
+    eps, w = 0.05, (1.0, 3.0, 1.0)
+    rng = np.random.default_rng(nx * ny + nt)
+    mu = rng.random(g.shape) ** 4 + 1e-6
+    nu = rng.random(g.shape) ** 4 + 1e-6
+    mu, nu = mu / mu.sum(), nu / nu.sum()
+    mu[0, 0, :3] = 0.0          # zero mass: log mu = -inf must propagate as alpha = -inf
+    mu /= mu.sum()
+    iters = 40
+    T = O.kernel_table(g, R, eps, w)
+    L = O.log_kernel_table(g, R, eps, w)
+    k = Kernel(nx, ny, nt, eps, w, R, max_batch=1, device=0)
+    a = torch.empty(g.shape, device="cuda")
+    b = torch.zeros(g.shape, device="cuda")
+    beta0 = None
+    if warm:
+        beta0 = rng.normal(0.0, 2.0, g.shape)
+        b.copy_(torch.from_numpy(beta0.astype(np.float32)))
+        beta0 = b.cpu().numpy().astype(np.float64)
+    n0 = se2_launch_count()
+    tr = se2_sinkhorn(k, _dev(mu), _dev(nu), a, b, iters, True, trace=True, warm_start=warm)
+    assert se2_launch_count() - n0 <= 3
+    # oracle: the same iteration from the same beta0 (log domain, P:557-560)
+    lmu, lnu = np.log(mu), np.log(nu)
+    beta = np.zeros(g.shape) if beta0 is None else beta0
+    errs = []
+    with np.errstate(divide="ignore", invalid="ignore"):
+        for _ in range(iters):
+            alpha = np.where(lmu == -np.inf, -np.inf, lmu - O.lse_conv(L, beta))
+            beta = lnu - O.lse_conv(L, alpha)
+            errs.append(np.abs(np.exp(alpha + O.lse_conv(L, beta)) - mu).sum())
+    ga, gb = _host(a), _host(b)
+    fin = np.isfinite(alpha)
+    assert np.array_equal(np.isfinite(ga), fin)
+    _cmp_pot("alpha", ga[fin], alpha[fin])
+    _cmp_pot("beta", gb, beta)
+    assert trace_err(tr[:, 0], np.array(errs)) <= TOL_TRACE
+
+
+def test_sinkhorn_k9_determinism(cuda_device):
+    from paper_2402_15322_b200 import se2_sinkhorn
+    pc0 = S.get_parity_case("c0")
+    cfg0, d0 = S.parity_inputs(pc0)
+    k0 = _kernel(cfg0, 1)
+    mu, nu = _dev(d0["mus"][0]), _dev(d0["mus"][1])
+    a1, b1, a2, b2 = (torch.empty_like(mu) for _ in range(4))
+    t1 = se2_sinkhorn(k0, mu, nu, a1, b1, 50, True, trace=True)
+    t2 = se2_sinkhorn(k0, mu, nu, a2, b2, 50, True, trace=True)
+    assert torch.equal(a1, a2) and torch.equal(b1, b2) and np.array_equal(t1, t2)
