@@ -8,7 +8,7 @@ import os
 import warnings
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libse2ot.so")
+LIB_PATH = os.environ.get("SE2_LIB_PATH") or os.path.join(HERE, "libse2ot.so")   # override: A/B diagnostics
 
 SE2_OK = 0
 SE2_LOG_DOMAIN = 0x1

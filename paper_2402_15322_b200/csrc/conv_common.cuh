@@ -91,6 +91,16 @@ __device__ __forceinline__ float lg2_approx(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// log2 of a positive normal x with ABSOLUTE error ~2^-22: the exponent is taken exactly from the bits
+// and lg2.approx only sees the mantissa in [1, 2) (where its error is absolute).  lg2.approx on large
+// arguments has a relative error, i.e. ~1e-5 absolute at x ~ 2^100, which biased the log-domain
+// convs systematically.  x <= 0 or subnormal -> -inf.
+__device__ __forceinline__ float lg2_norm(float x) {
+    const int ix = __float_as_int(x);
+    const int e = (ix >> 23) - 127;
+    const float m = __int_as_float((ix & 0x007fffff) | 0x3f800000);
+    return (ix >= 0x00800000) ? ((float)e + lg2_approx(m)) : -INFINITY;
+}
 
 // Block-wide deterministic sum of one float per thread; result valid in thread 0.
 template <int NT>

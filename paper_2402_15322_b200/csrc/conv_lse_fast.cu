@@ -42,7 +42,8 @@ struct LseFCfg {
     static constexpr int FIL = S * S * 4;
     static constexpr int RMX = S * 4;            // per tap row: max over dx of the L2 table (4 q)
     static constexpr int MAXNT = 128;
-    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL + 2 * RMX) * sizeof(float) + 64;
+    // window x2, L2 filter x2, exp filter x2 (FFMA candidates decided on the staged window), row max x2
+    static constexpr size_t SMEM = (size_t)(2 * WIN + 4 * FIL + 2 * RMX) * sizeof(float) + 64;
 };
 constexpr int kLseTileY = 32, kLseTileX = 16;
 constexpr int kStat = 8;   // per tile: a, gx, gy, rmin, rmax, vmin, vmax, valid-plane flag
@@ -155,12 +156,13 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     extern __shared__ __align__(16) float smem[];
     float* sWin = smem;
     float* sFil = smem + 2 * C::WIN;
-    float* sRmx = sFil + 2 * C::FIL;
+    float* sFilE = sFil + 2 * C::FIL;   // Eq copy of a candidate channel (path 3 / 5)
+    float* sRmx = sFilE + 2 * C::FIL;
     float* sRed = sRmx + 2 * C::RMX;
     __shared__ float sMu[C::MAXNT], sM[C::MAXNT], sLB[4];
     __shared__ float sA[C::MAXNT], sGx[C::MAXNT], sGy[C::MAXNT], sShift[C::MAXNT];
     __shared__ float sCoef[C::MAXNT][4];
-    __shared__ float sPart[C::NT / 32][4], sPartD[C::NT / 32][4];
+    __shared__ float sPart[C::NT / 32][4], sPartD[C::NT / 32][4], sWmax[C::NT / 32];
     __shared__ float sRhi[C::MAXNT];
     __shared__ int sList[C::MAXNT];
     __shared__ int sNAct, sNFast, sNTilt;
@@ -240,7 +242,10 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     }
     __syncthreads();
     const float ref = sRef;
-    // status per channel: 0 skip, 1 FFMA, 2 exact, 3 tilted FFMA
+    // status per channel: 0 skip, 1 FFMA, 2 exact, 3 tilt candidate, 5 FFMA candidate.  The bound M
+    // is the max over the 3 x 3 tile neighbourhood; candidates (3, 5) are decided on the exact max of
+    // the staged window (M - mu <= kFastRange with the window's own max), a tilt candidate then tries
+    // the tilted kernel, a plain candidate falls back to the exact path.
     for (int i = threadIdx.x; i < nt; i += C::NT) {
         const float M = sM[i], mu = sMu[i];
         int stt = 0;
@@ -256,11 +261,12 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 if (force_exact == 1) stt = 2;
                 else if (mu != NEG_INF && (M - mu) <= kFastRange) stt = 1;
                 else if (force_exact != 2 && sShift[i] == sShift[i]) stt = 3;   // not NaN: tilt valid
+                else if (mu != NEG_INF) stt = 5;
                 else stt = 2;
             }
         }
         sList[i] = stt;
-        if (stt == 1)
+        if (stt == 1 || stt == 3 || stt == 5)
             for (int q = 0; q < 4; ++q) {
                 const int to = 4 * qd + q;
                 const float lt = (to < nt) ? Lth[to * nt + i] : 0.f;
@@ -314,6 +320,11 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         const float* fsrc = (path == 1 ? Eq : Lq) + ((int64_t)qd * nt + ti) * C::FIL;
         float* df = sFil + buf * C::FIL;
         for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) cp_async16(df + 4 * i, fsrc + 4 * i);
+        if (path == 3 || path == 5) {
+            const float* esrc = Eq + ((int64_t)qd * nt + ti) * C::FIL;
+            float* de = sFilE + buf * C::FIL;
+            for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) cp_async16(de + 4 * i, esrc + 4 * i);
+        }
         const float* rsrc = LqRow + ((int64_t)qd * nt + ti) * C::RMX;
         float* dr = sRmx + buf * C::RMX;
         for (int i = threadIdx.x; i < C::RMX / 4; i += C::NT) cp_async16(dr + 4 * i, rsrc + 4 * i);
@@ -363,8 +374,30 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
         float* dw = sWin + buf * C::WIN;
         float* df = sFil + buf * C::FIL;
         // transform the elements this thread staged (its own cp.async copies are complete)
-        int epath = path;   // effective path of this channel (a tilt candidate may fall back to exact)
-        if (path == 3) {
+        int epath = path;   // effective path of this channel (a candidate may end FFMA, tilted or exact)
+        if (path == 3 || path == 5) {
+            // exact max of the staged window: the elements this thread staged, then the block
+            float wm = NEG_INF;
+            for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
+                const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+                wm = fmaxf(wm, dw[r * C::PITCH + c]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+            if (lane == 0) sWmax[wx] = wm;
+            __syncthreads();
+            wm = sWmax[0];
+#pragma unroll
+            for (int w2 = 1; w2 < C::NT / 32; ++w2) wm = fmaxf(wm, sWmax[w2]);
+            if (wm - sMu[ti] <= kFastRange) {
+                epath = 1;
+                df = sFilE + buf * C::FIL;
+                if (path == 5 && counters != nullptr && threadIdx.x == 0) atomicAdd(&counters[1], 1);
+            } else if (path == 5) {
+                epath = 2;
+            }
+        }
+        if (epath == 3) {
             // tilted candidate: T2(d) = (Ls(d) - g.d) log2 e from the staged L table.  c1 = max_d T2 over
             // the box; c1D = max over the taps valid for every output of the tile (a sub-box, clipped by
             // the zero padding).  The shift m = R_lo + 62 - dc, dc = max_q (c1 - c1D) (natural), is valid
@@ -456,7 +489,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             }
         }
         if (epath == 1 || epath == 2) {
-            const float shift = (epath == 1) ? (sMu[ti] + kShiftAbove) : ref;
+            const float shift = (epath == 1) ? (sMu[ti] + kShiftAbove) : ref;   // FFMA: m = mu + 62
             for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
                 int r = i / C::WIN_W, c = i - r * C::WIN_W;
                 float v = dw[r * C::PITCH + c];
@@ -506,7 +539,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
 #pragma unroll
                 for (int p = 0; p < C::P; ++p) {
                     const float tilt = gx2 * ((float)(x0 + wx * C::P + p) - cx0);
-                    const float t = lg2_approx(acc[q][p]) + (cf + tilt);     // lg2(0) = -inf: no contribution
+                    const float t = lg2_norm(acc[q][p]) + (cf + tilt);     // lg2(0) = -inf: no contribution
                     const float mx = fmaxf(Macc[q][p], t);
                     Sacc[q][p] = Sacc[q][p] * ex2_approx(Macc[q][p] - mx) + ex2_approx(t - mx);
                     Macc[q][p] = mx;

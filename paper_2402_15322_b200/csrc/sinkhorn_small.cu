@@ -85,7 +85,7 @@ __device__ __forceinline__ float k9_lse2(const float* __restrict__ f, const floa
     const bool none = (mg == -INFINITY);   // uniform over the group; every lane still reaches the shuffles
     s = (m == -INFINITY) ? 0.f : s * ex2_approx(m - mg);
     for (int o = 1; o < split; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return none ? -INFINITY : mg + lg2_approx(s);
+    return none ? -INFINITY : mg + lg2_norm(s);
 }
 
 template <int R>
