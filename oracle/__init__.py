@@ -15,3 +15,4 @@ against closed forms, worked values, brute force or invariants; see DESIGN.md
 those pins (the paper prints no worked numbers for them).
 """
 from .se2_oracle import *  # noqa: F401,F403
+from . import se2_lift  # noqa: F401  (lifting / projection, SURVEY §8f NEXT #3)
