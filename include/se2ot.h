@@ -243,6 +243,59 @@ SE2_API se2_status se2_timing_get(se2_kernel k, int64_t* n_launches, double* con
 /* Number of kernel launches this library has issued in this process (all entry points). */
 SE2_API int64_t se2_launch_count(void);
 
+/* ------------------------------------------------------------------------------------------
+ * Lifting and projection: images and orientation fields <-> measures on the
+ * SE(2) grid.  A lifting context (se2_cake) owns the cake-wavelet bank and the reduction scratch of
+ * these calls; all arrays are device fp32, images [batch][ny][nx], SE(2) fields
+ * [batch][ntheta][ny][nx] (theta_k = 2 pi k / ntheta), contiguous, caller-owned.  Calls returning
+ * host scalars synchronise the stream.
+ *
+ * se2_cake_build -- cake wavelets (App. B; reading R15): in the Fourier domain on the
+ *   size x size DFT lattice omega = 2 pi k / size,
+ *     psi^_j(omega) = B_deg( wrap(arg omega - theta_j - pi/2) / (2 pi / ntheta) ) W(|omega|),
+ *     W(rho) = 1 for rho <= c pi, exp(-(rho - c pi)^2 / (2 ((1 - c) pi / 2)^2)) beyond,  psi^_j(0) = 1/ntheta,
+ *   B_deg the centred cardinal B-spline, c = radial_cut; the table is Re psi_j(d) =
+ *   size^-2 sum_omega psi^_j(omega) cos(omega . d), d in [-R, R]^2 (size = 2R + 1 odd), computed on the
+ *   device in fp64.  Requires ntheta >= spline_degree + 1, 0 <= spline_degree <= 7, 0 < radial_cut < 1.
+ * se2_lift_image -- orientation score (eq. `eq:lift`): U[b][j][y][x] = sum_d Re psi_j(d)
+ *   f[b][y + dy][x + dx], zero padding outside the image.
+ * se2_split_signed -- (eq. `eq:tildeW-v1`): Upos = max(U, 0) / m+, Uneg = max(-U, 0) / m-
+ *   per field of n elements; masses_host[b][0..1] = (m+, m-) in fp64; a part with zero mass is all zeros.
+ *   floor_rel > 0 adds floor_rel * max(part) to every site of a nonempty part before normalising (the
+ *   configs' "1e-6 floor" input recipe; keeps the log-domain App. A iteration off empty windows, R17).
+ * se2_project -- (eq. `eq:proj`): img[b][y][x] = sum_j U[b][j][y][x].
+ * se2_project_signed -- (eq. `eq:final`): img = max(m+ P(Upos) - m- P(Uneg), 0) / sum, the
+ *   "dominant positive response" normalised to mass 1; masses from se2_split_signed (host [batch][2]);
+ *   mass_host[b] = the sum before normalisation (0 -> img all zeros).
+ * se2_lift_field -- orientation-field lift (eq. `equ:lifting_vector_field`): U[b][k][y][x] =
+ *   mag / m if k is the bin of angle (d_S1(angle, theta_k) < pi/ntheta, the lower bin at exactly pi/ntheta,
+ *   reading R16; decided in fp64 as k = ceil(wrap_[0,2pi)(angle) ntheta / 2pi - 1/2) mod ntheta), else 0;
+ *   m = sum mag (mass_host[b]).  mag must be >= 0.
+ * se2_reconstruct_field -- (eq. `equ:reconstruction_vector_field`): mag = sum_k U, angle =
+ *   theta of the first maximum over k; sites with mag < threshold or mag == 0 get (0, 0).
+ * ---------------------------------------------------------------------------------------- */
+typedef struct se2_cake_s* se2_cake; /* opaque lifting context */
+SE2_API se2_status se2_cake_build(int32_t ntheta, int32_t size, int32_t spline_degree, double radial_cut,
+                                  int32_t device, se2_cake* out);
+SE2_API se2_status se2_cake_get(se2_cake c, float* table_host /* ntheta*size*size, nullable */, int32_t* ntheta,
+                                int32_t* size);
+SE2_API void se2_cake_destroy(se2_cake c);
+SE2_API se2_status se2_lift_image(se2_cake c, const float* f, float* U, int32_t nx, int32_t ny, int32_t batch,
+                                  se2_stream stream);
+SE2_API se2_status se2_split_signed(se2_cake c, const float* U, float* Upos, float* Uneg, int64_t n, int32_t batch,
+                                    double floor_rel, double* masses_host, se2_stream stream);
+SE2_API se2_status se2_project(se2_cake c, const float* U, float* img, int32_t nx, int32_t ny, int32_t batch,
+                               se2_stream stream);
+SE2_API se2_status se2_project_signed(se2_cake c, const float* Upos, const float* Uneg, const double* masses_host,
+                                      float* img, int32_t nx, int32_t ny, int32_t batch, double* mass_host,
+                                      se2_stream stream);
+SE2_API se2_status se2_lift_field(se2_cake c, const float* angle, const float* mag, float* U, int32_t nx, int32_t ny,
+                                  int32_t batch, double* mass_host, se2_stream stream);
+SE2_API se2_status se2_reconstruct_field(se2_cake c, const float* U, float* angle, float* mag, int32_t nx, int32_t ny,
+                                         int32_t batch, float threshold, se2_stream stream);
+/* y[i] = exp(x[i]) (expf), e.g. a log-domain barycenter -> the measure the projection takes. */
+SE2_API se2_status se2_exp(const float* x, float* y, int64_t n, se2_stream stream);
+
 SE2_API const char* se2_last_error(void);
 SE2_API int32_t se2_abi_version(void);
 

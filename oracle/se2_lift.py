@@ -117,16 +117,26 @@ def lift_image(f, bank_real) -> np.ndarray:
     return U
 
 
-def split_signed(U):
+def split_signed(U, floor_rel: float = 0.0):
     """(U^+, U^-, m^+, m^-): positive and negative parts, each normalised to mass 1 (eq. tildeW-v1,
-    P:808-809).  A part with zero mass is returned as zeros with mass 0."""
+    P:808-809); m^+- are the parts' masses before normalisation.  floor_rel > 0 adds floor_rel * max(part)
+    to every site of a part before normalising (the configs' input recipe "plus a 1e-6 floor",
+    B:configs; keeps the log-domain App. A iteration away from empty windows -- reading R17).  A part
+    with zero mass is returned as zeros."""
     U = np.asarray(U, dtype=np.float64)
-    pos, neg = np.maximum(U, 0.0), np.maximum(-U, 0.0)
-    ax = (-3, -2, -1)
-    mp, mn = pos.sum(axis=ax), neg.sum(axis=ax)
-    sp = np.where(mp > 0, mp, 1.0)
-    sn = np.where(mn > 0, mn, 1.0)
-    return pos / sp[..., None, None, None], neg / sn[..., None, None, None], mp, mn
+    out = []
+    masses = []
+    for part in (np.maximum(U, 0.0), np.maximum(-U, 0.0)):
+        ax = (-3, -2, -1)
+        m = part.sum(axis=ax)
+        mx = part.max(axis=ax)
+        n = part.shape[-3] * part.shape[-2] * part.shape[-1]
+        fl = floor_rel * mx
+        tot = m + fl * n
+        x = (part + fl[..., None, None, None]) / np.where(tot > 0, tot, 1.0)[..., None, None, None]
+        out.append(np.where((m > 0)[..., None, None, None], x, 0.0))
+        masses.append(m)
+    return out[0], out[1], masses[0], masses[1]
 
 
 def project(U) -> np.ndarray:

@@ -36,6 +36,8 @@ EXPORTED = [
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
     "se2_last_error", "se2_abi_version", "se2_lse_path_stats", "se2_sum_rows", "se2_scale_rows",
     "se2_transport_cost", "se2_lse_row_stats",
+    "se2_cake_build", "se2_cake_get", "se2_cake_destroy", "se2_lift_image", "se2_split_signed", "se2_project",
+    "se2_project_signed", "se2_lift_field", "se2_reconstruct_field", "se2_exp",
 ]
 
 
@@ -105,6 +107,15 @@ def load(path: str = LIB_PATH):
                                ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
         "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
+        "se2_cake_build": [i32, i32, i32, dbl, i32, ctypes.POINTER(P)],
+        "se2_cake_get": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "se2_lift_image": [P, P, P, i32, i32, i32, P],
+        "se2_split_signed": [P, P, P, P, i64, i32, dbl, pd, P],
+        "se2_project": [P, P, P, i32, i32, i32, P],
+        "se2_project_signed": [P, P, P, pd, P, i32, i32, i32, pd, P],
+        "se2_lift_field": [P, P, P, P, i32, i32, i32, pd, P],
+        "se2_reconstruct_field": [P, P, P, P, i32, i32, i32, ctypes.c_float, P],
+        "se2_exp": [P, P, i64, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -112,6 +123,8 @@ def load(path: str = LIB_PATH):
         f.restype = ctypes.c_int
     lib.se2_kernel_destroy.argtypes = [P]
     lib.se2_kernel_destroy.restype = None
+    lib.se2_cake_destroy.argtypes = [P]
+    lib.se2_cake_destroy.restype = None
     lib.se2_last_error.argtypes = []
     lib.se2_last_error.restype = ctypes.c_char_p
     lib.se2_abi_version.argtypes = []

@@ -193,7 +193,7 @@ def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain
         raise ValueError(f"lambdas must be [nsolve][{n}]")
     nsolve = lam.shape[0]
     if bary is None:
-        bary = torch.empty((nsolve,) + tuple(mus.shape[-3:]), device=mus.device, dtype=torch.float32)
+        bary = torch.empty((nsolve, k.ntheta, k.ny, k.nx), device=mus.device, dtype=torch.float32)
     _check_field(bary, k, "bary", nsolve)
     for name, t in (("v_state", v_state), ("w_state", w_state)):
         if t is not None:

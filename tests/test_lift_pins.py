@@ -224,3 +224,18 @@ def test_field_lift_equivariance_quarter_turn():
     U2, _ = LF.lift_field(LF.quarter_turn_image(ang) + np.pi / 2, LF.quarter_turn_image(mag), N)
     assert np.max(np.abs(U2 - O.quarter_turn(U))) < 1e-15
     assert math.isclose(U.sum(), 1.0)
+
+
+def test_split_signed_floor():
+    """floor_rel adds floor_rel * max(part) everywhere before normalising (closed form)."""
+    U = np.random.default_rng(9).normal(size=(2, 4, 5, 6))
+    Up, Un, mp, mn = LF.split_signed(U, floor_rel=1e-3)
+    pos = np.maximum(U, 0)
+    for b in range(2):
+        fl = 1e-3 * pos[b].max()
+        ref = (pos[b] + fl) / (pos[b].sum() + fl * pos[b].size)
+        assert np.max(np.abs(Up[b] - ref)) < 1e-16
+        assert Up[b].min() > 0 and Up[b].sum() == pytest.approx(1.0, abs=1e-14)
+    assert np.allclose(mp, pos.sum(axis=(1, 2, 3)))
+    Z, _, m0, _ = LF.split_signed(-np.abs(U), floor_rel=1e-3)
+    assert not Z.any() and (m0 == 0).all()
