@@ -11,7 +11,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-fi
 python tools/prof_conv.py --cfg c4 --reps 2 > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:conv_linear -s 1 -c 1 -o gpurun_out/prof_c4_linear \
     python tools/prof_conv.py --cfg c4 --reps 2 > gpurun_out/ncu_full_c4.log 2>&1
-python tools/prof_state_conv.py --cfg c3 --iters 200 --reps 1 > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:conv_lse_fast -s 500 -c 1 -o gpurun_out/prof_c3_k3 \
-    python tools/prof_state_conv.py --cfg c3 --iters 200 --reps 1 > gpurun_out/ncu_full_c3.log 2>&1
+python tools/run_bary.py --cfg c3 --iters 210 --no-graph > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:conv_lse_fast -s 400 -c 1 -o gpurun_out/prof_c3_k3_solve \
+    python tools/run_bary.py --cfg c3 --iters 210 --no-graph > gpurun_out/ncu_full_c3.log 2>&1
+python tools/run_sinkhorn.py > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sinkhorn_small -s 1 -c 1 -o gpurun_out/prof_c0_k9 \
+    python tools/run_sinkhorn.py > gpurun_out/ncu_full_c0.log 2>&1
 echo done
