@@ -649,6 +649,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     // least at h - kHintDrop (sum >= e^-(kHintAbove + kHintDrop) relative to the shift h + kHintAbove: the
     // floor the row pruning assumed); otherwise the CTA redoes two-pass
     bool bad = false;
+    const float hint_floor = exp2f(-(kHintAbove + kHintDrop) * kLog2e);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -656,7 +657,7 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             const int to = 4 * qd + q, gyy = y0 + lane, gxx = x0 + wx * C::P + p;
             if (to < nt && gyy < ny && gxx < nx) {
                 const float sv = Sacc[q][p];
-                if (!(sv >= 9.3576230e-14f && sv <= 1.2676506e30f)) bad = true;   // [e^-30, 2^100]
+                if (!(sv >= hint_floor && sv <= 1.2676506e30f)) bad = true;   // [e^-(above+drop), 2^100]
             }
         }
     if (!__syncthreads_or(bad)) break;
