@@ -64,6 +64,9 @@ typedef enum {
 #define SE2_LSE_K3EXACT 0x20u /* diagnostics: K3 with every active channel on its exact path     */
 #define SE2_NO_GRAPH 0x40u    /* solvers: launch directly instead of replaying a CUDA graph       */
 #define SE2_NO_PERSISTENT 0x80u /* se2_sinkhorn: never use the one-launch cluster solver (K9)     */
+#define SE2_DEBUG_BAD_HINTS 0x100u /* diagnostics: K3 reads its exact-path hints 60 nats too high, so
+                                      every hinted output must take the verified fallback (redo) */
+#define SE2_DEBUG_NO_SPLIT 0x200u  /* diagnostics: K3 without the theta_i split (one CTA per tile-quad) */
 
 typedef struct {
     int32_t nx, ny, ntheta;
@@ -229,9 +232,10 @@ SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64
                                       int64_t* visited_pairs, int64_t* tilted_pairs, int64_t* hint_redos,
                                       int32_t reset);
 
-/* K3 exact-path row pruning counters since the last reset (synchronises the device): rows of taps
- * (warp, input orientation, dy) evaluated / visited.  A row is skipped when its largest possible term
- * lies more than 25 nats below a lower bound of every output of the warp (K3). */
+/* K3 exact-path row pruning counters since the last reset (synchronises the device): tap-row
+ * segments (warp, input orientation, dy, one of 3 dx segments) evaluated / visited.  A segment is
+ * skipped when its largest possible term lies more than 25 nats below a lower bound of every output
+ * of the warp (K3). */
 SE2_API se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_visited, int32_t reset);
 
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;

@@ -19,6 +19,8 @@ SE2_LSE_NOTILT = 0x10
 SE2_LSE_K3EXACT = 0x20
 SE2_NO_GRAPH = 0x40
 SE2_NO_PERSISTENT = 0x80
+SE2_DEBUG_BAD_HINTS = 0x100
+SE2_DEBUG_NO_SPLIT = 0x200
 SE2_EPI_DIVIDE = 1
 SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3

@@ -183,9 +183,10 @@ def se2_jko_step(k: Kernel, mu_k: torch.Tensor, mu_next: torch.Tensor, a: torch.
 def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain: bool,
                    bary: Optional[torch.Tensor] = None, v_state: Optional[torch.Tensor] = None,
                    w_state: Optional[torch.Tensor] = None, trace: bool = False, lse_exact: bool = False,
-                   no_graph: bool = False):
+                   no_graph: bool = False, debug_flags: int = 0):
     """App. A barycenter.  mus: [n][N]; lambdas: [nsolve][n] (host).  Returns
-    (bary [nsolve][N] -- log mu under log_domain --, err trace [iters][nsolve] or None)."""
+    (bary [nsolve][N] -- log mu under log_domain --, err trace [iters][nsolve] or None).
+    debug_flags: SE2_DEBUG_* bits (diagnostics / tests only)."""
     _check_field(mus, k, "mus")
     n = mus.numel() // k.N
     lam = np.ascontiguousarray(np.atleast_2d(np.asarray(lambdas, dtype=np.float64)))
@@ -198,7 +199,7 @@ def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain
     for name, t in (("v_state", v_state), ("w_state", w_state)):
         if t is not None:
             _check_field(t, k, name, nsolve * n)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace, lse_exact=lse_exact, no_graph=no_graph))
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace, lse_exact=lse_exact, no_graph=no_graph) | int(debug_flags))
     tr = np.zeros((max(iters, 1), nsolve), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None
     check(L.load().se2_barycenter(k.handle, n, nsolve, _ptr(mus), lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

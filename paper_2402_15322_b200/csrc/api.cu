@@ -111,7 +111,9 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
         e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->lstats,
-                                 (flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0), k->lse_counters,
+                                 ((flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0)) |
+                                     ((flags & SE2_DEBUG_BAD_HINTS) ? 4 : 0) | ((flags & SE2_DEBUG_NO_SPLIT) ? 8 : 0),
+                                 k->lse_counters,
                                  k->split, k->split_floats);
     if (e != cudaSuccess) {
         set_error(std::string("conv launch: ") + cudaGetErrorString(e));
@@ -242,7 +244,7 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
     const size_t tabl = (size_t)k->nt * k->nt * k->S * ((k->S + 3) / 4 * 4) * sizeof(float);
     cudaError_t e = cudaMalloc(&k->Eq, tab);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lq, tab);
-    if (e == cudaSuccess) e = cudaMalloc(&k->LqRow, (size_t)nquads * k->nt * k->S * 4 * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&k->LqRow, (size_t)nquads * k->nt * k->S * kRowSegs * 4 * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&k->Wl, tabl);
     if (e == cudaSuccess) e = cudaMalloc(&k->Lth, sizeof(float) * k->nt * k->nt);
     if (e == cudaSuccess) e = cudaMalloc(&k->LseS, sizeof(float) * k->nt * k->nt);

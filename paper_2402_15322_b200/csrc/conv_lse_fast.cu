@@ -40,7 +40,9 @@ struct LseFCfg {
     static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * S * 4;
-    static constexpr int RMX = S * 4;            // per tap row: max over dx of the L2 table (4 q)
+    static constexpr int NSEG = kRowSegs;        // tap-row segments with their own bound (exact path)
+    static constexpr int SEGW = (S + NSEG - 1) / NSEG;
+    static constexpr int RMX = S * NSEG * 4;     // per tap-row segment: max over its dx of the L2 table (4 q)
     static constexpr int MAXNT = 128;
     // window x2, L2 filter x2, exp filter x2 (FFMA candidates decided on the staged window), row max x2
     static constexpr size_t SMEM = (size_t)(2 * WIN + 4 * FIL + 2 * RMX) * sizeof(float) + 64;
@@ -258,9 +260,9 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 if (!(ub < sLB[q] - kPruneGap)) active = true;
             }
             if (active) {
-                if (force_exact == 1) stt = 2;
+                if ((force_exact & 3) == 1) stt = 2;
                 else if (mu != NEG_INF && (M - mu) <= kFastRange) stt = 1;
-                else if (force_exact != 2 && sShift[i] == sShift[i]) stt = 3;   // not NaN: tilt valid
+                else if ((force_exact & 3) != 2 && sShift[i] == sShift[i]) stt = 3;   // not NaN: tilt valid
                 else if (mu != NEG_INF) stt = 5;
                 else stt = 2;
             }
@@ -354,7 +356,8 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 // shift = previous output + 20 nats, relative to ref, log2 units
                 const int to = 4 * qd + q, gy = y0 + lane, gx = x0 + wx * C::P + p;
                 if (to < nt && gy < ny && gx < nx) {
-                    const float h = epi.hint_in[(int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx];
+                    const float h = epi.hint_in[(int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx] +
+                                    ((force_exact & 4) ? kDebugHintBias : 0.f);   // diagnostics: wrong hints
                     if (h > -1e30f && h < 1e30f) Macc[q][p] = ((h - ref) + kHintAbove) * kLog2e;
                 }
             }
@@ -566,15 +569,6 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     thr[q] = t - drop2;
                 }
             };
-            auto row_live = [&](const float* r, int dy) -> bool {
-                float sm = r[0];
-#pragma unroll
-                for (int j = 1; j < C::P + 2 * R; ++j) sm = fmaxf(sm, r[j]);
-                const float4 m4 = rmx[dy];
-                const bool live = (sm + m4.x >= thr[0]) || (sm + m4.y >= thr[1]) || (sm + m4.z >= thr[2]) ||
-                                  (sm + m4.w >= thr[3]);
-                return __any_sync(0xffffffffu, live);
-            };
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -622,22 +616,45 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     float4 t = rowp[j];
                     r[4 * j + 0] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
                 }
-                ++rows_seen;
-                if (!row_live(r, dy)) continue;
-                ++rows_live;
+                // per segment k (taps dx in [k SEGW, (k+1) SEGW)): bound = max_dx L2 + max of the r
+                // entries those taps read (indices 2R - dx + p); warp vote per segment
+                bool segl[C::NSEG];
+                bool any = false;
+#pragma unroll
+                for (int k = 0; k < C::NSEG; ++k) {
+                    const int dxlo = k * C::SEGW;
+                    const int dxhi = (dxlo + C::SEGW - 1 < C::S - 1) ? dxlo + C::SEGW - 1 : C::S - 1;
+                    float sm = -INFINITY;
+                    if (dxlo <= dxhi) {
+#pragma unroll
+                        for (int j = 2 * R - dxhi; j <= 2 * R - dxlo + C::P - 1; ++j) sm = fmaxf(sm, r[j]);
+                    }
+                    const float4 m4 = rmx[dy * C::NSEG + k];
+                    const bool live = (sm + m4.x >= thr[0]) || (sm + m4.y >= thr[1]) || (sm + m4.z >= thr[2]) ||
+                                      (sm + m4.w >= thr[3]);
+                    segl[k] = __any_sync(0xffffffffu, live);
+                    any |= segl[k];
+                    rows_seen += 1;
+                    rows_live += segl[k] ? 1 : 0;
+                }
+                if (!any) continue;
                 const float4* frow = fil + dy * C::S;
 #pragma unroll
-                for (int dx = 0; dx < C::S; ++dx) {
-                    const float4 w = frow[dx];
+                for (int k = 0; k < C::NSEG; ++k) {
+                    if (!segl[k]) continue;
 #pragma unroll
-                    for (int p = 0; p < C::P; ++p) {
-                        const float xv = r[p - dx + 2 * R];
-                        // (routing 3 of the 16 exps per tap to ex2_poly on the FMA pipe measured 4-7% slower
-                        //  on c3 states: this loop is issue-bound, not MUFU-bound)
-                        Sacc[0][p] += ex2_approx((xv + w.x) - Macc[0][p]);
-                        Sacc[1][p] += ex2_approx((xv + w.y) - Macc[1][p]);
-                        Sacc[2][p] += ex2_approx((xv + w.z) - Macc[2][p]);
-                        Sacc[3][p] += ex2_approx((xv + w.w) - Macc[3][p]);
+                    for (int dx = k * C::SEGW; dx < (k + 1) * C::SEGW && dx < C::S; ++dx) {
+                        const float4 w = frow[dx];
+#pragma unroll
+                        for (int p = 0; p < C::P; ++p) {
+                            const float xv = r[p - dx + 2 * R];
+                            // (routing 3 of the 16 exps per tap to ex2_poly on the FMA pipe measured 4-7%
+                            //  slower on c3 states: this loop is issue-bound, not MUFU-bound)
+                            Sacc[0][p] += ex2_approx((xv + w.x) - Macc[0][p]);
+                            Sacc[1][p] += ex2_approx((xv + w.y) - Macc[1][p]);
+                            Sacc[2][p] += ex2_approx((xv + w.z) - Macc[2][p]);
+                            Sacc[3][p] += ex2_approx((xv + w.w) - Macc[3][p]);
+                        }
                     }
                 }
             }
@@ -702,38 +719,34 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
 // Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
 // Same (tile, quad) blocks and thread -> output mapping as the main kernel, so the error partials have
 // the unsplit layout.
-// exact log-sum-exp of one output over every input orientation and tap (two passes, the definition):
-// the combine kernel's fallback when a hinted shift failed (expected never; correct always)
-__device__ __noinline__ float exact_lse_point(const float* __restrict__ vin, const float* __restrict__ Lq, int nx, int ny, int nt,
-                                 int R, int to, int y, int x) {
+// exact log-sum-exp of one output over every input orientation and tap (two passes, the definition),
+// computed by the whole warp (taps dealt over the lanes, warp max / sum): the combine kernel's fallback
+// when a hinted shift failed (rare; correct always).  Every lane must call it with the same output.
+__device__ __noinline__ float exact_lse_point_warp(const float* __restrict__ vin, const float* __restrict__ Lq, int nx,
+                                                   int ny, int nt, int R, int to, int y, int x, int lane) {
     const int S = 2 * R + 1, qd = to >> 2, q = to & 3;
+    const int total = nt * S * S;
     float m = -INFINITY;
-    for (int ti = 0; ti < nt; ++ti)
-        for (int dy = -R; dy <= R; ++dy) {
-            const int hy = y - dy;
-            if (hy < 0 || hy >= ny) continue;
-            for (int dx = -R; dx <= R; ++dx) {
-                const int hx = x - dx;
-                if (hx < 0 || hx >= nx) continue;
-                const float t = vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
-                                Lq[((((int64_t)qd * nt + ti) * S + dy + R) * S + dx + R) * 4 + q];
-                m = fmaxf(m, t);
-            }
-        }
+    for (int t = lane; t < total; t += 32) {
+        const int ti = t / (S * S), d = t - ti * S * S, dy = d / S - R, dx = d % S - R;
+        const int hy = y - dy, hx = x - dx;
+        if (hy < 0 || hy >= ny || hx < 0 || hx >= nx) continue;
+        m = fmaxf(m, vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
+                         Lq[((((int64_t)qd * nt + ti) * S * S) + d) * 4 + q]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (m == -INFINITY) return -INFINITY;
     float sacc = 0.f;
-    for (int ti = 0; ti < nt; ++ti)
-        for (int dy = -R; dy <= R; ++dy) {
-            const int hy = y - dy;
-            if (hy < 0 || hy >= ny) continue;
-            for (int dx = -R; dx <= R; ++dx) {
-                const int hx = x - dx;
-                if (hx < 0 || hx >= nx) continue;
-                const float t = vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
-                                Lq[((((int64_t)qd * nt + ti) * S + dy + R) * S + dx + R) * 4 + q];
-                sacc += ex2_approx(t - m);
-            }
-        }
+    for (int t = lane; t < total; t += 32) {
+        const int ti = t / (S * S), d = t - ti * S * S, dy = d / S - R, dx = d % S - R;
+        const int hy = y - dy, hx = x - dx;
+        if (hy < 0 || hy >= ny || hx < 0 || hx >= nx) continue;
+        sacc += ex2_approx(vin[((int64_t)ti * ny + hy) * nx + hx] * kLog2e +
+                           Lq[((((int64_t)qd * nt + ti) * S * S) + d) * 4 + q] - m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
     return (m + log2f(sacc)) * kLn2;
 }
 
@@ -741,7 +754,7 @@ template <int R>
 __global__ void __launch_bounds__(LseFCfg<R>::NT)
 lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x,
                          Epilogue epi, const float* __restrict__ in, const float* __restrict__ Lq,
-                         int* __restrict__ counters) {
+                         int* __restrict__ counters, float hint_bias) {
     using C = LseFCfg<R>;
     __shared__ float sRed[C::NT / 32];
     const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
@@ -751,17 +764,20 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
     const int lane = threadIdx.x & 31, wx = threadIdx.x >> 5;
     float err = 0.f;
     const int gy = y0 + lane;
-    if (gy < ny) {
-        for (int q = 0; q < 4; ++q) {
-            const int to = 4 * qd + q;
-            if (to >= nt) continue;
-            for (int p = 0; p < C::P; ++p) {
-                const int gx = x0 + wx * C::P + p;
-                if (gx >= nx) continue;
-                const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
+    const bool row_ok = gy < ny;
+    for (int q = 0; q < 4; ++q) {          // q, p uniform over the warp (the fallback is warp-cooperative)
+        const int to = 4 * qd + q;
+        if (to >= nt) continue;
+        for (int p = 0; p < C::P; ++p) {
+            const int gx = x0 + wx * C::P + p;
+            if (gx >= nx) continue;
+            const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + (row_ok ? gy : 0)) * nx + gx;
+            float ly = -INFINITY;
+            bool bad = false;
+            if (row_ok) {
                 float m = -INFINITY;
                 for (int g = 0; g < ngroups; ++g) m = fmaxf(m, part[g * GN + idx]);
-                float ly = m;
+                ly = m;
                 if (m != -INFINITY) {
                     float s = 0.f;
                     for (int g = 0; g < ngroups; ++g) s += expf(part[g * GN + idx] - m);
@@ -770,14 +786,22 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
                 if (epi.hint_in != nullptr) {
                     // the partials used shift = hint + kHintAbove and rows pruned against the floor
                     // h - kHintDrop: valid iff no overflow (finite) and the total reached that floor
-                    const float h = epi.hint_in[idx];
-                    if (!(ly < 1e30f && ly >= h - kHintDrop)) {
-                        ly = exact_lse_point(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, gy, gx);
-                        if (counters != nullptr) atomicAdd(&counters[4], 1);
-                    }
+                    const float h = epi.hint_in[idx] + hint_bias;
+                    bad = !(ly < 1e30f && ly >= h - kHintDrop);
                 }
-                err += apply_epilogue<true>(epi, idx, gx, gy, ly);
             }
+            unsigned mask = __ballot_sync(0xffffffffu, bad);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int yy = __shfl_sync(0xffffffffu, gy, src);
+                const float v = exact_lse_point_warp(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, yy, gx, lane);
+                if (lane == src) {
+                    ly = v;
+                    if (counters != nullptr) atomicAdd(&counters[4], 1);
+                }
+            }
+            if (row_ok) err += apply_epilogue<true>(epi, idx, gx, gy, ly);
         }
     }
     if (epi.err_partial != nullptr) {
@@ -815,7 +839,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     if (groups > k->nt) groups = k->nt;
     if (groups > 1 && (size_t)groups * batch * k->N() > split_floats)
         groups = (int)(split_floats / ((size_t)batch * k->N()));   // as many as the scratch holds
-    if (groups < 1) groups = 1;
+    if (groups < 1 || (force_exact & 8)) groups = 1;   // 8: diagnostics, no split
     if (bpf) *bpf = ntile * nquad;
     dim3 grid(ntile, nquad * groups, batch);
     conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->LqRow, k->Lth, k->LseS, stats, k->nx, k->ny,
@@ -825,7 +849,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     if (groups > 1) {
         dim3 g2(ntile, nquad, batch);
         lse_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi, in,
-                                                         k->Lq, counters);
+                                                         k->Lq, counters, (force_exact & 4) ? kDebugHintBias : 0.f);
         count_launch();
     }
     return cudaGetLastError();

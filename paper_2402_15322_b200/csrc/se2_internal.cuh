@@ -46,8 +46,10 @@ constexpr float kPruneGap = 30.f;     // channels whose upper bound is < lower b
 // more than kRowGap nats below a lower bound of every output of the warp; with a hint h (previous
 // output) the shift is h + kHintAbove and the result is accepted only if ly >= h - kHintDrop
 constexpr float kRowGap = 25.f;
+constexpr int kRowSegs = 3;   // each tap row is pruned in 3 segments of ceil(S/3) taps
 constexpr float kHintAbove = 20.f;
 constexpr float kHintDrop = 10.f;
+constexpr float kDebugHintBias = 60.f;   // SE2_DEBUG_BAD_HINTS: hints read 60 nats too high (tests the redo paths)
 
 // Epilogue ops of the fused conv (see se2_conv_update in se2ot.h)
 enum EpiOp : int {
@@ -104,7 +106,7 @@ struct se2_kernel_s {
     float* Lth = nullptr;   // [nt][nt] theta part of L (natural log)
     float* LseS = nullptr;  // [nt][nt] log sum_taps exp(Ls)
     float* Lq = nullptr;    // -rho^2/eps * log2(e) fp32
-    float* LqRow = nullptr; // [nt/4][nt][S][4] max over dx of Lq (row bounds of the exact path)
+    float* LqRow = nullptr; // [nt/4][nt][S][kRowSegs][4] max of Lq over each tap-row segment (exact path)
     float* Wl = nullptr;    // exp(-rho^2/eps) fp32, layout [to][ti][S][SP], SP = S rounded up to 4 (zero pad)
     float* Wcl = nullptr;   // cost tables (built on first se2_transport_cost): rho^2 exp(-rho^2/eps), Wl layout
     float* Lcq = nullptr;   //   and log2(rho^2) + L2, Lq layout

@@ -13,7 +13,8 @@
 //                                16-byte shared-memory broadcast feeds four output orientations)
 //   Eq [nt/4][nt][S][S][4]       exp(Ls + kEsShift) (factored LSE engine)
 //   Lth[to][ti], LseS[to][ti]    Lth and log sum_{dx,dy} exp(Ls) (natural logs)
-//   LqRow [nt/4][nt][S][4]       max over dx of Lq (per tap row: the exact path's row bounds)
+//   LqRow [nt/4][nt][S][G][4]    max of Lq over each of the G = kRowSegs segments of a tap row (the
+//                                exact path's bounds; an empty segment is -inf)
 #include <math.h>
 
 #include "se2_internal.cuh"
@@ -116,15 +117,17 @@ __global__ void tabulate_cost_kernel(double hx, double hy, int nt, int R, double
     }
 }
 
-// LqRow[qd][ti][dy][q] = max_dx Lq[qd][ti][dy][dx][q] (after tabulate_kernel; padding quads stay 0)
+// LqRow[qd][ti][dy][g][q] = max over dx in segment g of Lq[qd][ti][dy][dx][q] (after tabulate_kernel)
 __global__ void tabulate_rowmax_kernel(int nquads, int nt, int S, const float* __restrict__ Lq,
                                        float* __restrict__ LqRow) {
-    const int64_t total = (int64_t)nquads * nt * S * 4;
+    const int G = kRowSegs, W = (S + G - 1) / G;
+    const int64_t total = (int64_t)nquads * nt * S * G * 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int q = (int)(i & 3);
-        const int64_t row = i >> 2;   // (qd, ti, dy)
+        const int g = (int)((i >> 2) % G);
+        const int64_t row = (i >> 2) / G;   // (qd, ti, dy)
         float m = -INFINITY;
-        for (int dx = 0; dx < S; ++dx) m = fmaxf(m, Lq[(row * S + dx) * 4 + q]);
+        for (int dx = g * W; dx < (g + 1) * W && dx < S; ++dx) m = fmaxf(m, Lq[(row * S + dx) * 4 + q]);
         LqRow[i] = m;
     }
 }
@@ -156,7 +159,7 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
                                                                   k->w3, k->Lth, k->LseS);
     {
         const int nquads = (nt + 3) / 4;
-        const int64_t rows = (int64_t)nquads * nt * S * 4;
+        const int64_t rows = (int64_t)nquads * nt * S * kRowSegs * 4;
         tabulate_rowmax_kernel<<<(int)((rows + 255) / 256), 256, 0, s>>>(nquads, nt, S, k->Lq, k->LqRow);
     }
     e = cudaGetLastError();

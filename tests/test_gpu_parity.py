@@ -255,3 +255,27 @@ def test_sinkhorn_k9_determinism(cuda_device):
     t1 = se2_sinkhorn(k0, mu, nu, a1, b1, 50, True, trace=True)
     t2 = se2_sinkhorn(k0, mu, nu, a2, b2, 50, True, trace=True)
     assert torch.equal(a1, a2) and torch.equal(b1, b2) and np.array_equal(t1, t2)
+
+
+@pytest.mark.parametrize("no_split", [False, True], ids=["split-combine-fallback", "cta-redo"])
+def test_hint_fallback_paths(no_split, cuda_device):
+    """The exact-path hints are only an optimisation: with every hint read 60 nats too high
+    (SE2_DEBUG_BAD_HINTS) each hinted output must fail verification and be recomputed -- by the
+    warp-cooperative per-output fallback of the theta_i-split combine, or by the whole-CTA two-pass redo
+    without the split -- and the solve must still match the oracle (c2m, 300 log-domain iterations)."""
+    from paper_2402_15322_b200 import _lib as Lb
+    from paper_2402_15322_b200 import se2_barycenter
+    pc = S.get_parity_case("c2m")
+    cfg, d = S.parity_inputs(pc)
+    gold = _golden("c2m")
+    lams = gold["lambdas"]
+    n, nsolve = len(d["mus"]), lams.shape[0]
+    k = _kernel(cfg, n * nsolve)
+    mus = _dev(np.stack(d["mus"]))
+    flags = Lb.SE2_DEBUG_BAD_HINTS | (Lb.SE2_DEBUG_NO_SPLIT if no_split else 0)
+    k.lse_path_stats(reset=True)
+    bary, _ = se2_barycenter(k, mus, lams, cfg.iters, True, debug_flags=flags)
+    st = k.lse_path_stats(reset=True)
+    assert st["hint_redos"] > 0
+    _cmp_pot("log bary", _host(bary).reshape(nsolve, -1), gold["lbary"].reshape(nsolve, -1))
+    _cmp_meas("bary", np.exp(_host(bary)).reshape(nsolve, -1), gold["bary_lin"].reshape(nsolve, -1))
