@@ -716,9 +716,6 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     }
 }
 
-// Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
-// Same (tile, quad) blocks and thread -> output mapping as the main kernel, so the error partials have
-// the unsplit layout.
 // exact log-sum-exp of one output over every input orientation and tap (two passes, the definition),
 // computed by the whole warp (taps dealt over the lanes, warp max / sum): the combine kernel's fallback
 // when a hinted shift failed (rare; correct always).  Every lane must call it with the same output.
@@ -750,62 +747,64 @@ __device__ __noinline__ float exact_lse_point_warp(const float* __restrict__ vin
     return (m + log2f(sacc)) * kLn2;
 }
 
+// Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
+// One CTA per (tile, quad, field) as in the main kernel (so the error partials keep the unsplit
+// layout), but kCombT threads, each with a few outputs (x fastest: coalesced partial reads).
+constexpr int kCombT = 512;
 template <int R>
-__global__ void __launch_bounds__(LseFCfg<R>::NT)
+__global__ void __launch_bounds__(kCombT)
 lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x,
                          Epilogue epi, const float* __restrict__ in, const float* __restrict__ Lq,
                          int* __restrict__ counters, float hint_bias) {
     using C = LseFCfg<R>;
-    __shared__ float sRed[C::NT / 32];
+    __shared__ float sRed[kCombT / 32];
     const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
     const int x0 = (tile % tiles_x) * C::TX, y0 = (tile / tiles_x) * C::TY;
     const int64_t N = (int64_t)nx * ny * nt;
     const int64_t GN = (int64_t)gridDim.z * N;
-    const int lane = threadIdx.x & 31, wx = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    constexpr int NOUT = 4 * C::TY * C::TX;   // outputs of the (tile, quad) block
     float err = 0.f;
-    const int gy = y0 + lane;
-    const bool row_ok = gy < ny;
-    for (int q = 0; q < 4; ++q) {          // q, p uniform over the warp (the fallback is warp-cooperative)
-        const int to = 4 * qd + q;
-        if (to >= nt) continue;
-        for (int p = 0; p < C::P; ++p) {
-            const int gx = x0 + wx * C::P + p;
-            if (gx >= nx) continue;
-            const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + (row_ok ? gy : 0)) * nx + gx;
-            float ly = -INFINITY;
-            bool bad = false;
-            if (row_ok) {
-                float m = -INFINITY;
-                for (int g = 0; g < ngroups; ++g) m = fmaxf(m, part[g * GN + idx]);
-                ly = m;
-                if (m != -INFINITY) {
-                    float s = 0.f;
-                    for (int g = 0; g < ngroups; ++g) s += expf(part[g * GN + idx] - m);
-                    ly = m + logf(s);
-                }
-                if (epi.hint_in != nullptr) {
-                    // the partials used shift = hint + kHintAbove and rows pruned against the floor
-                    // h - kHintDrop: valid iff no overflow (finite) and the total reached that floor
-                    const float h = epi.hint_in[idx] + hint_bias;
-                    bad = !(ly < 1e30f && ly >= h - kHintDrop);
-                }
+    for (int o = threadIdx.x; o < NOUT; o += kCombT) {   // same trip count for every lane
+        const int q = o / (C::TY * C::TX), rem = o - q * (C::TY * C::TX);
+        const int to = 4 * qd + q, gy = y0 + rem / C::TX, gx = x0 + rem % C::TX;
+        const bool ok = to < nt && gy < ny && gx < nx;
+        const int64_t idx = ok ? (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx : 0;
+        float ly = -INFINITY;
+        bool bad = false;
+        if (ok) {
+            float m = -INFINITY;
+            for (int g = 0; g < ngroups; ++g) m = fmaxf(m, part[g * GN + idx]);
+            ly = m;
+            if (m != -INFINITY) {
+                float s = 0.f;
+                for (int g = 0; g < ngroups; ++g) s += expf(part[g * GN + idx] - m);
+                ly = m + logf(s);
             }
-            unsigned mask = __ballot_sync(0xffffffffu, bad);
-            while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int yy = __shfl_sync(0xffffffffu, gy, src);
-                const float v = exact_lse_point_warp(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, yy, gx, lane);
-                if (lane == src) {
-                    ly = v;
-                    if (counters != nullptr) atomicAdd(&counters[4], 1);
-                }
+            if (epi.hint_in != nullptr) {
+                // the partials used shift = hint + kHintAbove and rows pruned against the floor
+                // h - kHintDrop: valid iff no overflow (finite) and the total reached that floor
+                const float h = epi.hint_in[idx] + hint_bias;
+                bad = !(ly < 1e30f && ly >= h - kHintDrop);
             }
-            if (row_ok) err += apply_epilogue<true>(epi, idx, gx, gy, ly);
         }
+        unsigned mask = __ballot_sync(0xffffffffu, bad);
+        while (mask) {   // warp-cooperative exact recomputation of each failed output
+            const int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int tt = __shfl_sync(0xffffffffu, to, src);
+            const int yy = __shfl_sync(0xffffffffu, gy, src);
+            const int xx = __shfl_sync(0xffffffffu, gx, src);
+            const float v = exact_lse_point_warp(in + (int64_t)b * N, Lq, nx, ny, nt, R, tt, yy, xx, lane);
+            if (lane == src) {
+                ly = v;
+                if (counters != nullptr) atomicAdd(&counters[4], 1);
+            }
+        }
+        if (ok) err += apply_epilogue<true>(epi, idx, gx, gy, ly);
     }
     if (epi.err_partial != nullptr) {
-        float t = block_sum<C::NT>(err, sRed);
+        float t = block_sum<kCombT>(err, sRed);
         if (threadIdx.x == 0)
             epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
@@ -848,7 +847,7 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     count_launch();
     if (groups > 1) {
         dim3 g2(ntile, nquad, batch);
-        lse_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi, in,
+        lse_split_combine_kernel<R><<<g2, kCombT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi, in,
                                                          k->Lq, counters, (force_exact & 4) ? kDebugHintBias : 0.f);
         count_launch();
     }
