@@ -51,25 +51,45 @@ constexpr int kLseTileY = 32, kLseTileX = 16;
 constexpr int kStat = 8;   // per tile: a, gx, gy, rmin, rmax, vmin, vmax, valid-plane flag
 
 // Per (field, theta, tile): min/max of lv, least-squares plane psi = a + gx (x - cx) + gy (y - cy)
-// about the tile centre (pixel units), and min/max of the residual lv - psi.  One warp per tile.
-__global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, int nt, int tiles_x, int tiles_y,
-                                 float* __restrict__ st) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+// about the tile centre (pixel units), and min/max of the residual lv - psi.  One 128-thread block per
+// tile (4 values per thread; block reductions through shared memory).
+constexpr int kStatT = 128;
+__device__ __forceinline__ void stat_reduce3(float& a, float& b, float& c, bool is_min_max, float* sh) {
+    // is_min_max: (a, b) = (min, max), c unused; else (a, b, c) summed.  Result in every thread.
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ta = __shfl_xor_sync(0xffffffffu, a, o), tb = __shfl_xor_sync(0xffffffffu, b, o);
+        const float tc = __shfl_xor_sync(0xffffffffu, c, o);
+        if (is_min_max) { a = fminf(a, ta); b = fmaxf(b, tb); } else { a += ta; b += tb; c += tc; }
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) { sh[w] = a; sh[4 + w] = b; sh[8 + w] = c; }
+    __syncthreads();
+    a = sh[0]; b = sh[4]; c = sh[8];
+#pragma unroll
+    for (int i = 1; i < kStatT / 32; ++i) {
+        if (is_min_max) { a = fminf(a, sh[i]); b = fmaxf(b, sh[4 + i]); } else { a += sh[i]; b += sh[4 + i]; c += sh[8 + i]; }
+    }
+}
+
+__global__ void __launch_bounds__(kStatT)
+lse_stats_kernel(const float* __restrict__ in, int nx, int ny, int nt, int tiles_x, int tiles_y,
+                 float* __restrict__ st) {
+    __shared__ float sh[12];
     const int ntile = tiles_x * tiles_y;
+    const int th = blockIdx.x / ntile, t = blockIdx.x % ntile;
     const int b = blockIdx.y;
-    if (warp >= nt * ntile) return;
-    const int th = warp / ntile, t = warp % ntile;
     const int x0 = (t % tiles_x) * kLseTileX, y0 = (t / tiles_x) * kLseTileY;
     const int w = min(kLseTileX, nx - x0), h = min(kLseTileY, ny - y0);
     const float cx = x0 + 0.5f * (w - 1), cy = y0 + 0.5f * (h - 1);
     const float* src = in + ((int64_t)b * nt + th) * nx * ny;
-    constexpr int PER = kLseTileY * kLseTileX / 32;
+    constexpr int PER = kLseTileY * kLseTileX / kStatT;
     float v[PER];
-    float mn = INFINITY, mx = -INFINITY, s0 = 0.f, sx = 0.f, sy = 0.f;
+    float mn = INFINITY, mx = -INFINITY, dummy = 0.f;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-        const int i = lane + 32 * k;
+        const int i = threadIdx.x + kStatT * k;
         const int yy = i / kLseTileX, xx = i % kLseTileX;
         v[k] = 0.f;
         if (yy < h && xx < w) {
@@ -78,18 +98,15 @@ __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, i
             mx = fmaxf(mx, v[k]);
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
+    stat_reduce3(mn, mx, dummy, true, sh);
     const bool finite = (mn != -INFINITY) && (mx != INFINITY) && (mn == mn);
     float a = 0.f, gx = 0.f, gy = 0.f, rmn = mn, rmx = mx;
-    if (finite) {
+    if (finite) {   // uniform over the block
         // the valid cells form a w x h rectangle: the centred design is orthogonal
+        float s0 = 0.f, sx = 0.f, sy = 0.f;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int i = lane + 32 * k;
+            const int i = threadIdx.x + kStatT * k;
             const int yy = i / kLseTileX, xx = i % kLseTileX;
             if (yy < h && xx < w) {
                 const float d = v[k] - mn;      // shift for conditioning
@@ -98,12 +115,7 @@ __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, i
                 sy += d * ((float)(y0 + yy) - cy);
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-            sx += __shfl_xor_sync(0xffffffffu, sx, o);
-            sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        }
+        stat_reduce3(s0, sx, sy, false, sh);
         const float sxx = (float)h * (float)w * ((float)w * w - 1.f) / 12.f;
         const float syy = (float)w * (float)h * ((float)h * h - 1.f) / 12.f;
         a = mn + s0 / (float)(w * h);
@@ -113,7 +125,7 @@ __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, i
         rmx = -INFINITY;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int i = lane + 32 * k;
+            const int i = threadIdx.x + kStatT * k;
             const int yy = i / kLseTileX, xx = i % kLseTileX;
             if (yy < h && xx < w) {
                 const float r = (v[k] - a) - (gx * ((float)(x0 + xx) - cx) + gy * ((float)(y0 + yy) - cy));
@@ -121,13 +133,9 @@ __global__ void lse_stats_kernel(const float* __restrict__ in, int nx, int ny, i
                 rmx = fmaxf(rmx, r);
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            rmn = fminf(rmn, __shfl_xor_sync(0xffffffffu, rmn, o));
-            rmx = fmaxf(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
-        }
+        stat_reduce3(rmn, rmx, dummy, true, sh);
     }
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         float* o = st + (((int64_t)b * nt + th) * ntile + t) * kStat;
         o[0] = a; o[1] = gx; o[2] = gy; o[3] = rmn; o[4] = rmx; o[5] = mn; o[6] = mx;
         o[7] = finite ? 1.f : 0.f;
@@ -819,9 +827,8 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
     const int tiles_y = (k->ny + C::TY - 1) / C::TY;
     const int ntile = tiles_x * tiles_y;
     {
-        const int warps = k->nt * ntile;
-        dim3 g((warps * 32 + 255) / 256, batch);
-        lse_stats_kernel<<<g, 256, 0, s>>>(in, k->nx, k->ny, k->nt, tiles_x, tiles_y, stats);
+        dim3 g(k->nt * ntile, batch);
+        lse_stats_kernel<<<g, kStatT, 0, s>>>(in, k->nx, k->ny, k->nt, tiles_x, tiles_y, stats);
         count_launch();
     }
     cudaError_t e = cudaFuncSetAttribute(conv_lse_fast_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
