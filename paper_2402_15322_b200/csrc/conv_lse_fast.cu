@@ -835,17 +835,37 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
                                          (int)C::SMEM);
     if (e != cudaSuccess) return e;
     const int nquad = (k->nt + 3) / 4;
-    // split the input orientations over `groups` CTAs per (tile, quad) until ~16 CTAs per SM exist
-    // (the per-channel loop of one CTA is latency-bound and 3 CTAs fit per SM: more, smaller CTAs
-    // balance the SMs; measured c3 237 -> 261 it/s at 3 groups, c1/c2 unchanged), then combine
+    // split the input orientations over `groups` CTAs per (tile, quad), then combine.  The per-channel
+    // loop of one CTA is latency-bound and only a few CTAs fit per SM, so the grid is sized in waves:
+    // waves(g) / g = ceil(base g / slots) / g models the time of the busiest SM (per-CTA work ~ 1/g); up to
+    // 8 groups / the scratch / ~16 CTAs per SM.  Measured sweep (tools/sweep_groups.sh): c1 best at 5
+    // (6.6k it/s vs 6.3k at 8), c2 at 7-8 (4.68k vs 4.40k at 3), c3 at 3-4 (341-345 vs 299 unsplit).
     const int base_ctas = ntile * nquad * batch;
-    int groups = 1;
-    static const int split_min = getenv("SE2_K3_SPLIT_MIN") ? atoi(getenv("SE2_K3_SPLIT_MIN")) : 16 * 148;
-    if (base_ctas < split_min) groups = (split_min + base_ctas - 1) / base_ctas;
-    if (groups > k->nt) groups = k->nt;
-    if (groups > 1 && (size_t)groups * batch * k->N() > split_floats)
-        groups = (int)(split_floats / ((size_t)batch * k->N()));   // as many as the scratch holds
-    if (groups < 1 || (force_exact & 8)) groups = 1;   // 8: diagnostics, no split
+    static int slots = 0;
+    if (slots == 0) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_lse_fast_kernel<R>, C::NT, C::SMEM) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        slots = per_sm * nsm;
+        cudaGetLastError();
+    }
+    int gmax = k->nt < 8 ? k->nt : 8;
+    const int gcap = (16 * 148 + base_ctas - 1) / base_ctas;   // no more than ~16 CTAs per SM in total
+    if (gmax > gcap) gmax = gcap;
+    if ((size_t)gmax * batch * k->N() > split_floats) gmax = (int)(split_floats / ((size_t)batch * k->N()));
+    if (gmax < 1 || (force_exact & 8)) gmax = 1;   // 8: diagnostics, no split
+    double best = 1e30;
+    for (int g = 1; g <= gmax; ++g)
+        best = fmin(best, (double)(((int64_t)base_ctas * g + slots - 1) / slots) / g);
+    int groups = 1;   // the largest g within 13% of the best (small CTAs also balance uneven channel work)
+    for (int g = 1; g <= gmax; ++g)
+        if ((double)(((int64_t)base_ctas * g + slots - 1) / slots) / g <= 1.13 * best) groups = g;
+    static const int force_groups = getenv("SE2_K3_GROUPS") ? atoi(getenv("SE2_K3_GROUPS")) : 0;   // tuning
+    if (force_groups > 0) groups = force_groups < gmax ? force_groups : gmax;
     if (bpf) *bpf = ntile * nquad;
     dim3 grid(ntile, nquad * groups, batch);
     conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->LqRow, k->Lth, k->LseS, stats, k->nx, k->ny,
