@@ -235,6 +235,7 @@ PARITY_CASES: List[ParityCase] = [
     ParityCase("c2m", "c2", 40, 36, 32, 7, 300),
     ParityCase("c2f", "c2", 64, 64, 32, 7, 300, full_fields=False),   # the whole c2 run at full size
     ParityCase("c3p", "c3", 128, 128, 32, 10, 2, full_fields=False),
+    ParityCase("c3q", "c3", 128, 128, 32, 10, 20, full_fields=False),  # c3 at full size, first 20 iterations
     ParityCase("c3m", "c3", 44, 40, 32, 10, 40),
     ParityCase("c4p", "c4", 256, 256, 64, 15, 2, jko_steps=1, full_fields=False),
     ParityCase("c4m", "c4", 72, 60, 16, 4, 200, jko_steps=3),

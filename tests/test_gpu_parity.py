@@ -95,7 +95,7 @@ def test_sinkhorn_parity(case, persistent, cuda_device):
     assert trace_err(tr[:, 0], gold["err"]) <= TOL_TRACE
 
 
-@pytest.mark.parametrize("case", ["c1", "c2m", "c3m", "c2p", "c3p", "c2f"])
+@pytest.mark.parametrize("case", ["c1", "c2m", "c3m", "c2p", "c3p", "c2f", "c3q"])
 def test_barycenter_parity(case, cuda_device):
     from paper_2402_15322_b200 import se2_barycenter
     pc = S.get_parity_case(case)
