@@ -56,7 +56,7 @@ __device__ __forceinline__ float k9_lse2(const float* __restrict__ f, const floa
                                          int ny, int nt, int x, int y, int part, int split) {
     constexpr int S = 2 * R + 1;
     const int dylo = max(-R, y - (ny - 1)), dyhi = min(R, y);
-    float m = -INFINITY, s = 0.f;
+    float m = -INFINITY, s = 0.f, s2 = 0.f;   // two partial sums: shorter dependency chains
     for (int ti = part; ti < nt; ti += split) {
         const float* fp = f + ti * pp + x + R;          // padded column of x
         const float* tp = tab + ti * S * S + R;
@@ -64,22 +64,31 @@ __device__ __forceinline__ float k9_lse2(const float* __restrict__ f, const floa
             const float* frow = fp + (y - dy + R) * pw;
             const float* trow = tp + (dy + R) * S;
             float t[S];
-            float rm = -INFINITY;
 #pragma unroll
-            for (int dx = -R; dx <= R; ++dx) {
-                t[dx + R] = trow[dx] + frow[-dx];
-                rm = fmaxf(rm, t[dx + R]);
+            for (int dx = -R; dx <= R; ++dx) t[dx + R] = trow[dx] + frow[-dx];
+            float rm0 = t[0], rm1 = (S > 1) ? t[1] : -INFINITY;
+#pragma unroll
+            for (int j = 2; j < S; j += 2) {
+                rm0 = fmaxf(rm0, t[j]);
+                if (j + 1 < S) rm1 = fmaxf(rm1, t[j + 1]);
             }
+            const float rm = fmaxf(rm0, rm1);
             if (rm > m) {
-                s *= ex2_approx(m - rm);
+                const float sc = ex2_approx(m - rm);
+                s *= sc;
+                s2 *= sc;
                 m = rm;
             }
             if (m != -INFINITY) {
 #pragma unroll
-                for (int j = 0; j < S; ++j) s += ex2_approx(t[j] - m);
+                for (int j = 0; j < S; j += 2) {
+                    s += ex2_approx(t[j] - m);
+                    if (j + 1 < S) s2 += ex2_approx(t[j + 1] - m);
+                }
             }
         }
     }
+    s += s2;
     float mg = m;
     for (int o = 1; o < split; o <<= 1) mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
     const bool none = (mg == -INFINITY);   // uniform over the group; every lane still reaches the shuffles
