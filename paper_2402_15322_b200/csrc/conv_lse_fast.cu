@@ -156,7 +156,7 @@ __device__ __forceinline__ void plane_diff_range(float da, float dgx, float dgy,
 }
 
 template <int R>
-__global__ void __launch_bounds__(LseFCfg<R>::NT)
+__global__ void __launch_bounds__(LseFCfg<R>::NT, 4)
 conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq, const float* __restrict__ Lq,
                      const float* __restrict__ LqRow,
                      const float* __restrict__ Lth, const float* __restrict__ LseS, const float* __restrict__ st,
