@@ -231,6 +231,78 @@ def config_sweep(device: int):
     return out
 
 
+def next_rows(device: int):
+    """The SURVEY §8f NEXT rows built beyond the scaling loop, each measured (CUDA events, after a
+    warm-up) at a paper-sized workload:
+      #1 porous-medium JKO (m = 5, w = (1, sqrt 10, sqrt 2)) on the c4 grid, one JKO step of
+         200 inner iterations -> inner iterations/s;
+      #2 transport cost <pi, rho_b^2> of a c4 plan (one conv with the cost table) -> ms and TFLOP/s;
+      #3 lifting: the orientation-score correlation of a 256 x 256 image at 64 orientations (21 x 21
+         cake wavelets) -> ms and TFLOP/s (2 N L^2 flop) vs the FFMA peak, and the whole image
+         interpolation (Steps 1-4) on c1's 28 x 28 x 16 grid for 5 t-values x 200 iterations."""
+    import math
+
+    import torch
+
+    import se2_synth as S
+    from paper_2402_15322_b200 import (Cake, Kernel, interpolate_images, make_porous_prox, make_prox, se2_jko_step,
+                                       se2_lift_image, se2_sinkhorn, se2_transport_cost)
+
+    def timed(fn, reps=1):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {}
+    peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    cfg = S.get_config("c4")
+    d = S.config_inputs(cfg)
+    w5 = (1.0, math.sqrt(10.0), math.sqrt(2.0))
+    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, w5, cfg.R, max_batch=1, device=device)
+    mu = torch.from_numpy(d["mus"][0]).cuda()
+    nxt, a, b = torch.empty_like(mu), torch.empty_like(mu), torch.empty_like(mu)
+    prox = make_porous_prox(cfg.tau, 5.0)
+    ms = timed(lambda: se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, log_domain=False, trace=False))
+    out["porous_jko_c4"] = {"workload": "porous-medium JKO step (m = 5, w = (1, sqrt 10, sqrt 2)) on 256x256x64, "
+                                        "200 inner iterations", "ms_per_step": ms,
+                            "inner_iters_per_s": cfg.iters / (ms / 1000.0)}
+    k.close()
+    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1, device=device)
+    se2_jko_step(k, mu, nxt, a, b, cfg.iters, make_prox(k, cfg.tau), log_domain=False, trace=False)
+    ms = timed(lambda: se2_transport_cost(k, a, b, False), reps=5)
+    flop = 2.0 * cfg.N * k.stats()["nnz_taps"]
+    out["transport_cost_c4"] = {"workload": "<pi, rho_b^2> of the c4 JKO plan (one cost-table conv + dot)",
+                                "ms": ms, "tflops": flop / (ms / 1000.0) / 1e12, "frac_of_ffma_peak": flop / (ms / 1000.0) / 1e12 / peak}
+    k.close()
+    c = Cake(64, 21, device=device)
+    y, x = np.mgrid[0:256, 0:256]
+    img = torch.from_numpy(np.exp(-((x - 128.0) ** 2 + (y - 100.0) ** 2) / 800.0).astype(np.float32)).cuda()
+    U = torch.empty((1, 64, 256, 256), device="cuda")
+    ms = timed(lambda: se2_lift_image(c, img, U), reps=10)
+    flop = 2.0 * 64 * 256 * 256 * 21 * 21
+    out["lift_image_256"] = {"workload": "orientation score of a 256x256 image, 64 cake wavelets 21x21", "ms": ms,
+                             "tflops": flop / (ms / 1000.0) / 1e12, "frac_of_ffma_peak": flop / (ms / 1000.0) / 1e12 / peak}
+    c.close()
+    c1 = S.get_config("c1")
+    c = Cake(c1.ntheta, 15, device=device)
+    kk = Kernel(c1.nx, c1.ny, c1.ntheta, c1.eps, c1.w, c1.R, max_batch=10, device=device)
+    rng = np.random.default_rng(5)
+    f0, f1 = (torch.from_numpy(rng.random((28, 28)).astype(np.float32) ** 4).cuda() for _ in range(2))
+    ts = [0.0, 0.25, 0.5, 0.75, 1.0]
+    ms = timed(lambda: interpolate_images(kk, c, f0, f1, ts, c1.iters))
+    out["interpolate_images_c1"] = {"workload": "image interpolation (lift, +/- split, 2 x 5 barycenters of 200 "
+                                                "log-domain iterations, signed projection) on 28x28x16", "ms": ms}
+    kk.close()
+    c.close()
+    return out
+
+
 def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
     """c3's barycenter (4 inputs, 128x128x32, log domain) with the inputs sharded over the ranks
     (parallel.ShardedBarycenter): the only exchange per iteration is the NCCL allreduce of the partial
@@ -401,6 +473,10 @@ def run_gpu(args):
     if rank == 0:
         if not args.no_configs:
             out["configs"] = config_sweep(local)
+            try:
+                out["next_rows"] = next_rows(local)
+            except Exception as e:  # measurement extra: never fail the headline line
+                out["next_rows"] = {"error": str(e)[:300]}
         if not args.no_cpu_baseline:
             v, desc, threads, _ = cpu_oracle_sample(cfg)
             out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc}

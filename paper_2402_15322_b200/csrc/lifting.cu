@@ -93,7 +93,8 @@ __global__ void cake_tabulate_kernel(int nt, int L, int degree, double cut, floa
 }
 
 // U[b][j][y][x] = sum_{dy,dx} T[j][dy][dx] f[b][y+dy][x+dx]; 16 x 16 outputs per CTA, the f tile (with
-// an R halo, zero outside the image) and one orientation's filter in shared memory
+// an R halo, zero outside the image) and one orientation's filter in shared memory.  Generic kernel for
+// banks wider than 31 x 31 (the register-blocked one below covers R <= 15)
 constexpr int kLT = 16;
 __global__ void lift_image_kernel(const float* __restrict__ f, const float* __restrict__ T, float* __restrict__ U,
                                   int nx, int ny, int nt, int L) {
@@ -123,6 +124,116 @@ __global__ void lift_image_kernel(const float* __restrict__ f, const float* __re
             for (int c = 0; c < L; ++c) acc = fmaf(frow[c], trow[c], acc);
         }
         if (gx < nx && gy < ny) U[(((int64_t)b * nt + j) * ny + gy) * nx + gx] = acc;
+    }
+}
+
+// Register-blocked orientation scores (the K3 FFMA geometry): one CTA = a 16 x 32 output tile x one
+// quad of orientations; lanes are rows, each warp 4 columns; per filter row the thread loads its input
+// row segment (LDS.128) and issues 16 FFMA per tap against one LDS.128 broadcast of the 4 orientations'
+// filter values (the bank re-laid out quad-interleaved in shared memory).
+template <int R>
+struct LiftCfg {
+    static constexpr int L = 2 * R + 1, P = 4, WX = 4, NT = 32 * WX, TY = 32, TX = P * WX;
+    static constexpr int RL = ((P + 2 * R) + 3) / 4 * 4;
+    static constexpr int NEED = (WX - 1) * P + RL;
+    static constexpr int P0 = (NEED + 3) / 4 * 4;
+    static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;   // pitch/4 odd: conflict-free rows
+    static constexpr int WIN_H = TY + 2 * R;
+    static constexpr size_t SMEM = (size_t)(WIN_H * PITCH + 4 * L * L) * sizeof(float);
+};
+
+template <int R>
+__global__ void __launch_bounds__(LiftCfg<R>::NT)
+lift_image_rb_kernel(const float* __restrict__ f, const float* __restrict__ T, float* __restrict__ U, int nx, int ny,
+                     int nt, int tiles_x) {
+    using C = LiftCfg<R>;
+    extern __shared__ __align__(16) float sm[];
+    float* win = sm;                                                     // [WIN_H][PITCH]
+    float4* fil = reinterpret_cast<float4*>(sm + C::WIN_H * C::PITCH);   // [L*L] quad-interleaved
+    const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
+    const int x0 = (tile % tiles_x) * C::TX, y0 = (tile / tiles_x) * C::TY;
+    const float* fb = f + (int64_t)b * nx * ny;
+    for (int i = threadIdx.x; i < C::WIN_H * C::PITCH; i += C::NT) {
+        const int r = i / C::PITCH, c = i - r * C::PITCH;
+        const int gy = y0 - R + r, gx = x0 - R + c;
+        win[i] = (gy >= 0 && gy < ny && gx >= 0 && gx < nx) ? fb[(int64_t)gy * nx + gx] : 0.f;
+    }
+    for (int i = threadIdx.x; i < C::L * C::L; i += C::NT) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int to = 4 * qd + q;
+            v[q] = to < nt ? T[(int64_t)to * C::L * C::L + i] : 0.f;
+        }
+        fil[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wx = threadIdx.x >> 5;
+    float acc[4][C::P];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < C::P; ++p) acc[q][p] = 0.f;
+#pragma unroll 1
+    for (int dy = 0; dy < C::L; ++dy) {
+        const float4* rowp = reinterpret_cast<const float4*>(win + (lane + dy) * C::PITCH + wx * C::P);
+        float r[C::RL];
+#pragma unroll
+        for (int j = 0; j < C::RL / 4; ++j) {
+            const float4 t = rowp[j];
+            r[4 * j] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
+        }
+        const float4* frow = fil + dy * C::L;
+#pragma unroll
+        for (int dx = 0; dx < C::L; ++dx) {
+            const float4 w = frow[dx];
+#pragma unroll
+            for (int p = 0; p < C::P; ++p) {
+                const float xv = r[p + dx];
+                acc[0][p] = fmaf(w.x, xv, acc[0][p]);
+                acc[1][p] = fmaf(w.y, xv, acc[1][p]);
+                acc[2][p] = fmaf(w.z, xv, acc[2][p]);
+                acc[3][p] = fmaf(w.w, xv, acc[3][p]);
+            }
+        }
+    }
+    const int gy = y0 + lane;
+    if (gy >= ny) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int to = 4 * qd + q;
+        if (to >= nt) continue;
+        float* row = U + (((int64_t)b * nt + to) * ny + gy) * nx;
+#pragma unroll
+        for (int p = 0; p < C::P; ++p) {
+            const int gx = x0 + wx * C::P + p;
+            if (gx < nx) row[gx] = acc[q][p];
+        }
+    }
+}
+
+template <int R>
+static cudaError_t launch_lift_rb(const se2_cake_s* c, const float* f, float* U, int nx, int ny, int batch,
+                                  cudaStream_t s) {
+    using C = LiftCfg<R>;
+    cudaError_t e = cudaFuncSetAttribute(lift_image_rb_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    const int tiles_x = (nx + C::TX - 1) / C::TX, tiles_y = (ny + C::TY - 1) / C::TY;
+    dim3 grid(tiles_x * tiles_y, (c->nt + 3) / 4, batch);
+    lift_image_rb_kernel<R><<<grid, C::NT, C::SMEM, s>>>(f, c->table, U, nx, ny, c->nt, tiles_x);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_lift_image(const se2_cake_s* c, const float* f, float* U, int nx, int ny, int batch,
+                                     cudaStream_t s) {
+    switch (c->R) {
+#define SE2_LCASE(r) \
+    case r: return launch_lift_rb<r>(c, f, U, nx, ny, batch, s);
+        SE2_LCASE(0) SE2_LCASE(1) SE2_LCASE(2) SE2_LCASE(3) SE2_LCASE(4) SE2_LCASE(5) SE2_LCASE(6) SE2_LCASE(7)
+        SE2_LCASE(8) SE2_LCASE(9) SE2_LCASE(10) SE2_LCASE(11) SE2_LCASE(12) SE2_LCASE(13) SE2_LCASE(14) SE2_LCASE(15)
+#undef SE2_LCASE
+        default: return cudaErrorNotSupported;   // wider banks: the generic kernel
     }
 }
 
@@ -438,6 +549,15 @@ SE2_API se2_status se2_lift_image(se2_cake c, const float* f, float* U, int32_t 
     if (check_cake(c) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(f && U && nx >= 1 && ny >= 1 && batch >= 1, "bad arguments");
     Guard g(c->device);
+    if (c->R <= 15) {   // register-blocked kernel (FFMA-bound)
+        const cudaError_t e = launch_lift_image(c, f, U, nx, ny, batch, (cudaStream_t)stream);
+        count_launch();
+        if (e != cudaSuccess) {
+            set_error(std::string("lift_image: ") + cudaGetErrorString(e));
+            return SE2_ECUDA;
+        }
+        return SE2_OK;
+    }
     const int TW = kLT + 2 * c->R;
     const size_t smem = sizeof(float) * ((size_t)TW * TW + (size_t)c->L * c->L);
     SE2_CUDA_TRY(cudaFuncSetAttribute(lift_image_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -51,7 +51,7 @@ def test_cake_table_parity(N, L, k, cut, cuda_device):
 
 
 @pytest.mark.parametrize("ny,nx,batch,N,L", [(28, 28, 2, 16, 15), (37, 29, 3, 8, 11), (64, 48, 1, 32, 21),
-                                             (5, 7, 1, 4, 9)])
+                                             (5, 7, 1, 4, 9), (41, 35, 2, 6, 31), (20, 18, 1, 8, 33)])
 def test_lift_image_parity(ny, nx, batch, N, L, cuda_device):
     from paper_2402_15322_b200 import Cake, se2_lift_image
     c = Cake(N, L)
