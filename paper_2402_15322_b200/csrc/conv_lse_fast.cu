@@ -195,24 +195,27 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     const float LOW = -1e30f;   // "no term yet" sentinel of the running maxima (finite: no inf - inf)
     const float cx0 = x0 + 0.5f * (min(C::TX, nx - x0) - 1), cy0 = y0 + 0.5f * (min(C::TY, ny - y0) - 1);
 
-    // ---- per-channel bounds from the tile statistics -------------------------------------------
-    for (int i = threadIdx.x; i < nt; i += C::NT) {
-        const float* s0 = st + (((int64_t)b * nt + i) * ntile + tile) * kStat;
-        const float mu = s0[5];
-        float M = NEG_INF;
-        // tilted bounds of the residual r = lv - psi_0 over the window (3 x 3 tile neighbourhood)
-        const bool plane = s0[7] > 0.5f;
-        const float a0 = s0[0], gx0 = s0[1], gy0 = s0[2];
-        float rlo = INFINITY, rhi = -INFINITY;
-        bool tilt_ok = plane;
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int yy = ty + dy, xx = tx + dx;
+    // ---- per-channel bounds from the tile statistics: 4 threads per channel share its 9 neighbour
+    // tiles (independent loads in flight), then combine over the 4 lanes ----------------------------
+    for (int base = 0; base < nt; base += C::NT / 4) {
+        const int i = base + (threadIdx.x >> 2), part = threadIdx.x & 3;
+        const bool valid = i < nt;
+        float M = NEG_INF, rlo = INFINITY, rhi = -INFINITY, mu = 0.f, a0 = 0.f, gx0 = 0.f, gy0 = 0.f;
+        int tok = 0;
+        if (valid) {
+            const float* s0 = st + (((int64_t)b * nt + i) * ntile + tile) * kStat;
+            mu = s0[5];
+            a0 = s0[0];
+            gx0 = s0[1];
+            gy0 = s0[2];
+            tok = s0[7] > 0.5f ? 1 : 0;   // tilted bounds of the residual r = lv - psi_0 over the window
+            for (int n = part; n < 9; n += 4) {
+                const int yy = ty + n / 3 - 1, xx = tx + n % 3 - 1;
                 if (yy < 0 || yy >= tiles_y || xx < 0 || xx >= tiles_x) continue;
                 const float* sj = st + (((int64_t)b * nt + i) * ntile + yy * tiles_x + xx) * kStat;
                 M = fmaxf(M, sj[6]);
-                if (!tilt_ok) continue;
-                if (!(sj[7] > 0.5f)) { tilt_ok = false; continue; }
+                if (!tok) continue;
+                if (!(sj[7] > 0.5f)) { tok = 0; continue; }
                 const int xa = xx * C::TX, ya = yy * C::TY;
                 const int xb = min(xa + C::TX, nx) - 1, yb = min(ya + C::TY, ny) - 1;
                 const float cxj = xa + 0.5f * (xb - xa), cyj = ya + 0.5f * (yb - ya);
@@ -222,13 +225,23 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                 rlo = fminf(rlo, sj[3] + lo);
                 rhi = fmaxf(rhi, sj[4] + hi);
             }
-        sMu[i] = mu;
-        sM[i] = M;
-        sA[i] = a0;
-        sGx[i] = gx0;
-        sGy[i] = gy0;
-        sShift[i] = tilt_ok ? ((rhi - rlo <= kFastRange) ? rlo : NAN) : NAN;   // R_lo when a tilt may be valid
-        sRhi[i] = rhi;
+        }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            rlo = fminf(rlo, __shfl_xor_sync(0xffffffffu, rlo, o));
+            rhi = fmaxf(rhi, __shfl_xor_sync(0xffffffffu, rhi, o));
+            tok = min(tok, __shfl_xor_sync(0xffffffffu, tok, o));
+        }
+        if (valid && part == 0) {
+            sMu[i] = mu;
+            sM[i] = M;
+            sA[i] = a0;
+            sGx[i] = gx0;
+            sGy[i] = gy0;
+            sShift[i] = tok ? ((rhi - rlo <= kFastRange) ? rlo : NAN) : NAN;   // R_lo when a tilt may be valid
+            sRhi[i] = rhi;
+        }
     }
     __syncthreads();
     if (wx < 4) {   // warp q: lower bound LB(to_q) = max_j (Lth(to_q, j) + mu_j)
@@ -285,20 +298,41 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
             }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {   // compact the active list: entry = channel | (path << 16)
-        int n = 0, nf = 0, ntl = 0;
-        int seen = 0;   // active channels are dealt round-robin over the split groups (balanced)
-        for (int i = 0; i < nt; ++i) {
-            int s = sList[i];
-            if (s && ((seen++) % ngroups) == grp) {
-                sList[n++] = i | (s << 16);
-                nf += (s == 1 || s == 3);
-                ntl += (s == 3);
-            }
+    {   // compact the active list (entry = channel | (path << 16)); active channels are dealt
+        // round-robin over the split groups by their rank among the actives (ballot prefix counts)
+        __shared__ int sWc[C::NT / 32], sWf[C::NT / 32], sWt[C::NT / 32];
+        const int i = threadIdx.x;
+        const int stt = (i < nt) ? sList[i] : 0;
+        const bool act = stt != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (lane == 0) sWc[wx] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w2 = 0; w2 < wx; ++w2) off += sWc[w2];
+        const int rank = off + __popc(bal & ((1u << lane) - 1u));
+        const bool mine = act && (rank % ngroups) == grp;
+        const unsigned bm = __ballot_sync(0xffffffffu, mine);
+        const unsigned bf = __ballot_sync(0xffffffffu, mine && (stt == 1 || stt == 3));
+        const unsigned bt = __ballot_sync(0xffffffffu, mine && stt == 3);
+        __syncthreads();   // every sList[i] / sWc read before they are overwritten
+        if (mine) sList[rank / ngroups] = i | (stt << 16);
+        if (lane == 0) {
+            sWc[wx] = __popc(bm);
+            sWf[wx] = __popc(bf);
+            sWt[wx] = __popc(bt);
         }
-        sNAct = n;
-        sNFast = nf;
-        sNTilt = ntl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int n = 0, nf = 0, ntl = 0;
+            for (int w2 = 0; w2 < C::NT / 32; ++w2) {
+                n += sWc[w2];
+                nf += sWf[w2];
+                ntl += sWt[w2];
+            }
+            sNAct = n;
+            sNFast = nf;
+            sNTilt = ntl;
+        }
     }
     __syncthreads();
     const int nact = sNAct;
