@@ -658,10 +658,10 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                     float4 t = rowp[j];
                     r[4 * j + 0] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
                 }
-                // per segment k (taps dx in [k SEGW, (k+1) SEGW)): bound = max_dx L2 + max of the r
-                // entries those taps read (indices 2R - dx + p); warp vote per segment
-                bool segl[C::NSEG];
-                bool any = false;
+                // per segment k (taps dx in [k SEGW, (k+1) SEGW)) and output orientation q: bound = max_dx
+                // L2_q + max of the r entries those taps read (indices 2R - dx + p); warp vote per (k, q),
+                // so a live segment only spends exps on the orientations that can reach their outputs
+                unsigned segq = 0;   // bit 4 k + q
 #pragma unroll
                 for (int k = 0; k < C::NSEG; ++k) {
                     const int dxlo = k * C::SEGW;
@@ -672,30 +672,27 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
                         for (int j = 2 * R - dxhi; j <= 2 * R - dxlo + C::P - 1; ++j) sm = fmaxf(sm, r[j]);
                     }
                     const float4 m4 = rmx[dy * C::NSEG + k];
-                    const bool live = (sm + m4.x >= thr[0]) || (sm + m4.y >= thr[1]) || (sm + m4.z >= thr[2]) ||
-                                      (sm + m4.w >= thr[3]);
-                    segl[k] = __any_sync(0xffffffffu, live);
-                    any |= segl[k];
-                    rows_seen += 1;
-                    rows_live += segl[k] ? 1 : 0;
+                    const unsigned l = (__any_sync(0xffffffffu, sm + m4.x >= thr[0]) ? 1u : 0u) |
+                                       (__any_sync(0xffffffffu, sm + m4.y >= thr[1]) ? 2u : 0u) |
+                                       (__any_sync(0xffffffffu, sm + m4.z >= thr[2]) ? 4u : 0u) |
+                                       (__any_sync(0xffffffffu, sm + m4.w >= thr[3]) ? 8u : 0u);
+                    segq |= l << (4 * k);
+                    rows_seen += 4;
+                    rows_live += __popc(l);
                 }
-                if (!any) continue;
-                const float4* frow = fil + dy * C::S;
+                if (!segq) continue;
+                const float* frow = reinterpret_cast<const float*>(fil + dy * C::S);   // [dx][q]
 #pragma unroll
                 for (int k = 0; k < C::NSEG; ++k) {
-                    if (!segl[k]) continue;
 #pragma unroll
-                    for (int dx = k * C::SEGW; dx < (k + 1) * C::SEGW && dx < C::S; ++dx) {
-                        const float4 w = frow[dx];
+                    for (int q = 0; q < 4; ++q) {
+                        if (!((segq >> (4 * k + q)) & 1u)) continue;
 #pragma unroll
-                        for (int p = 0; p < C::P; ++p) {
-                            const float xv = r[p - dx + 2 * R];
-                            // (routing 3 of the 16 exps per tap to ex2_poly on the FMA pipe measured 4-7%
-                            //  slower on c3 states: this loop is issue-bound, not MUFU-bound)
-                            Sacc[0][p] += ex2_approx((xv + w.x) - Macc[0][p]);
-                            Sacc[1][p] += ex2_approx((xv + w.y) - Macc[1][p]);
-                            Sacc[2][p] += ex2_approx((xv + w.z) - Macc[2][p]);
-                            Sacc[3][p] += ex2_approx((xv + w.w) - Macc[3][p]);
+                        for (int dx = k * C::SEGW; dx < (k + 1) * C::SEGW && dx < C::S; ++dx) {
+                            const float w = frow[4 * dx + q];
+#pragma unroll
+                            for (int p = 0; p < C::P; ++p)
+                                Sacc[q][p] += ex2_approx((r[p - dx + 2 * R] + w) - Macc[q][p]);
                         }
                     }
                 }
