@@ -407,7 +407,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         if (st != SE2_OK) return st;
     }
     // K9: the whole loop in one cluster launch when the grid fits in shared memory (c0-sized)
-    const int k9c = (LOG && !jko && batch == 1 && s_out == nullptr &&
+    const int k9c = (LOG && !jko && batch == 1 && s_out == nullptr && iters > 0 &&
                      !(opts->flags & (SE2_NO_PERSISTENT | SE2_LSE_EXACT | SE2_LSE_K3EXACT | SE2_LSE_NOTILT)))
                         ? k9_cluster_size(k) : 0;
     if (k9c > 0) {
