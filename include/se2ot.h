@@ -299,6 +299,8 @@ SE2_API se2_status se2_reconstruct_field(se2_cake c, const float* U, float* angl
                                          int32_t batch, float threshold, se2_stream stream);
 /* y[i] = exp(x[i]) (expf), e.g. a log-domain barycenter -> the measure the projection takes. */
 SE2_API se2_status se2_exp(const float* x, float* y, int64_t n, se2_stream stream);
+/* y[i] = log(x[i]) (logf; log 0 = -inf), e.g. measures -> log-domain targets. */
+SE2_API se2_status se2_log(const float* x, float* y, int64_t n, se2_stream stream);
 
 SE2_API const char* se2_last_error(void);
 SE2_API int32_t se2_abi_version(void);

@@ -677,6 +677,18 @@ SE2_API se2_status se2_reconstruct_field(se2_cake c, const float* U, float* angl
     return launch_ok("reconstruct_field");
 }
 
+__global__ void log_elem_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = logf(x[i]);
+}
+
+SE2_API se2_status se2_log(const float* x, float* y, int64_t n, se2_stream stream) {
+    SE2_CHECK_ARG(x && y && n >= 1, "bad arguments");
+    log_elem_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, y, n);
+    count_launch();
+    return launch_ok("log");
+}
+
 SE2_API se2_status se2_exp(const float* x, float* y, int64_t n, se2_stream stream) {
     SE2_CHECK_ARG(x && y && n >= 1, "bad arguments");
     exp_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, y, n);

@@ -153,6 +153,15 @@ def se2_exp(x: torch.Tensor) -> torch.Tensor:
     return y
 
 
+def se2_log(x: torch.Tensor) -> torch.Tensor:
+    """log(x) elementwise in the library (measures -> log-domain targets; log 0 = -inf)."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise TypeError("x must be a contiguous float32 CUDA tensor")
+    y = torch.empty_like(x)
+    check(L.load().se2_log(_ptr(x), _ptr(y), x.numel(), _stream(x.device)))
+    return y
+
+
 def interpolate_images(k: Kernel, c: Cake, f0: torch.Tensor, f1: torch.Tensor, ts: Sequence[float], iters: int,
                        log_domain: bool = True, floor_rel: float = 1e-6) -> Tuple[torch.Tensor, np.ndarray]:
     """The paper's SE(2) image interpolation b_t (Steps 1-4) for every t in ts: lift both

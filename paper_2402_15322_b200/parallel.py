@@ -53,6 +53,10 @@ class CudaOps:
         from ._lib import SE2_EPI_PROX
         return self.api.se2_conv_update(self.k, x, None, out, SE2_EPI_PROX, self.log, prox=prox)
 
+    def log_of(self, x):                    # elementwise log (log 0 = -inf), a new tensor
+        from .lifting import se2_log
+        return se2_log(x.contiguous())
+
     def logmean(self, ld, lambdas, out):    # out = sum_i lambda_i ld_i  (lambda_i = 0 skipped)
         return self.api.se2_bary_logmean(ld, lambdas, self.k.N, out)
 
@@ -78,7 +82,7 @@ class ShardedBarycenter:
         self.group = group
         self.n = mus_local.shape[0]
         self.lam = np.asarray(lambdas_local, dtype=np.float64)
-        self.lmu = torch.log(mus_local)
+        self.lmu = ops.log_of(mus_local) if mus_local.numel() else mus_local.clone()
         self.lv = torch.zeros_like(mus_local)
         self.lw = torch.zeros_like(mus_local)
         self.ld = torch.empty_like(mus_local)

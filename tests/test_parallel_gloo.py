@@ -54,6 +54,10 @@ class OracleOps:
         p = tau / (self.eps + tau)
         out.copy_(torch.from_numpy(z ** (-p) * np.exp(-p * V)))
 
+    def log_of(self, x):
+        with np.errstate(divide="ignore"):
+            return torch.from_numpy(np.log(x.numpy()))
+
     def logmean(self, ld, lam, out):
         acc = np.zeros(out.shape)
         for i, l in enumerate(lam):
