@@ -689,8 +689,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             if (st != SE2_OK) return st;
             // mu = prod d_i^lambda_i ;  v_i <- v_i mu / d_i
             if (LOG) {
-                SE2_CUDA_TRY(launch_bary_logmean(n, nsolve, N, d, lam_dev, bary, s));
-                SE2_CUDA_TRY(launch_bary_update_log(n, nsolve, N, v, v_lo, d, bary, s));
+                SE2_CUDA_TRY(launch_bary_logmean_update(n, nsolve, N, d, lam_dev, bary, v, v_lo, s));
             } else {
                 SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
             }

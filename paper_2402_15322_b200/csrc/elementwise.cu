@@ -100,6 +100,42 @@ __global__ void bary_update_log_kernel(int n, int nsolve, int64_t N, float* lv, 
         }
     }
 }
+// fused single-GPU barycenter step (App. A): per (solve, site) lbar = sum_i lambda_i ld_i (lambda_i = 0
+// skipped, R6), then lv_i += lbar - ld_i with the compensated two-sum -- one pass over ld instead of two
+__global__ void bary_logmean_update_kernel(int n, int nsolve, int64_t N, const float* __restrict__ ld,
+                                           const float* __restrict__ lam, float* __restrict__ lbar,
+                                           float* __restrict__ lv, float* __restrict__ lv_lo) {
+    const int64_t total = (int64_t)nsolve * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int sv = (int)(t / N);
+        const int64_t x = t - (int64_t)sv * N;
+        float acc = 0.f;
+        for (int i = 0; i < n; ++i) {
+            const float l = lam[sv * n + i];
+            if (l != 0.f) acc += l * ld[((int64_t)sv * n + i) * N + x];
+        }
+        lbar[t] = acc;
+        for (int i = 0; i < n; ++i) {
+            const int64_t j = ((int64_t)sv * n + i) * N + x;
+            const float dlt = acc - ld[j];
+            const float hi = lv[j];
+            const float y = dlt + lv_lo[j];
+            const float s2 = hi + y;                       // two-sum (Knuth): s2 + e == hi + y exactly
+            const float bb = s2 - hi;
+            const float e = (hi - (s2 - bb)) + (y - bb);
+            lv[j] = s2;
+            lv_lo[j] = (s2 == s2 && fabsf(s2) != INFINITY) ? e : 0.f;
+        }
+    }
+}
+cudaError_t launch_bary_logmean_update(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev, float* lbar,
+                                       float* lv, float* lv_lo, cudaStream_t s) {
+    bary_logmean_update_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, ld, lam_dev, lbar, lv,
+                                                                                   lv_lo);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
                                    const float* lbar, cudaStream_t s) {
     bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, lv_lo, ld, lbar);
