@@ -238,6 +238,7 @@ PARITY_CASES: List[ParityCase] = [
     ParityCase("c3q", "c3", 128, 128, 32, 10, 20, full_fields=False),  # c3 at full size, first 20 iterations
     ParityCase("c3m", "c3", 44, 40, 32, 10, 40),
     ParityCase("c4p", "c4", 256, 256, 64, 15, 2, jko_steps=1, full_fields=False),
+    ParityCase("c4q", "c4", 256, 256, 64, 15, 20, jko_steps=1, full_fields=False),  # full c4 grid, 20 inner iterations
     ParityCase("c4m", "c4", 72, 60, 16, 4, 200, jko_steps=3),
     # NEXT #1: the paper's own gradient flow -- porous medium m = 5, w = (1, sqrt 10, sqrt 2)
     ParityCase("c5m", "c4", 64, 56, 16, 4, 100, jko_steps=2, energy="porous", m=5.0,
