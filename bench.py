@@ -320,7 +320,18 @@ def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
     lo, hi = partition(len(d["mus"]), ws, rank)
     k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=max(hi - lo, 1), device=local)
     mus = torch.from_numpy(np.stack(d["mus"][lo:hi]) if hi > lo else np.zeros((0,) + cfg.shape, np.float32)).cuda()
-    drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi])
+    # ws > 1: the fused exchange (peer buffers read in place by one reduce + update kernel, symmetric
+    # memory over NVLink); NCCL allreduce if symmetric memory is unavailable.  ws == 1: no exchange.
+    exchange = "nccl"
+    drv = None
+    if ws > 1:
+        try:
+            drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="p2p")
+            exchange = "p2p"
+        except Exception:
+            drv = None
+    if drv is None:
+        drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="nccl")
     drv.iterate(2)   # warm-up
     torch.cuda.synchronize()
     if ws > 1:
@@ -335,9 +346,11 @@ def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    how = {"p2p": "fused peer-memory reduce + v-update kernel (symmetric memory, one device barrier)",
+           "nccl": "NCCL allreduce of the weighted log-mean"}[exchange] if ws > 1 else "no exchange (1 rank)"
     return {"workload": "c3 barycenter, 4 inputs sharded over ranks (inputs per rank: "
-                        f"{[partition(4, ws, r)[1] - partition(4, ws, r)[0] for r in range(ws)]}), NCCL allreduce "
-                        "of the weighted log-mean per iteration", "iters": iters, "ms": ms,
+                        f"{[partition(4, ws, r)[1] - partition(4, ws, r)[0] for r in range(ws)]}), {how} per iteration",
+            "exchange": exchange if ws > 1 else None, "iters": iters, "ms": ms,
             "iters_per_s": iters / (ms / 1000.0), "n_gpus": ws}
 
 

@@ -215,6 +215,16 @@ SE2_API se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const
 SE2_API se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar,
                            se2_stream stream);
 
+/* Fused cross-rank log-mean reduction + v-update of the sharded barycenter (App. A with the inputs
+ * spread over ranks; the allreduce and the update in ONE kernel reading the peers' buffers directly):
+ *   lbar[x] = sum_{r < nranks} partials[r][x]      (rank order -> bit-identical on every rank)
+ *   lv[i][x] += lbar[x] - ld[i][x]                 for the n_local inputs of this rank (may be 0)
+ * partials_dev: DEVICE array of nranks device pointers to [N] fp32 buffers -- normally the peers'
+ * buffers mapped into this process (symmetric memory / CUDA IPC over NVLink); every buffer must be
+ * complete before the call (the caller's cross-rank barrier).  lbar: [N] out (may alias nothing). */
+SE2_API se2_status se2_bary_reduce_update(int32_t nranks, const float* const* partials_dev, int32_t n_local,
+                                          int64_t N, float* lv, const float* ld, float* lbar, se2_stream stream);
+
 /* Rows [row0, row0 + rows) of every plane of a [planes][ny][nx] device array (slab decomposition):
  * deterministic fp64 sum to the host, and in-place scaling by `factor`. */
 SE2_API se2_status se2_sum_rows(const float* x, int32_t planes, int32_t ny, int32_t nx, int32_t row0, int32_t rows,

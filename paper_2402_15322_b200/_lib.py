@@ -40,6 +40,7 @@ EXPORTED = [
     "se2_transport_cost", "se2_lse_row_stats",
     "se2_cake_build", "se2_cake_get", "se2_cake_destroy", "se2_lift_image", "se2_split_signed", "se2_project",
     "se2_project_signed", "se2_lift_field", "se2_reconstruct_field", "se2_exp", "se2_log",
+    "se2_bary_reduce_update",
 ]
 
 
@@ -119,6 +120,7 @@ def load(path: str = LIB_PATH):
         "se2_reconstruct_field": [P, P, P, P, i32, i32, i32, ctypes.c_float, P],
         "se2_exp": [P, P, i64, P],
         "se2_log": [P, P, i64, P],
+        "se2_bary_reduce_update": [i32, P, i32, i64, P, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

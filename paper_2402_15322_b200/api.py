@@ -257,6 +257,17 @@ def se2_bary_update(lv: torch.Tensor, ld: torch.Tensor, lbar: torch.Tensor, n: i
     check(L.load().se2_bary_update(n, N, _ptr(lv), _ptr(ld), _ptr(lbar), _stream(lv.device)))
 
 
+def se2_bary_reduce_update(partial_ptrs: torch.Tensor, n_local: int, N: int, lv: Optional[torch.Tensor],
+                           ld: Optional[torch.Tensor], lbar: Optional[torch.Tensor]):
+    """lbar = sum_r partials[r] (rank order), lv_i += lbar - ld_i: the sharded barycenter's allreduce fused
+    with the v-update.  partial_ptrs: int64 CUDA tensor of nranks device pointers (peer buffers)."""
+    if not (isinstance(partial_ptrs, torch.Tensor) and partial_ptrs.is_cuda and partial_ptrs.dtype == torch.int64):
+        raise TypeError("partial_ptrs must be an int64 CUDA tensor of device pointers")
+    dev = partial_ptrs.device
+    check(L.load().se2_bary_reduce_update(partial_ptrs.numel(), _ptr(partial_ptrs), int(n_local), int(N), _ptr(lv),
+                                          _ptr(ld), _ptr(lbar), _stream(dev)))
+
+
 def se2_sum(x: torch.Tensor) -> float:
     out = ctypes.c_double()
     check(L.load().se2_sum(_ptr(x), x.numel(), ctypes.byref(out), _stream(x.device)))

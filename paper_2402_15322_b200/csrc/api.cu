@@ -826,6 +826,14 @@ se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, con
     return SE2_OK;
 }
 
+se2_status se2_bary_reduce_update(int32_t nranks, const float* const* partials_dev, int32_t n_local, int64_t N,
+                                  float* lv, const float* ld, float* lbar, se2_stream stream) {
+    SE2_CHECK_ARG(nranks >= 1 && partials_dev && N >= 1 && n_local >= 0, "bad arguments");
+    SE2_CHECK_ARG(n_local == 0 || (lv && ld), "lv and ld required when n_local > 0");
+    SE2_CUDA_TRY(launch_bary_reduce_update(nranks, partials_dev, n_local, N, lv, ld, lbar, (cudaStream_t)stream));
+    return SE2_OK;
+}
+
 se2_status se2_sum(const float* xp, int64_t n, double* out_host, se2_stream stream) {
     SE2_CHECK_ARG(xp && n >= 1 && out_host, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;

@@ -136,6 +136,25 @@ cudaError_t launch_bary_logmean_update(int n, int nsolve, int64_t N, const float
     return cudaGetLastError();
 }
 
+// sharded barycenter: lbar = sum over ranks of the partial log-means (peer buffers, rank order), then
+// lv_i += lbar - ld_i for the local inputs -- the allreduce fused with the update
+__global__ void bary_reduce_update_kernel(int nranks, const float* const* __restrict__ parts, int n_local, int64_t N,
+                                          float* __restrict__ lv, const float* __restrict__ ld,
+                                          float* __restrict__ lbar) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N; x += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.f;
+        for (int r = 0; r < nranks; ++r) acc += parts[r][x];
+        if (lbar != nullptr) lbar[x] = acc;
+        for (int i = 0; i < n_local; ++i) lv[(int64_t)i * N + x] += acc - ld[(int64_t)i * N + x];
+    }
+}
+cudaError_t launch_bary_reduce_update(int nranks, const float* const* parts, int n_local, int64_t N, float* lv,
+                                      const float* ld, float* lbar, cudaStream_t s) {
+    bary_reduce_update_kernel<<<grid_for(N, 256), 256, 0, s>>>(nranks, parts, n_local, N, lv, ld, lbar);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
                                    const float* lbar, cudaStream_t s) {
     bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, lv_lo, ld, lbar);

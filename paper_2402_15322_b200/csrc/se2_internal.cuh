@@ -152,6 +152,8 @@ cudaError_t launch_reduce_partials(const float* partial, int batch, int nblocks,
                                    cudaStream_t s);
 cudaError_t launch_bary_logmean(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev,
                                 float* lbar, cudaStream_t s);
+cudaError_t launch_bary_reduce_update(int nranks, const float* const* parts, int n_local, int64_t N, float* lv,
+                                      const float* ld, float* lbar, cudaStream_t s);
 cudaError_t launch_bary_logmean_update(int n, int nsolve, int64_t N, const float* ld, const float* lam_dev, float* lbar,
                                        float* lv, float* lv_lo, cudaStream_t s);
 cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,

@@ -57,6 +57,17 @@ class CudaOps:
         from .lifting import se2_log
         return se2_log(x.contiguous())
 
+    def reduce_update(self, sources, lv, ld, lbar, n):
+        """lbar = sum over ranks of the partial log-means (rank order), lv_i += lbar - ld_i: one kernel
+        (se2_bary_reduce_update).  sources: an int64 device tensor of peer pointers (P2PExchange) or a
+        list of gathered tensors (GatherExchange)."""
+        if isinstance(sources, torch.Tensor):
+            table = sources
+        else:
+            table = torch.tensor([t.data_ptr() for t in sources], dtype=torch.int64, device=lbar.device)
+        N = lbar.numel()
+        self.api.se2_bary_reduce_update(table, n, N, lv if n > 0 else None, ld if n > 0 else None, lbar)
+
     def logmean(self, ld, lambdas, out):    # out = sum_i lambda_i ld_i  (lambda_i = 0 skipped)
         return self.api.se2_bary_logmean(ld, lambdas, self.k.N, out)
 
@@ -70,6 +81,54 @@ class CudaOps:
         self.api.se2_scale_rows(x, row0, rows, factor)
 
 
+class GatherExchange:
+    """Peer partial log-means by `dist.all_gather` into local copies (any backend: the gloo CPU tests,
+    or NCCL as the baseline transport); double-buffered by iteration parity like P2PExchange."""
+
+    def __init__(self, like: torch.Tensor, group=None):
+        self.group = group
+        self.ws = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.slots = [torch.empty_like(like), torch.empty_like(like)]
+
+    def slot(self, parity: int) -> torch.Tensor:
+        return self.slots[parity]
+
+    def sources(self, parity: int):
+        mine = self.slots[parity]
+        if self.ws == 1:
+            return [mine]
+        out = [torch.empty_like(mine) for _ in range(self.ws)]
+        dist.all_gather(out, mine, group=self.group)
+        return out
+
+
+class P2PExchange:
+    """Peer partial log-means read in place over NVLink: every rank owns a symmetric-memory buffer
+    [2][N] (torch SymmetricMemory: peer-mapped allocations), double-buffered by iteration parity; one
+    device barrier per iteration makes the slot of that parity complete on every rank, then the fused
+    reduce + update kernel reads all ranks' slots through the device pointer table.  A fast rank can
+    only overwrite a slot after the next iteration's barrier, i.e. after every rank finished reading
+    it (the reads precede that barrier on each rank's stream)."""
+
+    def __init__(self, like: torch.Tensor, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.group = group if group is not None else dist.group.WORLD
+        shape = tuple(like.shape)
+        self.buf = symm_mem.empty((2,) + shape, dtype=torch.float32, device=like.device)
+        self.hdl = symm_mem.rendezvous(self.buf, self.group)
+        base = self.buf.data_ptr() - int(self.hdl.buffer_ptrs[self.hdl.rank])   # offset inside the allocation
+        n = like.numel()
+        self.tables = [torch.tensor([int(p) + base + parity * n * 4 for p in self.hdl.buffer_ptrs], dtype=torch.int64,
+                                    device=like.device) for parity in (0, 1)]
+
+    def slot(self, parity: int) -> torch.Tensor:
+        return self.buf[parity]
+
+    def sources(self, parity: int) -> torch.Tensor:
+        self.hdl.barrier(channel=parity)
+        return self.tables[parity]
+
+
 class ShardedBarycenter:
     """App. A barycenter with inputs sharded over the ranks of the default process group.
 
@@ -77,7 +136,11 @@ class ShardedBarycenter:
     sums to 1 over all ranks).  Log domain (R7, R13).  After `run`, `lbar` holds log mu on every rank.
     """
 
-    def __init__(self, ops, mus_local: torch.Tensor, lambdas_local: Sequence[float], group=None):
+    def __init__(self, ops, mus_local: torch.Tensor, lambdas_local: Sequence[float], group=None,
+                 exchange: str = "nccl"):
+        """exchange: "nccl" (allreduce of the partial log-mean, then the update), "p2p" (peer buffers
+        read in place by the fused reduce + update kernel, P2PExchange) or "gather" (all_gather copies
+        into the same fused kernel; the CPU tests)."""
         self.ops = ops
         self.group = group
         self.n = mus_local.shape[0]
@@ -87,8 +150,18 @@ class ShardedBarycenter:
         self.lw = torch.zeros_like(mus_local)
         self.ld = torch.empty_like(mus_local)
         self.lbar = torch.empty(tuple(mus_local.shape[1:]), dtype=mus_local.dtype, device=mus_local.device)
+        self.xch = None
+        if exchange == "p2p":
+            self.xch = P2PExchange(self.lbar, group)
+        elif exchange == "gather":
+            self.xch = GatherExchange(self.lbar, group)
+        elif exchange != "nccl":
+            raise ValueError(f"unknown exchange {exchange!r}")
+        self.parity = 0
 
     def iterate(self, iters: int):
+        if self.xch is not None:
+            return self._iterate_fused(iters)
         for _ in range(iters):
             if self.n > 0:
                 self.ops.divide(self.lv, self.lmu, self.lw)        # w_i = mu_i / K v_i
@@ -100,6 +173,20 @@ class ShardedBarycenter:
                 dist.all_reduce(self.lbar, op=dist.ReduceOp.SUM, group=self.group)   # log mu
             if self.n > 0:
                 self.ops.bary_update(self.lv, self.ld, self.lbar, self.n)            # v_i <- v_i mu / d_i
+        return self.lbar
+
+    def _iterate_fused(self, iters: int):
+        for _ in range(iters):
+            slot = self.xch.slot(self.parity)
+            if self.n > 0:
+                self.ops.divide(self.lv, self.lmu, self.lw)        # w_i = mu_i / K v_i
+                self.ops.multiply(self.lw, self.lv, self.ld)       # d_i = v_i K w_i
+                self.ops.logmean(self.ld, self.lam, slot)          # this rank's partial sum_i lambda_i log d_i
+            else:
+                slot.zero_()
+            src = self.xch.sources(self.parity)                    # every rank's partial of this parity
+            self.ops.reduce_update(src, self.lv, self.ld, self.lbar, self.n)   # log mu; v_i <- v_i mu / d_i
+            self.parity ^= 1
         return self.lbar
 
 

@@ -47,3 +47,59 @@ def test_slab_jko_single_rank(cuda_device):
                 log_domain=False, trace=False)
     assert measure_err(out, ref["mus"][2]) < 1e-4
     np.testing.assert_allclose(masses, ref["masses"], rtol=1e-4)
+
+
+def test_bary_reduce_update_kernel(cuda_device):
+    """se2_bary_reduce_update on simulated peers (three local buffers behind a device pointer table):
+    lbar = sum in rank order, lv_i += lbar - ld_i."""
+    from paper_2402_15322_b200.api import se2_bary_reduce_update
+    rng = np.random.default_rng(5)
+    N, n = 1000, 2
+    parts = [torch.from_numpy(rng.normal(size=N).astype(np.float32)).cuda() for _ in range(3)]
+    table = torch.tensor([p.data_ptr() for p in parts], dtype=torch.int64, device="cuda")
+    lv0 = rng.normal(size=(n, N)).astype(np.float32)
+    ld = rng.normal(size=(n, N)).astype(np.float32)
+    lv = torch.from_numpy(lv0.copy()).cuda()
+    lbar = torch.empty(N, device="cuda")
+    se2_bary_reduce_update(table, n, N, lv, torch.from_numpy(ld).cuda(), lbar)
+    torch.cuda.synchronize()
+    ref = (parts[0].cpu().numpy() + parts[1].cpu().numpy()) + parts[2].cpu().numpy()   # float32, rank order
+    assert np.array_equal(lbar.cpu().numpy(), ref)
+    assert np.allclose(lv.cpu().numpy(), lv0 + (ref[None] - ld), rtol=0, atol=1e-6)
+    se2_bary_reduce_update(table, 0, N, None, None, lbar)          # a rank without inputs
+    assert np.array_equal(lbar.cpu().numpy(), ref)
+
+
+def _one_rank_group():
+    import socket
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    return dist
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "gather"])
+def test_sharded_barycenter_fused_exchange_single_rank(exchange, cuda_device):
+    """The fused exchange on a 1-rank NCCL group: symmetric-memory slots + device barrier + the
+    reduce/update kernel (p2p), or all_gather copies into the same kernel (gather), against the oracle."""
+    from paper_2402_15322_b200 import Kernel
+    from paper_2402_15322_b200.parallel import CudaOps, ShardedBarycenter
+    _one_rank_group()
+    nx, ny, nt, R, eps, w = 40, 36, 16, 5, 0.02, (1.0, 3.0, 1.0)
+    g = O.Grid(nx, ny, nt)
+    rng = np.random.default_rng(0)
+    mus = [(rng.random(g.shape) ** 3 + 1e-3).astype(np.float32) for _ in range(3)]
+    mus = [(m / m.sum()).astype(np.float32) for m in mus]
+    lam = np.array([0.2, 0.5, 0.3])
+    k = Kernel(nx, ny, nt, eps, w, R, max_batch=3)
+    drv = ShardedBarycenter(CudaOps(k, True), torch.from_numpy(np.stack(mus)).cuda(), lam, exchange=exchange)
+    lbar = drv.iterate(30).cpu().numpy().astype(np.float64)
+    ref = O.barycenter(O.kernel_table(g, R, eps, w), O.log_kernel_table(g, R, eps, w),
+                       [m.astype(np.float64) for m in mus], lam, 30, log_domain=True, trace=False)
+    assert potential_err(lbar, ref["lbary"]) < 1e-4
+    assert measure_err(np.exp(lbar), ref["bary"]) < 1e-4

@@ -58,6 +58,14 @@ class OracleOps:
         with np.errstate(divide="ignore"):
             return torch.from_numpy(np.log(x.numpy()))
 
+    def reduce_update(self, sources, lv, ld, lbar, n):
+        acc = np.zeros(lbar.shape)
+        for t in sources:                       # rank order
+            acc = acc + t.numpy()
+        lbar.copy_(torch.from_numpy(acc))
+        if n > 0:
+            lv += lbar[None] - ld
+
     def logmean(self, ld, lam, out):
         acc = np.zeros(out.shape)
         for i, l in enumerate(lam):
@@ -73,6 +81,32 @@ class OracleOps:
 
     def scale_rows(self, x, row0, rows, f):
         x[..., row0:row0 + rows, :] *= f
+
+
+def _bary_fused_worker(rank, world, port, q):
+    """The fused reduce + update exchange (GatherExchange transport, the P2P driver's sequence)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = O.Grid(12, 10, 8)
+        T = O.kernel_table(g, 2, 0.05, (1, 3, 1))
+        L = O.log_kernel_table(g, 2, 0.05, (1, 3, 1))
+        rng = np.random.default_rng(0)
+        mus = [rng.random(g.shape) ** 3 + 1e-3 for _ in range(3)]
+        mus = [m / m.sum() for m in mus]
+        lam = np.array([0.2, 0.5, 0.3])
+        lo, hi = partition(3, world, rank)
+        local = torch.from_numpy(np.stack(mus[lo:hi])) if hi > lo else torch.zeros((0,) + g.shape, dtype=torch.float64)
+        drv = ShardedBarycenter(OracleOps(T, L, True), local, lam[lo:hi], exchange="gather")
+        lbar = drv.iterate(12).numpy().copy()
+        ref = O.barycenter(T, L, mus, lam, 12, log_domain=True, trace=False)["lbary"]
+        errs = [None] * world
+        dist.all_gather_object(errs, float(np.max(np.abs(lbar - ref))))
+        if rank == 0:
+            q.put(max(errs))
+    finally:
+        dist.destroy_process_group()
 
 
 def _bary_worker(rank, world, port, q):
@@ -183,3 +217,10 @@ def _empty_rank_worker(rank, world, port, q):
 
 def test_sharded_barycenter_rank_without_inputs_gloo():
     assert _run(_empty_rank_worker, world=3) < 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_barycenter_fused_exchange_gloo(world):
+    """The fused exchange sequence (slot per parity, gather of every rank's partial, one reduce + update
+    per iteration), ranks 2 and 4 (4 > 3 inputs: one rank owns none)."""
+    assert _run(_bary_fused_worker, world=world) < 1e-10
