@@ -193,7 +193,13 @@ conv_lse_kernel(const float* __restrict__ in, const float* __restrict__ Lq, int 
     if (epi.err_partial != nullptr) {
         float t = block_sum<C::NT>(err, sRed);
         if (threadIdx.x == 0)
-            epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
+        {   // 4 slots per (field, quad, tile): the layout K3's split combine fills one per orientation
+            float* o = epi.err_partial + (((int64_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+            o[0] = t;
+            o[1] = 0.f;
+            o[2] = 0.f;
+            o[3] = 0.f;
+        }
     }
 }
 
@@ -207,7 +213,7 @@ static cudaError_t launch_lse_r(const se2_kernel_s* k, const float* in, int batc
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
     int tiles_y = (k->ny + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, (k->nt + 3) / 4, batch);
-    if (bpf) *bpf = (int)(grid.x * grid.y);
+    if (bpf) *bpf = (int)(grid.x * grid.y) * 4;
     conv_lse_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, epi.table ? epi.table : k->Lq, k->nx, k->ny, k->nt, tiles_x, epi);
     count_launch();
     return cudaGetLastError();
@@ -217,7 +223,7 @@ int conv_blocks_per_field_lse(const se2_kernel_s* k) {
     using C = LseCfg<1>;
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
     int tiles_y = (k->ny + C::TY - 1) / C::TY;
-    return tiles_x * tiles_y * ((k->nt + 3) / 4);
+    return tiles_x * tiles_y * ((k->nt + 3) / 4) * 4;   // 4 error-partial slots per (tile, quad)
 }
 
 cudaError_t launch_conv_lse(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,

@@ -750,8 +750,13 @@ conv_lse_fast_kernel(const float* __restrict__ in, const float* __restrict__ Eq,
     }
     if (ngroups == 1 && epi.err_partial != nullptr) {
         float t = block_sum<C::NT>(err, sRed);
-        if (threadIdx.x == 0)
-            epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
+        if (threadIdx.x == 0) {   // error partials: 4 slots per (field, quad, tile), the split combine fills one per q
+            float* o = epi.err_partial + (((int64_t)b * gridDim.y + qd) * gridDim.x + tile) * 4;
+            o[0] = t;
+            o[1] = 0.f;
+            o[2] = 0.f;
+            o[3] = 0.f;
+        }
     }
 }
 
@@ -789,24 +794,25 @@ __device__ __noinline__ float exact_lse_point_warp(const float* __restrict__ vin
 // Combine the theta_i-group partials of a split launch: ly = LSE_g ly_g, then the fused epilogue.
 // One CTA per (tile, quad, field) as in the main kernel (so the error partials keep the unsplit
 // layout), but kCombT threads, each with a few outputs (x fastest: coalesced partial reads).
-constexpr int kCombT = 512;
+constexpr int kCombT = 256;
 template <int R>
 __global__ void __launch_bounds__(kCombT)
 lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x,
                          Epilogue epi, const float* __restrict__ in, const float* __restrict__ Lq,
                          int* __restrict__ counters, float hint_bias) {
+    // one CTA per (tile, output orientation, field): 4x the CTAs of the main kernel's (tile, quad) grid
     using C = LseFCfg<R>;
     __shared__ float sRed[kCombT / 32];
-    const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
+    const int tile = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
+    const int qd = to >> 2, q = to & 3;
     const int x0 = (tile % tiles_x) * C::TX, y0 = (tile / tiles_x) * C::TY;
     const int64_t N = (int64_t)nx * ny * nt;
     const int64_t GN = (int64_t)gridDim.z * N;
     const int lane = threadIdx.x & 31;
-    constexpr int NOUT = 4 * C::TY * C::TX;   // outputs of the (tile, quad) block
+    constexpr int NOUT = C::TY * C::TX;   // outputs of the (tile, orientation) block
     float err = 0.f;
     for (int o = threadIdx.x; o < NOUT; o += kCombT) {   // same trip count for every lane
-        const int q = o / (C::TY * C::TX), rem = o - q * (C::TY * C::TX);
-        const int to = 4 * qd + q, gy = y0 + rem / C::TX, gx = x0 + rem % C::TX;
+        const int gy = y0 + o / C::TX, gx = x0 + o % C::TX;
         const bool ok = to < nt && gy < ny && gx < nx;
         const int64_t idx = ok ? (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx : 0;
         float ly = -INFINITY;
@@ -831,10 +837,9 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
         while (mask) {   // warp-cooperative exact recomputation of each failed output
             const int src = __ffs(mask) - 1;
             mask &= mask - 1;
-            const int tt = __shfl_sync(0xffffffffu, to, src);
             const int yy = __shfl_sync(0xffffffffu, gy, src);
             const int xx = __shfl_sync(0xffffffffu, gx, src);
-            const float v = exact_lse_point_warp(in + (int64_t)b * N, Lq, nx, ny, nt, R, tt, yy, xx, lane);
+            const float v = exact_lse_point_warp(in + (int64_t)b * N, Lq, nx, ny, nt, R, to, yy, xx, lane);
             if (lane == src) {
                 ly = v;
                 if (counters != nullptr) atomicAdd(&counters[4], 1);
@@ -844,8 +849,10 @@ lse_split_combine_kernel(const float* __restrict__ part, int ngroups, int nx, in
     }
     if (epi.err_partial != nullptr) {
         float t = block_sum<kCombT>(err, sRed);
-        if (threadIdx.x == 0)
-            epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
+        if (threadIdx.x == 0) {
+            const int ntile = gridDim.x, nquad = (gridDim.y + 3) / 4;
+            epi.err_partial[(((int64_t)b * nquad + qd) * ntile + tile) * 4 + q] = t;
+        }
     }
 }
 
@@ -897,14 +904,14 @@ static cudaError_t launch_lsef_r(const se2_kernel_s* k, const float* in, int bat
         if ((double)(((int64_t)base_ctas * g + slots - 1) / slots) / g <= 1.13 * best) groups = g;
     static const int force_groups = getenv("SE2_K3_GROUPS") ? atoi(getenv("SE2_K3_GROUPS")) : 0;   // tuning
     if (force_groups > 0) groups = force_groups < gmax ? force_groups : gmax;
-    if (bpf) *bpf = ntile * nquad;
+    if (bpf) *bpf = ntile * nquad * 4;
     dim3 grid(ntile, nquad * groups, batch);
     conv_lse_fast_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->Eq, k->Lq, k->LqRow, k->Lth, k->LseS, stats, k->nx, k->ny,
                                                           k->nt, tiles_x, tiles_y, force_exact, epi, counters,
                                                           groups, split_scratch);
     count_launch();
     if (groups > 1) {
-        dim3 g2(ntile, nquad, batch);
+        dim3 g2(ntile, nquad * 4, batch);   // one CTA per (tile, output orientation); slots of padding
         lse_split_combine_kernel<R><<<g2, kCombT, 0, s>>>(split_scratch, groups, k->nx, k->ny, k->nt, tiles_x, epi, in,
                                                          k->Lq, counters, (force_exact & 4) ? kDebugHintBias : 0.f);
         count_launch();
@@ -921,7 +928,7 @@ size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch) {
 int conv_blocks_per_field_lse_fast(const se2_kernel_s* k) {
     const int tiles_x = (k->nx + kLseTileX - 1) / kLseTileX;
     const int tiles_y = (k->ny + kLseTileY - 1) / kLseTileY;
-    return tiles_x * tiles_y * ((k->nt + 3) / 4);
+    return tiles_x * tiles_y * ((k->nt + 3) / 4) * 4;   // 4 error-partial slots per (tile, quad)
 }
 
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
