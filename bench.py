@@ -327,8 +327,13 @@ def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
     if ws > 1:
         try:
             drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="p2p")
-            exchange = "p2p"
         except Exception:
+            drv = None
+        ok = torch.tensor([1 if drv is not None else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank takes the same path
+        if int(ok.item()) == 1:
+            exchange = "p2p"
+        else:
             drv = None
     if drv is None:
         drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="nccl")
