@@ -495,7 +495,7 @@ def run_gpu(args):
                 out["next_rows"] = next_rows(local)
             except Exception as e:  # measurement extra: never fail the headline line
                 out["next_rows"] = {"error": str(e)[:300]}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and ws == 1:   # the oracle baseline: rank 0 at N = 1 only
             v, desc, threads, _ = cpu_oracle_sample(cfg)
             out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc}
         print(json.dumps(out), flush=True)
