@@ -215,6 +215,24 @@ SE2_API se2_status se2_bary_logmean(int32_t n, int64_t N, const float* ld, const
 SE2_API se2_status se2_bary_update(int32_t n, int64_t N, float* lv, const float* ld, const float* lbar,
                            se2_stream stream);
 
+/* Slab decomposition with peer-memory halos (a rank's grid rows [r0, r1) plus R halo rows each side):
+ * the conv's epilogue stores the output rows [own_lo, own_hi) of this slab only, and ALSO stores
+ * rows [own_lo, own_lo + halo) into the upper neighbour's array `up` at row (row + up_shift) and rows
+ * [own_hi - halo, own_hi) into the lower neighbour's array `dn` at row (row - dn_shift) (plane strides
+ * ny_up / ny_dn rows of nx); up / dn may be null (global edges).  Rows outside [own_lo, own_hi) are
+ * not stored and do not enter the marginal error.  The caller orders the peers' writes with a
+ * cross-rank barrier before the next conv reads its halos. */
+typedef struct {
+    int32_t own_lo, own_hi, halo;
+    float* up;
+    int32_t up_shift, ny_up;
+    float* dn;
+    int32_t dn_shift, ny_dn;
+} se2_slab;
+SE2_API se2_status se2_conv_update_slab(se2_kernel k, const float* in, const float* target, float* out, int32_t batch,
+                                        int32_t op, const se2_prox* prox, uint32_t flags, const se2_slab* slab,
+                                        se2_stream stream);
+
 /* Fused cross-rank log-mean reduction + v-update of the sharded barycenter (App. A with the inputs
  * spread over ranks; the allreduce and the update in ONE kernel reading the peers' buffers directly):
  *   lbar[x] = sum_{r < nranks} partials[r][x]      (rank order -> bit-identical on every rank)

@@ -40,7 +40,7 @@ EXPORTED = [
     "se2_transport_cost", "se2_lse_row_stats",
     "se2_cake_build", "se2_cake_get", "se2_cake_destroy", "se2_lift_image", "se2_split_signed", "se2_project",
     "se2_project_signed", "se2_lift_field", "se2_reconstruct_field", "se2_exp", "se2_log",
-    "se2_bary_reduce_update",
+    "se2_bary_reduce_update", "se2_conv_update_slab",
 ]
 
 
@@ -68,6 +68,12 @@ class se2_prox(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("tau", ctypes.c_double), ("cx", ctypes.c_double),
                 ("cy", ctypes.c_double), ("hx", ctypes.c_double), ("hy", ctypes.c_double),
                 ("m", ctypes.c_double)]
+
+
+class se2_slab(ctypes.Structure):
+    _fields_ = [("own_lo", ctypes.c_int32), ("own_hi", ctypes.c_int32), ("halo", ctypes.c_int32),
+                ("up", ctypes.c_void_p), ("up_shift", ctypes.c_int32), ("ny_up", ctypes.c_int32),
+                ("dn", ctypes.c_void_p), ("dn_shift", ctypes.c_int32), ("ny_dn", ctypes.c_int32)]
 
 
 class se2_opts(ctypes.Structure):
@@ -121,6 +127,7 @@ def load(path: str = LIB_PATH):
         "se2_exp": [P, P, i64, P],
         "se2_log": [P, P, i64, P],
         "se2_bary_reduce_update": [i32, P, i32, i64, P, P, P, P],
+        "se2_conv_update_slab": [P, P, P, P, i32, i32, ctypes.POINTER(se2_prox), u32, ctypes.POINTER(se2_slab), P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

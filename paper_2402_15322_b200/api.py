@@ -232,16 +232,23 @@ def se2_transport_cost(k: Kernel, a: torch.Tensor, b: torch.Tensor, log_domain: 
 
 
 def se2_conv_update(k: Kernel, x: torch.Tensor, target: Optional[torch.Tensor], out: torch.Tensor, op: int,
-                    log_domain: bool, prox: Optional[L.se2_prox] = None) -> torch.Tensor:
-    """Fused conv + scaling update (step-level entry point used by the multi-GPU driver)."""
+                    log_domain: bool, prox: Optional[L.se2_prox] = None,
+                    slab: Optional[L.se2_slab] = None) -> torch.Tensor:
+    """Fused conv + scaling update (step-level entry point used by the multi-GPU driver).  slab: the
+    rows this rank owns and the neighbours' peer-mapped arrays that receive its boundary rows
+    (se2_conv_update_slab)."""
     _check_field(x, k, "x")
     batch = x.numel() // k.N
     _check_field(out, k, "out", batch)
     if target is not None:
         _check_field(target, k, "target", batch)
-    check(L.load().se2_conv_update(k.handle, _ptr(x), _ptr(target), _ptr(out), batch, int(op),
-                                   ctypes.byref(prox) if prox is not None else None, _flags(log_domain),
-                                   _stream(x.device)))
+    pr = ctypes.byref(prox) if prox is not None else None
+    if slab is None:
+        check(L.load().se2_conv_update(k.handle, _ptr(x), _ptr(target), _ptr(out), batch, int(op), pr,
+                                       _flags(log_domain), _stream(x.device)))
+    else:
+        check(L.load().se2_conv_update_slab(k.handle, _ptr(x), _ptr(target), _ptr(out), batch, int(op), pr,
+                                            _flags(log_domain), ctypes.byref(slab), _stream(x.device)))
     return out
 
 

@@ -382,6 +382,48 @@ se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, f
     return run_conv(k, in, batch, flags, epi, (cudaStream_t)stream, nullptr);
 }
 
+se2_status se2_conv_update_slab(se2_kernel k, const float* in, const float* target, float* out, int32_t batch,
+                                int32_t op, const se2_prox* prox, uint32_t flags, const se2_slab* slab,
+                                se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(slab != nullptr, "slab required");
+    SE2_CHECK_ARG(slab->own_lo >= 0 && slab->own_hi > slab->own_lo && slab->own_hi <= k->ny && slab->halo >= 0 &&
+                      slab->halo <= slab->own_hi - slab->own_lo,
+                  "bad slab rows");
+    SE2_CHECK_ARG(!slab->up || (slab->ny_up >= 1 && slab->up_shift + slab->own_lo + slab->halo <= slab->ny_up &&
+                                slab->up_shift + slab->own_lo >= 0),
+                  "bad upper halo geometry");
+    SE2_CHECK_ARG(!slab->dn || (slab->ny_dn >= 1 && slab->own_hi - slab->halo - slab->dn_shift >= 0 &&
+                                slab->own_hi - slab->dn_shift <= slab->ny_dn),
+                  "bad lower halo geometry");
+    SE2_CHECK_ARG(in && out && in != out, "in/out must be distinct non-null device pointers");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    SE2_CHECK_ARG(op == SE2_EPI_DIVIDE || op == SE2_EPI_MULTIPLY || op == SE2_EPI_PROX, "bad epilogue op");
+    SE2_CHECK_ARG(op == SE2_EPI_PROX || target != nullptr, "target required");
+    SE2_CHECK_ARG(op != SE2_EPI_PROX || (prox != nullptr && prox->tau >= 0 &&
+                                         (prox->kind == SE2_PROX_ENTROPY_POTENTIAL ||
+                                          (prox->kind == SE2_PROX_POROUS && prox->m > 1.0))),
+                  "JKO prox required (entropy+potential, or porous with m > 1)");
+    DeviceGuard g(k->device);
+    Epilogue epi;
+    epi.op = op;
+    epi.target = target;
+    epi.out = out;
+    if (op == SE2_EPI_PROX) fill_prox(epi, k, prox);
+    epi.slab_lo = slab->own_lo;
+    epi.slab_hi = slab->own_hi;
+    epi.slab_halo = slab->halo;
+    epi.ny_self = k->ny;
+    epi.nx_self = k->nx;
+    epi.halo_up = slab->up;
+    epi.up_shift = slab->up_shift;
+    epi.ny_up = slab->ny_up;
+    epi.halo_dn = slab->dn;
+    epi.dn_shift = slab->dn_shift;
+    epi.ny_dn = slab->ny_dn;
+    return run_conv(k, in, batch, flags, epi, (cudaStream_t)stream, nullptr);
+}
+
 // ---- Sinkhorn / JKO inner solve -------------------------------------------------------------------
 static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* nu, float* a, float* b, int batch,
                                 const se2_prox* prox, const se2_opts* opts, double* err_trace_host,

@@ -123,6 +123,7 @@ __device__ __forceinline__ float block_sum(float v, float* red /* >= NT/32 float
 template <bool LOG>
 __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, int ix, int iy, float y) {
     float err = 0.f;
+    if (e.slab_hi > 0 && (iy < e.slab_lo || iy >= e.slab_hi)) return 0.f;   // a neighbour's row: not ours
     if (e.op == EPI_DOT) return LOG ? expf(e.err_a[idx] + y) : e.err_a[idx] * y;
     if (e.err_a != nullptr) {
         float a_old = e.err_a[idx];
@@ -176,6 +177,13 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
         default: return err;  // EPI_ERRONLY
     }
     e.out[idx] = o;
+    if (e.slab_hi > 0) {   // boundary rows into the neighbours' halo rows (peer memory)
+        const int64_t plane = idx / ((int64_t)e.ny_self * e.nx_self);
+        if (e.halo_up != nullptr && iy < e.slab_lo + e.slab_halo)
+            e.halo_up[(plane * e.ny_up + iy + e.up_shift) * e.nx_self + ix] = o;
+        if (e.halo_dn != nullptr && iy >= e.slab_hi - e.slab_halo)
+            e.halo_dn[(plane * e.ny_dn + iy - e.dn_shift) * e.nx_self + ix] = o;
+    }
     return err;
 }
 

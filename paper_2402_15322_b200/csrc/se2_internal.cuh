@@ -82,6 +82,13 @@ struct Epilogue {
     float prox_p = 0.f, prox_q = 0.f;
     float prox_c = 0.f, prox_m1 = 0.f; // porous: c = tau m / (eps (m-1)), m1 = m - 1
     float cx = 0.f, cy = 0.f, hx = 0.f, hy = 0.f;
+    // slab decomposition with peer-memory halos (se2_conv_update_slab): own rows [slab_lo, slab_hi) of a
+    // plane of ny_self x nx_self; slab_hi == 0: off
+    int slab_lo = 0, slab_hi = 0, slab_halo = 0, ny_self = 0, nx_self = 0;
+    float* halo_up = nullptr;
+    int up_shift = 0, ny_up = 0;
+    float* halo_dn = nullptr;
+    int dn_shift = 0, ny_dn = 0;
 };
 
 struct Timing {

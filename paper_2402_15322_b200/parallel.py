@@ -41,17 +41,18 @@ class CudaOps:
         self.k = kernel
         self.log = log_domain
 
-    def divide(self, x, target, out):       # out = target / K x   (log: target - LSE x)
+    # slab: optional se2_slab (the owned rows + the neighbours' peer arrays receiving the boundary rows)
+    def divide(self, x, target, out, slab=None):     # out = target / K x   (log: target - LSE x)
         from ._lib import SE2_EPI_DIVIDE
-        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_DIVIDE, self.log)
+        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_DIVIDE, self.log, slab=slab)
 
-    def multiply(self, x, target, out):     # out = target * K x   (log: target + LSE x)
+    def multiply(self, x, target, out, slab=None):   # out = target * K x   (log: target + LSE x)
         from ._lib import SE2_EPI_MULTIPLY
-        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_MULTIPLY, self.log)
+        return self.api.se2_conv_update(self.k, x, target, out, SE2_EPI_MULTIPLY, self.log, slab=slab)
 
-    def prox(self, x, out, prox):           # out = prox(K x) / K x   (JKO, R10)
+    def prox(self, x, out, prox, slab=None):         # out = prox(K x) / K x   (JKO, R10)
         from ._lib import SE2_EPI_PROX
-        return self.api.se2_conv_update(self.k, x, None, out, SE2_EPI_PROX, self.log, prox=prox)
+        return self.api.se2_conv_update(self.k, x, None, out, SE2_EPI_PROX, self.log, prox=prox, slab=slab)
 
     def log_of(self, x):                    # elementwise log (log 0 = -inf), a new tensor
         from .lifting import se2_log
@@ -199,7 +200,10 @@ class SlabJKO:
     the potential's centre row by the slab offset.
     """
 
-    def __init__(self, ops, mu_local_owned: torch.Tensor, R: int, prox, group=None):
+    def __init__(self, ops, mu_local_owned: torch.Tensor, R: int, prox, group=None, exchange: str = "nccl"):
+        """exchange: "nccl" (halo rows by send/recv before each conv) or "p2p" (each conv's epilogue
+        writes its boundary rows straight into the neighbours' halo rows in symmetric memory, one
+        device barrier after each conv; se2_conv_update_slab)."""
         self.ops = ops
         self.R = R
         self.prox = prox
@@ -209,8 +213,46 @@ class SlabJKO:
         nt, rows, nx = mu_local_owned.shape
         self.rows = rows
         self.mu = self._ext(mu_local_owned)
-        self.a = torch.zeros_like(self.mu)
-        self.b = torch.zeros_like(self.mu)
+        self.p2p = exchange == "p2p"
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        if self.p2p:
+            self._setup_p2p()
+        else:
+            self.a = torch.zeros_like(self.mu)
+            self.b = torch.zeros_like(self.mu)
+
+    def _setup_p2p(self):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import _lib as L
+        group = self.group if self.group is not None else dist.group.WORLD
+        rows_all = [None] * self.world
+        dist.all_gather_object(rows_all, self.rows, group=group)
+        nt, nyl, nx = self.mu.shape
+        R = self.R
+        shape = (nt, max(rows_all) + 2 * R, nx)   # symmetric allocations have one size; each rank uses a prefix
+        n_local = nt * nyl * nx
+        self._sym, self._hdl, arrays, ptrs = [], [], [], []
+        for _ in range(2):   # a, b
+            buf = symm_mem.empty(shape, dtype=torch.float32, device=self.mu.device)
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, group)
+            off = buf.data_ptr() - int(hdl.buffer_ptrs[hdl.rank])
+            self._sym.append(buf)
+            self._hdl.append(hdl)
+            arrays.append(buf.view(-1)[:n_local].view(nt, nyl, nx))
+            ptrs.append([int(p) + off for p in hdl.buffer_ptrs])
+        self.a, self.b = arrays
+        self._slabs = []
+        for k in range(2):
+            sl = L.se2_slab(R, R + self.rows, R, None, 0, 0, None, 0, 0)
+            if self.rank > 0:                       # my first R owned rows -> the upper rank's bottom halo
+                ru = rows_all[self.rank - 1]
+                sl.up, sl.up_shift, sl.ny_up = ptrs[k][self.rank - 1], ru, ru + 2 * R
+            if self.rank < self.world - 1:          # my last R owned rows -> the lower rank's top halo
+                rd = rows_all[self.rank + 1]
+                sl.dn, sl.dn_shift, sl.ny_dn = ptrs[k][self.rank + 1], self.rows, rd + 2 * R
+            self._slabs.append(sl)
 
     def _ext(self, owned):
         nt, rows, nx = owned.shape
@@ -250,7 +292,21 @@ class SlabJKO:
     def step(self, iters: int):
         """One JKO step: b <- 1; iters x (a = mu / K b ; b = prox(K a) / K a); s = b K a; normalise."""
         self.b.fill_(1.0)
-        for _ in range(iters):
+        if self.p2p:
+            # halo rows of b start as the neighbours' b (= 1) or the zero padding at the global edges; after
+            # that the neighbours' epilogues fill them (ordered by the device barrier after each conv: a
+            # rank's next conv, which reads its halos, runs after every rank's previous conv finished)
+            R = self.R
+            if R > 0 and self.rank == 0:
+                self.b[:, :R].zero_()
+            if R > 0 and self.rank == self.world - 1:
+                self.b[:, R + self.rows:].zero_()
+            for _ in range(iters):
+                self.ops.divide(self.b, self.mu, self.a, slab=self._slabs[0])
+                self._hdl[0].barrier(channel=0)
+                self.ops.prox(self.a, self.b, self.prox, slab=self._slabs[1])
+                self._hdl[1].barrier(channel=0)
+        for _ in range(0 if self.p2p else iters):
             self.halo_exchange(self.b)
             self.ops.divide(self.b, self.mu, self.a)
             self.halo_exchange(self.a)
