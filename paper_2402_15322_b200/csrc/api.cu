@@ -449,12 +449,12 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         if (st != SE2_OK) return st;
     }
     // K9: the whole loop in one cluster launch when the grid fits in shared memory (c0-sized)
-    const int k9c = (LOG && !jko && batch == 1 && s_out == nullptr && iters > 0 &&
+    const int k9c = (LOG && !jko && batch <= 64 && s_out == nullptr && iters > 0 &&
                      !(opts->flags & (SE2_NO_PERSISTENT | SE2_LSE_EXACT | SE2_LSE_K3EXACT | SE2_LSE_NOTILT)))
                         ? k9_cluster_size(k) : 0;
     if (k9c > 0) {
         if (trace) {
-            st = ensure(x->partial, (size_t)std::max(iters, 1) * k9c * sizeof(float), x);
+            st = ensure(x->partial, (size_t)std::max(iters, 1) * batch * k9c * sizeof(float), x);
             if (st != SE2_OK) return st;
         }
         float* kpart = trace ? reinterpret_cast<float*>(x->partial.ptr) : nullptr;
@@ -474,15 +474,15 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
             t.all_launches++;
             SE2_CUDA_TRY(cudaEventRecord(e0, s));
         }
-        cudaError_t ce = launch_sinkhorn_small(k, mu, nu, a, b, iters, (opts->flags & SE2_WARM_START) != 0, kpart, ktr,
-                                               k9c, s);
+        cudaError_t ce = launch_sinkhorn_small(k, mu, nu, a, b, batch, iters, (opts->flags & SE2_WARM_START) != 0, kpart,
+                                               ktr, k9c, s);
         if (ce != cudaSuccess) {
             set_error(std::string("K9 launch: ") + cudaGetErrorString(ce));
             return SE2_ECUDA;
         }
         if (e1) SE2_CUDA_TRY(cudaEventRecord(e1, s));
         if (trace && iters > 0)
-            SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, ktr, sizeof(double) * iters, cudaMemcpyDeviceToHost, s));
+            SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, ktr, sizeof(double) * iters * batch, cudaMemcpyDeviceToHost, s));
         return SE2_OK;
     }
     float* partial = reinterpret_cast<float*>(x->partial.ptr);

@@ -142,7 +142,8 @@ int conv_blocks_per_field_lse(const se2_kernel_s* k);
 // K9 (sinkhorn_small.cu): whole log-domain Sinkhorn of a small grid in one cluster launch
 int k9_cluster_size(const se2_kernel_s* k);   // 0: not applicable
 cudaError_t launch_sinkhorn_small(const se2_kernel_s* k, const float* mu, const float* nu, float* a, float* b,
-                                  int iters, bool warm, float* err_partial, double* trace, int C, cudaStream_t s);
+                                  int batch, int iters, bool warm, float* err_partial, double* trace, int C,
+                                  cudaStream_t s);
 cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
                                  cudaStream_t s, int* bpf, float* stats, int force_exact, int* counters,
                                  float* split_scratch, size_t split_floats);

@@ -43,7 +43,7 @@ struct K9Args {
     const float* Lq;      // [nt/4][nt][S][S][4] L log2(e)
     float* err_partial;   // [iters][C] (trace) or null
     double* trace;        // [iters] or null
-    int nx, ny, nt, iters, warm, C, split, per_cta;
+    int nx, ny, nt, iters, warm, C, split, per_cta, batch;
 };
 
 // exact log-sum-exp (log2 units) of one output over this lane's theta_i subset, combined over the
@@ -102,6 +102,12 @@ __global__ void __launch_bounds__(kK9Threads) sinkhorn_small_kernel(K9Args p) {
     constexpr int S = 2 * R + 1;
     extern __shared__ __align__(16) float smem[];
     const int N = p.nx * p.ny * p.nt;
+    // one cluster per problem of the batch (clusters are consecutive C-block groups along x)
+    const int prob = blockIdx.x / p.C;
+    p.mu += (int64_t)prob * N;
+    p.nu += (int64_t)prob * N;
+    p.a += (int64_t)prob * N;
+    p.b += (int64_t)prob * N;
     const int plane = p.nx * p.ny;
     const int pw = p.nx + 2 * R, pp = pw * (p.ny + 2 * R);   // padded plane (-inf border)
     const int NP = pp * p.nt;
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(kK9Threads) sinkhorn_small_kernel(K9Args p) {
         }
         if (err_slot >= 0) {
             const float t = block_sum<kK9Threads>(err, red);
-            if (threadIdx.x == 0) p.err_partial[(int64_t)err_slot * p.C + rank] = t;
+            if (threadIdx.x == 0) p.err_partial[((int64_t)err_slot * p.batch + prob) * p.C + rank] = t;
         }
         cluster_sync_all();
     };
@@ -190,8 +196,8 @@ __global__ void __launch_bounds__(kK9Threads) sinkhorn_small_kernel(K9Args p) {
         __threadfence();
         for (int l = threadIdx.x; l < p.iters; l += kK9Threads) {
             double acc = 0.0;
-            for (int r = 0; r < p.C; ++r) acc += (double)p.err_partial[(int64_t)l * p.C + r];
-            p.trace[l] = acc;
+            for (int r = 0; r < p.C; ++r) acc += (double)p.err_partial[((int64_t)l * p.batch + prob) * p.C + r];
+            p.trace[(int64_t)l * p.batch + prob] = acc;
         }
     }
 }
@@ -208,7 +214,8 @@ size_t k9_smem_bytes(const se2_kernel_s* k, int C) {
 
 template <int R>
 static cudaError_t launch_k9_r(const se2_kernel_s* k, const float* mu, const float* nu, float* a, float* b,
-                               int iters, bool warm, float* err_partial, double* trace, int C, cudaStream_t s) {
+                               int batch, int iters, bool warm, float* err_partial, double* trace, int C,
+                               cudaStream_t s) {
     const size_t smem = k9_smem_bytes(k, C);
     cudaError_t e = cudaFuncSetAttribute(sinkhorn_small_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -219,14 +226,14 @@ static cudaError_t launch_k9_r(const se2_kernel_s* k, const float* mu, const flo
     K9Args p;
     p.mu = mu; p.nu = nu; p.a = a; p.b = b; p.Lq = k->Lq;
     p.err_partial = err_partial; p.trace = trace;
-    p.nx = k->nx; p.ny = k->ny; p.nt = k->nt; p.iters = iters; p.warm = warm ? 1 : 0; p.C = C;
+    p.nx = k->nx; p.ny = k->ny; p.nt = k->nt; p.iters = iters; p.warm = warm ? 1 : 0; p.C = C; p.batch = batch;
     p.per_cta = (int)(k->N() / C);
     // lanes per output: enough to occupy the CTA, a power of two <= 8 that divides into a warp
     int split = 1;
     while (split * 2 <= 8 && split * 2 <= k->nt && p.per_cta * split * 2 <= kK9Threads) split *= 2;
     p.split = split;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(C, 1, 1);
+    cfg.gridDim = dim3(C * batch, 1, 1);
     cfg.blockDim = dim3(kK9Threads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -263,10 +270,11 @@ int k9_cluster_size(const se2_kernel_s* k) {
 }
 
 cudaError_t launch_sinkhorn_small(const se2_kernel_s* k, const float* mu, const float* nu, float* a, float* b,
-                                  int iters, bool warm, float* err_partial, double* trace, int C, cudaStream_t s) {
+                                  int batch, int iters, bool warm, float* err_partial, double* trace, int C,
+                                  cudaStream_t s) {
     switch (k->R) {
 #define SE2_CASE(r) \
-    case r: return launch_k9_r<r>(k, mu, nu, a, b, iters, warm, err_partial, trace, C, s);
+    case r: return launch_k9_r<r>(k, mu, nu, a, b, batch, iters, warm, err_partial, trace, C, s);
         SE2_CASE(0) SE2_CASE(1) SE2_CASE(2) SE2_CASE(3) SE2_CASE(4) SE2_CASE(5) SE2_CASE(6) SE2_CASE(7)
         SE2_CASE(8) SE2_CASE(9) SE2_CASE(10) SE2_CASE(11) SE2_CASE(12) SE2_CASE(13) SE2_CASE(14) SE2_CASE(15)
 #undef SE2_CASE

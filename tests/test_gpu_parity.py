@@ -279,3 +279,36 @@ def test_hint_fallback_paths(no_split, cuda_device):
     assert st["hint_redos"] > 0
     _cmp_pot("log bary", _host(bary).reshape(nsolve, -1), gold["lbary"].reshape(nsolve, -1))
     _cmp_meas("bary", np.exp(_host(bary)).reshape(nsolve, -1), gold["bary_lin"].reshape(nsolve, -1))
+
+
+def test_sinkhorn_k9_batched(cuda_device):
+    """K9 with a batch of independent problems (one cluster each) equals the oracle per problem."""
+    import oracle as O
+    from paper_2402_15322_b200 import Kernel, se2_launch_count, se2_sinkhorn
+    nx, ny, nt, R, B = 12, 10, 8, 2, 3
+    g = O.Grid(nx, ny, nt)
+    eps, w = 0.05, (1.0, 3.0, 1.0)
+    rng = np.random.default_rng(77)
+    mus = rng.random((B,) + g.shape) ** 3 + 1e-6
+    nus = rng.random((B,) + g.shape) ** 3 + 1e-6
+    mus /= mus.sum(axis=(1, 2, 3), keepdims=True)
+    nus /= nus.sum(axis=(1, 2, 3), keepdims=True)
+    L = O.log_kernel_table(g, R, eps, w)
+    k = Kernel(nx, ny, nt, eps, w, R, max_batch=B, device=0)
+    a = torch.empty((B,) + g.shape, device="cuda")
+    b = torch.empty_like(a)
+    n0 = se2_launch_count()
+    tr = se2_sinkhorn(k, _dev(mus), _dev(nus), a, b, 30, True, trace=True)
+    assert se2_launch_count() - n0 <= 3
+    ga, gb = _host(a), _host(b)
+    for i in range(B):
+        lmu, lnu = np.log(mus[i]), np.log(nus[i])
+        beta = np.zeros(g.shape)
+        errs = []
+        for _ in range(30):
+            alpha = lmu - O.lse_conv(L, beta)
+            beta = lnu - O.lse_conv(L, alpha)
+            errs.append(np.abs(np.exp(alpha + O.lse_conv(L, beta)) - mus[i]).sum())
+        _cmp_pot("alpha", ga[i], alpha)
+        _cmp_pot("beta", gb[i], beta)
+        assert trace_err(tr[:, i], np.array(errs)) <= TOL_TRACE
