@@ -12,6 +12,8 @@
 // cluster barrier (release/acquire) per half-iteration orders the exchange: a half-iteration reads one
 // potential and writes the other, and the barrier before it guarantees that no CTA still reads the
 // buffer being written.  No HBM traffic inside the loop except the per-iteration error partials.
+#include <stdlib.h>
+
 #include "conv_common.cuh"
 
 namespace se2 {
@@ -262,7 +264,8 @@ int k9_cluster_size(const se2_kernel_s* k) {
         cudaGetLastError();
     }
     if (k->R > 15) return 0;
-    for (int C = max_c; C >= 2; C /= 2) {
+    static const int cap = getenv("SE2_K9_CLUSTER") ? atoi(getenv("SE2_K9_CLUSTER")) : 16;   // tuning
+    for (int C = max_c < cap ? max_c : cap; C >= 2; C /= 2) {
         if (k->N() % C != 0) continue;
         if (k9_smem_bytes(k, C) <= (size_t)200 * 1024) return C;
     }
