@@ -59,7 +59,7 @@ typedef enum {
 #define SE2_LOG_DOMAIN 0x1u   /* state/fields are natural logs; conv is log-sum-exp (R7)      */
 #define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1        */
 #define SE2_TRACE_ERR 0x4u    /* compute the marginal error every iteration (fused)           */
-#define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4)   */
+#define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4; also used for ntheta > 128) */
 #define SE2_LSE_NOTILT 0x10u  /* diagnostics: K3 without its gradient-tilted FFMA path           */
 #define SE2_LSE_K3EXACT 0x20u /* diagnostics: K3 with every active channel on its exact path     */
 #define SE2_NO_GRAPH 0x40u    /* solvers: launch directly instead of replaying a CUDA graph       */

@@ -107,7 +107,7 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
     cudaError_t e;
     if (!log_domain)
         e = launch_conv_linear(k, in, batch, epi, s, bpf);
-    else if (flags & SE2_LSE_EXACT)
+    else if ((flags & SE2_LSE_EXACT) || k->nt > 128)   // K3 holds per-channel state for <= 128 orientations
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
         e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->lstats,

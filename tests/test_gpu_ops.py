@@ -42,6 +42,7 @@ ODD_GRIDS = [
     ("nt2", 17, 13, 2, 0.05, (1.0, 2.0, 1.0), 2),          # half-turn only: one partial quad
     ("r15", 40, 36, 8, 0.003, (1.0, 3.0, 1.0), 15),        # the largest supported support (31 x 31)
     ("nt128", 12, 10, 128, 0.05, (1.0, 3.0, 1.0), 1),      # the largest orientation count of K3
+    ("nt136", 9, 8, 136, 0.05, (1.0, 3.0, 1.0), 1),        # beyond it: the log domain runs on K4
     ("thin", 5, 70, 8, 0.05, (1.0, 2.0, 1.5), 3),
     ("r0", 33, 33, 8, 0.05, (1.0, 3.0, 1.0), 0),           # theta-only convolution
     ("nt1", 40, 24, 1, 0.01, (1.0, 2.0, 1.0), 6),          # plain anisotropic Gaussian
