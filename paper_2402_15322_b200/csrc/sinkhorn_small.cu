@@ -264,6 +264,10 @@ int k9_cluster_size(const se2_kernel_s* k) {
         cudaGetLastError();
     }
     if (k->R > 15) return 0;
+    // K9 evaluates every box tap exactly on <= 16 SMs: it beats the per-conv K3 path (pruning, FFMA
+    // factoring, all SMs) only while the per-conv work is small.  Measured (tools/k9_vs_k3.py, 100
+    // iterations): 0.8 M taps/conv 1.0 vs 3.0 ms, 1.8 M 2.6 vs 3.3 ms, 8.3 M 7.4 vs 3.5 ms.
+    if ((double)k->N() * k->S * k->S * k->nt > 3.0e6) return 0;
     static const int cap = getenv("SE2_K9_CLUSTER") ? atoi(getenv("SE2_K9_CLUSTER")) : 16;   // tuning
     for (int C = max_c < cap ? max_c : cap; C >= 2; C /= 2) {
         if (k->N() % C != 0) continue;

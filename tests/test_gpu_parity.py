@@ -198,8 +198,8 @@ def test_sinkhorn_jko_determinism(cuda_device):
     assert np.array_equal(outs[0][2], outs[1][2])
 
 
-@pytest.mark.parametrize("shape", [(12, 10, 8, 2, False), (9, 7, 4, 1, True), (16, 16, 8, 3, True), (20, 18, 12, 4, False)],
-                         ids=["12x10x8", "9x7x4-warm", "16x16x8-warm", "20x18x12"])
+@pytest.mark.parametrize("shape", [(12, 10, 8, 2, False), (9, 7, 4, 1, True), (16, 16, 8, 3, True), (18, 14, 12, 3, False)],
+                         ids=["12x10x8", "9x7x4-warm", "16x16x8-warm", "18x14x12"])
 def test_sinkhorn_k9_ragged(shape, cuda_device):
     """K9 (one cluster launch) on ragged grids (N not a multiple of 16 -> smaller clusters), with and
     without a warm start, against the fp64 oracle's log-domain Sinkhorn run on the same inputs."""
@@ -312,3 +312,23 @@ def test_sinkhorn_k9_batched(cuda_device):
         _cmp_pot("alpha", ga[i], alpha)
         _cmp_pot("beta", gb[i], beta)
         assert trace_err(tr[:, i], np.array(errs)) <= TOL_TRACE
+
+
+def test_sinkhorn_k9_selection(cuda_device):
+    """K9 is chosen only while the per-conv work is small (it evaluates every tap on <= 16 SMs); a
+    larger grid runs the per-conv K3 path (many launches) -- both give the same iterates."""
+    from paper_2402_15322_b200 import Kernel, se2_launch_count, se2_sinkhorn
+    rng = np.random.default_rng(3)
+    for (nx, ny, nt, R), small in (((16, 16, 8, 3), True), ((40, 40, 8, 4), False)):
+        mu = rng.random((nt, ny, nx)) ** 3 + 1e-6
+        nu = rng.random((nt, ny, nx)) ** 3 + 1e-6
+        mu, nu = _dev(mu / mu.sum()), _dev(nu / nu.sum())
+        k = _kernel(S.Config("x", nx, ny, nt, 0.05, (1.0, 3.0, 1.0), 2 * R + 1, "sinkhorn", 20, 2), 1)
+        a, b = torch.empty_like(mu), torch.empty_like(mu)
+        n0 = se2_launch_count()
+        se2_sinkhorn(k, mu, nu, a, b, 20, True)
+        launches = se2_launch_count() - n0
+        assert (launches <= 3) == small, launches
+        a2, b2 = torch.empty_like(mu), torch.empty_like(mu)
+        se2_sinkhorn(k, mu, nu, a2, b2, 20, True, persistent=False)
+        assert potential_err(_host(a), _host(a2)) < 1e-5 and potential_err(_host(b), _host(b2)) < 1e-5
