@@ -119,7 +119,7 @@ def test_barycenter_parity(case, cuda_device):
     assert trace_err(tr, gold["err"]) <= TOL_TRACE
 
 
-@pytest.mark.parametrize("case", ["c4m", "c4p", "c5m"])
+@pytest.mark.parametrize("case", ["c4m", "c4p", "c5m", "c4q"])
 def test_jko_parity(case, cuda_device):
     from paper_2402_15322_b200 import make_porous_prox, make_prox, se2_jko_step
     pc = S.get_parity_case(case)
