@@ -67,6 +67,8 @@ typedef enum {
 #define SE2_DEBUG_BAD_HINTS 0x100u /* diagnostics: K3 reads its exact-path hints 60 nats too high, so
                                       every hinted output must take the verified fallback (redo) */
 #define SE2_DEBUG_NO_SPLIT 0x200u  /* diagnostics: K3 without the theta_i split (one CTA per tile-quad) */
+#define SE2_LIN_FFMA 0x400u        /* linear domain: the fp32 FFMA conv (K2) instead of the tensor-core
+                                      conv (K10, 3-pass BF16 split) on the grids K10 covers */
 
 typedef struct {
     int32_t nx, ny, ntheta;

@@ -21,6 +21,7 @@ SE2_NO_GRAPH = 0x40
 SE2_NO_PERSISTENT = 0x80
 SE2_DEBUG_BAD_HINTS = 0x100
 SE2_DEBUG_NO_SPLIT = 0x200
+SE2_LIN_FFMA = 0x400
 SE2_EPI_DIVIDE = 1
 SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3

@@ -106,7 +106,8 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
     }
     cudaError_t e;
     if (!log_domain)
-        e = launch_conv_linear(k, in, batch, epi, s, bpf);
+        e = (conv_tc_active(k, flags) && epi.table == nullptr) ? launch_conv_tc(k, in, batch, epi, s, bpf)
+                                                               : launch_conv_linear(k, in, batch, epi, s, bpf);
     else if ((flags & SE2_LSE_EXACT) || k->nt > 128)   // K3 holds per-channel state for <= 128 orientations
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
@@ -277,6 +278,7 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
         }
     }
     e = tabulate(k, 0);
+    if (e == cudaSuccess) e = conv_tc_prepare(k);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         set_error(std::string("tabulate: ") + cudaGetErrorString(e));
@@ -316,6 +318,9 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->Lcq) cudaFree(k->Lcq);
     if (k->lstats) cudaFree(k->lstats);
     if (k->split) cudaFree(k->split);
+    if (k->tc_w) cudaFree(k->tc_w);
+    if (k->tc_x) cudaFree(k->tc_x);
+    se2::conv_tc_release(k);
     if (k->lse_counters) cudaFree(k->lse_counters);
     KernelExtra* x = extra(k);
     if (x) {
@@ -441,7 +446,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     size_t need = (size_t)(LOG ? 4 : 0) * BN * sizeof(float);
     se2_status st = ensure(x->ws, std::max<size_t>(need, 16), x);
     if (st != SE2_OK) return st;
-    const int bpf = conv_blocks_per_field(k, LOG);
+    const int bpf = conv_blocks_per_field(k, LOG, opts->flags);
     if (trace) {
         st = ensure(x->partial, (size_t)batch * bpf * sizeof(float), x);
         if (st != SE2_OK) return st;
@@ -673,7 +678,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     float* hint2 = hints ? lmu_rep + 6 * FN : nullptr;
     st = ensure(x->misc, 4096 + sizeof(float) * F, x);
     if (st != SE2_OK) return st;
-    const int bpf = conv_blocks_per_field(k, LOG);
+    const int bpf = conv_blocks_per_field(k, LOG, opts->flags);
     if (trace) {
         st = ensure(x->partial, (size_t)F * bpf * sizeof(float), x);
         if (st != SE2_OK) return st;
@@ -776,7 +781,7 @@ se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, cons
     cudaStream_t s = (cudaStream_t)stream;
     const bool LOG = (flags & SE2_LOG_DOMAIN) != 0;
     KernelExtra* x = extra(k);
-    const int bpf = conv_blocks_per_field(k, LOG);
+    const int bpf = conv_blocks_per_field(k, LOG, flags);
     se2_status st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
     if (st != SE2_OK) return st;
     st = ensure(x->trace, (size_t)batch * sizeof(double));

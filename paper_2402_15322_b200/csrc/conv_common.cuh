@@ -10,6 +10,8 @@
 namespace se2 {
 
 bool make_field_tmap(CUtensorMap* map, const float* base, int nx, int ny, int planes, int boxw, int boxh);
+bool make_tmap_5d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, const uint64_t* dims,
+                  const uint64_t* strides, const uint32_t* box);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -52,6 +54,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// 5-D tensor tile global -> shared (TMA), destination / barrier as shared-window addresses
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, uint32_t bar, int c0, int c1, int c2, int c3,
+                                            int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 // contiguous bulk copy global -> shared (bytes % 16 == 0), completion counted on `bar`

@@ -238,8 +238,9 @@ cudaError_t launch_conv_lse(const se2_kernel_s* k, const float* in, int batch, c
     }
 }
 
-int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain) {
-    return log_domain ? conv_blocks_per_field_lse(k) : conv_blocks_per_field_linear(k);
+int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain, uint32_t flags) {
+    if (log_domain) return conv_blocks_per_field_lse(k);
+    return conv_tc_active(k, flags) ? conv_blocks_per_field_tc(k) : conv_blocks_per_field_linear(k);
 }
 
 }  // namespace se2

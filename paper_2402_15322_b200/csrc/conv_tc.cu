@@ -1,0 +1,411 @@
+// K10: SE(2) group convolution, linear domain, on the 5th-generation tensor cores (tcgen05), with
+// fp32 accuracy recovered by a 3-pass BF16 split (the same operator as K2).
+//
+//   y[b, to, y, x] = sum_ti sum_{dyi, dxi < S} Wl[to, ti, dyi, dxi] * v[b, ti, y + R - dyi, x + R - dxi]
+//
+// Formulation: one CTA owns 8 output rows y0..y0+7 x one block of 16 output
+// orientations x all nx pixels of those rows.  For every input row yi and every filter column dxi one
+// tcgen05 MMA chain computes
+//
+//   D[(r, to)][x] += sum_{ti in window} A[(r, to)][ti] * B[x][ti],
+//   A[(r, to)][ti] = Wl[to, ti, y0 + r + R - yi, dxi]    (rows with dyi outside the box: 0)
+//   B[x][ti]       = v[ti, yi, x + R - dxi]               (pixels shifted by a descriptor offset)
+//
+// with M = 128 = 8 rows x 16 orientations, N = the row's pixels (<= 256), K = the theta window of the
+// orientation block (32 orientations covering the fp32 band, or all of them when nt <= 32).  Both
+// operands are K-major SWIZZLE_NONE ("interleave") shared-memory tiles:
+//   * B is a padded input row stored [ti chunk][x'][8 ti] (16 B per pixel), so a pixel shift dxi is
+//     a +16 B start-address change of the descriptor -- no im2col;
+//   * A is stored [dxi][chunk][j = dyi + 7][16 to][8 ti], so the 8 output rows r of one input row yi
+//     (dyi = y0 + r + R - yi, consecutive) form one contiguous 2 KB tile per chunk.
+// fp32 accuracy: x = hi + lo with hi = bf16(x), lo = bf16(x - hi) for both operands; the chain adds
+// hi.hi + hi.lo + lo.hi (per-term error <= 3 * 2^-18 relative; simulated on c4m in DESIGN.md).
+//
+// Roles: thread 0 is the TMA producer (bulk copies into a 2-stage input-row ring and an NA-stage
+// weight ring, mbarrier-tracked), thread 32 issues the MMAs and commits each stage back to the
+// producer; the 128 x N fp32 accumulator lives in TMEM.  Epilogue: all 4 warps move TMEM -> shared
+// (transpose) -> the fused epilogue of K2 (apply_epilogue), coalesced along x.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "conv_common.cuh"
+
+namespace se2 {
+
+namespace {
+
+constexpr int kTcRows = 8;     // output rows per CTA
+constexpr int kTcBlk = 16;     // output orientations per CTA
+constexpr int kTcPadX = 16;    // zero pixels left of x = 0 in the split input rows (>= R)
+constexpr int kTcNA = 6;       // weight-ring stages
+constexpr int kTcThreads = 128;
+
+struct TcGeom {
+    int npad;    // MMA N: nx rounded up to 16
+    int nxp;     // padded row length (pixels) of the split input: npad + 2 * kTcPadX
+    int nch;     // theta chunks of 8
+    int nwin;    // chunks in the theta window of one orientation block (2 or 4)
+    int nj;      // dyi + 7 range: S + 14
+    int nblk;    // orientation blocks
+    size_t a_stage, b_stage, smem;
+    int tmem_cols;
+};
+
+__host__ __device__ inline int tc_chunk0(int blk, int nch, int nwin) {
+    return (nwin == nch) ? 0 : ((2 * blk - 1 + nch) % nch);
+}
+
+TcGeom tc_geom(const se2_kernel_s* k) {
+    TcGeom g;
+    g.npad = (k->nx + 15) / 16 * 16;
+    g.nxp = g.npad + 2 * kTcPadX;
+    g.nch = k->nt / 8;
+    g.nwin = g.nch <= 4 ? g.nch : 4;
+    g.nj = k->S + 14;
+    g.nblk = k->nt / kTcBlk;
+    g.a_stage = (size_t)2 * g.nwin * kTcRows * kTcBlk * 16;          // hi + lo, 2 KB per chunk
+    g.b_stage = (size_t)2 * g.nwin * g.nxp * 16;                     // hi + lo rows
+    size_t pipe = 2 * g.b_stage + kTcNA * g.a_stage;
+    size_t epi = (size_t)128 * (g.npad + 1) * sizeof(float);         // TMEM -> smem transpose
+    g.smem = std::max(pipe, epi) + 1024;                              // + barriers / scratch
+    g.tmem_cols = 32;
+    while (g.tmem_cols < g.npad) g.tmem_cols *= 2;
+    g.tmem_cols *= 2;   // main (hi.hi) + correction (hi.lo + lo.hi) accumulators
+    return g;
+}
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;   // descriptor version (sm_100); base offset 0; layout SWIZZLE_NONE
+    return d;
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// bounded wait: a pipeline bug traps (a launch error) instead of hanging the device
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    long long spins = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (++spins > (1ll << 31)) __trap();
+    }
+}
+
+struct TcArgs {
+    const __nv_bfloat16* xk;   // split input rows: [hl][batch][ny][nch][nxp][8]
+    const __nv_bfloat16* wk;   // split weights:    [hl][nblk][S][nwin][nj][16][8]
+    size_t xk_hl, wk_hl;       // elements between the hi and lo halves
+    int nx, ny, nt, R, S;
+    int npad, nxp, nch, nwin, nj;
+    uint32_t a_stage, b_stage;
+    int tmem_cols;
+};
+
+// input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]
+__global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl,
+                                      int nx, int ny, int nt, int nxp, int batch) {
+    const int nch = nt / 8;
+    const int64_t total = (int64_t)batch * ny * nch * nxp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int xp = (int)(i % nxp);
+        int64_t t = i / nxp;
+        const int c = (int)(t % nch);
+        t /= nch;
+        const int y = (int)(t % ny);
+        const int b = (int)(t / ny);
+        const int x = xp - kTcPadX;
+        __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float f = 0.f;
+            if (x >= 0 && x < nx) f = v[(((int64_t)b * nt + c * 8 + e) * ny + y) * nx + x];
+            const __nv_bfloat16 h = __float2bfloat16_rn(f);
+            hi[e] = h;
+            lo[e] = __float2bfloat16_rn(f - __bfloat162float(h));
+        }
+        reinterpret_cast<uint4*>(xk)[i] = *reinterpret_cast<const uint4*>(hi);
+        reinterpret_cast<uint4*>(xk + xk_hl)[i] = *reinterpret_cast<const uint4*>(lo);
+    }
+}
+
+// weight split: Wl[to][ti][S][SP] (fp32) -> hi/lo [blk][dxi][c][j][to_l][8]
+__global__ void tc_split_weights_kernel(const float* __restrict__ Wl, __nv_bfloat16* __restrict__ wk, size_t wk_hl,
+                                        int nt, int S, int nch, int nwin, int nj, int nblk) {
+    const int SP = (S + 3) / 4 * 4;
+    const int64_t total = (int64_t)nblk * S * nwin * nj * kTcBlk;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int tol = (int)(i % kTcBlk);
+        int64_t t = i / kTcBlk;
+        const int j = (int)(t % nj);
+        t /= nj;
+        const int c = (int)(t % nwin);
+        t /= nwin;
+        const int dxi = (int)(t % S);
+        const int blk = (int)(t / S);
+        const int to = blk * kTcBlk + tol;
+        const int chunk = (tc_chunk0(blk, nch, nwin) + c) % nch;
+        const int dyi = j - 7;
+        __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int ti = chunk * 8 + e;
+            float w = 0.f;
+            if (dyi >= 0 && dyi < S) w = Wl[(((int64_t)to * nt + ti) * S + dyi) * SP + dxi];
+            const __nv_bfloat16 h = __float2bfloat16_rn(w);
+            hi[e] = h;
+            lo[e] = __float2bfloat16_rn(w - __bfloat162float(h));
+        }
+        reinterpret_cast<uint4*>(wk)[i] = *reinterpret_cast<const uint4*>(hi);
+        reinterpret_cast<uint4*>(wk + wk_hl)[i] = *reinterpret_cast<const uint4*>(lo);
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* sB = smem;                                   // [2][hl][nwin][nxp][16 B]
+    unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwin][8 j][16 to][16 B]
+    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], done;
+    __shared__ uint32_t tmem_base;
+    __shared__ float sRed[kTcThreads / 32];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int y0 = blockIdx.x * kTcRows;
+    const int blk = blockIdx.y;
+    const int b = blockIdx.z;
+    const int ylo = max(0, y0 - a.R), yhi = min(a.ny - 1, y0 + kTcRows - 1 + a.R);
+    const int nrows = yhi - ylo + 1;
+    const int chunk0 = tc_chunk0(blk, a.nch, a.nwin);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(a.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
+        for (int i = 0; i < kTcNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
+        mbar_init(&done, 1);
+        mbar_fence_init();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+
+    const size_t row_elems = (size_t)a.nch * a.nxp * 8;               // one (b, y) row of the split input
+    const uint32_t chunk_bytes_b = (uint32_t)a.nxp * 16;
+    if (warp == 0) {
+      if (lane == 0) {
+        // ---------------- producer ----------------
+        auto load_b = [&](int yy) {
+            const int st = yy & 1;
+            if (yy >= 2) tc_wait(&emptyB[st], (uint32_t)(((yy >> 1) - 1) & 1));
+            mbar_expect_tx(&fullB[st], a.b_stage);
+            const int yi = ylo + yy;
+            for (int hl = 0; hl < 2; ++hl) {
+                const __nv_bfloat16* row = a.xk + hl * a.xk_hl + ((size_t)b * a.ny + yi) * row_elems;
+                for (int c = 0; c < a.nwin; ++c) {
+                    const int ch = (chunk0 + c) % a.nch;
+                    bulk_load(sB + st * (size_t)a.b_stage + (size_t)(hl * a.nwin + c) * chunk_bytes_b,
+                              row + (size_t)ch * a.nxp * 8, chunk_bytes_b, &fullB[st]);
+                }
+            }
+        };
+        load_b(0);
+        const int b_after = min(kTcNA - 1, a.S - 1);
+        const uint32_t sA_u = smem_u32(sA), fullA_u = smem_u32(&fullA[0]);
+        const CUtensorMap* wm = &wmap;
+        for (int yy = 0; yy < nrows; ++yy) {
+            const int yi = ylo + yy;
+            const int j0 = y0 + a.R - yi + 7;
+            for (int dxi = 0; dxi < a.S; ++dxi) {
+                const int t = yy * a.S + dxi;
+                const int st = t % kTcNA;
+                if (t >= kTcNA) tc_wait(&emptyA[st], (uint32_t)(((t / kTcNA) - 1) & 1));
+                mbar_expect_tx(&fullA[st], a.a_stage);
+                // one TMA box per stage: [hl 2][chunk nwin][j 8][16 to x 8 ti]
+                tma_load_5d(sA_u + (uint32_t)st * a.a_stage, wm, fullA_u + 8u * (uint32_t)st, 0, j0, 0, blk * a.S + dxi, 0);
+                if (dxi == b_after && yy + 1 < nrows) load_b(yy + 1);
+            }
+        }
+      }
+      __syncwarp();
+    } else if (warp == 1) {
+      if (lane == 0) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(a.npad >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        const uint64_t dA0 = tc_desc(smem_u32(sA), 2048, 128);
+        const uint64_t dB0 = tc_desc(smem_u32(sB), chunk_bytes_b, 128);
+        const int ksteps = a.nwin / 2;
+        uint32_t acc = 0;
+        const uint32_t tcor = tmem + (uint32_t)(a.tmem_cols / 2);   // correction accumulator
+        for (int yy = 0; yy < nrows; ++yy) {
+            const int stb = yy & 1;
+            tc_wait(&fullB[stb], (uint32_t)((yy >> 1) & 1));
+            for (int dxi = 0; dxi < a.S; ++dxi) {
+                const int t = yy * a.S + dxi;
+                const int st = t % kTcNA;
+                tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t offA = (uint32_t)(st * a.a_stage);
+                const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
+                    const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
+                    tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, acc);
+                    tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc);
+                    acc = 1;
+                    tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
+                }
+                tc_commit(&emptyA[st]);
+            }
+            tc_commit(&emptyB[stb]);
+        }
+        tc_commit(&done);
+      }
+      __syncwarp();
+    }
+    // ---------------- epilogue ----------------
+    tc_wait(&done, 0);
+    __syncwarp();   // tcgen05.ld is .sync.aligned: the warp must be converged
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float* T = reinterpret_cast<float*>(smem);   // [128][npad + 1]; the pipeline buffers are drained
+    const int pitch = a.npad + 1;
+    {
+        const int m = 32 * warp + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
+        for (int c = 0; c < a.npad; c += 16) {
+            uint32_t v[16], u[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(taddr + (uint32_t)c));
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+                  "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+                : "r"(taddr + (uint32_t)(a.tmem_cols / 2 + c)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) T[m * pitch + c + j] = __uint_as_float(v[j]) + __uint_as_float(u[j]);
+        }
+    }
+    __syncwarp();
+    float err = 0.f;
+    const int64_t N = (int64_t)a.nx * a.ny * a.nt;
+    for (int mm = 0; mm < 32; ++mm) {
+        const int m = 32 * warp + mm;
+        const int r = m / kTcBlk, tol = m % kTcBlk;
+        const int y = y0 + r, to = blk * kTcBlk + tol;
+        if (y >= a.ny) continue;
+        const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
+        for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
+    }
+    if (epi.err_partial != nullptr) {
+        const float t = block_sum<kTcThreads>(err, sRed);
+        if (tid == 0) epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+}
+
+}  // namespace
+
+bool conv_tc_eligible(const se2_kernel_s* k) {
+    if (getenv("SE2_NO_TC") != nullptr) return false;
+    if (k->nt % 16 != 0 || k->nx > 256 || k->R > kTcPadX) return false;
+    if (k->nt / 8 > 4 && k->band > 8) return false;   // the 32-orientation window must cover the band
+    return true;
+}
+
+int conv_blocks_per_field_tc(const se2_kernel_s* k) {
+    return (k->ny + kTcRows - 1) / kTcRows * (k->nt / kTcBlk);
+}
+
+cudaError_t conv_tc_prepare(se2_kernel_s* k) {
+    if (!conv_tc_eligible(k)) return cudaSuccess;
+    const TcGeom g = tc_geom(k);
+    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
+    const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
+    cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
+    if (e != cudaSuccess) return e;
+    k->tc_w_hl = wk_hl;
+    k->tc_x_hl = xk_hl;
+    {
+        CUtensorMap* m = new CUtensorMap;
+        const uint64_t dims[5] = {(uint64_t)kTcBlk * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};
+        const uint64_t strides[4] = {(uint64_t)kTcBlk * 8 * 2, (uint64_t)g.nj * kTcBlk * 8 * 2,
+                                     (uint64_t)g.nwin * g.nj * kTcBlk * 8 * 2, (uint64_t)wk_hl * 2};
+        const uint32_t box[5] = {(uint32_t)kTcBlk * 8, (uint32_t)kTcRows, (uint32_t)g.nwin, 1, 2};
+        if (!make_tmap_5d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, k->tc_w, dims, strides, box)) {
+            delete m;
+            return cudaErrorInvalidValue;
+        }
+        k->tc_wmap = m;
+    }
+    tc_split_weights_kernel<<<592, 256>>>(k->Wl, reinterpret_cast<__nv_bfloat16*>(k->tc_w), wk_hl, k->nt, k->S, g.nch,
+                                          g.nwin, g.nj, g.nblk);
+    count_launch();
+    // the attribute is per function: set the maximum once (each launch passes its own size)
+    int optin = 0;
+    cudaFuncAttributes fa;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, k->device);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, conv_tc_kernel);
+    if (e != cudaSuccess) return e;
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;
+    if ((int)g.smem > dyn_max) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+void conv_tc_release(se2_kernel_s* k) {
+    delete reinterpret_cast<CUtensorMap*>(k->tc_wmap);
+    k->tc_wmap = nullptr;
+}
+
+cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
+                           int* bpf) {
+    const TcGeom g = tc_geom(k);
+    __nv_bfloat16* xk = reinterpret_cast<__nv_bfloat16*>(k->tc_x);
+    tc_split_input_kernel<<<148 * 8, 256, 0, s>>>(in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, batch);
+    count_launch();
+    TcArgs a;
+    a.xk = xk;
+    a.wk = reinterpret_cast<const __nv_bfloat16*>(k->tc_w);
+    a.xk_hl = k->tc_x_hl;
+    a.wk_hl = k->tc_w_hl;
+    a.nx = k->nx; a.ny = k->ny; a.nt = k->nt; a.R = k->R; a.S = k->S;
+    a.npad = g.npad; a.nxp = g.nxp; a.nch = g.nch; a.nwin = g.nwin; a.nj = g.nj;
+    a.a_stage = (uint32_t)g.a_stage;
+    a.b_stage = (uint32_t)g.b_stage;
+    a.tmem_cols = g.tmem_cols;
+    dim3 grid((k->ny + kTcRows - 1) / kTcRows, g.nblk, batch);
+    if (bpf) *bpf = (int)(grid.x * grid.y);
+    conv_tc_kernel<<<grid, kTcThreads, g.smem, s>>>(a, epi, *reinterpret_cast<const CUtensorMap*>(k->tc_wmap));
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace se2

@@ -124,6 +124,12 @@ struct se2_kernel_s {
                                   // hint redos; [8..11] = two uint64: exact-path rows live / visited
     float* split = nullptr;       // K3 theta_i-split partials (small grids): [groups][max_batch][N]
     size_t split_floats = 0;
+    // K10 (conv_tc.cu): BF16 hi/lo split weights [2][nblk][S][nwin][S+14][16][8] and input rows
+    // [2][max_batch][ny][nt/8][nx_pad + 32][8]; null when K10 does not apply to this grid
+    void* tc_w = nullptr;
+    void* tc_x = nullptr;
+    size_t tc_w_hl = 0, tc_x_hl = 0;
+    void* tc_wmap = nullptr;      // CUtensorMap (5-D) over tc_w: one TMA per weight stage
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -136,7 +142,17 @@ cudaError_t launch_conv_linear(const se2_kernel_s* k, const float* in, int batch
                                cudaStream_t s, int* blocks_per_field);
 cudaError_t launch_conv_lse(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi,
                             cudaStream_t s, int* blocks_per_field);
-int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain);
+int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain, uint32_t flags = 0);
+// K10 (conv_tc.cu): tensor-core linear conv; used for the Gibbs-kernel linear conv when prepared
+bool conv_tc_eligible(const se2_kernel_s* k);
+cudaError_t conv_tc_prepare(se2_kernel_s* k);
+void conv_tc_release(se2_kernel_s* k);
+int conv_blocks_per_field_tc(const se2_kernel_s* k);
+cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
+                           int* bpf);
+inline bool conv_tc_active(const se2_kernel_s* k, uint32_t flags) {
+    return k->tc_w != nullptr && (flags & SE2_LIN_FFMA) == 0;
+}
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);
 // K9 (sinkhorn_small.cu): whole log-domain Sinkhorn of a small grid in one cluster launch

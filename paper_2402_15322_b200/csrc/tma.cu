@@ -44,4 +44,19 @@ bool make_field_tmap(CUtensorMap* map, const float* base, int nx, int ny, int pl
     return r == CUDA_SUCCESS;
 }
 
+// generic 5-D tiled map (dims / box innermost first, strides in bytes of dims 1..4), no swizzle, no
+// OOB handling needed by the caller; false if the driver rejects it
+bool make_tmap_5d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, const uint64_t* dims,
+                  const uint64_t* strides, const uint32_t* box) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], estr[5] = {1, 1, 1, 1, 1};
+    for (int i = 0; i < 5; ++i) { d[i] = dims[i]; b[i] = box[i]; }
+    for (int i = 0; i < 4; ++i) st[i] = strides[i];
+    CUresult r = fn(map, dtype, 5, const_cast<void*>(base), d, st, b, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace se2
