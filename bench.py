@@ -39,6 +39,51 @@ WORKLOADS = {
 }
 
 
+def _tc_executed_flop(cfg, R, batch=1):
+    """MMA flops K10 executes per launch (3 BF16 passes over the dense theta window, every input row of
+    each 8-row group, N = nx rounded up to 16): the 'executed' rate next to the algorithmic one."""
+    npad = (cfg.nx + 15) // 16 * 16
+    nwin = min(cfg.ntheta // 8, 4)
+    S_ = 2 * R + 1
+    total = 0
+    for y0 in range(0, cfg.ny, 8):
+        nrows = min(cfg.ny - 1, y0 + 7 + R) - max(0, y0 - R) + 1
+        total += nrows * S_ * (nwin // 2) * 3
+    return total * (cfg.ntheta // 16) * batch * 2.0 * 128 * npad * 16
+
+
+def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, conv_ms, dev_ms, ffma_peak, sm_max,
+                   peaks, peak_src, clocks, workload):
+    """Roofline object of the dominant kernel (the linear group conv): K10 on the tensor cores when the
+    kernel uses it, else K2 on the FP32 pipes.  achieved = ALGORITHMIC flops (2 nnz per output) / the
+    average launch time measured with CUDA events on the launching stream."""
+    common = {"achieved": achieved, "unit": "TFLOP/s", "flop_per_launch": flop_per_conv, "conv_launches": n_conv,
+              "conv_avg_ms": conv_avg_ms, "conv_share_of_step": conv_ms / dev_ms if dev_ms else None}
+    traffic_all = {}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic_all = json.load(f)
+    if k.uses_tensor_cores:
+        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+        executed = _tc_executed_flop(cfg, cfg.R) / (conv_avg_ms / 1000.0) / 1e12
+        return {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 BF16, 3-pass split) + tc_split_input_kernel",
+                "peak": peak, "frac": achieved / peak, "traffic": traffic_all.get(f"{workload}_conv_tc_bytes_per_launch"),
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({peak_src}; the kernel runs inside a "
+                               f"long step); dense BF16 is the dtype the MMAs execute",
+                "executed_mma_tflops": executed, "executed_frac": executed / peak,
+                "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the dense 32-orientation window and "
+                                 "the 8 + 2R input rows of each 8-row group: executed / algorithmic = "
+                                 f"{_tc_executed_flop(cfg, cfg.R) / flop_per_conv:.1f}",
+                "vs_ffma_roofline": achieved / ffma_peak, **common}
+    return {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "peak": ffma_peak,
+            "frac": achieved / ffma_peak, "traffic": traffic_all.get(f"{workload}_conv_linear_bytes_per_launch"),
+            "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (clock from "
+                           f"MEASURED_PEAKS.json, {peak_src}); FFMA has no measured peak",
+            "peak_at_run_clock": (148 * 128 * 2 * clocks["sm_mhz"] * 1e6 / 1e12) if clocks.get("sm_mhz") else None,
+            **common}
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -453,11 +498,6 @@ def run_gpu(args):
         flop_per_conv = 2.0 * cfg.N * st["nnz_taps"]
         conv_avg_ms = conv_ms / max(n_conv, 1)
         achieved = flop_per_conv / (conv_avg_ms / 1000.0) / 1e12
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                traffic = json.load(f).get(f"{args.workload}_conv_linear_bytes_per_launch")
         out = {
             "metric": "Sinkhorn iters/s on SE(2) grid", "value": value, "unit": "iters/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -465,14 +505,8 @@ def run_gpu(args):
             "config": {"workload": WORKLOADS[args.workload], "inner_iters_per_step": iters,
                        "l2": "flushed before every timed step (256 MiB write, outside the step events)",
                        "parallelism": f"replicas x{ws} (independent JKO flows)"},
-            "roofline": {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "achieved": achieved,
-                         "peak": ffma_peak, "unit": "TFLOP/s", "frac": achieved / ffma_peak, "traffic": traffic,
-                         "peak_source": f"148 SM x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (clock from "
-                                        f"MEASURED_PEAKS.json, {peak_src}); FFMA has no measured peak",
-                         "flop_per_launch": flop_per_conv, "conv_launches": n_conv,
-                         "conv_avg_ms": conv_avg_ms, "conv_share_of_step": conv_ms / dev_ms if dev_ms else None,
-                         "peak_at_run_clock": (148 * 128 * 2 * clocks["sm_mhz"] * 1e6 / 1e12)
-                         if clocks.get("sm_mhz") else None},
+            "roofline": _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, conv_ms, dev_ms,
+                                       ffma_peak, sm_max, peaks, peak_src, clocks, args.workload),
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
             "gpu_launches": int(launches),
             "clocks": clocks,

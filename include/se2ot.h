@@ -67,8 +67,10 @@ typedef enum {
 #define SE2_DEBUG_BAD_HINTS 0x100u /* diagnostics: K3 reads its exact-path hints 60 nats too high, so
                                       every hinted output must take the verified fallback (redo) */
 #define SE2_DEBUG_NO_SPLIT 0x200u  /* diagnostics: K3 without the theta_i split (one CTA per tile-quad) */
-#define SE2_LIN_FFMA 0x400u        /* linear domain: the fp32 FFMA conv (K2) instead of the tensor-core
-                                      conv (K10, 3-pass BF16 split) on the grids K10 covers */
+#define SE2_LIN_FFMA 0x400u        /* linear domain: force the fp32 FFMA conv (K2)                     */
+#define SE2_LIN_TC 0x800u          /* linear domain: force the tensor-core conv (K10, 3-pass BF16 split)
+                                      on every grid it covers (default: only where its cost model
+                                      predicts it beats K2; see se2_kernel_stats.tensor_cores)        */
 
 typedef struct {
     int32_t nx, ny, ntheta;
@@ -89,6 +91,9 @@ typedef struct {
     int32_t radius;
     double zeta;          /* spatial anisotropy max(w1,w2)/min(w1,w2)                      */
     size_t table_bytes;   /* device bytes held by the tables                                       */
+    int32_t tensor_cores; /* 1: linear convs with the Gibbs kernel run on the tensor-core engine (K10,
+                             3-pass BF16 split) by default; 0: on the fp32 FFMA engine (K2) unless
+                             SE2_LIN_TC (2: K10 available on request only)                          */
 } se2_kernel_stats;
 
 /* ------------------------------------------------------------------------------------------

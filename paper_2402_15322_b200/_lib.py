@@ -22,6 +22,7 @@ SE2_NO_PERSISTENT = 0x80
 SE2_DEBUG_BAD_HINTS = 0x100
 SE2_DEBUG_NO_SPLIT = 0x200
 SE2_LIN_FFMA = 0x400
+SE2_LIN_TC = 0x800
 SE2_EPI_DIVIDE = 1
 SE2_EPI_MULTIPLY = 2
 SE2_EPI_PROX = 3
@@ -62,7 +63,8 @@ class se2_metric(ctypes.Structure):
 
 class se2_kernel_stats(ctypes.Structure):
     _fields_ = [("box_taps", ctypes.c_int64), ("nnz_taps", ctypes.c_int64), ("theta_band", ctypes.c_int32),
-                ("radius", ctypes.c_int32), ("zeta", ctypes.c_double), ("table_bytes", ctypes.c_size_t)]
+                ("radius", ctypes.c_int32), ("zeta", ctypes.c_double), ("table_bytes", ctypes.c_size_t),
+                ("tensor_cores", ctypes.c_int32)]
 
 
 class se2_prox(ctypes.Structure):

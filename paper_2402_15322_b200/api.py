@@ -65,7 +65,17 @@ class Kernel:
         s = L.se2_kernel_stats()
         check(L.load().se2_kernel_stats_get(self._h, ctypes.byref(s)))
         return dict(box_taps=s.box_taps, nnz_taps=s.nnz_taps, theta_band=s.theta_band, radius=s.radius,
-                    zeta=s.zeta, table_bytes=s.table_bytes)
+                    zeta=s.zeta, table_bytes=s.table_bytes, tensor_cores=int(s.tensor_cores))
+
+    @property
+    def uses_tensor_cores(self) -> bool:
+        """True when linear convs run on the tensor-core engine (K10) by default."""
+        return self.stats()["tensor_cores"] == 1
+
+    @property
+    def has_tensor_cores(self) -> bool:
+        """True when K10 covers this grid (default or forced with SE2_LIN_TC)."""
+        return self.stats()["tensor_cores"] != 0
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -167,11 +177,12 @@ def se2_sinkhorn(k: Kernel, mu: torch.Tensor, nu: Optional[torch.Tensor], a: tor
 
 
 def se2_jko_step(k: Kernel, mu_k: torch.Tensor, mu_next: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
-                 iters: int, prox: L.se2_prox, log_domain: bool = False, trace: bool = False):
-    """One entropic JKO step (R10).  Returns (mass before normalisation, err trace)."""
+                 iters: int, prox: L.se2_prox, log_domain: bool = False, trace: bool = False, engine_flags: int = 0):
+    """One entropic JKO step (R10).  Returns (mass before normalisation, err trace).
+    engine_flags: SE2_LIN_FFMA / SE2_LIN_TC to force the linear conv engine (tests, A/B)."""
     for name, t in (("mu_k", mu_k), ("mu_next", mu_next), ("a", a), ("b", b)):
         _check_field(t, k, name, 1)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace))
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace) | int(engine_flags))
     mass = ctypes.c_double()
     tr = np.zeros((max(iters, 1), 1), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None

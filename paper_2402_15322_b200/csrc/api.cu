@@ -302,6 +302,7 @@ se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* o) {
     o->radius = k->R;
     o->zeta = std::max(k->w1, k->w2) / std::min(k->w1, k->w2);
     o->table_bytes = k->table_bytes;
+    o->tensor_cores = k->tc_w == nullptr ? 0 : (k->tc_fast ? 1 : 2);
     return SE2_OK;
 }
 

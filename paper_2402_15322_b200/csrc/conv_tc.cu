@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "conv_common.cuh"
@@ -40,7 +41,8 @@ constexpr int kTcRows = 8;     // output rows per CTA
 constexpr int kTcBlk = 16;     // output orientations per CTA
 constexpr int kTcPadX = 16;    // zero pixels left of x = 0 in the split input rows (>= R)
 constexpr int kTcNA = 6;       // weight-ring stages
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 320;   // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: accumulators / epilogue
+constexpr int kTcFlushWarps = 8;
 
 struct TcGeom {
     int npad;    // MMA N: nx rounded up to 16
@@ -181,7 +183,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sB = smem;                                   // [2][hl][nwin][nxp][16 B]
     unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwin][8 j][16 to][16 B]
-    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], done;
+    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone, flushed;
     __shared__ uint32_t tmem_base;
     __shared__ float sRed[kTcThreads / 32];
 
@@ -201,7 +203,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
         for (int i = 0; i < kTcNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
-        mbar_init(&done, 1);
+        mbar_init(&rowdone, 1);
+        mbar_init(&flushed, kTcFlushWarps);
         mbar_fence_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -255,8 +258,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
         const uint64_t dA0 = tc_desc(smem_u32(sA), 2048, 128);
         const uint64_t dB0 = tc_desc(smem_u32(sB), chunk_bytes_b, 128);
         const int ksteps = a.nwin / 2;
-        uint32_t acc = 0;
-        const uint32_t tcor = tmem + (uint32_t)(a.tmem_cols / 2);   // correction accumulator
+        const uint32_t tcor = tmem + (uint32_t)(a.tmem_cols / 2);   // correction accumulator (hi.lo + lo.hi)
+        uint32_t acc_c = 0;
         for (int yy = 0; yy < nrows; ++yy) {
             const int stb = yy & 1;
             tc_wait(&fullB[stb], (uint32_t)((yy >> 1) & 1));
@@ -267,58 +270,106 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t offA = (uint32_t)(st * a.a_stage);
                 const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
-                for (int ks = 0; ks < ksteps; ++ks) {
+                for (int ks = 0; ks < ksteps; ++ks) {   // corrections first: they overlap the row flush below
                     const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
                     const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
-                    tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, acc);
-                    tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc);
-                    acc = 1;
+                    tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);
+                    acc_c = 1;
                     tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
+                }
+                // the main accumulator restarts every input row; the accumulator warps must have read the
+                // previous row's value first
+                if (dxi == 0 && yy > 0) {
+                    tc_wait(&flushed, (uint32_t)((yy - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048;
+                    const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b;
+                    tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (dxi > 0 || ks > 0) ? 1u : 0u);
                 }
                 tc_commit(&emptyA[st]);
             }
             tc_commit(&emptyB[stb]);
+            tc_commit(&rowdone);
         }
-        tc_commit(&done);
       }
       __syncwarp();
     }
-    // ---------------- epilogue ----------------
-    tc_wait(&done, 0);
-    __syncwarp();   // tcgen05.ld is .sync.aligned: the warp must be converged
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    float* T = reinterpret_cast<float*>(smem);   // [128][npad + 1]; the pipeline buffers are drained
+    // ---------------- accumulation of the per-row partial sums (fp32, round to nearest) ----------------
+    // The tensor core's fp32 accumulation truncates; restarting the main accumulator every input row
+    // bounds that to one row's chain (S x K/16 steps) and the row sums are added here in registers.
+    float* T = reinterpret_cast<float*>(smem);   // [128][npad + 1] after the pipeline has drained
     const int pitch = a.npad + 1;
-    {
-        const int m = 32 * warp + lane;
-        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
-        for (int c = 0; c < a.npad; c += 16) {
-            uint32_t v[16], u[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                : "r"(taddr + (uint32_t)c));
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-                  "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
-                : "r"(taddr + (uint32_t)(a.tmem_cols / 2 + c)));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
+    float err = 0.f;
+    const int half = a.npad / 2;
+    if (warp >= 2) {
+        const int q = warp & 3, h = (warp - 2) >> 2;        // TMEM lane quarter (warp % 4) and column half
+        const int m = 32 * q + lane;
+        const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * half);
+        float sum[128];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) T[m * pitch + c + j] = __uint_as_float(v[j]) + __uint_as_float(u[j]);
+        for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+        for (int yy = 0; yy < nrows; ++yy) {
+            tc_wait(&rowdone, (uint32_t)(yy & 1));
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int c = 0; c < 128; c += 32) {
+                if (c < half) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(tl + (uint32_t)c));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&flushed)) : "memory");
+        }
+        // the correction accumulator (complete with the last row's commit), then out through shared memory
+        const uint32_t tc2 = tl + (uint32_t)(a.tmem_cols / 2);
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+            if (c < half) {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(tc2 + (uint32_t)c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (c + j < half) T[m * pitch + h * half + c + j] = sum[c + j] + __uint_as_float(v[j]);
+            }
         }
     }
-    __syncwarp();
-    float err = 0.f;
-    const int64_t N = (int64_t)a.nx * a.ny * a.nt;
-    for (int mm = 0; mm < 32; ++mm) {
-        const int m = 32 * warp + mm;
-        const int r = m / kTcBlk, tol = m % kTcBlk;
-        const int y = y0 + r, to = blk * kTcBlk + tol;
-        if (y >= a.ny) continue;
-        const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
-        for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
+    __syncthreads();   // T complete (every warp reaches this; the role warps have finished their loops)
+    if (warp >= 2) {
+        const int64_t N = (int64_t)a.nx * a.ny * a.nt;
+        const int f = warp - 2;
+        for (int mm = 0; mm < 128 / kTcFlushWarps; ++mm) {
+            const int m = (128 / kTcFlushWarps) * f + mm;
+            const int r = m / kTcBlk, tol = m % kTcBlk;
+            const int y = y0 + r, to = blk * kTcBlk + tol;
+            if (y >= a.ny) continue;
+            const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
+            for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
+        }
     }
     if (epi.err_partial != nullptr) {
         const float t = block_sum<kTcThreads>(err, sRed);
@@ -352,6 +403,17 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     if (e != cudaSuccess) return e;
     k->tc_w_hl = wk_hl;
     k->tc_x_hl = xk_hl;
+    {
+        // cost model at batch 1 (measured on B200, K10): K10 = waves x one CTA's MMA chain
+        // ((8 + 2R) rows x S taps x K/16 steps x 3 passes x N/2 cycles) at ~70% of the tensor floor,
+        // K2 = 2 nnz N flop at ~60 TFLOP/s (0.82 of the FFMA peak)
+        const double ctas = (double)((k->ny + kTcRows - 1) / kTcRows) * g.nblk;
+        const double waves = std::ceil(ctas / 148.0);
+        const double cyc = (double)std::min(k->ny, kTcRows + 2 * k->R) * k->S * (g.nwin / 2) * 3 * (g.npad / 2);
+        const double t10 = waves * cyc / 0.7 / 1.9e9 + 8e-6;
+        const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
+        k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
+    }
     {
         CUtensorMap* m = new CUtensorMap;
         const uint64_t dims[5] = {(uint64_t)kTcBlk * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};

@@ -130,6 +130,7 @@ struct se2_kernel_s {
     void* tc_x = nullptr;
     size_t tc_w_hl = 0, tc_x_hl = 0;
     void* tc_wmap = nullptr;      // CUtensorMap (5-D) over tc_w: one TMA per weight stage
+    bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -150,8 +151,10 @@ void conv_tc_release(se2_kernel_s* k);
 int conv_blocks_per_field_tc(const se2_kernel_s* k);
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
                            int* bpf);
+// K10 when prepared and either forced (SE2_LIN_TC) or predicted faster than K2 (tc_fast, cost model in
+// conv_tc.cu); SE2_LIN_FFMA forces K2
 inline bool conv_tc_active(const se2_kernel_s* k, uint32_t flags) {
-    return k->tc_w != nullptr && (flags & SE2_LIN_FFMA) == 0;
+    return k->tc_w != nullptr && (flags & SE2_LIN_FFMA) == 0 && (k->tc_fast || (flags & SE2_LIN_TC) != 0);
 }
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);

@@ -11,13 +11,18 @@ import numpy as np
 import pytest
 import torch
 
+from paper_2402_15322_b200 import _lib as L
+
 import oracle as O
 import se2_synth as S
 from gpu_util import measure_err, potential_err
 
 pytestmark = pytest.mark.gpu
 
-TOL_CONV = 1e-5     # fp32 sums of positive terms vs fp64 (relative, elementwise)
+TOL_CONV = 1e-5     # fp32 sums of positive terms vs fp64 (relative, elementwise): K2 (FFMA)
+TOL_CONV_TC = 3e-5  # K10 (tensor cores, 3-pass BF16 split): per-term split error <= 3 * 2^-18 plus the
+                    # truncating fp32 accumulation of one input row's chain (S * K/16 steps <= 62 at R 15,
+                    # <= 62 * 2^-23); reading R18 in DESIGN.md
 TOL_LSE = 1e-5      # |d ly| / max(1, |ly|)
 
 
@@ -50,6 +55,25 @@ ODD_GRIDS = [
 ]
 
 
+# grids K10 (tensor cores) covers: nt % 16 == 0, nx <= 256, theta band <= 8 when nt > 32
+TC_GRIDS = [
+    ("tc-ragged", 37, 53, 32, 0.01, (1.0, 3.0, 1.0), 7),    # N = 48 (nx padded), last 8-row group partial
+    ("tc-r15", 72, 44, 16, 0.003, (1.0, 3.0, 1.0), 15),     # the largest support, nt 16 (window = all)
+    ("tc-nt64", 100, 40, 64, 0.003, (1.0, 3.0, 1.0), 9),    # the 32-orientation window of the band
+    ("tc-nt48", 256, 12, 48, 0.003, (1.0, 3.0, 1.0), 3),    # N = 256, wrapped theta window (6 chunks)
+    ("tc-r0", 64, 16, 16, 0.01, (1.0, 3.0, 1.0), 0),        # theta-only convolution
+    ("tc-thin", 16, 5, 32, 0.02, (1.0, 2.0, 1.5), 2),       # fewer rows than one group
+]
+
+
+@pytest.mark.parametrize("case", TC_GRIDS, ids=lambda c: c[0])
+def test_conv_tc_parity(case, cuda_device):
+    """K10 forced on grids it covers, against the fp64 oracle (full fields), at TOL_CONV_TC."""
+    name, nx, ny, nt, eps, w, R = case
+    assert _kernel(nx, ny, nt, eps, w, R, 2).has_tensor_cores
+    _conv_check(name, nx, ny, nt, eps, w, R, False, batch=2, full=True, extra_flags=L.SE2_LIN_TC)
+
+
 @pytest.mark.parametrize("case", CFG_GRIDS + ODD_GRIDS, ids=lambda c: c[0])
 def test_kernel_stats(case, cuda_device):
     name, nx, ny, nt, eps, w, R = case
@@ -70,7 +94,8 @@ def test_kernel_stats(case, cuda_device):
     assert st["theta_band"] == band
 
 
-def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse_exact=False, log_span=200.0):
+def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse_exact=False, log_span=200.0,
+                extra_flags=0):
     k = _kernel(nx, ny, nt, eps, w, R, batch)
     g = O.Grid(nx, ny, nt)
     shape = (batch, nt, ny, nx)
@@ -82,7 +107,7 @@ def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse
         v = S.random_positive_field(shape, seed=zlib.crc32(name.encode()), log_range=30.0)
         Tt = O.kernel_table(g, R, eps, w)
     from paper_2402_15322_b200 import se2_conv
-    y = _host(se2_conv(k, _dev(v), log_domain=log_domain, lse_exact=lse_exact))
+    y = _host(se2_conv(k, _dev(v), log_domain=log_domain, lse_exact=lse_exact, extra_flags=extra_flags))
     if full:
         ref = O.lse_conv(Lt, v.astype(np.float64)) if log_domain else O.conv(Tt, v.astype(np.float64))
         got = y
@@ -105,15 +130,21 @@ def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse
         assert e < TOL_LSE, (name, e)
     else:
         e = float(np.max(np.abs(got - ref) / np.abs(ref)))
-        assert e < TOL_CONV, (name, e)
+        tc = not (extra_flags & L.SE2_LIN_FFMA) and (
+            k.uses_tensor_cores or (bool(extra_flags & L.SE2_LIN_TC) and k.has_tensor_cores))
+        assert e < (TOL_CONV_TC if tc else TOL_CONV), (name, tc, e)
 
 
 @pytest.mark.parametrize("case", CFG_GRIDS + ODD_GRIDS, ids=lambda c: c[0])
-@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
-def test_conv_parity(case, log_domain, cuda_device):
+@pytest.mark.parametrize("engine", ["linear", "linear-ffma", "linear-tc", "log"])
+def test_conv_parity(case, engine, cuda_device):
+    """linear: the default engine (K10 on the tensor cores where its cost model picks it, else K2);
+    linear-ffma: K2 forced (SE2_LIN_FFMA); linear-tc: K10 forced (SE2_LIN_TC) on every grid it covers
+    (nt % 16 == 0, nx <= 256); log: K3."""
     name, nx, ny, nt, eps, w, R = case
     big = nx * ny * nt > 200000
-    _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=1 if big else 2, full=not big)
+    flags = {"linear-ffma": L.SE2_LIN_FFMA, "linear-tc": L.SE2_LIN_TC}.get(engine, 0)
+    _conv_check(name, nx, ny, nt, eps, w, R, engine == "log", batch=1 if big else 2, full=not big, extra_flags=flags)
 
 
 @pytest.mark.parametrize("case", CFG_GRIDS[:3] + ODD_GRIDS, ids=lambda c: c[0])
@@ -217,19 +248,20 @@ def test_fused_epilogues(log_domain, cuda_device):
     else:
         Kv = O.conv(O.kernel_table(g, R, eps, w), xin32.astype(np.float64))
     t64 = tin32.astype(np.float64)
+    tol_lin = TOL_CONV_TC if k.uses_tensor_cores else TOL_CONV
     out = torch.empty(shape, device="cuda")
     se2_conv_update(k, _dev(xin32), _dev(tin32), out, L.SE2_EPI_DIVIDE, log_domain)
     got = _host(out)
     if log_domain:
         assert potential_err(got, t64 - np.log(Kv)) < TOL_LSE
     else:
-        assert measure_err(got, t64 / Kv) < TOL_CONV
+        assert measure_err(got, t64 / Kv) < tol_lin
     se2_conv_update(k, _dev(xin32), _dev(tin32), out, L.SE2_EPI_MULTIPLY, log_domain)
     got = _host(out)
     if log_domain:
         assert potential_err(got, t64 + np.log(Kv)) < TOL_LSE
     else:
-        assert measure_err(got, t64 * Kv) < TOL_CONV
+        assert measure_err(got, t64 * Kv) < tol_lin
     # JKO prox: b = z^{-tau/(eps+tau)} exp(-tau V/(eps+tau)), V = |x - c|^2 (R10)
     tau = 1e-3
     prox = make_prox(k, tau)

@@ -119,9 +119,12 @@ def test_barycenter_parity(case, cuda_device):
     assert trace_err(tr, gold["err"]) <= TOL_TRACE
 
 
-@pytest.mark.parametrize("case", ["c4m", "c4p", "c5m", "c4q"])
+@pytest.mark.parametrize("case", ["c4m", "c4p", "c5m", "c4q", "c4m-tc", "c4m-ffma", "c4q-ffma"])
 def test_jko_parity(case, cuda_device):
-    from paper_2402_15322_b200 import make_porous_prox, make_prox, se2_jko_step
+    """The JKO runs on the default linear engine; -tc / -ffma force K10 (tensor cores) / K2 (FFMA)."""
+    from paper_2402_15322_b200 import _lib as L, make_porous_prox, make_prox, se2_jko_step
+    case, _, eng = case.partition("-")
+    engine_flags = {"tc": L.SE2_LIN_TC, "ffma": L.SE2_LIN_FFMA}.get(eng, 0)
     pc = S.get_parity_case(case)
     cfg, d = S.parity_inputs(pc)
     gold = _golden(case)
@@ -133,7 +136,8 @@ def test_jko_parity(case, cuda_device):
     b = torch.empty_like(mu)
     full = pc.full_fields
     for step in range(cfg.jko_steps):
-        mass, tr = se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, cfg.log_domain, trace=True)
+        mass, tr = se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, cfg.log_domain, trace=True,
+                                engine_flags=engine_flags)
         assert abs(mass - gold["masses"][step]) <= TOL_MEAS * abs(gold["masses"][step])
         assert trace_err(tr, gold["err"][step]) <= TOL_TRACE
         _cmp_meas(f"mu_{step + 1}", _sel(_host(nxt), gold, full), gold["mus"][step + 1].reshape(-1))
