@@ -260,35 +260,47 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
         const int ksteps = a.nwin / 2;
         const uint32_t tcor = tmem + (uint32_t)(a.tmem_cols / 2);   // correction accumulator (hi.lo + lo.hi)
         uint32_t acc_c = 0;
+        auto issue_corr = [&](int t, int stb, int dxi) {
+            const int st = t % kTcNA;
+            tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t offA = (uint32_t)(st * a.a_stage);
+            const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
+            for (int ks = 0; ks < ksteps; ++ks) {
+                const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
+                const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
+                tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);
+                acc_c = 1;
+                tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
+            }
+        };
+        auto issue_main = [&](int t, int stb, int dxi) {
+            const int st = t % kTcNA;
+            const uint32_t offA = (uint32_t)(st * a.a_stage);
+            const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
+            for (int ks = 0; ks < ksteps; ++ks) {
+                const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048;
+                const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b;
+                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (dxi > 0 || ks > 0) ? 1u : 0u);
+            }
+            tc_commit(&emptyA[st]);
+        };
         for (int yy = 0; yy < nrows; ++yy) {
             const int stb = yy & 1;
             tc_wait(&fullB[stb], (uint32_t)((yy >> 1) & 1));
-            for (int dxi = 0; dxi < a.S; ++dxi) {
-                const int t = yy * a.S + dxi;
-                const int st = t % kTcNA;
-                tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
+            // The main accumulator restarts every input row and the accumulator warps must first have read
+            // the previous row's sums: the correction MMAs of the row's first P stages (the whole weight
+            // ring) are issued before that wait so the tensor pipe stays busy during the flush.
+            const int P = yy > 0 ? min(kTcNA, a.S) : 0;
+            for (int dxi = 0; dxi < P; ++dxi) issue_corr(yy * a.S + dxi, stb, dxi);
+            if (yy > 0) {
+                tc_wait(&flushed, (uint32_t)((yy - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t offA = (uint32_t)(st * a.a_stage);
-                const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
-                for (int ks = 0; ks < ksteps; ++ks) {   // corrections first: they overlap the row flush below
-                    const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
-                    const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
-                    tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);
-                    acc_c = 1;
-                    tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
-                }
-                // the main accumulator restarts every input row; the accumulator warps must have read the
-                // previous row's value first
-                if (dxi == 0 && yy > 0) {
-                    tc_wait(&flushed, (uint32_t)((yy - 1) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                for (int ks = 0; ks < ksteps; ++ks) {
-                    const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048;
-                    const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b;
-                    tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (dxi > 0 || ks > 0) ? 1u : 0u);
-                }
-                tc_commit(&emptyA[st]);
+            }
+            for (int dxi = 0; dxi < P; ++dxi) issue_main(yy * a.S + dxi, stb, dxi);
+            for (int dxi = P; dxi < a.S; ++dxi) {
+                issue_corr(yy * a.S + dxi, stb, dxi);
+                issue_main(yy * a.S + dxi, stb, dxi);
             }
             tc_commit(&emptyB[stb]);
             tc_commit(&rowdone);
