@@ -37,7 +37,7 @@ namespace se2 {
 
 namespace {
 
-constexpr int kTcRows = 8;     // output rows per CTA
+constexpr int kTcRows = 8;     // rows of the MMA M tile (8 rows x 16 orientations = 128)
 constexpr int kTcBlk = 16;     // output orientations per CTA
 constexpr int kTcPadX = 16;    // zero pixels left of x = 0 in the split input rows (>= R)
 constexpr int kTcNA = 6;       // weight-ring stages
@@ -117,6 +117,7 @@ struct TcArgs {
     int npad, nxp, nch, nwin, nj;
     uint32_t a_stage, b_stage;
     int tmem_cols;
+    int rows_out;              // output rows a CTA owns (<= kTcRows; the M tile's remaining rows are discarded)
 };
 
 // input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]
@@ -188,10 +189,10 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     __shared__ float sRed[kTcThreads / 32];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int y0 = blockIdx.x * kTcRows;
+    const int y0 = blockIdx.x * a.rows_out;
     const int blk = blockIdx.y;
     const int b = blockIdx.z;
-    const int ylo = max(0, y0 - a.R), yhi = min(a.ny - 1, y0 + kTcRows - 1 + a.R);
+    const int ylo = max(0, y0 - a.R), yhi = min(a.ny - 1, y0 + a.rows_out - 1 + a.R);
     const int nrows = yhi - ylo + 1;
     const int chunk0 = tc_chunk0(blk, a.nch, a.nwin);
 
@@ -378,7 +379,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             const int m = (128 / kTcFlushWarps) * f + mm;
             const int r = m / kTcBlk, tol = m % kTcBlk;
             const int y = y0 + r, to = blk * kTcBlk + tol;
-            if (y >= a.ny) continue;
+            if (y >= a.ny || r >= a.rows_out) continue;
             const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
             for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
         }
@@ -401,8 +402,23 @@ bool conv_tc_eligible(const se2_kernel_s* k) {
     return true;
 }
 
+// output rows per CTA: fewer than the M tile's 8 when that fills the SMs in the same number of waves
+// (c4: 7 rows -> 37 x 4 = 148 CTAs, one wave, each chain 37 instead of 38 input rows).  Chosen for the
+// kernel's max_batch so that every launch (and the error-partial layout) uses one geometry.
+static int tc_rows_out(const se2_kernel_s* k) {
+    int best = kTcRows;
+    double best_cost = 1e300;
+    for (int rows = kTcRows; rows >= 4; --rows) {
+        const double ctas = (double)((k->ny + rows - 1) / rows) * (k->nt / kTcBlk) * k->max_batch;
+        const double cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
+        if (cost < best_cost - 1e-9) { best_cost = cost; best = rows; }
+    }
+    return best;
+}
+
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
-    return (k->ny + kTcRows - 1) / kTcRows * (k->nt / kTcBlk);
+    const int rows = tc_rows_out(k);
+    return (k->ny + rows - 1) / rows * (k->nt / kTcBlk);
 }
 
 cudaError_t conv_tc_prepare(se2_kernel_s* k) {
@@ -419,9 +435,10 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
         // cost model at batch 1 (measured on B200, K10): K10 = waves x one CTA's MMA chain
         // ((8 + 2R) rows x S taps x K/16 steps x 3 passes x N/2 cycles) at ~70% of the tensor floor,
         // K2 = 2 nnz N flop at ~60 TFLOP/s (0.82 of the FFMA peak)
-        const double ctas = (double)((k->ny + kTcRows - 1) / kTcRows) * g.nblk;
+        const int rows = tc_rows_out(k);
+        const double ctas = (double)((k->ny + rows - 1) / rows) * g.nblk;
         const double waves = std::ceil(ctas / 148.0);
-        const double cyc = (double)std::min(k->ny, kTcRows + 2 * k->R) * k->S * (g.nwin / 2) * 3 * (g.npad / 2);
+        const double cyc = (double)std::min(k->ny, rows + 2 * k->R) * k->S * (g.nwin / 2) * 3 * (g.npad / 2);
         const double t10 = waves * cyc / 0.7 / 1.9e9 + 8e-6;
         const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
@@ -475,7 +492,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.tmem_cols = g.tmem_cols;
-    dim3 grid((k->ny + kTcRows - 1) / kTcRows, g.nblk, batch);
+    a.rows_out = tc_rows_out(k);
+    dim3 grid((k->ny + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
     conv_tc_kernel<<<grid, kTcThreads, g.smem, s>>>(a, epi, *reinterpret_cast<const CUtensorMap*>(k->tc_wmap));
     count_launch();
