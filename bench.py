@@ -44,12 +44,20 @@ def _tc_executed_flop(cfg, R, batch=1):
     each 8-row group, N = nx rounded up to 16): the 'executed' rate next to the algorithmic one."""
     npad = (cfg.nx + 15) // 16 * 16
     nwin = min(cfg.ntheta // 8, 4)
+    nblk = cfg.ntheta // 16
     S_ = 2 * R + 1
+    # output rows per CTA as conv_tc.cu's tc_rows_out picks them (max_batch = batch)
+    best, rows_out = None, 8
+    for rows in range(8, 3, -1):
+        ctas = -(-cfg.ny // rows) * nblk * batch
+        cost = -(-ctas // 148) * min(cfg.ny, rows + 2 * R)
+        if best is None or cost < best:
+            best, rows_out = cost, rows
     total = 0
-    for y0 in range(0, cfg.ny, 8):
-        nrows = min(cfg.ny - 1, y0 + 7 + R) - max(0, y0 - R) + 1
+    for y0 in range(0, cfg.ny, rows_out):
+        nrows = min(cfg.ny - 1, y0 + rows_out - 1 + R) - max(0, y0 - R) + 1
         total += nrows * S_ * (nwin // 2) * 3
-    return total * (cfg.ntheta // 16) * batch * 2.0 * 128 * npad * 16
+    return total * nblk * batch * 2.0 * 128 * npad * 16
 
 
 def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, conv_ms, dev_ms, ffma_peak, sm_max,
@@ -71,9 +79,13 @@ def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, con
                 "peak": peak, "frac": achieved / peak, "traffic": traffic_all.get(f"{workload}_conv_tc_bytes_per_launch"),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({peak_src}; the kernel runs inside a "
                                f"long step); dense BF16 is the dtype the MMAs execute",
-                "executed_mma_tflops": executed, "executed_frac": executed / peak,
+                "executed_mma_tflops": executed,
+                "executed_frac": executed / float(peaks.get("bf16_tflops", peak)),
+                "executed_frac_note": "executed MMA rate / the BURST bf16 peak (cuBLAS 8192^3 best of 10): the SM clock "
+                                      "stays at max through the step (clocks.sm_mhz), while the sustained figure was "
+                                      "measured at a power-capped clock",
                 "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the dense 32-orientation window and "
-                                 "the 8 + 2R input rows of each 8-row group: executed / algorithmic = "
+                                 "the rows + 2R input rows of each CTA's row group (M tile 128): executed / algorithmic = "
                                  f"{_tc_executed_flop(cfg, cfg.R) / flop_per_conv:.1f}",
                 "vs_ffma_roofline": achieved / ffma_peak, **common}
     return {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "peak": ffma_peak,
