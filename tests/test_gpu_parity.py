@@ -336,3 +336,41 @@ def test_sinkhorn_k9_selection(cuda_device):
         a2, b2 = torch.empty_like(mu), torch.empty_like(mu)
         se2_sinkhorn(k, mu, nu, a2, b2, 20, True, persistent=False)
         assert potential_err(_host(a), _host(a2)) < 1e-5 and potential_err(_host(b), _host(b2)) < 1e-5
+
+
+@pytest.mark.parametrize("engine", ["tc", "ffma"])
+def test_linear_solvers_engines(engine, cuda_device):
+    """Linear-domain Sinkhorn and App. A barycenter (20 iterations each) on a K10-covered grid with
+    each linear engine forced (SE2_LIN_TC / SE2_LIN_FFMA), against the fp64 oracle run in the test:
+    potentials (log a, log b) at TOL_POT, barycenter at TOL_MEAS.  20 iterations keep the linear
+    scalings inside fp32's range at this eps (by 60 both engines leave it: log a spans [-84, 63],
+    reading R13 -- such runs belong to the log domain)."""
+    import oracle as O
+    from paper_2402_15322_b200 import Kernel, _lib as L, se2_barycenter, se2_sinkhorn
+    nx, ny, nt, R, eps, w = 48, 40, 16, 5, 0.02, (1.0, 3.0, 1.0)
+    flags = L.SE2_LIN_TC if engine == "tc" else L.SE2_LIN_FFMA
+    k = Kernel(nx, ny, nt, eps, w, R, max_batch=2)
+    assert k.has_tensor_cores
+    g = O.Grid(nx, ny, nt)
+    T, Lt = O.kernel_table(g, R, eps, w), O.log_kernel_table(g, R, eps, w)
+    mu = S.stroke_measure(nx, ny, nt, 3, seed=71).astype(np.float32).astype(np.float64)
+    nu = S.stroke_measure(nx, ny, nt, 3, seed=72).astype(np.float32).astype(np.float64)
+    # Sinkhorn: the engine flag rides on the solver's option flags (binding: no_graph path unchanged)
+    ref = O.sinkhorn(T, Lt, mu, nu, 20, log_domain=False, trace=True)
+    a, b = torch.empty((1, nt, ny, nx), device="cuda"), torch.empty((1, nt, ny, nx), device="cuda")
+    opts = L.se2_opts(20, L.SE2_TRACE_ERR | flags)
+    tr = np.zeros((20, 1))
+    import ctypes
+    from paper_2402_15322_b200.api import _ptr, _stream
+    mu_d, nu_d = _dev(mu[None]), _dev(nu[None])
+    L.check(L.load().se2_sinkhorn(k.handle, _ptr(mu_d), _ptr(nu_d), _ptr(a), _ptr(b), 1, None, ctypes.byref(opts),
+                                  tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(mu_d.device)))
+    _cmp_pot("log a", np.log(_host(a)[0]).ravel(), np.log(ref["a"]).ravel())
+    _cmp_pot("log b", np.log(_host(b)[0]).ravel(), np.log(ref["b"]).ravel())
+    assert trace_err(tr[:, 0], ref["err"]) <= TOL_TRACE
+    # barycenter of (mu, nu) with lambda = (0.3, 0.7)
+    lam = np.array([[0.3, 0.7]])
+    refb = O.barycenter(T, Lt, [mu, nu], lam[0], 20, log_domain=False, trace=True)
+    bary, trb = se2_barycenter(k, _dev(np.stack([mu, nu])), lam, 20, False, trace=True, debug_flags=flags)
+    _cmp_meas("bary", _host(bary)[0].ravel(), refb["bary"].ravel())
+    assert trace_err(trb[:, 0], refb["err"]) <= TOL_TRACE
