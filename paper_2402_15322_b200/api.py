@@ -231,13 +231,15 @@ def se2_marginal_error(k: Kernel, a: torch.Tensor, b: torch.Tensor, mu: torch.Te
     return out
 
 
-def se2_transport_cost(k: Kernel, a: torch.Tensor, b: torch.Tensor, log_domain: bool) -> np.ndarray:
-    """<pi, rho_b^2> of the plan pi = a K b (one conv with the cost table; NEXT #2)."""
+def se2_transport_cost(k: Kernel, a: torch.Tensor, b: torch.Tensor, log_domain: bool,
+                       engine_flags: int = 0) -> np.ndarray:
+    """<pi, rho_b^2> of the plan pi = a K b (one conv with the cost table; NEXT #2).
+    engine_flags: SE2_LIN_FFMA / SE2_LIN_TC to force the linear conv engine (tests, A/B)."""
     _check_field(a, k, "a")
     batch = a.numel() // k.N
     _check_field(b, k, "b", batch)
     out = np.zeros(batch, dtype=np.float64)
-    check(L.load().se2_transport_cost(k.handle, _ptr(a), _ptr(b), batch, _flags(log_domain),
+    check(L.load().se2_transport_cost(k.handle, _ptr(a), _ptr(b), batch, _flags(log_domain) | int(engine_flags),
                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream(a.device)))
     return out
 

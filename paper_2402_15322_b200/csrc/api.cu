@@ -106,8 +106,8 @@ static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t
     }
     cudaError_t e;
     if (!log_domain)
-        e = (conv_tc_active(k, flags) && epi.table == nullptr) ? launch_conv_tc(k, in, batch, epi, s, bpf)
-                                                               : launch_conv_linear(k, in, batch, epi, s, bpf);
+        e = conv_tc_route(k, flags, epi) ? launch_conv_tc(k, in, batch, epi, s, bpf)
+                                         : launch_conv_linear(k, in, batch, epi, s, bpf);
     else if ((flags & SE2_LSE_EXACT) || k->nt > 128)   // K3 holds per-channel state for <= 128 orientations
         e = launch_conv_lse(k, in, batch, epi, s, bpf);
     else
@@ -832,15 +832,23 @@ se2_status se2_transport_cost(se2_kernel k, const float* a, const float* b, int3
         }
         k->table_bytes += tabl + tab;
     }
+    {
+        cudaError_t e = conv_tc_prepare_cost(k, s);
+        if (e != cudaSuccess) {
+            set_error(std::string("cost table (K10 weights): ") + cudaGetErrorString(e));
+            return SE2_ECUDA;
+        }
+    }
     KernelExtra* x = extra(k);
-    const int bpf = LOG ? conv_blocks_per_field_lse(k) : conv_blocks_per_field_linear(k);
+    Epilogue e;
+    e.op = EPI_DOT;
+    e.table = LOG ? k->Lcq : k->Wcl;
+    const int bpf = LOG ? conv_blocks_per_field_lse(k)
+                        : (conv_tc_route(k, flags, e) ? conv_blocks_per_field_tc(k) : conv_blocks_per_field_linear(k));
     se2_status st = ensure(x->partial, (size_t)batch * bpf * sizeof(float));
     if (st != SE2_OK) return st;
     st = ensure(x->trace, (size_t)batch * sizeof(double));
     if (st != SE2_OK) return st;
-    Epilogue e;
-    e.op = EPI_DOT;
-    e.table = LOG ? k->Lcq : k->Wcl;
     e.err_a = a;
     e.err_partial = reinterpret_cast<float*>(x->partial.ptr);
     // cost = sum_x a(x) sum_y K(x,y) rho^2(x,y) b(y): one conv of b with the cost table (the log domain

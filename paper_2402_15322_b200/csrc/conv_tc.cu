@@ -421,6 +421,38 @@ int conv_blocks_per_field_tc(const se2_kernel_s* k) {
     return (k->ny + rows - 1) / rows * (k->nt / kTcBlk);
 }
 
+// 5-D tensor map over split weights w: one TMA box per pipeline stage ([hl][chunk][8 j][16 to x 8 ti])
+static cudaError_t tc_weight_map(const se2_kernel_s* k, void* w, void** map_out) {
+    const TcGeom g = tc_geom(k);
+    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
+    CUtensorMap* m = new CUtensorMap;
+    const uint64_t dims[5] = {(uint64_t)kTcBlk * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};
+    const uint64_t strides[4] = {(uint64_t)kTcBlk * 8 * 2, (uint64_t)g.nj * kTcBlk * 8 * 2,
+                                 (uint64_t)g.nwin * g.nj * kTcBlk * 8 * 2, (uint64_t)wk_hl * 2};
+    const uint32_t box[5] = {(uint32_t)kTcBlk * 8, (uint32_t)kTcRows, (uint32_t)g.nwin, 1, 2};
+    if (!make_tmap_5d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, dims, strides, box)) {
+        delete m;
+        return cudaErrorInvalidValue;
+    }
+    *map_out = m;
+    return cudaSuccess;
+}
+
+// K10 weights of the transport-cost table rho^2 exp(-rho^2/eps) (se2_transport_cost, NEXT #2): same
+// layout as the Gibbs weights, built on the first cost evaluation after k->Wcl is tabulated
+cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s) {
+    if (k->tc_w == nullptr || k->tc_wc != nullptr || k->Wcl == nullptr) return cudaSuccess;
+    const TcGeom g = tc_geom(k);
+    cudaError_t e = cudaMalloc(&k->tc_wc, 2 * k->tc_w_hl * sizeof(__nv_bfloat16));
+    if (e != cudaSuccess) return e;
+    e = tc_weight_map(k, k->tc_wc, &k->tc_wcmap);
+    if (e != cudaSuccess) return e;
+    tc_split_weights_kernel<<<592, 256, 0, s>>>(k->Wcl, reinterpret_cast<__nv_bfloat16*>(k->tc_wc), k->tc_w_hl, k->nt,
+                                                k->S, g.nch, g.nwin, g.nj, g.nblk);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     if (!conv_tc_eligible(k)) return cudaSuccess;
     const TcGeom g = tc_geom(k);
@@ -443,18 +475,8 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
         const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
     }
-    {
-        CUtensorMap* m = new CUtensorMap;
-        const uint64_t dims[5] = {(uint64_t)kTcBlk * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};
-        const uint64_t strides[4] = {(uint64_t)kTcBlk * 8 * 2, (uint64_t)g.nj * kTcBlk * 8 * 2,
-                                     (uint64_t)g.nwin * g.nj * kTcBlk * 8 * 2, (uint64_t)wk_hl * 2};
-        const uint32_t box[5] = {(uint32_t)kTcBlk * 8, (uint32_t)kTcRows, (uint32_t)g.nwin, 1, 2};
-        if (!make_tmap_5d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, k->tc_w, dims, strides, box)) {
-            delete m;
-            return cudaErrorInvalidValue;
-        }
-        k->tc_wmap = m;
-    }
+    e = tc_weight_map(k, k->tc_w, &k->tc_wmap);
+    if (e != cudaSuccess) return e;
     tc_split_weights_kernel<<<592, 256>>>(k->Wl, reinterpret_cast<__nv_bfloat16*>(k->tc_w), wk_hl, k->nt, k->S, g.nch,
                                           g.nwin, g.nj, g.nblk);
     count_launch();
@@ -473,7 +495,9 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
 
 void conv_tc_release(se2_kernel_s* k) {
     delete reinterpret_cast<CUtensorMap*>(k->tc_wmap);
-    k->tc_wmap = nullptr;
+    delete reinterpret_cast<CUtensorMap*>(k->tc_wcmap);
+    if (k->tc_wc) cudaFree(k->tc_wc);
+    k->tc_wmap = k->tc_wcmap = k->tc_wc = nullptr;
 }
 
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
@@ -484,7 +508,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     count_launch();
     TcArgs a;
     a.xk = xk;
-    a.wk = reinterpret_cast<const __nv_bfloat16*>(k->tc_w);
+    const bool cost = epi.table != nullptr;   // the transport-cost table (launch only when tc_wc exists)
+    a.wk = reinterpret_cast<const __nv_bfloat16*>(cost ? k->tc_wc : k->tc_w);
     a.xk_hl = k->tc_x_hl;
     a.wk_hl = k->tc_w_hl;
     a.nx = k->nx; a.ny = k->ny; a.nt = k->nt; a.R = k->R; a.S = k->S;
@@ -495,7 +520,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.rows_out = tc_rows_out(k);
     dim3 grid((k->ny + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_tc_kernel<<<grid, kTcThreads, g.smem, s>>>(a, epi, *reinterpret_cast<const CUtensorMap*>(k->tc_wmap));
+    conv_tc_kernel<<<grid, kTcThreads, g.smem, s>>>(a, epi, *reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmap : k->tc_wmap));
     count_launch();
     return cudaGetLastError();
 }

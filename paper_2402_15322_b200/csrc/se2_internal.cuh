@@ -130,6 +130,8 @@ struct se2_kernel_s {
     void* tc_x = nullptr;
     size_t tc_w_hl = 0, tc_x_hl = 0;
     void* tc_wmap = nullptr;      // CUtensorMap (5-D) over tc_w: one TMA per weight stage
+    void* tc_wc = nullptr;        // the same for the transport-cost table Wcl (built with it)
+    void* tc_wcmap = nullptr;
     bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
@@ -148,6 +150,7 @@ int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain, uint32_t flags
 bool conv_tc_eligible(const se2_kernel_s* k);
 cudaError_t conv_tc_prepare(se2_kernel_s* k);
 void conv_tc_release(se2_kernel_s* k);
+cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s);
 int conv_blocks_per_field_tc(const se2_kernel_s* k);
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
                            int* bpf);
@@ -155,6 +158,12 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
 // conv_tc.cu); SE2_LIN_FFMA forces K2
 inline bool conv_tc_active(const se2_kernel_s* k, uint32_t flags) {
     return k->tc_w != nullptr && (flags & SE2_LIN_FFMA) == 0 && (k->tc_fast || (flags & SE2_LIN_TC) != 0);
+}
+// a linear conv with this epilogue runs on K10: the Gibbs table, or the cost table once its K10
+// weights exist
+inline bool conv_tc_route(const se2_kernel_s* k, uint32_t flags, const Epilogue& epi) {
+    if (!conv_tc_active(k, flags)) return false;
+    return epi.table == nullptr || (epi.table == k->Wcl && k->tc_wc != nullptr);
 }
 int conv_blocks_per_field_linear(const se2_kernel_s* k);
 int conv_blocks_per_field_lse(const se2_kernel_s* k);

@@ -312,19 +312,25 @@ def test_bary_pieces(cuda_device):
     np.testing.assert_allclose(_host(lv_t), lv + (ref[None] - ld), rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("log_domain", [False, True], ids=["linear", "log"])
+@pytest.mark.parametrize("log_domain", [False, True, "tc", "ffma"], ids=["linear", "log", "linear-tc", "linear-ffma"])
 @pytest.mark.parametrize("grid", [(28, 28, 16, 0.02, (1.0, 3.0, 1.0), 5), (37, 23, 12, 0.02, (1.0, 3.0, 1.0), 5)],
                          ids=["c1grid", "ragged"])
 def test_transport_cost(grid, log_domain, cuda_device):
+    """linear-tc / linear-ffma force K10 (tensor cores, cost-table weights) / K2 on the linear path."""
     from paper_2402_15322_b200 import se2_transport_cost
     nx, ny, nt, eps, w, R = grid
+    engine = log_domain if isinstance(log_domain, str) else None
+    flags = {"tc": L.SE2_LIN_TC, "ffma": L.SE2_LIN_FFMA}.get(engine, 0)
+    log_domain = log_domain is True
     k = _kernel(nx, ny, nt, eps, w, R, 2)
+    if engine == "tc" and not k.has_tensor_cores:
+        pytest.skip("grid not covered by K10 (ntheta % 16 != 0)")
     g = O.Grid(nx, ny, nt)
     shape = (2, nt, ny, nx)
     a = S.random_positive_field(shape, seed=41, log_range=10.0)
     b = S.random_positive_field(shape, seed=42, log_range=10.0)
     ain, bin_ = (np.log(a), np.log(b)) if log_domain else (a, b)
-    got = se2_transport_cost(k, _dev(ain), _dev(bin_), log_domain)
+    got = se2_transport_cost(k, _dev(ain), _dev(bin_), log_domain, engine_flags=flags)
     Tc = O.cost_table(g, R, eps, w)
     ref = [O.transport_cost(Tc, a[i].astype(np.float64), b[i].astype(np.float64)) for i in range(2)]
     np.testing.assert_allclose(got, ref, rtol=2e-5)
