@@ -29,7 +29,11 @@ def test_sharded_barycenter_single_rank(cuda_device):
     assert measure_err(np.exp(lbar), ref["bary"]) < 1e-4
 
 
-def test_slab_jko_single_rank(cuda_device):
+@pytest.mark.parametrize("engine", ["default", "tc"])
+def test_slab_jko_single_rank(engine, cuda_device, monkeypatch):
+    """engine tc: K10 made the default linear engine of the slab kernels (SE2_TC_DEFAULT=1 at build)."""
+    if engine == "tc":
+        monkeypatch.setenv("SE2_TC_DEFAULT", "1")
     from paper_2402_15322_b200 import Kernel, make_prox
     from paper_2402_15322_b200.parallel import CudaOps, SlabJKO
     nx, ny, nt, R, eps, tau = 48, 40, 16, 4, 0.003, 1e-3
@@ -39,6 +43,7 @@ def test_slab_jko_single_rank(cuda_device):
     mu = (mu / mu.sum()).astype(np.float32)
     # slab kernel: the grid plus R halo rows on each side, global cell sizes (R1)
     k = Kernel(nx, ny + 2 * R, nt, eps, (1, 3, 1), R, hx=1.0 / nx, hy=1.0 / ny)
+    assert k.uses_tensor_cores == (engine == "tc")
     prox = make_prox(k, tau, global_ny=ny, row_offset=-R)
     drv = SlabJKO(CudaOps(k, False), torch.from_numpy(mu).cuda(), R, prox)
     masses = [drv.step(50) for _ in range(2)]
@@ -105,13 +110,16 @@ def test_sharded_barycenter_fused_exchange_single_rank(exchange, cuda_device):
     assert measure_err(np.exp(lbar), ref["bary"]) < 1e-4
 
 
+@pytest.mark.parametrize("engine", ["default", "tc"])
 @pytest.mark.parametrize("split", [(21,), (13, 11)], ids=["2-slabs", "3-slabs"])
-def test_slab_jko_peer_halos_simulated_ranks(split, cuda_device):
+def test_slab_jko_peer_halos_simulated_ranks(split, engine, cuda_device, monkeypatch):
     """se2_conv_update_slab: each slab's conv stores its owned rows and writes its boundary rows straight
     into the neighbours' halo rows (what peer-mapped memory gives across GPUs).  Here the slabs of 2 or
     3 'ranks' live on one GPU and run one after the other on one stream (stream order stands in for the
     cross-rank barrier -- no kernel waits on another); 2 JKO steps x 50 iterations against the
     unsharded oracle."""
+    if engine == "tc":      # K10 as the slab kernels' default engine: its epilogue writes the peer halos
+        monkeypatch.setenv("SE2_TC_DEFAULT", "1")
     from paper_2402_15322_b200 import Kernel, make_prox
     from paper_2402_15322_b200 import _lib as Lb
     from paper_2402_15322_b200.api import se2_conv_update, se2_sum_rows, se2_scale_rows
@@ -174,9 +182,12 @@ def test_slab_jko_peer_halos_simulated_ranks(split, cuda_device):
     np.testing.assert_allclose(masses, ref["masses"], rtol=1e-4)
 
 
-def test_slab_jko_p2p_single_rank(cuda_device):
+@pytest.mark.parametrize("engine", ["default", "tc"])
+def test_slab_jko_p2p_single_rank(engine, cuda_device, monkeypatch):
     """SlabJKO with the peer-memory halo path (symmetric memory slabs, se2_conv_update_slab, a device
-    barrier after each conv) on a 1-rank NCCL group, against the oracle."""
+    barrier after each conv) on a 1-rank NCCL group, against the oracle; tc: K10 as the slab engine."""
+    if engine == "tc":
+        monkeypatch.setenv("SE2_TC_DEFAULT", "1")
     from paper_2402_15322_b200 import Kernel, make_prox
     from paper_2402_15322_b200.parallel import CudaOps, SlabJKO
     _one_rank_group()
@@ -186,6 +197,7 @@ def test_slab_jko_p2p_single_rank(cuda_device):
     mu = (rng.random(g.shape) + 0.05)
     mu = (mu / mu.sum()).astype(np.float32)
     k = Kernel(nx, ny + 2 * R, nt, eps, (1, 3, 1), R, hx=1.0 / nx, hy=1.0 / ny)
+    assert k.uses_tensor_cores == (engine == "tc")
     prox = make_prox(k, tau, global_ny=ny, row_offset=-R)
     drv = SlabJKO(CudaOps(k, False), torch.from_numpy(mu).cuda(), R, prox, exchange="p2p")
     masses = [drv.step(50) for _ in range(2)]
