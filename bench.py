@@ -40,24 +40,32 @@ WORKLOADS = {
 
 
 def _tc_executed_flop(cfg, R, batch=1):
-    """MMA flops K10 executes per launch (3 BF16 passes over the dense theta window, every input row of
-    each 8-row group, N = nx rounded up to 16): the 'executed' rate next to the algorithmic one."""
+    """MMA flops K10 executes per launch (3 BF16 passes over the dense theta window, N = nx rounded up to
+    16): the 'executed' rate next to the algorithmic one.  Mirrors conv_tc.cu's geometry choice: the
+    balanced mode (8-row tiles, chain units spread evenly over 148 CTAs) when its per-SM chain is below
+    0.95 of the row-count mode's, else tc_rows_out's output rows per CTA (max_batch = batch)."""
     npad = (cfg.nx + 15) // 16 * 16
     nwin = min(cfg.ntheta // 8, 4)
     nblk = cfg.ntheta // 16
     S_ = 2 * R + 1
-    # output rows per CTA as conv_tc.cu's tc_rows_out picks them (max_batch = batch)
+    per_row = S_ * (nwin // 2) * 3 * 2.0 * 128 * npad * 16
+
+    def chain(y0, rows):
+        return min(cfg.ny - 1, y0 + rows - 1 + R) - max(0, y0 - R) + 1
+
     best, rows_out = None, 8
     for rows in range(8, 3, -1):
         ctas = -(-cfg.ny // rows) * nblk * batch
         cost = -(-ctas // 148) * min(cfg.ny, rows + 2 * R)
         if best is None or cost < best:
             best, rows_out = cost, rows
-    total = 0
-    for y0 in range(0, cfg.ny, rows_out):
-        nrows = min(cfg.ny - 1, y0 + rows_out - 1 + R) - max(0, y0 - R) + 1
-        total += nrows * S_ * (nwin // 2) * 3
-    return total * nblk * batch * 2.0 * 128 * npad * 16
+    ug = sum(chain(y0, 8) for y0 in range(0, cfg.ny, 8))
+    lmax = max(chain(y0, 8) for y0 in range(0, cfg.ny, 8))
+    q = max(-(-batch * nblk * ug // 148), (lmax + 1) // 2)
+    if q < 0.95 * best:                      # balanced mode
+        return batch * nblk * ug * per_row
+    total = sum(chain(y0, rows_out) for y0 in range(0, cfg.ny, rows_out))
+    return total * nblk * batch * per_row
 
 
 def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, conv_ms, dev_ms, ffma_peak, sm_max,
@@ -85,7 +93,7 @@ def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, con
                                       "stays at max through the step (clocks.sm_mhz), while the sustained figure was "
                                       "measured at a power-capped clock",
                 "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the dense 32-orientation window and "
-                                 "the rows + 2R input rows of each CTA's row group (M tile 128): executed / algorithmic = "
+                                 "the 8 + 2R input rows of each 8-row tile (M tile 128): executed / algorithmic = "
                                  f"{_tc_executed_flop(cfg, cfg.R) / flop_per_conv:.1f}",
                 "vs_ffma_roofline": achieved / ffma_peak, **common}
     return {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "peak": ffma_peak,

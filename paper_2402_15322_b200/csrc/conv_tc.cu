@@ -118,7 +118,69 @@ struct TcArgs {
     uint32_t a_stage, b_stage;
     int tmem_cols;
     int rows_out;              // output rows a CTA owns (<= kTcRows; the M tile's remaining rows are discarded)
+    // balanced mode (PIECES): 8-row tiles, CTA c takes chain units [c q, (c + 1) q) of the concatenated
+    // (tile, input row) list; every piece's sums go to `part` [tile][piece < 3][128][npad]
+    int batch, nblk, ngroups, ug, q;
+    float* part;
 };
+
+// chain length (input rows) of 8-row group g, and the units before it within one (field, block)
+__device__ __forceinline__ int tc_group_len(const TcArgs& a, int g) {
+    const int y0 = g * kTcRows;
+    return min(a.ny - 1, y0 + kTcRows - 1 + a.R) - max(0, y0 - a.R) + 1;
+}
+__device__ __forceinline__ int tc_group_prefix(const TcArgs& a, int g) {
+    int s = 0;
+    for (int i = 0; i < g; ++i) s += tc_group_len(a, i);
+    return s;
+}
+
+struct TcPiece {
+    int b, blk, y0, ylo;   // field, orientation block, first output row, first input row of the tile's chain
+    int r0, r1;            // this piece: chain rows [r0, r1) (input rows ylo + r0 ...)
+    int tile, p;           // tile index (field, block, group) and the piece's index within the tile
+};
+
+// piece k of this CTA; false when the CTA has fewer pieces
+template <bool PIECES>
+__device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
+    if (!PIECES) {
+        if (k > 0) return false;
+        pc.y0 = blockIdx.x * a.rows_out;
+        pc.blk = blockIdx.y;
+        pc.b = blockIdx.z;
+        pc.ylo = max(0, pc.y0 - a.R);
+        pc.r0 = 0;
+        pc.r1 = min(a.ny - 1, pc.y0 + a.rows_out - 1 + a.R) - pc.ylo + 1;
+        pc.tile = 0;
+        pc.p = 0;
+        return true;
+    }
+    const int U = a.batch * a.nblk * a.ug;
+    const int c = blockIdx.x;
+    const int uend = min(U, (c + 1) * a.q);
+    int u = c * a.q;
+    for (int kk = 0; u < uend; ++kk) {
+        const int grp = u / a.ug, rem = u - grp * a.ug;
+        int g = 0, pre = 0;
+        while (pre + tc_group_len(a, g) <= rem) { pre += tc_group_len(a, g); ++g; }
+        const int st = grp * a.ug + pre, len = tc_group_len(a, g);
+        const int r1 = min(len, uend - st);
+        if (kk == k) {
+            pc.b = grp / a.nblk;
+            pc.blk = grp - pc.b * a.nblk;
+            pc.y0 = g * kTcRows;
+            pc.ylo = max(0, pc.y0 - a.R);
+            pc.r0 = u - st;
+            pc.r1 = r1;
+            pc.tile = grp * a.ngroups + g;
+            pc.p = c - st / a.q;
+            return true;
+        }
+        u = st + r1;
+    }
+    return false;
+}
 
 // input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]
 __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl,
@@ -179,22 +241,17 @@ __global__ void tc_split_weights_kernel(const float* __restrict__ Wl, __nv_bfloa
     }
 }
 
+template <bool PIECES>
 __global__ void __launch_bounds__(kTcThreads, 1)
 conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap) {
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sB = smem;                                   // [2][hl][nwin][nxp][16 B]
     unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwin][8 j][16 to][16 B]
-    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone, flushed;
+    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone, flushed, cflushed;
     __shared__ uint32_t tmem_base;
     __shared__ float sRed[kTcThreads / 32];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int y0 = blockIdx.x * a.rows_out;
-    const int blk = blockIdx.y;
-    const int b = blockIdx.z;
-    const int ylo = max(0, y0 - a.R), yhi = min(a.ny - 1, y0 + a.rows_out - 1 + a.R);
-    const int nrows = yhi - ylo + 1;
-    const int chunk0 = tc_chunk0(blk, a.nch, a.nwin);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -206,6 +263,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
         for (int i = 0; i < kTcNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
         mbar_init(&rowdone, 1);
         mbar_init(&flushed, kTcFlushWarps);
+        mbar_init(&cflushed, kTcFlushWarps);
         mbar_fence_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -218,13 +276,14 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     if (warp == 0) {
       if (lane == 0) {
         // ---------------- producer ----------------
-        auto load_b = [&](int yy) {
-            const int st = yy & 1;
-            if (yy >= 2) tc_wait(&emptyB[st], (uint32_t)(((yy >> 1) - 1) & 1));
+        // global input-row counter gr (all pieces of this CTA): B ring stage gr & 1, weight stage (gr S + dxi)
+        auto load_b = [&](int gr, const TcPiece& pc, int yi) {
+            const int st = gr & 1;
+            if (gr >= 2) tc_wait(&emptyB[st], (uint32_t)(((gr >> 1) - 1) & 1));
             mbar_expect_tx(&fullB[st], a.b_stage);
-            const int yi = ylo + yy;
+            const int chunk0 = tc_chunk0(pc.blk, a.nch, a.nwin);
             for (int hl = 0; hl < 2; ++hl) {
-                const __nv_bfloat16* row = a.xk + hl * a.xk_hl + ((size_t)b * a.ny + yi) * row_elems;
+                const __nv_bfloat16* row = a.xk + hl * a.xk_hl + ((size_t)pc.b * a.ny + yi) * row_elems;
                 for (int c = 0; c < a.nwin; ++c) {
                     const int ch = (chunk0 + c) % a.nch;
                     bulk_load(sB + st * (size_t)a.b_stage + (size_t)(hl * a.nwin + c) * chunk_bytes_b,
@@ -232,21 +291,29 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 }
             }
         };
-        load_b(0);
         const int b_after = min(kTcNA - 1, a.S - 1);
         const uint32_t sA_u = smem_u32(sA), fullA_u = smem_u32(&fullA[0]);
         const CUtensorMap* wm = &wmap;
-        for (int yy = 0; yy < nrows; ++yy) {
-            const int yi = ylo + yy;
-            const int j0 = y0 + a.R - yi + 7;
-            for (int dxi = 0; dxi < a.S; ++dxi) {
-                const int t = yy * a.S + dxi;
-                const int st = t % kTcNA;
-                if (t >= kTcNA) tc_wait(&emptyA[st], (uint32_t)(((t / kTcNA) - 1) & 1));
-                mbar_expect_tx(&fullA[st], a.a_stage);
-                // one TMA box per stage: [hl 2][chunk nwin][j 8][16 to x 8 ti]
-                tma_load_5d(sA_u + (uint32_t)st * a.a_stage, wm, fullA_u + 8u * (uint32_t)st, 0, j0, 0, blk * a.S + dxi, 0);
-                if (dxi == b_after && yy + 1 < nrows) load_b(yy + 1);
+        TcPiece pc, pn;
+        int gr = 0;
+        if (tc_piece<PIECES>(a, 0, pc)) load_b(0, pc, pc.ylo + pc.r0);
+        for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
+            for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
+                const int yi = pc.ylo + rr;
+                const int j0 = pc.y0 + a.R - yi + 7;
+                for (int dxi = 0; dxi < a.S; ++dxi) {
+                    const int t = gr * a.S + dxi;
+                    const int st = t % kTcNA;
+                    if (t >= kTcNA) tc_wait(&emptyA[st], (uint32_t)(((t / kTcNA) - 1) & 1));
+                    mbar_expect_tx(&fullA[st], a.a_stage);
+                    // one TMA box per stage: [hl 2][chunk nwin][j 8][16 to x 8 ti]
+                    tma_load_5d(sA_u + (uint32_t)st * a.a_stage, wm, fullA_u + 8u * (uint32_t)st, 0, j0, 0,
+                                pc.blk * a.S + dxi, 0);
+                    if (dxi == b_after) {   // the next input row (this piece's, or the next piece's first)
+                        if (rr + 1 < pc.r1) load_b(gr + 1, pc, yi + 1);
+                        else if (tc_piece<PIECES>(a, k + 1, pn)) load_b(gr + 1, pn, pn.ylo + pn.r0);
+                    }
+                }
             }
         }
       }
@@ -286,25 +353,34 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             }
             tc_commit(&emptyA[st]);
         };
-        for (int yy = 0; yy < nrows; ++yy) {
-            const int stb = yy & 1;
-            tc_wait(&fullB[stb], (uint32_t)((yy >> 1) & 1));
-            // The main accumulator restarts every input row and the accumulator warps must first have read
-            // the previous row's sums: the correction MMAs of the row's first P stages (the whole weight
-            // ring) are issued before that wait so the tensor pipe stays busy during the flush.
-            const int P = yy > 0 ? min(kTcNA, a.S) : 0;
-            for (int dxi = 0; dxi < P; ++dxi) issue_corr(yy * a.S + dxi, stb, dxi);
-            if (yy > 0) {
-                tc_wait(&flushed, (uint32_t)((yy - 1) & 1));
+        TcPiece pc;
+        int gr = 0;
+        for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
+            if (k > 0) {   // the correction accumulator restarts per piece: the previous piece's was read
+                tc_wait(&cflushed, (uint32_t)((k - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                acc_c = 0;
             }
-            for (int dxi = 0; dxi < P; ++dxi) issue_main(yy * a.S + dxi, stb, dxi);
-            for (int dxi = P; dxi < a.S; ++dxi) {
-                issue_corr(yy * a.S + dxi, stb, dxi);
-                issue_main(yy * a.S + dxi, stb, dxi);
+            for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
+                const int stb = gr & 1;
+                tc_wait(&fullB[stb], (uint32_t)((gr >> 1) & 1));
+                // The main accumulator restarts every input row and the accumulator warps must first have
+                // read the previous row's sums: the correction MMAs of the row's first P stages (the whole
+                // weight ring) are issued before that wait so the tensor pipe stays busy during the flush.
+                const int P = gr > 0 ? min(kTcNA, a.S) : 0;
+                for (int dxi = 0; dxi < P; ++dxi) issue_corr(gr * a.S + dxi, stb, dxi);
+                if (gr > 0) {
+                    tc_wait(&flushed, (uint32_t)((gr - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                for (int dxi = 0; dxi < P; ++dxi) issue_main(gr * a.S + dxi, stb, dxi);
+                for (int dxi = P; dxi < a.S; ++dxi) {
+                    issue_corr(gr * a.S + dxi, stb, dxi);
+                    issue_main(gr * a.S + dxi, stb, dxi);
+                }
+                tc_commit(&emptyB[stb]);
+                tc_commit(&rowdone);
             }
-            tc_commit(&emptyB[stb]);
-            tc_commit(&rowdone);
         }
       }
       __syncwarp();
@@ -316,17 +392,46 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     const int pitch = a.npad + 1;
     float err = 0.f;
     const int half = a.npad / 2;
+    TcPiece pc;
     if (warp >= 2) {
         const int q = warp & 3, h = (warp - 2) >> 2;        // TMEM lane quarter (warp % 4) and column half
         const int m = 32 * q + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * half);
-        float sum[128];
+        int gr = 0;
+        for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
+            float sum[128];
 #pragma unroll
-        for (int j = 0; j < 128; ++j) sum[j] = 0.f;
-        for (int yy = 0; yy < nrows; ++yy) {
-            tc_wait(&rowdone, (uint32_t)(yy & 1));
-            __syncwarp();
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+            for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
+                tc_wait(&rowdone, (uint32_t)(gr & 1));
+                __syncwarp();
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int c = 0; c < 128; c += 32) {
+                    if (c < half) {
+                        uint32_t v[32];
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                            : "r"(tl + (uint32_t)c));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&flushed)) : "memory");
+            }
+            // the correction accumulator (complete with the piece's last row commit)
+            const uint32_t tc2 = tl + (uint32_t)(a.tmem_cols / 2);
+            float* prow = PIECES ? a.part + ((size_t)pc.tile * 3 + pc.p) * 128 * a.npad + (size_t)m * a.npad + h * half
+                                 : nullptr;
 #pragma unroll
             for (int c = 0; c < 128; c += 32) {
                 if (c < half) {
@@ -339,58 +444,85 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                           "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
                           "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
                           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                        : "r"(tl + (uint32_t)c));
+                        : "r"(tc2 + (uint32_t)c));
                     asm volatile("tcgen05.wait::ld.sync.aligned;");
+                    if (PIECES) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+                        for (int j = 0; j < 32; j += 4)
+                            if (c + j < half)
+                                *reinterpret_cast<float4*>(prow + c + j) =
+                                    make_float4(sum[c + j] + __uint_as_float(v[j]), sum[c + j + 1] + __uint_as_float(v[j + 1]),
+                                                sum[c + j + 2] + __uint_as_float(v[j + 2]),
+                                                sum[c + j + 3] + __uint_as_float(v[j + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c + j < half) T[m * pitch + h * half + c + j] = sum[c + j] + __uint_as_float(v[j]);
+                    }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&flushed)) : "memory");
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&cflushed)) : "memory");
         }
-        // the correction accumulator (complete with the last row's commit), then out through shared memory
-        const uint32_t tc2 = tl + (uint32_t)(a.tmem_cols / 2);
-#pragma unroll
-        for (int c = 0; c < 128; c += 32) {
-            if (c < half) {
-                uint32_t v[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(tc2 + (uint32_t)c));
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c + j < half) T[m * pitch + h * half + c + j] = sum[c + j] + __uint_as_float(v[j]);
+    }
+    if (!PIECES) {
+        __syncthreads();   // T complete (every warp reaches this; the role warps have finished their loops)
+        tc_piece<false>(a, 0, pc);
+        if (warp >= 2) {
+            const int64_t N = (int64_t)a.nx * a.ny * a.nt;
+            const int f = warp - 2;
+            for (int mm = 0; mm < 128 / kTcFlushWarps; ++mm) {
+                const int m = (128 / kTcFlushWarps) * f + mm;
+                const int r = m / kTcBlk, tol = m % kTcBlk;
+                const int y = pc.y0 + r, to = pc.blk * kTcBlk + tol;
+                if (y >= a.ny || r >= a.rows_out) continue;
+                const int64_t rowbase = (int64_t)pc.b * N + ((int64_t)to * a.ny + y) * a.nx;
+                for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
             }
         }
-    }
-    __syncthreads();   // T complete (every warp reaches this; the role warps have finished their loops)
-    if (warp >= 2) {
-        const int64_t N = (int64_t)a.nx * a.ny * a.nt;
-        const int f = warp - 2;
-        for (int mm = 0; mm < 128 / kTcFlushWarps; ++mm) {
-            const int m = (128 / kTcFlushWarps) * f + mm;
-            const int r = m / kTcBlk, tol = m % kTcBlk;
-            const int y = y0 + r, to = blk * kTcBlk + tol;
-            if (y >= a.ny || r >= a.rows_out) continue;
-            const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
-            for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
+        if (epi.err_partial != nullptr) {
+            const float t = block_sum<kTcThreads>(err, sRed);
+            if (tid == 0)
+                epi.err_partial[(int64_t)pc.b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
         }
-    }
-    if (epi.err_partial != nullptr) {
-        const float t = block_sum<kTcThreads>(err, sRed);
-        if (tid == 0) epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+}
+
+// balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
+// one block per (8-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
+__global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
+    __shared__ float sRed[8];
+    __shared__ int sNp;
+    const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
+    const int blk = to / kTcBlk, grp = b * a.nblk + blk;
+    if (threadIdx.x == 0) {
+        const int st = grp * a.ug + tc_group_prefix(a, g), len = tc_group_len(a, g);
+        sNp = (st + len - 1) / a.q - st / a.q + 1;
+    }
+    __syncthreads();
+    const int np = sNp;
+    const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * 3) * 128 * a.npad;
+    const int64_t N = (int64_t)a.nx * a.ny * a.nt;
+    float err = 0.f;
+    for (int r = 0; r < kTcRows; ++r) {
+        const int y = g * kTcRows + r;
+        if (y >= a.ny) break;
+        const float* src = tile + (size_t)(r * kTcBlk + (to % kTcBlk)) * a.npad;
+        const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
+        for (int x = threadIdx.x; x < a.nx; x += blockDim.x) {
+            float v = src[x];
+            for (int p = 1; p < np; ++p) v += src[(size_t)p * 128 * a.npad + x];
+            err += apply_epilogue<false>(epi, rowbase + x, x, y, v);
+        }
+    }
+    if (epi.err_partial != nullptr) {
+        const float t = block_sum<256>(err, sRed);
+        if (threadIdx.x == 0) epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + (int64_t)to * gridDim.x + g] = t;
+    }
 }
 
 }  // namespace
@@ -416,7 +548,31 @@ static int tc_rows_out(const se2_kernel_s* k) {
     return best;
 }
 
+// balanced mode geometry (host mirror of tc_group_len / tc_group_prefix)
+static int tc_group_len_h(const se2_kernel_s* k, int g) {
+    const int y0 = g * kTcRows;
+    return std::min(k->ny - 1, y0 + kTcRows - 1 + k->R) - std::max(0, y0 - k->R) + 1;
+}
+static void tc_units(const se2_kernel_s* k, int batch, int* ug, int* lmax, long long* U) {
+    const int ngroups = (k->ny + kTcRows - 1) / kTcRows;
+    *ug = 0;
+    *lmax = 0;
+    for (int g = 0; g < ngroups; ++g) {
+        *ug += tc_group_len_h(k, g);
+        *lmax = std::max(*lmax, tc_group_len_h(k, g));
+    }
+    *U = (long long)batch * (k->nt / kTcBlk) * (*ug);
+}
+// units per CTA in the balanced mode: ceil(U / 148), at least half the longest chain (<= 3 pieces per tile)
+static int tc_units_per_cta(const se2_kernel_s* k, int batch) {
+    int ug, lmax;
+    long long U;
+    tc_units(k, batch, &ug, &lmax, &U);
+    return (int)std::max<long long>((U + 147) / 148, (lmax + 1) / 2);
+}
+
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
+    if (k->tc_part != nullptr) return (k->ny + kTcRows - 1) / kTcRows * k->nt;   // balanced: epilogue blocks
     const int rows = tc_rows_out(k);
     return (k->ny + rows - 1) / rows * (k->nt / kTcBlk);
 }
@@ -475,6 +631,23 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
         const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
     }
+    {
+        // balanced mode (8-row tiles split into equal runs of input rows over 148 CTAs + an epilogue
+        // kernel) when its per-SM chain beats the row-count mode's; decided for max_batch
+        int ug, lmax;
+        long long U;
+        tc_units(k, k->max_batch, &ug, &lmax, &U);
+        const int q = tc_units_per_cta(k, k->max_batch);
+        const int rows = tc_rows_out(k);
+        const double ctas = (double)((k->ny + rows - 1) / rows) * g.nblk * k->max_batch;
+        const double rows_cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
+        const bool want = getenv("SE2_TC_PIECES") ? (atoi(getenv("SE2_TC_PIECES")) != 0) : (q < 0.95 * rows_cost);
+        if (want) {
+            const size_t tiles = (size_t)k->max_batch * g.nblk * ((k->ny + kTcRows - 1) / kTcRows);
+            e = cudaMalloc(&k->tc_part, tiles * 3 * 128 * g.npad * sizeof(float));
+            if (e != cudaSuccess) return e;
+        }
+    }
     e = tc_weight_map(k, k->tc_w, &k->tc_wmap);
     if (e != cudaSuccess) return e;
     tc_split_weights_kernel<<<592, 256>>>(k->Wl, reinterpret_cast<__nv_bfloat16*>(k->tc_w), wk_hl, k->nt, k->S, g.nch,
@@ -484,11 +657,15 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     int optin = 0;
     cudaFuncAttributes fa;
     e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, k->device);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, conv_tc_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, conv_tc_kernel<false>);
     if (e != cudaSuccess) return e;
     const int dyn_max = optin - (int)fa.sharedSizeBytes;
     if ((int)g.smem > dyn_max) return cudaErrorInvalidValue;
-    e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+    e = cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, conv_tc_kernel<true>);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -497,7 +674,9 @@ void conv_tc_release(se2_kernel_s* k) {
     delete reinterpret_cast<CUtensorMap*>(k->tc_wmap);
     delete reinterpret_cast<CUtensorMap*>(k->tc_wcmap);
     if (k->tc_wc) cudaFree(k->tc_wc);
+    if (k->tc_part) cudaFree(k->tc_part);
     k->tc_wmap = k->tc_wcmap = k->tc_wc = nullptr;
+    k->tc_part = nullptr;
 }
 
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
@@ -517,10 +696,31 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.tmem_cols = g.tmem_cols;
+    const CUtensorMap* wm = reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmap : k->tc_wmap);
+    if (k->tc_part != nullptr) {
+        // balanced mode: 8-row tiles, equal runs of chain units per CTA, partials + epilogue kernel
+        long long U;
+        int lmax;
+        tc_units(k, batch, &a.ug, &lmax, &U);
+        a.rows_out = kTcRows;
+        a.batch = batch;
+        a.nblk = g.nblk;
+        a.ngroups = (k->ny + kTcRows - 1) / kTcRows;
+        a.q = tc_units_per_cta(k, batch);
+        a.part = reinterpret_cast<float*>(k->tc_part);
+        const int ncta = (int)((U + a.q - 1) / a.q);
+        conv_tc_kernel<true><<<ncta, kTcThreads, g.smem, s>>>(a, epi, *wm);
+        count_launch();
+        tc_pieces_epilogue_kernel<<<dim3(a.ngroups, k->nt, batch), 256, 0, s>>>(a, epi);
+        count_launch();
+        if (bpf) *bpf = a.ngroups * k->nt;
+        return cudaGetLastError();
+    }
     a.rows_out = tc_rows_out(k);
+    a.part = nullptr;
     dim3 grid((k->ny + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_tc_kernel<<<grid, kTcThreads, g.smem, s>>>(a, epi, *reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmap : k->tc_wmap));
+    conv_tc_kernel<false><<<grid, kTcThreads, g.smem, s>>>(a, epi, *wm);
     count_launch();
     return cudaGetLastError();
 }
