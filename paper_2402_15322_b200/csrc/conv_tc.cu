@@ -495,29 +495,48 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
 // balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
 // one block per (8-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
 __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
-    __shared__ float sRed[8];
+    __shared__ float sRed[32];
     __shared__ int sNp;
     const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
     const int blk = to / kTcBlk, grp = b * a.nblk + blk;
-    if (threadIdx.x == 0) {
-        const int st = grp * a.ug + tc_group_prefix(a, g), len = tc_group_len(a, g);
-        sNp = (st + len - 1) / a.q - st / a.q + 1;
+    if (threadIdx.x < 32) {   // warp 0: the group's unit offset as a strided sum + shuffle reduction
+        int pre = 0;
+        for (int i = threadIdx.x; i < g; i += 32) pre += tc_group_len(a, i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+        if (threadIdx.x == 0) {
+            const int st = grp * a.ug + pre, len = tc_group_len(a, g);
+            sNp = (st + len - 1) / a.q - st / a.q + 1;
+        }
     }
     __syncthreads();
     const int np = sNp;
     const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * 3) * 128 * a.npad;
     const int64_t N = (int64_t)a.nx * a.ny * a.nt;
-    float err = 0.f;
-    for (int r = 0; r < kTcRows; ++r) {
-        const int y = g * kTcRows + r;
-        if (y >= a.ny) break;
-        const float* src = tile + (size_t)(r * kTcBlk + (to % kTcBlk)) * a.npad;
-        const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
-        for (int x = threadIdx.x; x < a.nx; x += blockDim.x) {
-            float v = src[x];
-            for (int p = 1; p < np; ++p) v += src[(size_t)p * 128 * a.npad + x];
-            err += apply_epilogue<false>(epi, rowbase + x, x, y, v);
+    // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r and r + 4
+    const int x0 = (threadIdx.x & 63) * 4, r0 = threadIdx.x >> 6;
+    float4 v[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = r0 + 4 * k;
+        if (x0 >= a.npad) break;   // narrow rows: no load past the row (npad % 16 == 0, so x0 + 3 < npad)
+        const float4* src = reinterpret_cast<const float4*>(tile + (size_t)(r * kTcBlk + (to % kTcBlk)) * a.npad + x0);
+        v[k] = src[0];
+        for (int p = 1; p < np; ++p) {
+            const float4 w = src[(size_t)p * 32 * a.npad];   // 128 * npad floats = 32 * npad float4
+            v[k].x += w.x; v[k].y += w.y; v[k].z += w.z; v[k].w += w.w;
         }
+    }
+    float err = 0.f;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = r0 + 4 * k, y = g * kTcRows + r;
+        if (y >= a.ny || x0 >= a.nx) continue;
+        const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
+        const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (x0 + j < a.nx) err += apply_epilogue<false>(epi, rowbase + x0 + j, x0 + j, y, vv[j]);
     }
     if (epi.err_partial != nullptr) {
         const float t = block_sum<256>(err, sRed);
@@ -626,8 +645,10 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
         const int rows = tc_rows_out(k);
         const double ctas = (double)((k->ny + rows - 1) / rows) * g.nblk;
         const double waves = std::ceil(ctas / 148.0);
-        const double cyc = (double)std::min(k->ny, rows + 2 * k->R) * k->S * (g.nwin / 2) * 3 * (g.npad / 2);
-        const double t10 = waves * cyc / 0.7 / 1.9e9 + 8e-6;
+        const double row_cyc = (double)k->S * (g.nwin / 2) * 3 * (g.npad / 2);   // one input row's MMA chain
+        double t10 = waves * std::min(k->ny, rows + 2 * k->R) * row_cyc / 0.7 / 1.9e9 + 8e-6;
+        // the balanced mode (chosen below when it is cheaper): q input rows per SM + its epilogue pass
+        t10 = std::min(t10, tc_units_per_cta(k, 1) * row_cyc / 0.7 / 1.9e9 + 20e-6);
         const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
     }
