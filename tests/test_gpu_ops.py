@@ -66,9 +66,14 @@ TC_GRIDS = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["auto", "rows"])
 @pytest.mark.parametrize("case", TC_GRIDS, ids=lambda c: c[0])
-def test_conv_tc_parity(case, cuda_device):
-    """K10 forced on grids it covers, against the fp64 oracle (full fields), at TOL_CONV_TC."""
+def test_conv_tc_parity(case, mode, cuda_device, monkeypatch):
+    """K10 forced on grids it covers, against the fp64 oracle (full fields), at TOL_CONV_TC.  auto: the
+    geometry K10 picks (the balanced mode on these grids: pieces of 8-row tiles over the SMs); rows:
+    the rows-per-CTA mode (SE2_TC_PIECES=0 at kernel build)."""
+    if mode == "rows":
+        monkeypatch.setenv("SE2_TC_PIECES", "0")
     name, nx, ny, nt, eps, w, R = case
     assert _kernel(nx, ny, nt, eps, w, R, 2).has_tensor_cores
     _conv_check(name, nx, ny, nt, eps, w, R, False, batch=2, full=True, extra_flags=L.SE2_LIN_TC)
