@@ -21,10 +21,17 @@
 // fp32 accuracy: x = hi + lo with hi = bf16(x), lo = bf16(x - hi) for both operands; the chain adds
 // hi.hi + hi.lo + lo.hi (per-term error <= 3 * 2^-18 relative; simulated on c4m in DESIGN.md).
 //
-// Roles: thread 0 is the TMA producer (bulk copies into a 2-stage input-row ring and an NA-stage
-// weight ring, mbarrier-tracked), thread 32 issues the MMAs and commits each stage back to the
-// producer; the 128 x N fp32 accumulator lives in TMEM.  Epilogue: all 4 warps move TMEM -> shared
-// (transpose) -> the fused epilogue of K2 (apply_epilogue), coalesced along x.
+// Roles (320 threads): warp 0 lane 0 is the TMA producer (an NA-stage weight ring, one 5-D tensor copy
+// per stage, and a 2-stage ring of split input rows, 8 bulk copies per row); warp 1 lane 0 issues the
+// MMAs and commits each stage back; warps 2-9 add every input row's TMEM sums into registers (round to
+// nearest; the tensor core's own accumulation truncates) and read the correction accumulator.
+//
+// Geometry (chosen per kernel for its max_batch):
+//   * rows mode: one CTA per (rows <= 8 output rows, orientation block, field); the epilogue runs in the
+//     kernel through a shared-memory transpose (coalesced along x);
+//   * balanced mode: 8-row tiles; the tiles' input-row chains are concatenated and split into equal runs
+//     over <= 148 CTAs (<= 3 pieces per tile); every piece writes its sums to an L2-resident partial
+//     buffer and tc_pieces_epilogue_kernel adds the pieces in order and applies the fused epilogue.
 #include <cuda_bf16.h>
 
 #include <algorithm>
