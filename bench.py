@@ -89,9 +89,9 @@ def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, con
                                f"long step); dense BF16 is the dtype the MMAs execute",
                 "executed_mma_tflops": executed,
                 "executed_frac": executed / float(peaks.get("bf16_tflops", peak)),
-                "executed_frac_note": "executed MMA rate / the BURST bf16 peak (cuBLAS 8192^3 best of 10): the SM clock "
-                                      "stays at max through the step (clocks.sm_mhz), while the sustained figure was "
-                                      "measured at a power-capped clock",
+                "executed_frac_vs_nominal": executed / (148 * 4096 * 2 * sm_max * 1e6 / 1e12),
+                "executed_frac_note": "executed MMA rate / the BURST bf16 peak (cuBLAS 8192^3 best of 10); "
+                                      "executed_frac_vs_nominal: / 148 SM x 4096 BF16 MAC/cycle x 2 x sm_max_mhz",
                 "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the dense 32-orientation window and "
                                  "the 8 + 2R input rows of each 8-row tile (M tile 128): executed / algorithmic = "
                                  f"{_tc_executed_flop(cfg, cfg.R) / flop_per_conv:.1f}",
