@@ -52,6 +52,9 @@ constexpr int kTcNA = 6;       // weight-ring stages
 // rest interleave main and corrections per K-step, which keeps consecutive MMAs on different TMEM
 // accumulators: 0.579 -> 0.524 ms at c4; 1 early stage measured best, 0.511 ms, against 0/2/4/6)
 constexpr int kTcEarly = 1;
+// input rows per main-accumulator chain (flushed to registers after each): 2 halves the flush bubbles;
+// truncation bound 2 x S x K/16 = 124 steps of 2^-23 at R 15, inside R18
+constexpr int kTcFlushRows = 2;
 constexpr int kTcThreads = 320;   // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: accumulators / epilogue
 constexpr int kTcFlushWarps = 8;
 
@@ -353,19 +356,19 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
             }
         };
-        auto issue_main = [&](int t, int stb, int dxi) {
+        auto issue_main = [&](int t, int stb, int dxi, bool restart) {
             const int st = t % kTcNA;
             const uint32_t offA = (uint32_t)(st * a.a_stage);
             const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
             for (int ks = 0; ks < ksteps; ++ks) {
                 const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048;
                 const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b;
-                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (dxi > 0 || ks > 0) ? 1u : 0u);
+                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (!restart || dxi > 0 || ks > 0) ? 1u : 0u);
             }
             tc_commit(&emptyA[st]);
         };
         // steady state: per K-step main (hi.hi), then the two corrections sharing its A / B operand
-        auto issue_both = [&](int t, int stb, int dxi) {
+        auto issue_both = [&](int t, int stb, int dxi, bool restart) {
             const int st = t % kTcNA;
             tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -376,13 +379,13 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
                 tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);              // A_hi shared with
                 acc_c = 1;
-                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (dxi > 0 || ks > 0) ? 1u : 0u);   // <- B_hi
+                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (!restart || dxi > 0 || ks > 0) ? 1u : 0u);   // <- B_hi
                 tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);                   // shared with
             }
             tc_commit(&emptyA[st]);
         };
         TcPiece pc;
-        int gr = 0;
+        int gr = 0, gs = 0;   // input rows and main-accumulator chains issued so far
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
             if (k > 0) {   // the correction accumulator restarts per piece: the previous piece's was read
                 tc_wait(&cflushed, (uint32_t)((k - 1) & 1));
@@ -392,19 +395,21 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 const int stb = gr & 1;
                 tc_wait(&fullB[stb], (uint32_t)((gr >> 1) & 1));
-                // The main accumulator restarts every input row and the accumulator warps must first have
-                // read the previous row's sums: the correction MMAs of the row's first P stages are issued
-                // before that wait so the tensor pipe stays busy during the flush.
-                const int P = gr > 0 ? min(kTcEarly, a.S) : 0;
+                // The main accumulator restarts every kTcFlushRows input rows of a piece and the
+                // accumulator warps must first have read the previous chain's sums: the correction MMAs
+                // of the row's first P stages are issued before that wait so the tensor pipe stays busy.
+                const bool restart = (rr - pc.r0) % kTcFlushRows == 0;
+                const int P = (restart && gs > 0) ? min(kTcEarly, a.S) : 0;
                 for (int dxi = 0; dxi < P; ++dxi) issue_corr(gr * a.S + dxi, stb, dxi);
-                if (gr > 0) {
-                    tc_wait(&flushed, (uint32_t)((gr - 1) & 1));
+                if (restart && gs > 0) {
+                    tc_wait(&flushed, (uint32_t)((gs - 1) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
                 }
-                for (int dxi = 0; dxi < P; ++dxi) issue_main(gr * a.S + dxi, stb, dxi);
-                for (int dxi = P; dxi < a.S; ++dxi) issue_both(gr * a.S + dxi, stb, dxi);
+                for (int dxi = 0; dxi < P; ++dxi) issue_main(gr * a.S + dxi, stb, dxi, restart);
+                for (int dxi = P; dxi < a.S; ++dxi) issue_both(gr * a.S + dxi, stb, dxi, restart);
                 tc_commit(&emptyB[stb]);
                 tc_commit(&rowdone);
+                if ((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1) ++gs;   // chain end
             }
         }
       }
@@ -429,6 +434,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             for (int j = 0; j < 128; ++j) sum[j] = 0.f;
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 tc_wait(&rowdone, (uint32_t)(gr & 1));
+                if (!((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1)) continue;   // mid-chain
                 __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
