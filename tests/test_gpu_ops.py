@@ -140,6 +140,14 @@ def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse
         assert e < (TOL_CONV_TC if tc else TOL_CONV), (name, tc, e)
 
 
+def test_conv_tc_balanced_batch3(cuda_device):
+    """K10's balanced mode with 3 fields: CTA runs of chain units cross tile and field boundaries, tiles
+    split into up to 3 pieces; full fields against the oracle."""
+    nx, ny, nt, eps, w, R = 72, 90, 32, 0.01, (1.0, 3.0, 1.0), 7
+    assert _kernel(nx, ny, nt, eps, w, R, 3).has_tensor_cores
+    _conv_check("tc-batch3", nx, ny, nt, eps, w, R, False, batch=3, full=True, extra_flags=L.SE2_LIN_TC)
+
+
 @pytest.mark.parametrize("case", CFG_GRIDS + ODD_GRIDS, ids=lambda c: c[0])
 @pytest.mark.parametrize("engine", ["linear", "linear-ffma", "linear-tc", "log"])
 def test_conv_parity(case, engine, cuda_device):
