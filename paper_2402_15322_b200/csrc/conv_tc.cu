@@ -92,6 +92,10 @@ TcGeom tc_geom(const se2_kernel_s* k) {
     return g;
 }
 
+// programmatic dependent launch: block until the preceding kernel in the stream has completed and its
+// writes are visible (a no-op for a normally launched kernel)
+__device__ __forceinline__ void tc_grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
@@ -199,6 +203,7 @@ __device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
 // input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]
 __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl,
                                       int nx, int ny, int nt, int nxp, int batch) {
+    tc_grid_dep_wait();   // reads the previous kernel's output (launched with PDL)
     const int nch = nt / 8;
     const int64_t total = (int64_t)batch * ny * nch * nxp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -310,7 +315,9 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
         const CUtensorMap* wm = &wmap;
         TcPiece pc, pn;
         int gr = 0;
-        if (tc_piece<PIECES>(a, 0, pc)) load_b(0, pc, pc.ylo + pc.r0);
+        // PDL: the weight stages do not depend on the preceding kernels, the input rows do (the split
+        // kernel): B(0) is loaded after the first weight stages, behind the grid-dependency wait
+        bool b0 = false;
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 const int yi = pc.ylo + rr;
@@ -323,6 +330,13 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                     // one TMA box per stage: [hl 2][chunk nwin][j 8][16 to x 8 ti]
                     tma_load_5d(sA_u + (uint32_t)st * a.a_stage, wm, fullA_u + 8u * (uint32_t)st, 0, j0, 0,
                                 pc.blk * a.S + dxi, 0);
+                    if (!b0 && dxi == b_after) {
+                        tc_grid_dep_wait();
+                        TcPiece p0;
+                        tc_piece<PIECES>(a, 0, p0);
+                        load_b(0, p0, p0.ylo + p0.r0);
+                        b0 = true;
+                    }
                     if (dxi == b_after) {   // the next input row (this piece's, or the next piece's first)
                         if (rr + 1 < pc.r1) load_b(gr + 1, pc, yi + 1);
                         else if (tc_piece<PIECES>(a, k + 1, pn)) load_b(gr + 1, pn, pn.ylo + pn.r0);
@@ -424,6 +438,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     const int half = a.npad / 2;
     TcPiece pc;
     if (warp >= 2) {
+        tc_grid_dep_wait();   // partial / output writes after the preceding kernels (PDL launch)
         const int q = warp & 3, h = (warp - 2) >> 2;        // TMEM lane quarter (warp % 4) and column half
         const int m = 32 * q + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * half);
@@ -528,6 +543,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
 __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
     __shared__ int sNp;
+    tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
     const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
     const int blk = to / kTcBlk, grp = b * a.nblk + blk;
     if (threadIdx.x < 32) {   // warp 0: the group's unit offset as a strided sum + shuffle reduction
@@ -735,7 +751,26 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
                            int* bpf) {
     const TcGeom g = tc_geom(k);
     __nv_bfloat16* xk = reinterpret_cast<__nv_bfloat16*>(k->tc_x);
-    tc_split_input_kernel<<<148 * 8, 256, 0, s>>>(in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, batch);
+    // the three K10 kernels are launched with programmatic stream serialization (PDL): each may start
+    // while its predecessor drains and waits (griddepcontrol.wait) before consuming its results
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    auto cfg_of = [&](dim3 grid, dim3 block, size_t smem) {
+        cudaLaunchConfig_t c = {};
+        c.gridDim = grid;
+        c.blockDim = block;
+        c.dynamicSmemBytes = smem;
+        c.stream = s;
+        c.attrs = pdl;
+        c.numAttrs = 1;
+        return c;
+    };
+    {
+        cudaLaunchConfig_t c = cfg_of(dim3(148 * 8), dim3(256), 0);
+        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, batch);
+        if (e != cudaSuccess) return e;
+    }
     count_launch();
     TcArgs a;
     a.xk = xk;
@@ -761,9 +796,17 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         a.q = tc_units_per_cta(k, batch);
         a.part = reinterpret_cast<float*>(k->tc_part);
         const int ncta = (int)((U + a.q - 1) / a.q);
-        conv_tc_kernel<true><<<ncta, kTcThreads, g.smem, s>>>(a, epi, *wm);
+        {
+            cudaLaunchConfig_t c = cfg_of(dim3(ncta), dim3(kTcThreads), g.smem);
+            cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<true>, a, epi, *wm);
+            if (e != cudaSuccess) return e;
+        }
         count_launch();
-        tc_pieces_epilogue_kernel<<<dim3(a.ngroups, k->nt, batch), 256, 0, s>>>(a, epi);
+        {
+            cudaLaunchConfig_t c = cfg_of(dim3(a.ngroups, k->nt, batch), dim3(256), 0);
+            cudaError_t e = cudaLaunchKernelEx(&c, tc_pieces_epilogue_kernel, a, epi);
+            if (e != cudaSuccess) return e;
+        }
         count_launch();
         if (bpf) *bpf = a.ngroups * k->nt;
         return cudaGetLastError();
@@ -772,7 +815,11 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.part = nullptr;
     dim3 grid((k->ny + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_tc_kernel<false><<<grid, kTcThreads, g.smem, s>>>(a, epi, *wm);
+    {
+        cudaLaunchConfig_t c = cfg_of(grid, dim3(kTcThreads), g.smem);
+        cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<false>, a, epi, *wm);
+        if (e != cudaSuccess) return e;
+    }
     count_launch();
     return cudaGetLastError();
 }
