@@ -767,7 +767,9 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         return c;
     };
     {
-        cudaLaunchConfig_t c = cfg_of(dim3(148 * 8), dim3(256), 0);
+        // one (field, row, chunk, pixel) item per thread: all 8 plane loads of every item in flight
+        const long long items = (long long)batch * k->ny * (k->nt / 8) * g.nxp;
+        cudaLaunchConfig_t c = cfg_of(dim3((unsigned)std::min<long long>((items + 255) / 256, 1 << 20)), dim3(256), 0);
         cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, batch);
         if (e != cudaSuccess) return e;
     }
