@@ -81,20 +81,24 @@ def spatial_anisotropy(w):
 
 class Grid:
     """nx x ny x ntheta lattice on [0,1]^2 x [0, 2pi): cell centres x_i = (i + 1/2)/nx,
-    theta_k = 2 pi k / ntheta.  Field arrays are [ntheta][ny][nx]."""
+    theta_k = 2 pi k / ntheta.  Field arrays are [ntheta][ny][nx].
+    hx, hy: cell sizes (default 1/nx, 1/ny, reading R1); a window cut from a finer lattice keeps its
+    cell, x_i = (i + 1/2) hx on [0, nx hx]."""
 
-    def __init__(self, nx: int, ny: int, ntheta: int):
+    def __init__(self, nx: int, ny: int, ntheta: int, hx: float = 0.0, hy: float = 0.0):
         self.nx, self.ny, self.ntheta = int(nx), int(ny), int(ntheta)
+        self.hx = float(hx) if hx else 1.0 / self.nx
+        self.hy = float(hy) if hy else 1.0 / self.ny
 
     @property
     def shape(self):
         return (self.ntheta, self.ny, self.nx)
 
     def x(self, i):
-        return (np.asarray(i, dtype=np.float64) + 0.5) / self.nx
+        return (np.asarray(i, dtype=np.float64) + 0.5) * self.hx
 
     def y(self, j):
-        return (np.asarray(j, dtype=np.float64) + 0.5) / self.ny
+        return (np.asarray(j, dtype=np.float64) + 0.5) * self.hy
 
     def theta(self, k):
         return TWO_PI * np.asarray(k, dtype=np.float64) / self.ntheta
@@ -164,7 +168,21 @@ def dense_kernel_matrix(grid: Grid, R: int, eps: float, w) -> np.ndarray:
 # ----------------------------------------------------------------------------------------------
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libse2oracle.so")
+
+
+def _host_has_avx2() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = f.read()
+        return " avx2" in flags and " fma" in flags
+    except OSError:
+        return False
+
+
+# x86-64-v3 (AVX2) build where the host has it: the x loops vectorise 4-wide.  Same source, same
+# operations per output (contraction off), so both builds give bit-identical results.
+_MARCH = ["-march=x86-64-v3"] if _host_has_avx2() else []
+_LIB_PATH = os.path.join(_HERE, "libse2oracle_v3.so" if _MARCH else "libse2oracle.so")
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -174,8 +192,8 @@ def build_oracle_lib(force: bool = False) -> str:
     src = os.path.join(_HERE, "se2_conv_ref.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99",
-                               "-fno-fast-math", "-o", tmp, src, "-lm"])
+        subprocess.check_call(["gcc", "-O3", *_MARCH, "-fopenmp", "-fPIC", "-shared", "-std=c99",
+                               "-fno-fast-math", "-ffp-contract=off", "-o", tmp, src, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -322,22 +340,25 @@ def sinkhorn(T, L, mu, nu, iters: int, log_domain: bool, trace: bool = True) -> 
     err = []
     if not log_domain:
         b = np.ones_like(mu)
+        Kb = conv(T, b)                      # K b of the current b (reused by the trace and the next a)
         for _ in range(iters):
-            a = mu / np.maximum(conv(T, b), DIV_FLOOR)
+            a = mu / np.maximum(Kb, DIV_FLOOR)
             Kta = conv_adjoint(T, a)
             b = nu / np.maximum(Kta, DIV_FLOOR)
+            Kb = conv(T, b)
             if trace:
-                err.append(marginal_error(a, conv(T, b), mu))
-        Kb = conv(T, b)
+                err.append(marginal_error(a, Kb, mu))
         return dict(a=a, b=b, row=a * Kb, col=b * conv_adjoint(T, a), err=np.array(err))
     lmu, lnu = _log(mu), _log(nu)
     beta = np.zeros_like(mu)
+    lKb = lse_conv(L, beta)
     for _ in range(iters):
-        alpha = _ldiv(lmu, lse_conv(L, beta))
+        alpha = _ldiv(lmu, lKb)
         beta = _ldiv(lnu, lse_conv_adjoint(L, alpha))
+        lKb = lse_conv(L, beta)
         if trace:
-            err.append(float(np.sum(np.abs(np.exp(alpha + lse_conv(L, beta)) - mu))))
-    return dict(alpha=alpha, beta=beta, row=np.exp(alpha + lse_conv(L, beta)),
+            err.append(float(np.sum(np.abs(np.exp(alpha + lKb) - mu))))
+    return dict(alpha=alpha, beta=beta, row=np.exp(alpha + lKb),
                 col=np.exp(beta + lse_conv_adjoint(L, alpha)), err=np.array(err))
 
 
@@ -358,36 +379,40 @@ def barycenter(T, L, mus: Sequence[np.ndarray], lambdas, iters: int, log_domain:
     if not log_domain:
         v = [np.ones_like(mus[0]) for _ in range(n)]
         w = [np.ones_like(mus[0]) for _ in range(n)]
+        Kv = [conv(T, v[i]) for i in range(n)]      # K v_i of the current v_i (trace + next w-update)
         for _ in range(iters):
             mubar = np.ones_like(mus[0])
             d = [None] * n
             for i in range(n):
-                w[i] = mus[i] / np.maximum(conv(T, v[i]), DIV_FLOOR)
+                w[i] = mus[i] / np.maximum(Kv[i], DIV_FLOOR)
                 d[i] = v[i] * conv(T, w[i])
                 if lam[i] != 0.0:
                     mubar = mubar * d[i] ** lam[i]
             for i in range(n):
                 v[i] = v[i] * mubar / np.maximum(d[i], DIV_FLOOR)
+                Kv[i] = conv(T, v[i])
             if trace:
-                e = [float(np.sum(np.abs(w[i] * conv(T, v[i]) - mus[i]))) for i in range(n)]
+                e = [float(np.sum(np.abs(w[i] * Kv[i] - mus[i]))) for i in range(n)]
                 errs.append(e)
                 err.append(float(np.dot(lam, e)))
         return dict(bary=mubar, v=np.stack(v), w=np.stack(w), err=np.array(err), errs=np.array(errs))
     lmus = [_log(m) for m in mus]
     lv = [np.zeros_like(mus[0]) for _ in range(n)]
     lw = [np.zeros_like(mus[0]) for _ in range(n)]
+    lKv = [lse_conv(L, lv[i]) for i in range(n)]
     for _ in range(iters):
         lbar = np.zeros_like(mus[0])
         ld = [None] * n
         for i in range(n):
-            lw[i] = _ldiv(lmus[i], lse_conv(L, lv[i]))
+            lw[i] = _ldiv(lmus[i], lKv[i])
             ld[i] = lv[i] + lse_conv(L, lw[i])
             if lam[i] != 0.0:
                 lbar = lbar + lam[i] * ld[i]
         for i in range(n):
             lv[i] = lv[i] + lbar - ld[i]
+            lKv[i] = lse_conv(L, lv[i])
         if trace:
-            e = [float(np.sum(np.abs(np.exp(lw[i] + lse_conv(L, lv[i])) - mus[i]))) for i in range(n)]
+            e = [float(np.sum(np.abs(np.exp(lw[i] + lKv[i]) - mus[i]))) for i in range(n)]
             errs.append(e)
             err.append(float(np.dot(lam, e)))
     return dict(lbary=lbar, bary=np.exp(lbar), lv=np.stack(lv), lw=np.stack(lw), err=np.array(err),
@@ -399,13 +424,14 @@ def jko_potential(grid: Grid) -> np.ndarray:
     |x - c|^2 / 256^2 in pixel units on the 256 grid); broadcast over theta (R10)."""
     X = grid.x(np.arange(grid.nx))[None, None, :]
     Y = grid.y(np.arange(grid.ny))[None, :, None]
-    V = (X - 0.5) ** 2 + (Y - 0.5) ** 2
+    cx, cy = 0.5 * grid.nx * grid.hx, 0.5 * grid.ny * grid.hy
+    V = (X - cx) ** 2 + (Y - cy) ** 2
     return np.broadcast_to(V, grid.shape).copy()
 
 
 def haar_cell(grid: Grid) -> float:
     """Haar measure of one lattice cell, dx dy dtheta with the [0,1]^2 x [0,2pi) window (R1)."""
-    return (1.0 / grid.nx) * (1.0 / grid.ny) * (TWO_PI / grid.ntheta)
+    return grid.hx * grid.hy * (TWO_PI / grid.ntheta)
 
 
 def porous_prox(z, eps: float, tau: float, m: float, cell: float):
@@ -462,28 +488,34 @@ def jko(T, L, mu0, grid: Grid, eps: float, tau: float, steps: int, iters: int, l
         err = []
         if not log_domain:
             b = np.ones_like(mu)
+            Kb = conv(T, b)
             for _l in range(iters):
-                a = mu / np.maximum(conv(T, b), DIV_FLOOR)
+                a = mu / np.maximum(Kb, DIV_FLOOR)
                 z = np.maximum(conv_adjoint(T, a), DIV_FLOOR)
                 if porous:
                     b = porous_prox(z, eps, tau, m, cell) / z            # b = prox(z)/z
                 else:
                     b = z ** (-p) * np.exp(-q * V)
+                if _l + 1 < iters or trace:
+                    Kb = conv(T, b)
                 if trace:
-                    err.append(marginal_error(a, conv(T, b), mu))
+                    err.append(marginal_error(a, Kb, mu))
             s = b * z
         else:
             lmu = _log(mu)
             beta = np.zeros_like(mu)
+            lKb = lse_conv(L, beta)
             for _l in range(iters):
-                alpha = _ldiv(lmu, lse_conv(L, beta))
+                alpha = _ldiv(lmu, lKb)
                 lz = lse_conv_adjoint(L, alpha)
                 if porous:
                     beta = np.log(porous_prox(np.exp(lz), eps, tau, m, cell)) - lz
                 else:
                     beta = -p * lz - q * V
+                if _l + 1 < iters or trace:
+                    lKb = lse_conv(L, beta)
                 if trace:
-                    err.append(float(np.sum(np.abs(np.exp(alpha + lse_conv(L, beta)) - mu))))
+                    err.append(float(np.sum(np.abs(np.exp(alpha + lKb) - mu))))
             s = np.exp(beta + lz)
         mass = float(s.sum())
         masses.append(mass)

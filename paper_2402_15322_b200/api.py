@@ -49,6 +49,8 @@ class Kernel:
         self.eps, self.w, self.radius = float(eps), tuple(float(v) for v in w), int(radius)
         self.max_batch, self.device = int(max_batch), int(device)
         self.N = self.nx * self.ny * self.ntheta
+        self.hx = float(hx) if hx else 1.0 / self.nx      # cell sizes (R1); a window of a finer
+        self.hy = float(hy) if hy else 1.0 / self.ny      # lattice keeps that lattice's cell
         h = ctypes.c_void_p()
         g = L.se2_grid(self.nx, self.ny, self.ntheta, float(hx), float(hy))
         m = L.se2_metric(*self.w)
@@ -139,11 +141,11 @@ def se2_conv(k: Kernel, x: torch.Tensor, out: Optional[torch.Tensor] = None, log
 
 def make_prox(k: Kernel, tau: float, global_ny: Optional[int] = None, row_offset: int = 0) -> L.se2_prox:
     """Entropy + potential prox of the JKO step (R10): V(x) = |x - c|^2 in [0,1]^2 units, c the window
-    centre, cell sizes 1/nx, 1/global_ny.  For a slab whose local row 0 is global row `row_offset`,
-    the centre row shifts by -row_offset (cells)."""
+    centre, the kernel's cell sizes.  For a slab of a grid with global_ny rows whose local row 0 is
+    global row `row_offset`, the centre row is global_ny / 2 - row_offset (cells)."""
     gny = k.ny if global_ny is None else int(global_ny)
     return L.se2_prox(L.SE2_PROX_ENTROPY_POTENTIAL, float(tau), k.nx / 2.0, gny / 2.0 - row_offset,
-                      1.0 / k.nx, 1.0 / gny, 0.0)
+                      k.hx, k.hy, 0.0)
 
 
 def make_porous_prox(tau: float, m: float) -> L.se2_prox:

@@ -86,8 +86,10 @@ TcGeom tc_geom(const se2_kernel_s* k) {
     size_t pipe = 2 * g.b_stage + kTcNA * g.a_stage;
     size_t epi = (size_t)128 * (g.npad + 1) * sizeof(float);         // TMEM -> smem transpose
     g.smem = std::max(pipe, epi) + 1024;                              // + barriers / scratch
+    // per accumulator: the npad columns, and every x32 tcgen05.ld of the column-half flush
+    // (columns h * npad/2 + c .. + 31 with c < npad/2) must stay inside the allocation
     g.tmem_cols = 32;
-    while (g.tmem_cols < g.npad) g.tmem_cols *= 2;
+    while (g.tmem_cols < std::max(g.npad, g.npad / 2 + 32)) g.tmem_cols *= 2;
     g.tmem_cols *= 2;   // main (hi.hi) + correction (hi.lo + lo.hi) accumulators
     return g;
 }
@@ -266,7 +268,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sB = smem;                                   // [2][hl][nwin][nxp][16 B]
     unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwin][8 j][16 to][16 B]
-    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone, flushed, cflushed;
+    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone[2], flushed, cflushed;
     __shared__ uint32_t tmem_base;
     __shared__ float sRed[kTcThreads / 32];
 
@@ -280,7 +282,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
         for (int i = 0; i < kTcNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
-        mbar_init(&rowdone, 1);
+        mbar_init(&rowdone[0], 1);
+        mbar_init(&rowdone[1], 1);
         mbar_init(&flushed, kTcFlushWarps);
         mbar_init(&cflushed, kTcFlushWarps);
         mbar_fence_init();
@@ -422,7 +425,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 for (int dxi = 0; dxi < P; ++dxi) issue_main(gr * a.S + dxi, stb, dxi, restart);
                 for (int dxi = P; dxi < a.S; ++dxi) issue_both(gr * a.S + dxi, stb, dxi, restart);
                 tc_commit(&emptyB[stb]);
-                tc_commit(&rowdone);
+                tc_commit(&rowdone[gr & 1]);   // 2-deep ring: the issuer runs at most one chain (<= 2 rows) ahead
                 if ((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1) ++gs;   // chain end
             }
         }
@@ -448,7 +451,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.f;
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
-                tc_wait(&rowdone, (uint32_t)(gr & 1));
+                tc_wait(&rowdone[gr & 1], (uint32_t)((gr >> 1) & 1));
                 if (!((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1)) continue;   // mid-chain
                 __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;");

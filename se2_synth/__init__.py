@@ -48,6 +48,8 @@ class Config:
     jko_steps: int = 0
     tau: float = 0.0
     log_domain: bool = False            # reading L12: decided from the oracle probes
+    cell: float = 0.0                   # cell size in [0,1]^2 units; 0 -> 1/nx by 1/ny (reading R1).  A
+                                        # window cut from a larger grid keeps that grid's cell.
 
     @property
     def R(self) -> int:
@@ -226,6 +228,7 @@ class ParityCase:
     energy: str = "entropy_potential"   # JKO energy: BASELINE configs[4], or the paper's porous medium
     m: float = 5.0                      # porous-medium exponent
     w: Optional[Tuple[float, float, float]] = None   # metric override
+    cell: float = 0.0                   # cell size override (0: 1/nx by 1/ny)
 
 
 PARITY_CASES: List[ParityCase] = [
@@ -235,11 +238,17 @@ PARITY_CASES: List[ParityCase] = [
     ParityCase("c2m", "c2", 40, 36, 32, 7, 300),
     ParityCase("c2f", "c2", 64, 64, 32, 7, 300, full_fields=False),   # the whole c2 run at full size
     ParityCase("c3p", "c3", 128, 128, 32, 10, 2, full_fields=False),
-    ParityCase("c3q", "c3", 128, 128, 32, 10, 20, full_fields=False),  # c3 at full size, first 20 iterations
-    ParityCase("c3m", "c3", 44, 40, 32, 10, 40),
+    ParityCase("c3q", "c3", 128, 128, 32, 10, 100, full_fields=False),  # c3 at full size, first 100 iterations
+    ParityCase("c3m", "c3", 44, 40, 32, 10, 500),                       # ragged c3 analogue, the full 500
     ParityCase("c4p", "c4", 256, 256, 64, 15, 2, jko_steps=1, full_fields=False),
     ParityCase("c4q", "c4", 256, 256, 64, 15, 20, jko_steps=1, full_fields=False),  # full c4 grid, 20 inner iterations
     ParityCase("c4m", "c4", 72, 60, 16, 4, 200, jko_steps=3),
+    # the headline geometry on a reduced, ragged window: a 100 x 92 window of the c4 lattice (cells of
+    # 1/256, so R = 15, ntheta = 64, eps = 0.003, w = (1,3,1) give exactly the c4 kernel), 3 JKO steps x
+    # 200 inner iterations; V centred on the window
+    ParityCase("c4w", "c4", 100, 92, 64, 15, 200, jko_steps=3, full_fields=False, cell=1.0 / 256.0),
+    # the full c4 grid, JKO step 0: all 200 inner iterations (sampled)
+    ParityCase("c4f", "c4", 256, 256, 64, 15, 200, jko_steps=1, full_fields=False),
     # NEXT #1: the paper's own gradient flow -- porous medium m = 5, w = (1, sqrt 10, sqrt 2)
     ParityCase("c5m", "c4", 64, 56, 16, 4, 100, jko_steps=2, energy="porous", m=5.0,
                w=(1.0, math.sqrt(10.0), math.sqrt(2.0))),
@@ -260,7 +269,7 @@ def parity_inputs(pc: ParityCase):
     cfg = dataclasses.replace(base, name=base.name, nx=pc.nx, ny=pc.ny, ntheta=pc.ntheta,
                               support=2 * pc.R + 1, iters=pc.iters,
                               jko_steps=pc.jko_steps if pc.jko_steps else base.jko_steps,
-                              w=pc.w if pc.w is not None else base.w)
+                              w=pc.w if pc.w is not None else base.w, cell=pc.cell)
     return cfg, config_inputs(cfg)
 
 

@@ -30,7 +30,7 @@ def _store(out, name, arr, pc, idx):
 
 def make(pc):
     cfg, d = S.parity_inputs(pc)
-    g = O.Grid(cfg.nx, cfg.ny, cfg.ntheta)
+    g = O.Grid(cfg.nx, cfg.ny, cfg.ntheta, cfg.cell, cfg.cell)
     T = O.kernel_table(g, cfg.R, cfg.eps, cfg.w)
     L = O.log_kernel_table(g, cfg.R, cfg.eps, cfg.w)
     N = cfg.N

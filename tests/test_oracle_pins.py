@@ -481,3 +481,70 @@ def test_transport_cost_two_diracs_and_dense():
     a, b = rng.random(g.shape), rng.random(g.shape)
     dense = a.reshape(-1) @ ((K * C) @ b.reshape(-1))
     assert abs(O.transport_cost(Tc, a, b) - dense) < 1e-12 * dense
+
+
+# ---------------------------------------------------------------- units of V and of the Haar cell --
+def test_jko_potential_units_baseline_formula():
+    """BASELINE configs[4]: V(x, theta) = |x - c|^2 / 256^2 in PIXEL units on the 256 x 256 grid, c the
+    grid centre, pixel centres at i + 1/2 (reading R10).  Hand-computed values at lattice points
+    ((i + 1/2 - 128)^2 + (j + 1/2 - 128)^2) / 65536: a [0,1]-vs-pixel slip (factor 65536), a centre at
+    128 - 1/2, or a missing half-cell offset each change them."""
+    g = O.Grid(256, 256, 4)
+    V = O.jko_potential(g)
+    # (i, j) -> exact value (all dyadic rationals, representable in fp64)
+    cases = {
+        (0, 0): 32512.5 / 65536.0,          # 127.5^2 * 2
+        (128, 128): 0.5 / 65536.0,          # 0.5^2 * 2
+        (127, 128): 0.5 / 65536.0,          # (-0.5)^2 + 0.5^2
+        (255, 0): 32512.5 / 65536.0,
+        (200, 64): 9288.5 / 65536.0,        # 72.5^2 + (-63.5)^2 = 5256.25 + 4032.25
+        (10, 250): 28812.5 / 65536.0,       # (-117.5)^2 + 122.5^2 = 13806.25 + 15006.25
+    }
+    for (i, j), want in cases.items():
+        for k in range(4):                   # V does not depend on theta
+            assert V[k, j, i] == want, ((i, j, k), V[k, j, i], want)
+    # a window cut from the 256 lattice (cell 1/256) centres V on the window: same formula in pixels
+    gw = O.Grid(100, 92, 2, 1.0 / 256.0, 1.0 / 256.0)
+    Vw = O.jko_potential(gw)
+    assert Vw[0, 0, 0] == ((0.5 - 50.0) ** 2 + (0.5 - 46.0) ** 2) / 65536.0
+
+
+def test_haar_cell_units():
+    """Haar measure of one cell dx dy dtheta on [0,1]^2 x [0, 2pi): the cells partition the window,
+    so N cells have total measure 2 pi (a 1/ntheta-for-2pi/ntheta slip gives 1, a pixel-unit slip
+    nx ny 2pi); the c4 lattice's cell is 2 pi / (256 * 256 * 64) = pi / 2^21."""
+    for (nx, ny, nt) in [(256, 256, 64), (28, 28, 16), (37, 23, 12)]:
+        g = O.Grid(nx, ny, nt)
+        assert abs(O.haar_cell(g) * nx * ny * nt - 2.0 * np.pi) < 1e-12
+    assert O.haar_cell(O.Grid(256, 256, 64)) == np.pi / 2.0 ** 21
+    # a window of the 256 lattice keeps its cell
+    assert O.haar_cell(O.Grid(100, 92, 64, 1.0 / 256.0, 1.0 / 256.0)) == np.pi / 2.0 ** 21
+
+
+def test_full_field_loops_equal_point_definition():
+    """The full-field C loops (x innermost, vectorised) add each output's terms in the definition's order
+    (theta_i, dy, dx), so they equal the one-output definitions oracle_conv_point / oracle_lse_point BIT
+    FOR BIT; ragged grids with the box wider than the window, -inf inputs, and log ranges beyond the
+    fp64 exp underflow (the skipped exp(x <= -746) terms are exactly 0)."""
+    rng = np.random.default_rng(21)
+    for (nx, ny, nt, R) in [(11, 7, 4, 3), (5, 9, 3, 4), (16, 12, 8, 2)]:
+        g = O.Grid(nx, ny, nt)
+        T = O.kernel_table(g, R, 0.05, (1.0, 3.0, 1.0))
+        L = O.log_kernel_table(g, R, 0.05, (1.0, 3.0, 1.0))
+        v = rng.random(g.shape)
+        lv = rng.uniform(-1500.0, 1500.0, g.shape)
+        lv[0, 0, :2] = -np.inf
+        lv[:, 1, :] = -np.inf
+        y, ly = O.conv(T, v), O.lse_conv(L, lv)
+        for to in range(nt):
+            for iy in range(ny):
+                for ix in range(nx):
+                    assert y[to, iy, ix] == O.conv_point(T, v, to, iy, ix)
+                    p = O.lse_conv_point(L, lv, to, iy, ix)
+                    assert ly[to, iy, ix] == p or (np.isnan(p) and np.isnan(ly[to, iy, ix])), (to, iy, ix)
+        # adjoint scatter loops: K = K^T (P:598) to rounding
+        np.testing.assert_allclose(O.conv_adjoint(T, v), y, rtol=1e-13)
+        la = O.lse_conv_adjoint(L, lv)
+        fin = np.isfinite(ly)
+        assert np.array_equal(np.isfinite(la), fin)
+        np.testing.assert_allclose(la[fin], ly[fin], rtol=1e-13, atol=1e-10)
