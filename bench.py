@@ -7,8 +7,9 @@ Workload (default c4, the largest config, which fits one GPU): the entropic JKO 
 the 256x256x64 grid, eps = 0.003, w = (1,3,1), support 31x31x64, tau = 1e-3.  One step = one JKO
 step = 200 inner scaling iterations (2 group convolutions each, fused prox / division / error
 epilogues) + the normalisation of mu_{k+1}.  value = inner Sinkhorn iterations per second summed
-over ranks.  Multi-GPU (torchrun): every rank runs its own JKO flow (independent problems, no
-data-path collective) -> "scaling": "weak".
+of the one flow.  Multi-GPU (torchrun, N ranks): the SAME flow with the grid's rows split into N slabs
+(se2_jko_step_dist: owned-row convs, R-row NCCL halo exchange after every conv) -> "scaling": "strong";
+independent per-GPU flows are reported as the extra key "replicas".
 
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the launching
 stream, with an L2 flush (write of a 256 MiB buffer, outside the events) before each step; barrier
@@ -218,7 +219,10 @@ def run_reference(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg.iters / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload]},
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "oracle",
+                         "sample": desc + " -- a PROJECTION of the oracle's iteration rate from that timed sample, "
+                                          "not a timed full iteration"},
+        "projected": True,
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -370,47 +374,41 @@ def next_rows(device: int):
     return out
 
 
-def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
-    """c3's barycenter (4 inputs, 128x128x32, log domain) with the inputs sharded over the ranks
-    (parallel.ShardedBarycenter): the only exchange per iteration is the NCCL allreduce of the partial
-    weighted log-mean (0.5 MB).  Strong scaling over the 4 inputs (ranks beyond 4 hold none).
-    Returns iterations/s (max time over ranks, CUDA events) -- or an error string."""
+def sharded_barycenter(ws: int, rank: int, local: int, world, iters: int = 100):
+    """c3's barycenter (4 inputs, 128x128x32, log domain) through se2_barycenter_dist: the inputs sharded
+    over the ranks (NCCL allreduce of the partial weighted log-mean, 2 MB, every iteration) and, at 8
+    ranks, each input's grid split into 2 row slabs as well ("sharded one input per GPU pair",
+    B:configs[3]; halo exchange of w_i and v_i per iteration).  Strong scaling of one problem.
+    Returns iterations/s (max device time over ranks, CUDA events)."""
     import torch
     import torch.distributed as dist
 
     import se2_synth as S
-    from paper_2402_15322_b200 import Kernel
-    from paper_2402_15322_b200.parallel import CudaOps, ShardedBarycenter, partition
+    from paper_2402_15322_b200.dist import Dist, local_rows, se2_barycenter_dist, slab_kernel
+    from paper_2402_15322_b200.parallel import partition
     cfg = S.get_config("c3")
     d = S.config_inputs(cfg)
     lam = np.asarray(d["lambdas"][0])
-    lo, hi = partition(len(d["mus"]), ws, rank)
-    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=max(hi - lo, 1), device=local)
-    mus = torch.from_numpy(np.stack(d["mus"][lo:hi]) if hi > lo else np.zeros((0,) + cfg.shape, np.float32)).cuda()
-    # ws > 1: the fused exchange (peer buffers read in place by one reduce + update kernel, symmetric
-    # memory over NVLink); NCCL allreduce if symmetric memory is unavailable.  ws == 1: no exchange.
-    exchange = "nccl"
-    drv = None
-    if ws > 1:
-        try:
-            drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="p2p")
-        except Exception:
-            drv = None
-        ok = torch.tensor([1 if drv is not None else 0], device="cuda")
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank takes the same path
-        if int(ok.item()) == 1:
-            exchange = "p2p"
-        else:
-            drv = None
-    if drv is None:
-        drv = ShardedBarycenter(CudaOps(k, True), mus, lam[lo:hi], exchange="nccl")
-    drv.iterate(2)   # warm-up
+    nin = min(ws, 4)                      # input groups
+    nsl = ws // nin if ws % nin == 0 else 1
+    if nin * nsl != ws:
+        nin, nsl = ws, 1
+    ii, si = rank // nsl, rank % nsl
+    lo, hi = partition(4, nin, ii)
+    reduce = world.split(si, ii) if world is not None and nin > 1 else None
+    slabs = world.split(1000 + ii, si) if world is not None and nsl > 1 else None
+    k, row0, rows, top, bot = slab_kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, nsl, si,
+                                          max_batch=max(hi - lo, 1), device=local)
+    dd = Dist(reduce=reduce, slabs=slabs, halo_top=top, halo_bot=bot)
+    mus = torch.from_numpy(np.stack([local_rows(m, row0, rows, top, bot) for m in d["mus"][lo:hi]])).cuda()
+    lam_local = lam[lo:hi][None]
+    se2_barycenter_dist(k, dd, mus, lam_local, 2)   # warm-up (graph capture at 1 rank)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    drv.iterate(iters)
+    se2_barycenter_dist(k, dd, mus, lam_local, iters)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -418,12 +416,37 @@ def sharded_barycenter(ws: int, rank: int, local: int, iters: int = 100):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    how = {"p2p": "fused peer-memory reduce + v-update kernel (symmetric memory, one device barrier)",
-           "nccl": "NCCL allreduce of the weighted log-mean"}[exchange] if ws > 1 else "no exchange (1 rank)"
-    return {"workload": "c3 barycenter, 4 inputs sharded over ranks (inputs per rank: "
-                        f"{[partition(4, ws, r)[1] - partition(4, ws, r)[0] for r in range(ws)]}), {how} per iteration",
-            "exchange": exchange if ws > 1 else None, "iters": iters, "ms": ms,
-            "iters_per_s": iters / (ms / 1000.0), "n_gpus": ws}
+    return {"workload": f"c3 barycenter (4 inputs, 128x128x32, log domain) via se2_barycenter_dist: {nin} input "
+                        f"group(s) x {nsl} row slab(s); NCCL allreduce of the weighted log-mean per iteration"
+                        + ("; halo exchange of w_i, v_i" if nsl > 1 else ""),
+            "iters": iters, "ms": ms, "iters_per_s": iters / (ms / 1000.0), "n_gpus": ws}
+
+
+def replicas(ws: int, rank: int, local: int, cfg, d, steps: int = 2):
+    """Every rank runs its own c4 JKO flow (independent problems, no collective): the weak-scaling extra."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_15322_b200 import Kernel, make_prox, se2_jko_step
+    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1, device=local)
+    prox = make_prox(k, cfg.tau)
+    mu = torch.from_numpy(d["mus"][0]).cuda()
+    nxt, a, b = torch.empty_like(mu), torch.empty_like(mu), torch.empty_like(mu)
+    se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, log_domain=False)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        se2_jko_step(k, mu, nxt, a, b, cfg.iters, prox, log_domain=False)
+        mu, nxt = nxt, mu
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    k.close()
+    return {"workload": f"{ws} independent c4 JKO flows (one per GPU, no collective)", "value": ws * cfg.iters * steps /
+            (float(t.item()) / 1000.0), "unit": "iters/s", "scaling": "weak"}
 
 
 def run_gpu(args):
@@ -431,19 +454,24 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import se2_synth as S
-    from paper_2402_15322_b200 import Kernel, make_prox, se2_jko_step, se2_launch_count
+    from paper_2402_15322_b200 import make_prox, se2_launch_count
+    from paper_2402_15322_b200.dist import Comm, Dist, local_rows, se2_jko_step_dist, slab_kernel
 
     ws, rank, local = _dist_env()
     torch.cuda.set_device(local)
+    world = None
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        world = Comm.from_process_group(local)
     cfg = S.get_config(args.workload)
     d = S.config_inputs(cfg)
-    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1, device=local)
+    # the c4 grid's rows split into ws slabs (ws = 1: the whole grid; the same call path)
+    k, row0, rows, top, bot = slab_kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, ws, rank, 1, local)
+    dd = Dist(slabs=world, halo_top=top, halo_bot=bot)
     st = k.stats()
-    prox = make_prox(k, cfg.tau)
-    mu0 = torch.from_numpy(d["mus"][0]).cuda()
-    mu = mu0.clone()
+    prox = make_prox(k, cfg.tau, global_ny=cfg.ny, row_offset=row0 - top)
+    mu_local0 = local_rows(d["mus"][0], row0, rows, top, bot)
+    mu = torch.from_numpy(mu_local0).cuda()
     nxt = torch.empty_like(mu)
     a = torch.empty_like(mu)
     b = torch.empty_like(mu)
@@ -453,7 +481,7 @@ def run_gpu(args):
 
     def step():
         nonlocal mu, nxt
-        se2_jko_step(k, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
+        se2_jko_step_dist(k, dd, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
         mu, nxt = nxt, mu
 
     for _ in range(args.warmup):
@@ -485,10 +513,10 @@ def run_gpu(args):
         dev_ms = float(t.item())
         dist.barrier()
     ms_per_step = dev_ms / args.steps
-    value = ws * iters * args.steps / (dev_ms / 1000.0)
+    value = iters * args.steps / (dev_ms / 1000.0)     # inner iterations of the one flow all ranks share
 
     # ---- e2e: same step through the C ABI with host buffers, H2D + D2H inside the timed region
-    host_in = torch.from_numpy(d["mus"][0]).pin_memory()
+    host_in = torch.from_numpy(mu_local0).pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
@@ -499,7 +527,7 @@ def run_gpu(args):
     e0.record(stream)
     for _ in range(e2e_steps):
         mu.copy_(host_in, non_blocking=True)
-        se2_jko_step(k, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
+        se2_jko_step_dist(k, dd, mu, nxt, a, b, iters, prox, log_domain=False, trace=False)
         host_out.copy_(nxt, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -508,7 +536,7 @@ def run_gpu(args):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = ws * iters * e2e_steps / (e2e_ms / 1000.0)
+    e2e_value = iters * e2e_steps / (e2e_ms / 1000.0)
     nbytes = mu.numel() * 4
 
     out = None
@@ -517,16 +545,22 @@ def run_gpu(args):
         clocks = clk.summary()
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12           # TFLOP/s
-        flop_per_conv = 2.0 * cfg.N * st["nnz_taps"]
+        # algorithmic work of one conv launch on this rank: 2 flop per fp32-NORMAL tap of every owned output
+        flop_per_conv = 2.0 * cfg.nx * rows * cfg.ntheta * st["nnz_normal_taps"]
         conv_avg_ms = conv_ms / max(n_conv, 1)
         achieved = flop_per_conv / (conv_avg_ms / 1000.0) / 1e12
+        par = (f"slabs x{ws}: one c4 JKO flow, the 256 rows split into {ws} slabs (se2_jko_step_dist: owned-row "
+               f"convs, R-row NCCL halo exchange after every conv, mass allreduce per step)") if ws > 1 else \
+            "1 GPU (se2_jko_step_dist with one slab == se2_jko_step)"
         out = {
             "metric": "Sinkhorn iters/s on SE(2) grid", "value": value, "unit": "iters/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 fields; linear conv on tensor cores as 3 BF16 products (hi.hi + hi.lo + lo.hi) "
+                     "with fp32 accumulation" if k.uses_tensor_cores else "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "inner_iters_per_step": iters,
                        "l2": "flushed before every timed step (256 MiB write, outside the step events)",
-                       "parallelism": f"replicas x{ws} (independent JKO flows)"},
+                       "parallelism": par, "rows_on_rank0": rows},
             "roofline": _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, conv_ms, dev_ms,
                                        ffma_peak, sm_max, peaks, peak_src, clocks, args.workload),
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
@@ -534,15 +568,24 @@ def run_gpu(args):
             "clocks": clocks,
             "wall_s_timed_region": t_wall,
         }
+    k.close()
+    if ws > 1:
+        try:
+            rep = replicas(ws, rank, local, cfg, d)
+        except Exception as exc:
+            rep = {"error": f"{type(exc).__name__}: {exc}"}
+        if rank == 0:
+            out["replicas"] = rep
     if not args.no_configs:
         try:
-            sharded = sharded_barycenter(ws, rank, local)
+            sharded = sharded_barycenter(ws, rank, local, world)
         except Exception as exc:  # the headline must not depend on this extra measurement
             sharded = {"error": f"{type(exc).__name__}: {exc}"}
         if rank == 0:
             out["sharded_barycenter_c3"] = sharded
     if ws > 1:
         dist.barrier()
+        world.close()
         dist.destroy_process_group()
     if rank == 0:
         if not args.no_configs:
@@ -553,7 +596,8 @@ def run_gpu(args):
                 out["next_rows"] = {"error": str(e)[:300]}
         if not args.no_cpu_baseline and ws == 1:   # the oracle baseline: rank 0 at N = 1 only
             v, desc, threads, _ = cpu_oracle_sample(cfg)
-            out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle", "sample": desc}
+            out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle",
+                                   "sample": desc + " (a PROJECTION of one inner iteration from that timed sample)"}
         print(json.dumps(out), flush=True)
     return 0
 

@@ -50,14 +50,20 @@ typedef enum {
     SE2_EINVAL = 1,       /* bad argument (null pointer, size, eps <= 0, lambdas off simplex ...) */
     SE2_ENOMEM = 2,       /* device allocation failed                                            */
     SE2_ECUDA = 3,        /* CUDA runtime error (message has the CUDA error string)              */
+    SE2_ENCCL = 4,        /* NCCL error / NCCL unavailable (multi-GPU calls)                     */
     SE2_ENONFINITE = 5,   /* NaN/Inf produced by the iteration (SPEC NonFiniteIterate)           */
     SE2_EUNSUPPORTED = 6, /* configuration the kernels do not implement (e.g. radius > 15)       */
-    SE2_WKERNEL_TOO_WIDE = 100 /* warning: support box exceeds the grid (call succeeded)         */
+    SE2_WKERNEL_TOO_WIDE = 100, /* warning: support box exceeds the grid (call succeeded)        */
+    SE2_WGUARD_HIT = 101,       /* warning: the solve clamped linear-domain denominators at 1e-30
+                                   (R9; "counted and reported"); se2_guard_stats has the count */
+    SE2_WPROX_NOCONV = 102      /* warning: porous-medium prox sites whose safeguarded Newton iteration
+                                   missed its tolerance in 64 steps (count in se2_guard_stats)     */
 } se2_status;
 
 /* Flags */
 #define SE2_LOG_DOMAIN 0x1u   /* state/fields are natural logs; conv is log-sum-exp (R7)      */
-#define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1        */
+#define SE2_WARM_START 0x2u   /* sinkhorn: use the b (beta) array as b^(0) instead of 1;
+                                 barycenter: use v_state as the initial v_i (resume)              */
 #define SE2_TRACE_ERR 0x4u    /* compute the marginal error every iteration (fused)           */
 #define SE2_LSE_EXACT 0x8u    /* log domain: force the exact per-tap log-sum-exp engine (K4; also used for ntheta > 128) */
 #define SE2_LSE_NOTILT 0x10u  /* diagnostics: K3 without its gradient-tilted FFMA path           */
@@ -94,6 +100,9 @@ typedef struct {
     int32_t tensor_cores; /* 1: linear convs with the Gibbs kernel run on the tensor-core engine (K10,
                              3-pass BF16 split) by default; 0: on the fp32 FFMA engine (K2) unless
                              SE2_LIN_TC (2: K10 available on request only)                          */
+    int64_t nnz_normal_taps; /* taps per output whose fp32 value is a NORMAL number: the algorithmic work
+                             count of the roofline (subnormal taps < 2^-126 are below every retained
+                             term's resolution)                                          */
 } se2_kernel_stats;
 
 /* ------------------------------------------------------------------------------------------
@@ -109,6 +118,14 @@ SE2_API se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metr
                             int32_t max_batch, int32_t device, se2_kernel* out);
 SE2_API se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* out);
 SE2_API void se2_kernel_destroy(se2_kernel k); /* idempotent on NULL */
+
+/* Output window of a slab kernel (multi-GPU slab decomposition, B:north_star "split into spatial
+ * slabs"): after this call every conv of `k` computes and stores only the output rows
+ * [row_lo, row_hi) of each plane (marginal errors / sums likewise); the other rows of the kernel's grid
+ * are input-only halo rows holding the neighbours' boundary rows (or zero padding at the global
+ * edges).  The tensor-core and FFMA linear engines launch only the window's tiles; the log-domain
+ * engines mask their stores.  (0, ny) restores the whole grid.  Errors: SE2_EINVAL. */
+SE2_API se2_status se2_kernel_set_window(se2_kernel k, int32_t row_lo, int32_t row_hi);
 
 /* ------------------------------------------------------------------------------------------
  * se2_conv -- y = K v (the same operator serves K^T), batch fields at once.
@@ -176,7 +193,11 @@ SE2_API se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next,
  *   mus: device [n][N] input measures.  lambdas: HOST [nsolve][n], each row on the simplex
  *   within 1e-9 (SE2_EINVAL otherwise); lambda_i = 0 terms are skipped (R6).
  *   bary: device [nsolve][N] output mu (log mu under SE2_LOG_DOMAIN), as returned by App. A.
- *   v_state, w_state: nullable device [nsolve][n][N] outputs (v_i, w_i or their logs).
+ *   v_state, w_state: nullable device [nsolve][n][N] outputs (v_i, w_i or their logs).  With
+ *   SE2_WARM_START, v_state (required) is also the INPUT: the iteration resumes from those v_i instead of
+ *   v_i = 1 (w_i is recomputed from them first): a solve split into calls of j1 and j2 iterations
+ *   continues the same iterates as one call of j1 + j2 (up to fp32 rounding: the log-domain running
+ *   sum's compensation term restarts at 0).
  *   err_trace_host: nullable host [iters][nsolve]; with SE2_TRACE_ERR receives
  *   sum_i lambda_i sum|w_i K v_i - mu_i| after each v-update (R8).
  * ---------------------------------------------------------------------------------------- */
@@ -279,6 +300,12 @@ SE2_API se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* 
 SE2_API se2_status se2_timing_enable(se2_kernel k, int32_t on);
 SE2_API se2_status se2_timing_get(se2_kernel k, int64_t* n_launches, double* conv_ms, int64_t* all_launches);
 
+/* Guard counters of the kernel object since its last solve started (se2_sinkhorn / se2_jko_step /
+ * se2_barycenter reset them; step-level calls such as se2_conv_update accumulate): linear-domain
+ * denominators clamped at 1e-30 (R9) and porous prox sites without convergence.  reset != 0
+ * zeroes them after reading.  Synchronises the device. */
+SE2_API se2_status se2_guard_stats(se2_kernel k, int64_t* div_clamps, int64_t* prox_noconv, int32_t reset);
+
 /* Number of kernel launches this library has issued in this process (all entry points). */
 SE2_API int64_t se2_launch_count(void);
 
@@ -336,6 +363,60 @@ SE2_API se2_status se2_reconstruct_field(se2_cake c, const float* U, float* angl
 SE2_API se2_status se2_exp(const float* x, float* y, int64_t n, se2_stream stream);
 /* y[i] = log(x[i]) (logf; log 0 = -inf), e.g. measures -> log-domain targets. */
 SE2_API se2_status se2_log(const float* x, float* y, int64_t n, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Multi-GPU (B:north_star: "independent barycenter inputs ... go per GPU, with an NCCL allreduce over
+ * NVLink for the barycenter log-mean, and a single large grid is split into spatial slabs with NVLink
+ * halo exchange").  One rank per GPU (one process each); every rank calls every function below
+ * collectively, in the same order.
+ *
+ * se2_comm_unique_id -- 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it, e.g. with
+ *   torch.distributed).  NCCL is resolved at run time (dlopen libnccl.so.2; the build torch loaded is
+ *   reused).  Errors: SE2_ENCCL (no NCCL).
+ * se2_comm_init -- communicator of nranks ranks on `device` (ncclCommInitRank; nranks = 1 needs no id
+ *   and no NCCL).  se2_comm_init_loopback -- nranks communicators in ONE process on one device (out
+ *   [nranks]), each to be driven by its own host thread: the exchanges are device copies / reductions
+ *   ordered by CUDA events and host rendezvous (no kernel waits on another rank's kernel) -- the test
+ *   transport of the multi-rank logic on one GPU.
+ * se2_comm_split -- sub-communicator of the ranks with the same color, ordered by key (ncclCommSplit);
+ *   c3 on 8 GPUs: color = slab index -> the 4 input ranks of a slab (log-mean allreduce), color = input
+ *   -> the 2 slab ranks of an input (halo exchange).
+ * se2_comm_allreduce -- in-place sum of count floats (f64 = 0) or doubles over the ranks.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct se2_comm_s* se2_comm;
+#define SE2_COMM_ID_BYTES 128
+SE2_API se2_status se2_comm_unique_id(uint8_t* id_out /* SE2_COMM_ID_BYTES */);
+SE2_API se2_status se2_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, se2_comm* out);
+SE2_API se2_status se2_comm_init_loopback(int32_t nranks, int32_t device, se2_comm* out /* [nranks] */);
+SE2_API se2_status se2_comm_split(se2_comm parent, int32_t color, int32_t key, se2_comm* out);
+SE2_API se2_status se2_comm_info(se2_comm c, int32_t* nranks, int32_t* rank);
+SE2_API se2_status se2_comm_allreduce(se2_comm c, void* buf, int64_t count, int32_t f64, se2_stream stream);
+SE2_API void se2_comm_destroy(se2_comm c); /* idempotent on NULL */
+
+/* Decomposition of one rank.  The kernel is built on the LOCAL grid: the rank's owned rows plus halo_top
+ * rows above and halo_bot rows below (halo = R toward a neighbour slab, 0 at a global edge; cell sizes of
+ * the global grid, R1), and its output window is set to the owned rows.  Fields are local arrays
+ * [..][ntheta][halo_top + rows + halo_bot][nx]. */
+typedef struct {
+    se2_comm reduce;     /* ranks whose inputs form the same barycenters (allreduce of the log-mean); NULL: none */
+    se2_comm slabs;      /* the row slabs of the same fields, rank order = row order; NULL: the whole grid */
+    int32_t halo_top, halo_bot;
+} se2_dist;
+
+/* se2_jko_step_dist -- se2_jko_step on a row slab: per inner iteration two convs over the owned rows,
+ *   each followed by the exchange of R boundary rows with the neighbour slabs (packed by the conv
+ *   epilogue); mass and error trace summed over the slabs (the same values on every rank).  mu_next's
+ *   halo rows are zero.  One rank (dist with NULL communicators) is se2_jko_step exactly. */
+SE2_API se2_status se2_jko_step_dist(se2_kernel k, const se2_dist* dist, const float* mu_k, float* mu_next, float* a,
+                                     float* b, const se2_prox* prox, const se2_opts* opts, double* mass_host,
+                                     double* err_trace_host, se2_stream stream);
+/* se2_barycenter_dist -- App. A (log domain) with this rank's n inputs (mus [n][N_local], lambdas HOST
+ *   [nsolve][n]: this rank's share of weights that sum to 1 over all `reduce` ranks); per iteration one
+ *   allreduce of the partial sum_i lambda_i log d_i over `reduce` and, with slabs, halo exchanges of w_i and
+ *   v_i.  bary: [nsolve][N_local] log mu on every rank.  Trace: sum over all inputs and slabs. */
+SE2_API se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve, const float* mus,
+                                       const double* lambdas, float* bary, float* v_state, float* w_state,
+                                       const se2_opts* opts, double* err_trace_host, se2_stream stream);
 
 SE2_API const char* se2_last_error(void);
 SE2_API int32_t se2_abi_version(void);

@@ -31,7 +31,10 @@ SE2_PROX_ENTROPY_POTENTIAL = 1
 SE2_PROX_POROUS = 2
 
 STATUS_NAMES = {0: "SE2_OK", 1: "SE2_EINVAL", 2: "SE2_ENOMEM", 3: "SE2_ECUDA", 5: "SE2_ENONFINITE",
-                6: "SE2_EUNSUPPORTED", 100: "SE2_WKERNEL_TOO_WIDE"}
+                6: "SE2_EUNSUPPORTED", 100: "SE2_WKERNEL_TOO_WIDE", 101: "SE2_WGUARD_HIT",
+                102: "SE2_WPROX_NOCONV"}
+SE2_WGUARD_HIT = 101
+SE2_WPROX_NOCONV = 102
 
 # every symbol include/se2ot.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -42,7 +45,9 @@ EXPORTED = [
     "se2_transport_cost", "se2_lse_row_stats",
     "se2_cake_build", "se2_cake_get", "se2_cake_destroy", "se2_lift_image", "se2_split_signed", "se2_project",
     "se2_project_signed", "se2_lift_field", "se2_reconstruct_field", "se2_exp", "se2_log",
-    "se2_bary_reduce_update", "se2_conv_update_slab",
+    "se2_bary_reduce_update", "se2_conv_update_slab", "se2_guard_stats", "se2_kernel_set_window",
+    "se2_comm_unique_id", "se2_comm_init", "se2_comm_init_loopback", "se2_comm_split", "se2_comm_info",
+    "se2_comm_allreduce", "se2_comm_destroy", "se2_jko_step_dist", "se2_barycenter_dist",
 ]
 
 
@@ -64,7 +69,7 @@ class se2_metric(ctypes.Structure):
 class se2_kernel_stats(ctypes.Structure):
     _fields_ = [("box_taps", ctypes.c_int64), ("nnz_taps", ctypes.c_int64), ("theta_band", ctypes.c_int32),
                 ("radius", ctypes.c_int32), ("zeta", ctypes.c_double), ("table_bytes", ctypes.c_size_t),
-                ("tensor_cores", ctypes.c_int32)]
+                ("tensor_cores", ctypes.c_int32), ("nnz_normal_taps", ctypes.c_int64)]
 
 
 class se2_prox(ctypes.Structure):
@@ -77,6 +82,11 @@ class se2_slab(ctypes.Structure):
     _fields_ = [("own_lo", ctypes.c_int32), ("own_hi", ctypes.c_int32), ("halo", ctypes.c_int32),
                 ("up", ctypes.c_void_p), ("up_shift", ctypes.c_int32), ("ny_up", ctypes.c_int32),
                 ("dn", ctypes.c_void_p), ("dn_shift", ctypes.c_int32), ("ny_dn", ctypes.c_int32)]
+
+
+class se2_dist(ctypes.Structure):
+    _fields_ = [("reduce", ctypes.c_void_p), ("slabs", ctypes.c_void_p), ("halo_top", ctypes.c_int32),
+                ("halo_bot", ctypes.c_int32)]
 
 
 class se2_opts(ctypes.Structure):
@@ -119,6 +129,17 @@ def load(path: str = LIB_PATH):
                                ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_timing_get": [P, ctypes.POINTER(i64), pd, ctypes.POINTER(i64)],
         "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
+        "se2_guard_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
+        "se2_kernel_set_window": [P, i32, i32],
+        "se2_comm_unique_id": [ctypes.c_char_p],
+        "se2_comm_init": [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(P)],
+        "se2_comm_init_loopback": [i32, i32, ctypes.POINTER(P)],
+        "se2_comm_split": [P, i32, i32, ctypes.POINTER(P)],
+        "se2_comm_info": [P, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "se2_comm_allreduce": [P, P, i64, i32, P],
+        "se2_jko_step_dist": [P, ctypes.POINTER(se2_dist), P, P, P, P, ctypes.POINTER(se2_prox),
+                              ctypes.POINTER(se2_opts), pd, pd, P],
+        "se2_barycenter_dist": [P, ctypes.POINTER(se2_dist), i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],
         "se2_cake_build": [i32, i32, i32, dbl, i32, ctypes.POINTER(P)],
         "se2_cake_get": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), ctypes.POINTER(i32)],
         "se2_lift_image": [P, P, P, i32, i32, i32, P],
@@ -138,6 +159,8 @@ def load(path: str = LIB_PATH):
         f.restype = ctypes.c_int
     lib.se2_kernel_destroy.argtypes = [P]
     lib.se2_kernel_destroy.restype = None
+    lib.se2_comm_destroy.argtypes = [P]
+    lib.se2_comm_destroy.restype = None
     lib.se2_cake_destroy.argtypes = [P]
     lib.se2_cake_destroy.restype = None
     lib.se2_last_error.argtypes = []

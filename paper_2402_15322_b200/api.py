@@ -67,7 +67,8 @@ class Kernel:
         s = L.se2_kernel_stats()
         check(L.load().se2_kernel_stats_get(self._h, ctypes.byref(s)))
         return dict(box_taps=s.box_taps, nnz_taps=s.nnz_taps, theta_band=s.theta_band, radius=s.radius,
-                    zeta=s.zeta, table_bytes=s.table_bytes, tensor_cores=int(s.tensor_cores))
+                    zeta=s.zeta, table_bytes=s.table_bytes, tensor_cores=int(s.tensor_cores),
+                    nnz_normal_taps=s.nnz_normal_taps)
 
     @property
     def uses_tensor_cores(self) -> bool:
@@ -103,6 +104,13 @@ class Kernel:
         live, vis = ctypes.c_int64(), ctypes.c_int64()
         check(L.load().se2_lse_row_stats(self._h, ctypes.byref(live), ctypes.byref(vis), 1 if reset else 0))
         return dict(live=live.value, visited=vis.value)
+
+    def guard_stats(self, reset: bool = False) -> dict:
+        """Division-guard clamps (R9) and porous prox non-convergences since the last solve
+        started (se2_guard_stats)."""
+        d, p = ctypes.c_int64(), ctypes.c_int64()
+        check(L.load().se2_guard_stats(self._h, ctypes.byref(d), ctypes.byref(p), 1 if reset else 0))
+        return dict(div_clamps=d.value, prox_noconv=p.value)
 
     def timing_enable(self, on: bool = True):
         check(L.load().se2_timing_enable(self._h, 1 if on else 0))
@@ -196,9 +204,10 @@ def se2_jko_step(k: Kernel, mu_k: torch.Tensor, mu_next: torch.Tensor, a: torch.
 def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain: bool,
                    bary: Optional[torch.Tensor] = None, v_state: Optional[torch.Tensor] = None,
                    w_state: Optional[torch.Tensor] = None, trace: bool = False, lse_exact: bool = False,
-                   no_graph: bool = False, debug_flags: int = 0):
+                   no_graph: bool = False, debug_flags: int = 0, warm_start: bool = False):
     """App. A barycenter.  mus: [n][N]; lambdas: [nsolve][n] (host).  Returns
     (bary [nsolve][N] -- log mu under log_domain --, err trace [iters][nsolve] or None).
+    warm_start: resume from v_state (required) instead of v_i = 1.
     debug_flags: SE2_DEBUG_* bits (diagnostics / tests only)."""
     _check_field(mus, k, "mus")
     n = mus.numel() // k.N
@@ -212,7 +221,10 @@ def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain
     for name, t in (("v_state", v_state), ("w_state", w_state)):
         if t is not None:
             _check_field(t, k, name, nsolve * n)
-    opts = L.se2_opts(int(iters), _flags(log_domain, trace, lse_exact=lse_exact, no_graph=no_graph) | int(debug_flags))
+    if warm_start and v_state is None:
+        raise ValueError("warm_start needs v_state")
+    opts = L.se2_opts(int(iters), _flags(log_domain, trace, warm=warm_start, lse_exact=lse_exact, no_graph=no_graph)
+                      | int(debug_flags))
     tr = np.zeros((max(iters, 1), nsolve), dtype=np.float64) if trace else None
     trp = tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None
     check(L.load().se2_barycenter(k.handle, n, nsolve, _ptr(mus), lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

@@ -23,181 +23,7 @@ using namespace se2;
 
 extern "C" int64_t se2_launch_count(void);
 
-namespace {
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
-
-// grow-only device workspace owned by the kernel object
-struct Workspace {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-};
-
-}  // namespace
-
-// a captured solve (CUDA graph) keyed by everything its launches depend on
-struct GraphEntry {
-    std::vector<uint64_t> key;
-    cudaGraphExec_t exec = nullptr;
-    int64_t nlaunch = 0;
-};
-
-// extra per-kernel state not in the header struct
-struct KernelExtra {
-    Workspace ws;         // fields
-    Workspace trace;      // device error trace
-    Workspace partial;    // conv error partials
-    Workspace misc;       // lambdas, counters, sums
-    std::vector<GraphEntry> graphs;   // small-problem solves replayed as CUDA graphs
-    cudaStream_t cap = nullptr;       // private stream for capture / replay
-    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    void clear_graphs() {
-        for (auto& gph : graphs)
-            if (gph.exec) cudaGraphExecDestroy(gph.exec);
-        graphs.clear();
-    }
-};
-
-static KernelExtra* extra(se2_kernel_s* k) { return reinterpret_cast<KernelExtra*>(k->extra); }
-
-static se2_status ensure(Workspace& w, size_t bytes, KernelExtra* owner = nullptr) {
-    if (w.bytes >= bytes) return SE2_OK;
-    if (owner) owner->clear_graphs();   // captured graphs reference the old buffers
-    if (w.ptr) cudaFree(w.ptr);
-    w.ptr = nullptr;
-    w.bytes = 0;
-    cudaError_t e = cudaMalloc(&w.ptr, bytes);
-    if (e != cudaSuccess) {
-        set_error(std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
-        return SE2_ENOMEM;
-    }
-    w.bytes = bytes;
-    return SE2_OK;
-}
-
-// ---- conv dispatch with optional event timing ---------------------------------------------------
-static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t flags, const Epilogue& epi,
-                           cudaStream_t s, int* bpf) {
-    const bool log_domain = (flags & SE2_LOG_DOMAIN) != 0;
-    Timing& t = k->timing;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (t.on) {
-        if (t.used == t.events.size()) {
-            cudaEvent_t a, b;
-            SE2_CUDA_TRY(cudaEventCreate(&a));
-            SE2_CUDA_TRY(cudaEventCreate(&b));
-            t.events.push_back({a, b});
-        }
-        e0 = t.events[t.used].first;
-        e1 = t.events[t.used].second;
-        t.used++;
-        SE2_CUDA_TRY(cudaEventRecord(e0, s));
-    }
-    cudaError_t e;
-    if (!log_domain)
-        e = conv_tc_route(k, flags, epi) ? launch_conv_tc(k, in, batch, epi, s, bpf)
-                                         : launch_conv_linear(k, in, batch, epi, s, bpf);
-    else if ((flags & SE2_LSE_EXACT) || k->nt > 128)   // K3 holds per-channel state for <= 128 orientations
-        e = launch_conv_lse(k, in, batch, epi, s, bpf);
-    else
-        e = launch_conv_lse_fast(k, in, batch, epi, s, bpf, k->lstats,
-                                 ((flags & SE2_LSE_K3EXACT) ? 1 : ((flags & SE2_LSE_NOTILT) ? 2 : 0)) |
-                                     ((flags & SE2_DEBUG_BAD_HINTS) ? 4 : 0) | ((flags & SE2_DEBUG_NO_SPLIT) ? 8 : 0),
-                                 k->lse_counters,
-                                 k->split, k->split_floats);
-    if (e != cudaSuccess) {
-        set_error(std::string("conv launch: ") + cudaGetErrorString(e));
-        return SE2_ECUDA;
-    }
-    t.all_launches++;
-    if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
-    return SE2_OK;
-}
-
-// Replay `enqueue` (a launch sequence on a given stream) as a CUDA graph for small problems, where the
-// ~10 launches per scaling iteration are latency-bound; the graph is captured on first use and cached
-// under `key`.  Work is ordered after / before the caller's stream with events.  `use` = false runs
-// the sequence directly on the caller's stream (large problems, timing instrumentation on).
-template <class F>
-static se2_status run_graph(se2_kernel_s* k, cudaStream_t s, std::vector<uint64_t> key, bool use, F&& enqueue) {
-    static const bool disabled = getenv("SE2_NO_GRAPH") != nullptr;
-    if (!use || disabled || k->timing.on) return enqueue(s);
-    KernelExtra* x = extra(k);
-    if (!x->cap) {
-        SE2_CUDA_TRY(cudaStreamCreateWithFlags(&x->cap, cudaStreamNonBlocking));
-        SE2_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming));
-        SE2_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
-    }
-    GraphEntry* hit = nullptr;
-    for (auto& gph : x->graphs)
-        if (gph.key == key) hit = &gph;
-    SE2_CUDA_TRY(cudaEventRecord(x->ev_in, s));
-    SE2_CUDA_TRY(cudaStreamWaitEvent(x->cap, x->ev_in, 0));
-    if (!hit) {
-        if (x->graphs.size() >= 8) {   // small cache: drop the oldest
-            if (x->graphs.front().exec) cudaGraphExecDestroy(x->graphs.front().exec);
-            x->graphs.erase(x->graphs.begin());
-        }
-        SE2_CUDA_TRY(cudaStreamBeginCapture(x->cap, cudaStreamCaptureModeThreadLocal));
-        const int64_t l0 = se2_launch_count();
-        se2_status st = enqueue(x->cap);
-        cudaGraph_t graph = nullptr;
-        cudaError_t e = cudaStreamEndCapture(x->cap, &graph);
-        if (st != SE2_OK) {
-            if (graph) cudaGraphDestroy(graph);
-            return st;
-        }
-        if (e != cudaSuccess) {
-            set_error(std::string("graph capture: ") + cudaGetErrorString(e));
-            return SE2_ECUDA;
-        }
-        GraphEntry ge;
-        ge.key = std::move(key);
-        ge.nlaunch = se2_launch_count() - l0;
-        e = cudaGraphInstantiate(&ge.exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) {
-            set_error(std::string("graph instantiate: ") + cudaGetErrorString(e));
-            return SE2_ECUDA;
-        }
-        x->graphs.push_back(ge);
-        hit = &x->graphs.back();
-        SE2_CUDA_TRY(cudaGraphLaunch(hit->exec, x->cap));   // the capture itself executed nothing
-    } else {
-        SE2_CUDA_TRY(cudaGraphLaunch(hit->exec, x->cap));
-        count_launch(hit->nlaunch);
-    }
-    SE2_CUDA_TRY(cudaEventRecord(x->ev_out, x->cap));
-    SE2_CUDA_TRY(cudaStreamWaitEvent(s, x->ev_out, 0));
-    return SE2_OK;
-}
-
-static uint64_t as_key(const void* p) { return (uint64_t)(uintptr_t)p; }
-static uint64_t as_key(double v) {
-    uint64_t u;
-    memcpy(&u, &v, sizeof(u));
-    return u;
-}
-constexpr int64_t kGraphMaxElems = (int64_t)1 << 21;   // batch * N at or below which solves use graphs
-
-static se2_status check_kernel(se2_kernel k) {
-    if (!k) {
-        set_error("null kernel");
-        return SE2_EINVAL;
-    }
-    return SE2_OK;
-}
+#include "api_internal.cuh"
 
 extern "C" {
 
@@ -262,6 +88,8 @@ se2_status se2_kernel_build(const se2_grid* grid, const se2_metric* metric, doub
         const size_t nst = lse_fast_stats_floats(k, max_batch);
         cudaError_t e2 = cudaMalloc(&k->lstats, sizeof(float) * nst);
         if (e2 == cudaSuccess) e2 = cudaMalloc(&k->lse_counters, sizeof(int) * 16);
+        if (e2 == cudaSuccess) e2 = cudaMalloc(&k->guard, sizeof(unsigned int) * 4);
+        if (e2 == cudaSuccess) e2 = cudaMemset(k->guard, 0, sizeof(unsigned int) * 4);
         if (e2 == cudaSuccess) e2 = cudaMemset(k->lse_counters, 0, sizeof(int) * 16);
         // theta_i-split scratch for grids that give fewer than 2 CTAs per SM (at most 8 groups, 64 MB)
         {
@@ -303,6 +131,7 @@ se2_status se2_kernel_stats_get(se2_kernel k, se2_kernel_stats* o) {
     o->zeta = std::max(k->w1, k->w2) / std::min(k->w1, k->w2);
     o->table_bytes = k->table_bytes;
     o->tensor_cores = k->tc_w == nullptr ? 0 : (k->tc_fast ? 1 : 2);
+    o->nnz_normal_taps = k->nnz_normal_taps;
     return SE2_OK;
 }
 
@@ -323,6 +152,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->tc_x) cudaFree(k->tc_x);
     se2::conv_tc_release(k);
     if (k->lse_counters) cudaFree(k->lse_counters);
+    if (k->guard) cudaFree(k->guard);
     KernelExtra* x = extra(k);
     if (x) {
         x->clear_graphs();
@@ -340,6 +170,21 @@ void se2_kernel_destroy(se2_kernel k) {
     delete k;
 }
 
+se2_status se2_kernel_set_window(se2_kernel k, int32_t row_lo, int32_t row_hi) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(row_lo >= 0 && row_hi > row_lo && row_hi <= k->ny, "window must satisfy 0 <= lo < hi <= ny");
+    DeviceGuard g(k->device);
+    k->win_lo = row_lo;
+    k->win_hi = (row_lo == 0 && row_hi == k->ny) ? 0 : row_hi;
+    extra(k)->clear_graphs();   // captured solves used the previous geometry
+    cudaError_t e = conv_tc_decide(k);
+    if (e != cudaSuccess) {
+        set_error(std::string("K10 geometry: ") + cudaGetErrorString(e));
+        return SE2_ECUDA;
+    }
+    return SE2_OK;
+}
+
 se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, uint32_t flags, se2_stream stream) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(in && out && in != out, "in/out must be distinct non-null device pointers");
@@ -349,23 +194,6 @@ se2_status se2_conv(se2_kernel k, const float* in, float* out, int32_t batch, ui
     epi.op = EPI_STORE;
     epi.out = out;
     return run_conv(k, in, batch, flags, epi, (cudaStream_t)stream, nullptr);
-}
-
-static void fill_prox(Epilogue& epi, const se2_kernel_s* k, const se2_prox* prox) {
-    epi.prox_kind = prox->kind;
-    if (prox->kind == SE2_PROX_POROUS) {
-        // C = tau m / (eps (m-1)) cell^{1-m}: the energy acts on the density s / cell, cell = dx dy dtheta
-        const double cell = k->hx * k->hy * (6.283185307179586476925286766559 / k->nt);
-        epi.prox_c = (float)(prox->tau * prox->m / (k->eps * (prox->m - 1.0)) * pow(cell, 1.0 - prox->m));
-        epi.prox_m1 = (float)(prox->m - 1.0);
-    }
-    const double p = prox->tau / (k->eps + prox->tau);
-    epi.prox_p = (float)p;
-    epi.prox_q = (float)p;
-    epi.cx = (float)prox->cx;
-    epi.cy = (float)prox->cy;
-    epi.hx = (float)prox->hx;
-    epi.hy = (float)prox->hy;
 }
 
 se2_status se2_conv_update(se2_kernel k, const float* in, const float* target, float* out, int32_t batch,
@@ -455,7 +283,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
         if (st != SE2_OK) return st;
     }
     // K9: the whole loop in one cluster launch when the grid fits in shared memory (c0-sized)
-    const int k9c = (LOG && !jko && batch <= 64 && s_out == nullptr && iters > 0 &&
+    const int k9c = (LOG && !jko && batch <= 64 && s_out == nullptr && iters > 0 && k->win_hi == 0 &&
                      !(opts->flags & (SE2_NO_PERSISTENT | SE2_LSE_EXACT | SE2_LSE_K3EXACT | SE2_LSE_NOTILT)))
                         ? k9_cluster_size(k) : 0;
     if (k9c > 0) {
@@ -573,25 +401,6 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     return SE2_OK;
 }
 
-static se2_status check_finite(se2_kernel_s* k, const float* const* ptrs, const int64_t* ns, int count,
-                               cudaStream_t s) {
-    KernelExtra* x = extra(k);
-    se2_status st = ensure(x->misc, 4096);
-    if (st != SE2_OK) return st;
-    int* cnt = reinterpret_cast<int*>(x->misc.ptr);
-    SE2_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), s));
-    for (int i = 0; i < count; ++i)
-        if (ptrs[i]) SE2_CUDA_TRY(launch_count_nonfinite(ptrs[i], ns[i], cnt, s));
-    int h = 0;
-    SE2_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SE2_CUDA_TRY(cudaStreamSynchronize(s));
-    if (h != 0) {
-        set_error("non-finite values produced by the iteration (" + std::to_string(h) + " entries)");
-        return SE2_ENONFINITE;
-    }
-    return SE2_OK;
-}
-
 se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a, float* b, int32_t batch,
                         const se2_prox* prox, const se2_opts* opts, double* err_trace_host, se2_stream stream) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
@@ -605,7 +414,9 @@ se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a
     SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
-    se2_status st = sinkhorn_impl(k, mu, nu, a, b, batch, prox, opts, err_trace_host, nullptr, s);
+    se2_status st = reset_guard(k, s);
+    if (st != SE2_OK) return st;
+    st = sinkhorn_impl(k, mu, nu, a, b, batch, prox, opts, err_trace_host, nullptr, s);
     if (st != SE2_OK) return st;
     const float* ps[2] = {a, b};
     const int64_t ns[2] = {(int64_t)batch * k->N(), (int64_t)batch * k->N()};
@@ -622,7 +433,9 @@ se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* 
     SE2_CHECK_ARG(mu_k && mu_next && a && b && mu_k != mu_next, "bad pointers");
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
-    se2_status st = sinkhorn_impl(k, mu_k, nullptr, a, b, 1, prox, opts, err_trace_host, mu_next, s);
+    se2_status st = reset_guard(k, s);
+    if (st != SE2_OK) return st;
+    st = sinkhorn_impl(k, mu_k, nullptr, a, b, 1, prox, opts, err_trace_host, mu_next, s);
     if (st != SE2_OK) return st;
     KernelExtra* x = extra(k);
     st = ensure(x->misc, 4096);
@@ -655,12 +468,16 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         }
         SE2_CHECK_ARG(fabs(sum - 1.0) <= 1e-9, "lambdas must lie on the simplex");
     }
+    const bool warm = (opts->flags & SE2_WARM_START) != 0;
+    SE2_CHECK_ARG(!warm || v_state != nullptr, "SE2_WARM_START needs v_state (the initial v_i)");
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
     const bool LOG = (opts->flags & SE2_LOG_DOMAIN) != 0;
     const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
     const int64_t N = k->N();
     const int F = n * nsolve;
+    se2_status st0 = reset_guard(k, s);
+    if (st0 != SE2_OK) return st0;
     const int64_t FN = (int64_t)F * N;
     const int iters = opts->iters;
     KernelExtra* x = extra(k);
@@ -707,7 +524,9 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             SE2_CUDA_TRY(launch_log(mu_rep, lmu_rep, FN, s));
             tmu = lmu_rep;
         }
-        SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
+        // v_i, w_i <- 1 (App. A), or resume from the caller's v_i (SE2_WARM_START; w_i is recomputed
+        // from v_i by the first half-step before it is read)
+        if (!warm) SE2_CUDA_TRY(launch_fill(v, FN, LOG ? 0.f : 1.f, s));
         SE2_CUDA_TRY(launch_fill(v_lo, FN, 0.f, s));
         SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
         for (int j = 0; j < iters; ++j) {
@@ -739,7 +558,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
             if (LOG) {
                 SE2_CUDA_TRY(launch_bary_logmean_update(n, nsolve, N, d, lam_dev, bary, v, v_lo, s));
             } else {
-                SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, s));
+                SE2_CUDA_TRY(launch_bary_update_lin(n, nsolve, N, v, d, lam_dev, bary, k->guard, s));
             }
         }
         if (trace && iters > 0) {
@@ -936,6 +755,18 @@ se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64_t* ffma
     if (tilted_pairs) *tilted_pairs = h[3];
     if (hint_redos) *hint_redos = h[4];
     if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters, 0, sizeof(int) * 5));
+    return SE2_OK;
+}
+
+se2_status se2_guard_stats(se2_kernel k, int64_t* div_clamps, int64_t* prox_noconv, int32_t reset) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    DeviceGuard g(k->device);
+    unsigned int h[4] = {0, 0, 0, 0};
+    SE2_CUDA_TRY(cudaDeviceSynchronize());
+    SE2_CUDA_TRY(cudaMemcpy(h, k->guard, sizeof(h), cudaMemcpyDeviceToHost));
+    if (div_clamps) *div_clamps = h[0];
+    if (prox_noconv) *prox_noconv = h[1];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->guard, 0, sizeof(h)));
     return SE2_OK;
 }
 

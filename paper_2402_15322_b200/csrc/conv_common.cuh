@@ -133,6 +133,9 @@ __device__ __forceinline__ float block_sum(float v, float* red /* >= NT/32 float
 template <bool LOG>
 __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, int ix, int iy, float y) {
     float err = 0.f;
+    // the engine's own shift hint for the next iteration: every row it computed, halo rows included
+    // (their outputs are not stored, but a stale hint there would only force the verified redo)
+    if (LOG && e.hint_out != nullptr && e.slab_hi > 0) e.hint_out[idx] = y;
     if (e.slab_hi > 0 && (iy < e.slab_lo || iy >= e.slab_hi)) return 0.f;   // a neighbour's row: not ours
     if (e.op == EPI_DOT) return LOG ? expf(e.err_a[idx] + y) : e.err_a[idx] * y;
     if (e.err_a != nullptr) {
@@ -141,7 +144,7 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
         float row = LOG ? expf(a_old + y) : a_old * y;
         err = fabsf(row - mu);
     }
-    if (LOG && e.hint_out != nullptr) e.hint_out[idx] = y;
+    if (LOG && e.hint_out != nullptr && e.slab_hi == 0) e.hint_out[idx] = y;
     float o;
     switch (e.op) {
         case EPI_STORE: o = y; break;
@@ -150,24 +153,39 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
                 const float t = e.target[idx];
                 o = (t == -INFINITY) ? -INFINITY : t - y;   // log(0 / y) = -inf, as 0 / max(y, floor) = 0
             } else {
+                if (y < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
                 o = e.target[idx] / fmaxf(y, kDivFloor);
             }
             break;
         case EPI_MULTIPLY: o = LOG ? (e.target[idx] + y) : (e.target[idx] * y); break;
         case EPI_PROX: {
             if (e.prox_kind == 2) {
-                // porous medium: u = log s solves c e^{(m-1) u} + u - log z = 0; Newton from
-                // u = log z (the root is <= log z; g is convex increasing, so the iterates decrease
-                // monotonically to it)
+                // porous medium: u = log s solves g(u) = c e^{(m-1) u} + u - log z = 0, g convex
+                // and increasing.  Bracket: g(lz) > 0, and at lo = min(lz - 50, (ln 50 - ln c)/(m-1)) both
+                // c e^{(m-1) lo} <= 50 and lo - lz <= -50, so g(lo) <= 0.  Newton from lz, falling back to
+                // bisection of the bracket whenever a step leaves it or fails to halve it (safeguarded
+                // Newton); c e^{...} is evaluated as exp(ln c + (m-1) u) with the exponent capped at 88
+                // (no overflow far above the root).  Sites not converged in 64 steps are counted.
+                if (!LOG && y < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
                 const float lz = LOG ? y : logf(fmaxf(y, kDivFloor));
-                float u = lz;
-                for (int it = 0; it < 60; ++it) {
-                    const float ex = e.prox_c * expf(e.prox_m1 * u);
+                float lo = fminf(lz - 50.f, (3.9120230054f - e.prox_lnc) / e.prox_m1), hi = lz;
+                float u = lz, dold = hi - lo;
+                bool conv = false;
+                for (int it = 0; it < 64; ++it) {
+                    const float ex = expf(fminf(e.prox_lnc + e.prox_m1 * u, 88.f));
                     const float g = ex + u - lz;
-                    const float du = g / (e.prox_m1 * ex + 1.f);
-                    u -= du;
-                    if (fabsf(du) <= 1e-7f * (1.f + fabsf(u))) break;
+                    if (g > 0.f) hi = u; else lo = u;
+                    const float dg = e.prox_m1 * ex + 1.f;
+                    float un = u - g / dg;
+                    if (!(un > lo && un < hi) || fabsf(2.f * g) > fabsf(dold * dg)) un = 0.5f * (lo + hi);
+                    dold = un - u;
+                    u = un;
+                    if (fabsf(dold) <= 1e-7f * (1.f + fabsf(u)) || hi - lo <= 1e-7f * (1.f + fabsf(u))) {
+                        conv = true;
+                        break;
+                    }
                 }
+                if (!conv && e.guard != nullptr) atomicAdd(&e.guard[1], 1u);
                 o = LOG ? (u - lz) : expf(u - lz);
                 if (e.out2 != nullptr) e.out2[idx] = expf(u);
                 break;
@@ -178,6 +196,7 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
                 o = -e.prox_p * y - e.prox_q * V;
                 if (e.out2 != nullptr) e.out2[idx] = expf(o + y);
             } else {
+                if (y < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
                 float z = fmaxf(y, kDivFloor);
                 o = exp2f(-e.prox_p * log2f(z) - e.prox_q * V * kLog2e);
                 if (e.out2 != nullptr) e.out2[idx] = o * z;

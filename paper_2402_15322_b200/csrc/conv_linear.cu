@@ -45,7 +45,7 @@ struct LinCfg {
 template <int R, int WX, bool TMA, int NBUF = 2, int PP = 16>
 __global__ void __launch_bounds__(LinCfg<R, WX>::NT)
 conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, int nx, int ny, int nt,
-                   int band, int tiles_x, Epilogue epi, const __grid_constant__ CUtensorMap tmap) {
+                   int band, int tiles_x, int y_lo, int y_hi, Epilogue epi, const __grid_constant__ CUtensorMap tmap) {
     using C = LinCfg<R, WX, TMA, PP>;
     extern __shared__ __align__(128) float smem[];
     constexpr int WSTRIDE = TMA ? C::WINA : C::WIN;   // floats between the two window buffers
@@ -58,7 +58,7 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
     const int to = blockIdx.y;
     const int b = blockIdx.z;
     const int x0 = (tile % tiles_x) * C::TX;
-    const int y0 = (tile / tiles_x) * C::TY;
+    const int y0 = y_lo + (tile / tiles_x) * C::TY;   // output window [y_lo, y_hi) (slab kernels)
     const int64_t N = (int64_t)nx * ny * nt;
     const float* vin = in + (int64_t)b * N;
     const int lane = threadIdx.x & 31;
@@ -167,7 +167,7 @@ conv_linear_kernel(const float* __restrict__ in, const float* __restrict__ Wl, i
     // fused epilogue
     float err = 0.f;
     const int gy = y0 + lane;
-    if (gy < ny) {
+    if (gy < y_hi) {
 #pragma unroll
         for (int p = 0; p < C::P; ++p) {
             const int gx = x0 + wx * C::P + p;
@@ -193,8 +193,9 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
     using C = LinCfg<R, kLinWX, false>;
     using CT = LinCfg<R, kLinWX, true>;
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
-    int tiles_y = (k->ny + C::TY - 1) / C::TY;
+    int tiles_y = (k->wrows() + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, k->nt, batch);
+    const int ylo = k->wlo(), yhi = k->whi();
     if (bpf) *bpf = (int)(grid.x * grid.y);
     CUtensorMap tmap;
     const bool tma = make_field_tmap(&tmap, in, k->nx, k->ny, k->nt * batch, CT::PITCH, CT::WIN_H);
@@ -215,7 +216,7 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
                                  (int)smem);
         if (e != cudaSuccess) return e;
         conv_linear_kernel<R, kLinWX, true, 1><<<grid, CT::NT, smem, s>>>(in, epi.table ? epi.table : k->Wl, k->nx,
-                                                                         k->ny, k->nt, k->band, tiles_x, epi, tmap);
+                                                                         k->ny, k->nt, k->band, tiles_x, ylo, yhi, epi, tmap);
     } else if (tma) {
         size_t smem = CT::SMEM_TMA;
         if (occ > 0) {
@@ -226,13 +227,13 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
                                  (int)smem);
         if (e != cudaSuccess) return e;
         conv_linear_kernel<R, kLinWX, true><<<grid, CT::NT, smem, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
-                                                                            tiles_x, epi, tmap);
+                                                                            tiles_x, ylo, yhi, epi, tmap);
     } else {
         e = cudaFuncSetAttribute(conv_linear_kernel<R, kLinWX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)C::SMEM);
         if (e != cudaSuccess) return e;
         conv_linear_kernel<R, kLinWX, false><<<grid, C::NT, C::SMEM, s>>>(in, epi.table ? epi.table : k->Wl, k->nx, k->ny, k->nt, k->band,
-                                                                         tiles_x, epi, tmap);
+                                                                         tiles_x, ylo, yhi, epi, tmap);
     }
     count_launch();
     return cudaGetLastError();
@@ -241,7 +242,7 @@ static cudaError_t launch_lin_r(const se2_kernel_s* k, const float* in, int batc
 int conv_blocks_per_field_linear(const se2_kernel_s* k) {
     using C = LinCfg<1, kLinWX, false>;   // all radii and variants share the tile geometry
     int tiles_x = (k->nx + C::TX - 1) / C::TX;
-    int tiles_y = (k->ny + C::TY - 1) / C::TY;
+    int tiles_y = (k->wrows() + C::TY - 1) / C::TY;
     return tiles_x * tiles_y * k->nt;
 }
 

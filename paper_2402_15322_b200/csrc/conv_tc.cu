@@ -138,6 +138,7 @@ struct TcArgs {
     uint32_t a_stage, b_stage;
     int tmem_cols;
     int rows_out;              // output rows a CTA owns (<= kTcRows; the M tile's remaining rows are discarded)
+    int y_lo, y_hi;            // output window (kernel's win_lo / win_hi): rows outside are input-only halos
     // balanced mode (PIECES): 8-row tiles, CTA c takes chain units [c q, (c + 1) q) of the concatenated
     // (tile, input row) list; every piece's sums go to `part` [tile][piece < 3][128][npad]
     int batch, nblk, ngroups, ug, q;
@@ -146,8 +147,8 @@ struct TcArgs {
 
 // chain length (input rows) of 8-row group g, and the units before it within one (field, block)
 __device__ __forceinline__ int tc_group_len(const TcArgs& a, int g) {
-    const int y0 = g * kTcRows;
-    return min(a.ny - 1, y0 + kTcRows - 1 + a.R) - max(0, y0 - a.R) + 1;
+    const int y0 = a.y_lo + g * kTcRows;
+    return min(a.ny - 1, min(a.y_hi - 1, y0 + kTcRows - 1) + a.R) - max(0, y0 - a.R) + 1;
 }
 __device__ __forceinline__ int tc_group_prefix(const TcArgs& a, int g) {
     int s = 0;
@@ -166,12 +167,12 @@ template <bool PIECES>
 __device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
     if (!PIECES) {
         if (k > 0) return false;
-        pc.y0 = blockIdx.x * a.rows_out;
+        pc.y0 = a.y_lo + blockIdx.x * a.rows_out;
         pc.blk = blockIdx.y;
         pc.b = blockIdx.z;
         pc.ylo = max(0, pc.y0 - a.R);
         pc.r0 = 0;
-        pc.r1 = min(a.ny - 1, pc.y0 + a.rows_out - 1 + a.R) - pc.ylo + 1;
+        pc.r1 = min(a.ny - 1, min(a.y_hi - 1, pc.y0 + a.rows_out - 1) + a.R) - pc.ylo + 1;
         pc.tile = 0;
         pc.p = 0;
         return true;
@@ -189,7 +190,7 @@ __device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
         if (kk == k) {
             pc.b = grp / a.nblk;
             pc.blk = grp - pc.b * a.nblk;
-            pc.y0 = g * kTcRows;
+            pc.y0 = a.y_lo + g * kTcRows;
             pc.ylo = max(0, pc.y0 - a.R);
             pc.r0 = u - st;
             pc.r1 = r1;
@@ -525,7 +526,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                 const int m = (128 / kTcFlushWarps) * f + mm;
                 const int r = m / kTcBlk, tol = m % kTcBlk;
                 const int y = pc.y0 + r, to = pc.blk * kTcBlk + tol;
-                if (y >= a.ny || r >= a.rows_out) continue;
+                if (y >= a.y_hi || r >= a.rows_out) continue;
                 const int64_t rowbase = (int64_t)pc.b * N + ((int64_t)to * a.ny + y) * a.nx;
                 for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
             }
@@ -580,8 +581,8 @@ __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilo
     float err = 0.f;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const int r = r0 + 4 * k, y = g * kTcRows + r;
-        if (y >= a.ny || x0 >= a.nx) continue;
+        const int r = r0 + 4 * k, y = a.y_lo + g * kTcRows + r;
+        if (y >= a.y_hi || x0 >= a.nx) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
         const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
 #pragma unroll
@@ -610,7 +611,7 @@ static int tc_rows_out(const se2_kernel_s* k) {
     int best = kTcRows;
     double best_cost = 1e300;
     for (int rows = kTcRows; rows >= 4; --rows) {
-        const double ctas = (double)((k->ny + rows - 1) / rows) * (k->nt / kTcBlk) * k->max_batch;
+        const double ctas = (double)((k->wrows() + rows - 1) / rows) * (k->nt / kTcBlk) * k->max_batch;
         const double cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
         if (cost < best_cost - 1e-9) { best_cost = cost; best = rows; }
     }
@@ -619,11 +620,12 @@ static int tc_rows_out(const se2_kernel_s* k) {
 
 // balanced mode geometry (host mirror of tc_group_len / tc_group_prefix)
 static int tc_group_len_h(const se2_kernel_s* k, int g) {
-    const int y0 = g * kTcRows;
-    return std::min(k->ny - 1, y0 + kTcRows - 1 + k->R) - std::max(0, y0 - k->R) + 1;
+    const int y0 = k->wlo() + g * kTcRows;
+    return std::min(k->ny - 1, std::min(k->whi() - 1, y0 + kTcRows - 1) + k->R) - std::max(0, y0 - k->R) + 1;
 }
+static int tc_ngroups(const se2_kernel_s* k) { return (k->wrows() + kTcRows - 1) / kTcRows; }
 static void tc_units(const se2_kernel_s* k, int batch, int* ug, int* lmax, long long* U) {
-    const int ngroups = (k->ny + kTcRows - 1) / kTcRows;
+    const int ngroups = tc_ngroups(k);
     *ug = 0;
     *lmax = 0;
     for (int g = 0; g < ngroups; ++g) {
@@ -641,9 +643,9 @@ static int tc_units_per_cta(const se2_kernel_s* k, int batch) {
 }
 
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
-    if (k->tc_part != nullptr) return (k->ny + kTcRows - 1) / kTcRows * k->nt;   // balanced: epilogue blocks
+    if (k->tc_part != nullptr) return tc_ngroups(k) * k->nt;   // balanced: epilogue blocks
     const int rows = tc_rows_out(k);
-    return (k->ny + rows - 1) / rows * (k->nt / kTcBlk);
+    return (k->wrows() + rows - 1) / rows * (k->nt / kTcBlk);
 }
 
 // 5-D tensor map over split weights w: one TMA box per pipeline stage ([hl][chunk][8 j][16 to x 8 ti])
@@ -678,28 +680,25 @@ cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t conv_tc_prepare(se2_kernel_s* k) {
-    if (!conv_tc_eligible(k)) return cudaSuccess;
+// default-engine and geometry decisions for the kernel's output window (at build, and again when
+// se2_kernel_set_window changes the window): tc_fast (K10 vs K2 cost model) and the balanced mode's
+// partial buffer (allocated when that mode is chosen)
+cudaError_t conv_tc_decide(se2_kernel_s* k) {
+    if (k->tc_w == nullptr) return cudaSuccess;
     const TcGeom g = tc_geom(k);
-    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
-    const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
-    cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
-    if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
-    if (e != cudaSuccess) return e;
-    k->tc_w_hl = wk_hl;
-    k->tc_x_hl = xk_hl;
+    cudaError_t e = cudaSuccess;
     {
         // cost model at batch 1 (measured on B200, K10): K10 = waves x one CTA's MMA chain
         // ((8 + 2R) rows x S taps x K/16 steps x 3 passes x N/2 cycles) at ~70% of the tensor floor,
         // K2 = 2 nnz N flop at ~60 TFLOP/s (0.82 of the FFMA peak)
         const int rows = tc_rows_out(k);
-        const double ctas = (double)((k->ny + rows - 1) / rows) * g.nblk;
+        const double ctas = (double)((k->wrows() + rows - 1) / rows) * g.nblk;
         const double waves = std::ceil(ctas / 148.0);
         const double row_cyc = (double)k->S * (g.nwin / 2) * 3 * (g.npad / 2);   // one input row's MMA chain
         double t10 = waves * std::min(k->ny, rows + 2 * k->R) * row_cyc / 0.7 / 1.9e9 + 8e-6;
         // the balanced mode (chosen below when it is cheaper): q input rows per SM + its epilogue pass
         t10 = std::min(t10, tc_units_per_cta(k, 1) * row_cyc / 0.7 / 1.9e9 + 20e-6);
-        const double t2 = 2.0 * (double)k->nnz_taps * (double)k->N() / 60e12 + 4e-6;
+        const double t2 = 2.0 * (double)k->nnz_taps * k->nx * k->wrows() * k->nt / 60e12 + 4e-6;
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
     }
     {
@@ -710,15 +709,34 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
         tc_units(k, k->max_batch, &ug, &lmax, &U);
         const int q = tc_units_per_cta(k, k->max_batch);
         const int rows = tc_rows_out(k);
-        const double ctas = (double)((k->ny + rows - 1) / rows) * g.nblk * k->max_batch;
+        const double ctas = (double)((k->wrows() + rows - 1) / rows) * g.nblk * k->max_batch;
         const double rows_cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
         const bool want = getenv("SE2_TC_PIECES") ? (atoi(getenv("SE2_TC_PIECES")) != 0) : (q < 0.95 * rows_cost);
-        if (want) {
+        if (want && k->tc_part == nullptr) {
+            // sized for the whole grid: any later output window has at most as many 8-row tiles
             const size_t tiles = (size_t)k->max_batch * g.nblk * ((k->ny + kTcRows - 1) / kTcRows);
             e = cudaMalloc(&k->tc_part, tiles * 3 * 128 * g.npad * sizeof(float));
             if (e != cudaSuccess) return e;
+        } else if (!want && k->tc_part != nullptr) {
+            cudaFree(k->tc_part);
+            k->tc_part = nullptr;
         }
     }
+    return e;
+}
+
+cudaError_t conv_tc_prepare(se2_kernel_s* k) {
+    if (!conv_tc_eligible(k)) return cudaSuccess;
+    const TcGeom g = tc_geom(k);
+    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
+    const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
+    cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
+    if (e != cudaSuccess) return e;
+    k->tc_w_hl = wk_hl;
+    k->tc_x_hl = xk_hl;
+    e = conv_tc_decide(k);
+    if (e != cudaSuccess) return e;
     e = tc_weight_map(k, k->tc_w, &k->tc_wmap);
     if (e != cudaSuccess) return e;
     tc_split_weights_kernel<<<592, 256>>>(k->Wl, reinterpret_cast<__nv_bfloat16*>(k->tc_w), wk_hl, k->nt, k->S, g.nch,
@@ -788,6 +806,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.tmem_cols = g.tmem_cols;
+    a.y_lo = k->wlo();
+    a.y_hi = k->whi();
     const CUtensorMap* wm = reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmap : k->tc_wmap);
     if (k->tc_part != nullptr) {
         // balanced mode: 8-row tiles, equal runs of chain units per CTA, partials + epilogue kernel
@@ -797,7 +817,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         a.rows_out = kTcRows;
         a.batch = batch;
         a.nblk = g.nblk;
-        a.ngroups = (k->ny + kTcRows - 1) / kTcRows;
+        a.ngroups = tc_ngroups(k);
         a.q = tc_units_per_cta(k, batch);
         a.part = reinterpret_cast<float*>(k->tc_part);
         const int ncta = (int)((U + a.q - 1) / a.q);
@@ -818,7 +838,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     }
     a.rows_out = tc_rows_out(k);
     a.part = nullptr;
-    dim3 grid((k->ny + a.rows_out - 1) / a.rows_out, g.nblk, batch);
+    dim3 grid((k->wrows() + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
     {
         cudaLaunchConfig_t c = cfg_of(grid, dim3(kTcThreads), g.smem);

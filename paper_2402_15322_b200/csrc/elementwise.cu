@@ -164,7 +164,7 @@ cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, floa
 
 // Linear domain: mu = prod_i d_i^lambda_i ; v_i <- v_i * mu / max(d_i, floor); bary = mu.
 __global__ void bary_update_lin_kernel(int n, int nsolve, int64_t N, float* v, const float* d, const float* lam,
-                                       float* bary) {
+                                       float* bary, unsigned int* guard) {
     const int64_t total = (int64_t)nsolve * N;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int sv = (int)(t / N);
@@ -176,14 +176,15 @@ __global__ void bary_update_lin_kernel(int n, int nsolve, int64_t N, float* v, c
         }
         for (int i = 0; i < n; ++i) {
             int64_t o = ((int64_t)sv * n + i) * N + x;
+            if (d[o] < kDivFloor && guard != nullptr) atomicAdd(&guard[0], 1u);   // counted clamp (R9)
             v[o] = v[o] * mu / fmaxf(d[o], kDivFloor);
         }
         bary[t] = mu;
     }
 }
 cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const float* d, const float* lam_dev,
-                                   float* bary, cudaStream_t s) {
-    bary_update_lin_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, v, d, lam_dev, bary);
+                                   float* bary, unsigned int* guard, cudaStream_t s) {
+    bary_update_lin_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, v, d, lam_dev, bary, guard);
     count_launch();
     return cudaGetLastError();
 }

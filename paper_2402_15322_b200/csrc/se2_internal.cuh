@@ -80,7 +80,10 @@ struct Epilogue {
     // prox (entropy + potential): p = tau/(eps+tau) exponent, q = tau/(eps+tau) potential factor
     int prox_kind = 1;               // 1 entropy + potential, 2 porous medium
     float prox_p = 0.f, prox_q = 0.f;
-    float prox_c = 0.f, prox_m1 = 0.f; // porous: c = tau m / (eps (m-1)), m1 = m - 1
+    float prox_lnc = 0.f, prox_m1 = 0.f; // porous: ln c, c = tau m / (eps (m-1)) cell^{1-m}; m1 = m - 1
+    // guard counters (device, k->guard): [0] linear-domain denominators clamped at kDivFloor (R9, SPEC
+    // S:219 "counted and reported"), [1] porous prox sites whose safeguarded Newton did not converge
+    unsigned int* guard = nullptr;
     float cx = 0.f, cy = 0.f, hx = 0.f, hy = 0.f;
     // slab decomposition with peer-memory halos (se2_conv_update_slab): own rows [slab_lo, slab_hi) of a
     // plane of ny_self x nx_self; slab_hi == 0: off
@@ -108,6 +111,7 @@ struct se2_kernel_s {
     int max_batch = 1;
     int band = 0;           // fp32-nonzero theta half band (bins)
     int64_t nnz_taps = 0;   // per output
+    int64_t nnz_normal_taps = 0;   // per output: taps whose fp32 value is a normal number (the algorithmic work)
     // device tables, theta-quad interleaved: [nt/4][nt][S][S][4]  (to = 4*qd + q)
     float* Eq = nullptr;    // exp(Ls + kEsShift) fp32, quad-interleaved (factored LSE engine)
     float* Lth = nullptr;   // [nt][nt] theta part of L (natural log)
@@ -134,6 +138,13 @@ struct se2_kernel_s {
     void* tc_part = nullptr;      // balanced mode: per-piece partial sums [tiles][3][128][npad] (null: off)
     void* tc_wcmap = nullptr;
     bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
+    unsigned int* guard = nullptr;  // [4] guard counters (Epilogue::guard), zeroed per solve
+    // output window (slab decomposition, se2_kernel_set_window): every conv computes and stores only the
+    // output rows [win_lo, win_hi) of each plane; rows outside are input-only halo rows.  Default: all.
+    int win_lo = 0, win_hi = 0;
+    int wlo() const { return win_lo; }
+    int whi() const { return win_hi > 0 ? win_hi : ny; }
+    int wrows() const { return whi() - wlo(); }
     se2::Timing timing;
     int64_t N() const { return (int64_t)nx * ny * nt; }
 };
@@ -150,6 +161,7 @@ int conv_blocks_per_field(const se2_kernel_s* k, bool log_domain, uint32_t flags
 // K10 (conv_tc.cu): tensor-core linear conv; used for the Gibbs-kernel linear conv when prepared
 bool conv_tc_eligible(const se2_kernel_s* k);
 cudaError_t conv_tc_prepare(se2_kernel_s* k);
+cudaError_t conv_tc_decide(se2_kernel_s* k);   // re-run K10's engine / geometry choice (window changes)
 void conv_tc_release(se2_kernel_s* k);
 cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s);
 int conv_blocks_per_field_tc(const se2_kernel_s* k);
@@ -196,7 +208,7 @@ cudaError_t launch_bary_logmean_update(int n, int nsolve, int64_t N, const float
 cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
                                    const float* lbar, cudaStream_t s);
 cudaError_t launch_bary_update_lin(int n, int nsolve, int64_t N, float* v, const float* d,
-                                   const float* lam_dev, float* bary, cudaStream_t s);
+                                   const float* lam_dev, float* bary, unsigned int* guard, cudaStream_t s);
 cudaError_t launch_sum(const float* x, int64_t n, double* out_dev, double* scratch, cudaStream_t s);
 cudaError_t launch_scale(float* x, int64_t n, const double* sum_dev, cudaStream_t s);
 cudaError_t launch_sum_rows(const float* x, int planes, int ny, int nx, int row0, int rows, double* out_dev,

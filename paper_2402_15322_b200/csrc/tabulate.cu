@@ -59,6 +59,7 @@ __global__ void tabulate_kernel(double hx, double hy, int nt, int R, double eps,
         const int SP = (S + 3) / 4 * 4;
         Wl[(((int64_t)to * nt + ti) * S + dyi) * SP + dxi] = wv;
         if (wv != 0.0f) atomicAdd(&nnz_pair[to * nt + ti], 1);
+        if (wv >= 1.17549435e-38f) atomicAdd(&nnz_pair[nt * nt + to * nt + ti], 1);   // fp32 normals
     }
 }
 
@@ -146,9 +147,9 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     const int nt = k->nt, S = k->S;
     const int64_t total = (int64_t)nt * nt * S * S;
     int* nnz_dev = nullptr;
-    cudaError_t e = cudaMalloc(&nnz_dev, sizeof(int) * nt * nt);
+    cudaError_t e = cudaMalloc(&nnz_dev, 2 * sizeof(int) * nt * nt);   // nonzero, normal
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(nnz_dev, 0, sizeof(int) * nt * nt, s);
+    cudaMemsetAsync(nnz_dev, 0, 2 * sizeof(int) * nt * nt, s);
     // padding entries of a partial last quad (nt % 4 != 0) stay zero / -inf-like
     int threads = 256;
     int blocks = (int)((total + threads - 1) / threads);
@@ -164,13 +165,14 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(nnz_dev); return e; }
-    std::vector<int> nnz(nt * nt);
-    e = cudaMemcpyAsync(nnz.data(), nnz_dev, sizeof(int) * nt * nt, cudaMemcpyDeviceToHost, s);
+    std::vector<int> nnz(2 * nt * nt);
+    e = cudaMemcpyAsync(nnz.data(), nnz_dev, 2 * sizeof(int) * nt * nt, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(nnz_dev);
     if (e != cudaSuccess) return e;
     int band = 0;
-    int64_t nnz_total = 0;
+    int64_t nnz_total = 0, nnz_normal = 0;
+    for (int i = 0; i < nt * nt; ++i) nnz_normal += nnz[nt * nt + i];
     for (int to = 0; to < nt; ++to)
         for (int ti = 0; ti < nt; ++ti) {
             if (nnz[to * nt + ti] == 0) continue;
@@ -182,6 +184,7 @@ cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s) {
         }
     k->band = band;
     k->nnz_taps = nnz_total / nt;
+    k->nnz_normal_taps = nnz_normal / nt;
     return cudaSuccess;
 }
 

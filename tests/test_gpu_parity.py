@@ -343,7 +343,7 @@ def test_sinkhorn_k9_selection(cuda_device):
         a2, b2 = torch.empty_like(mu), torch.empty_like(mu)
         se2_sinkhorn(k, mu, nu, a2, b2, 20, True, persistent=False)
         e = gauge_fixed_pair_err(_host(a), _host(b), _host(a2), _host(b2))
-        assert max(e.values()) < 1e-5, e
+        assert max(e.values()) < TOL_POT, e
 
 
 @pytest.mark.parametrize("engine", ["tc", "ffma"])
