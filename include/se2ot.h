@@ -206,6 +206,21 @@ SE2_API se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const
                           double* err_trace_host, se2_stream stream);
 
 /* ------------------------------------------------------------------------------------------
+ * se2_barycenter_precise -- App. A in the log domain with the potentials held in fp64 and every
+ *   conv on K4P (exact per-tap log-sum-exp with exact exponents: TwoSum of float pairs, integer shifts,
+ *   fp64 row-sum accumulation; ~1e-7 nats per conv): the engine of the north star's elementwise 1e-4
+ *   parity on potentials of 10^2..10^3 nats (reading R19, SURVEY ledger L16).  Same arguments as
+ *   se2_barycenter with fp64 outputs: lbary [nsolve][N] = log mu, lv_state / lw_state (nullable)
+ *   [nsolve][n][N] = log v_i / log w_i (with SE2_WARM_START lv_state is also the initial log v_i).
+ *   SE2_LOG_DOMAIN is implied.  The L2 pair table is built on the first call.
+ * se2_conv_precise -- out = log(K exp(in)) on K4P, fp64 fields [batch][N].
+ * ---------------------------------------------------------------------------------------- */
+SE2_API se2_status se2_barycenter_precise(se2_kernel k, int32_t n, int32_t nsolve, const float* mus,
+                                          const double* lambdas, double* lbary, double* lv_state, double* lw_state,
+                                          const se2_opts* opts, double* err_trace_host, se2_stream stream);
+SE2_API se2_status se2_conv_precise(se2_kernel k, const double* in, double* out, int32_t batch, se2_stream stream);
+
+/* ------------------------------------------------------------------------------------------
  * se2_marginal_error -- err_host[i] = sum_x |a_i(x) (K b_i)(x) - mu_i(x)|  (R8) for
  *   i < batch.  Under SE2_LOG_DOMAIN a, b are logs.  Deterministic two-stage reduction.
  * ---------------------------------------------------------------------------------------- */

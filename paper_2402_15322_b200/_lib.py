@@ -48,6 +48,7 @@ EXPORTED = [
     "se2_bary_reduce_update", "se2_conv_update_slab", "se2_guard_stats", "se2_kernel_set_window",
     "se2_comm_unique_id", "se2_comm_init", "se2_comm_init_loopback", "se2_comm_split", "se2_comm_info",
     "se2_comm_allreduce", "se2_comm_destroy", "se2_jko_step_dist", "se2_barycenter_dist",
+    "se2_barycenter_precise", "se2_conv_precise",
 ]
 
 
@@ -131,6 +132,8 @@ def load(path: str = LIB_PATH):
         "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_guard_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_kernel_set_window": [P, i32, i32],
+        "se2_barycenter_precise": [P, i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],
+        "se2_conv_precise": [P, P, P, i32, P],
         "se2_comm_unique_id": [ctypes.c_char_p],
         "se2_comm_init": [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(P)],
         "se2_comm_init_loopback": [i32, i32, ctypes.POINTER(P)],

@@ -233,6 +233,54 @@ def se2_barycenter(k: Kernel, mus: torch.Tensor, lambdas, iters: int, log_domain
     return bary, (tr[:iters] if trace else None)
 
 
+def _check_field64(t, k: Kernel, name: str, batch: Optional[int] = None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor (the precise path's fp64 potentials)")
+    if t.numel() % k.N != 0 or (batch is not None and t.numel() != batch * k.N):
+        raise ValueError(f"{name} must hold {batch if batch is not None else 'whole'} fields of N={k.N}")
+
+
+def se2_conv_precise(k: Kernel, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """log(K exp(x)) on K4P (fp64 fields; exact exponents, ~1e-7 nats per conv)."""
+    _check_field64(x, k, "x")
+    batch = x.numel() // k.N
+    if out is None:
+        out = torch.empty_like(x)
+    _check_field64(out, k, "out", batch)
+    check(L.load().se2_conv_precise(k.handle, _ptr(x), _ptr(out), batch, _stream(x.device)))
+    return out
+
+
+def se2_barycenter_precise(k: Kernel, mus: torch.Tensor, lambdas, iters: int,
+                           lbary: Optional[torch.Tensor] = None, lv_state: Optional[torch.Tensor] = None,
+                           lw_state: Optional[torch.Tensor] = None, trace: bool = False, no_graph: bool = False,
+                           warm_start: bool = False):
+    """App. A in the log domain with fp64 potentials on K4P (reading R19).  mus: float32
+    [n][N]; returns (log mu [nsolve][N] float64, err trace [iters][nsolve] or None)."""
+    _check_field(mus, k, "mus")
+    n = mus.numel() // k.N
+    lam = np.ascontiguousarray(np.atleast_2d(np.asarray(lambdas, dtype=np.float64)))
+    if lam.shape[1] != n:
+        raise ValueError(f"lambdas must be [nsolve][{n}]")
+    nsolve = lam.shape[0]
+    if lbary is None:
+        lbary = torch.empty((nsolve, k.ntheta, k.ny, k.nx), device=mus.device, dtype=torch.float64)
+    _check_field64(lbary, k, "lbary", nsolve)
+    for name, t in (("lv_state", lv_state), ("lw_state", lw_state)):
+        if t is not None:
+            _check_field64(t, k, name, nsolve * n)
+    if warm_start and lv_state is None:
+        raise ValueError("warm_start needs lv_state")
+    opts = L.se2_opts(int(iters), _flags(True, trace, warm=warm_start, no_graph=no_graph))
+    tr = np.zeros((max(iters, 1), nsolve), dtype=np.float64) if trace else None
+    check(L.load().se2_barycenter_precise(k.handle, n, nsolve, _ptr(mus),
+                                          lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _ptr(lbary),
+                                          _ptr(lv_state), _ptr(lw_state), ctypes.byref(opts),
+                                          tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None,
+                                          _stream(mus.device)))
+    return lbary, (tr[:iters] if trace else None)
+
+
 def se2_marginal_error(k: Kernel, a: torch.Tensor, b: torch.Tensor, mu: torch.Tensor, log_domain: bool) -> np.ndarray:
     """err_i = sum |a_i K b_i - mu_i| (R8)."""
     _check_field(mu, k, "mu")

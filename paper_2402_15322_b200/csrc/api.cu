@@ -153,6 +153,8 @@ void se2_kernel_destroy(se2_kernel k) {
     se2::conv_tc_release(k);
     if (k->lse_counters) cudaFree(k->lse_counters);
     if (k->guard) cudaFree(k->guard);
+    if (k->L2hi) cudaFree(k->L2hi);
+    if (k->L2lo) cudaFree(k->L2lo);
     KernelExtra* x = extra(k);
     if (x) {
         x->clear_graphs();
@@ -590,6 +592,170 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
     const float* ps[3] = {bary, v, w};
     const int64_t ns[3] = {(int64_t)nsolve * N, FN, FN};
     return check_finite(k, ps, ns, 3, s);
+}
+
+// ---- barycenter with fp64 potentials (K4P; the elementwise 1e-4 parity of reading R19) --------------
+static se2_status run_conv_precise(se2_kernel_s* k, const double* in, int batch, const EpiP& epi, cudaStream_t s) {
+    Timing& t = k->timing;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (t.on) {
+        if (t.used == t.events.size()) {
+            cudaEvent_t a, b;
+            SE2_CUDA_TRY(cudaEventCreate(&a));
+            SE2_CUDA_TRY(cudaEventCreate(&b));
+            t.events.push_back({a, b});
+        }
+        e0 = t.events[t.used].first;
+        e1 = t.events[t.used].second;
+        t.used++;
+        SE2_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    cudaError_t e = launch_conv_lse_precise(k, in, batch, epi, s, nullptr);
+    if (e != cudaSuccess) {
+        set_error(std::string("precise conv launch: ") + cudaGetErrorString(e));
+        return SE2_ECUDA;
+    }
+    t.all_launches++;
+    if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
+    return SE2_OK;
+}
+
+se2_status se2_conv_precise(se2_kernel k, const double* in, double* out, int32_t batch, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(in && out && (const void*)in != (const void*)out, "in/out must be distinct non-null device pointers");
+    SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    SE2_CUDA_TRY(tabulate_precise(k, s));
+    EpiP epi;
+    epi.op = EPI_STORE;
+    epi.out = out;
+    return run_conv_precise(k, in, batch, epi, s);
+}
+
+se2_status se2_barycenter_precise(se2_kernel k, int32_t n, int32_t nsolve, const float* mus, const double* lambdas,
+                                  double* lbary, double* lv_state, double* lw_state, const se2_opts* opts,
+                                  double* err_trace_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
+    SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n, nsolve >= 1");
+    SE2_CHECK_ARG((int64_t)n * nsolve <= k->max_batch, "n*nsolve exceeds max_batch");
+    SE2_CHECK_ARG(mus && lambdas && lbary, "null pointer");
+    for (int sv = 0; sv < nsolve; ++sv) {
+        double sum = 0;
+        for (int i = 0; i < n; ++i) {
+            SE2_CHECK_ARG(lambdas[sv * n + i] >= 0 && isfinite(lambdas[sv * n + i]), "lambda must be >= 0");
+            sum += lambdas[sv * n + i];
+        }
+        SE2_CHECK_ARG(fabs(sum - 1.0) <= 1e-9, "lambdas must lie on the simplex");
+    }
+    const bool warm = (opts->flags & SE2_WARM_START) != 0;
+    SE2_CHECK_ARG(!warm || lv_state != nullptr, "SE2_WARM_START needs lv_state");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    SE2_CUDA_TRY(tabulate_precise(k, s));
+    se2_status st = reset_guard(k, s);
+    if (st != SE2_OK) return st;
+    const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
+    const int64_t N = k->N();
+    const int F = n * nsolve;
+    const int64_t FN = (int64_t)F * N;
+    const int iters = opts->iters;
+    KernelExtra* x = extra(k);
+    // workspace: mu_rep (float) [F][N]; lmu, v, w, d (double) [F][N]
+    st = ensure(x->ws, (size_t)FN * (sizeof(float) + 4 * sizeof(double)) + 64, x);
+    if (st != SE2_OK) return st;
+    float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
+    double* lmu = reinterpret_cast<double*>(reinterpret_cast<char*>(x->ws.ptr) + ((FN * sizeof(float) + 63) / 64) * 64);
+    double* v = lv_state ? lv_state : lmu + FN;
+    double* w = lw_state ? lw_state : lmu + 2 * FN;
+    double* d = lmu + 3 * FN;
+    st = ensure(x->misc, 4096 + sizeof(double) * F, x);
+    if (st != SE2_OK) return st;
+    const int bpf = conv_blocks_per_field_precise(k);
+    if (trace) {
+        st = ensure(x->partial, (size_t)F * bpf * sizeof(float), x);
+        if (st != SE2_OK) return st;
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * F * sizeof(double), x);
+        if (st != SE2_OK) return st;
+    }
+    float* partial = reinterpret_cast<float*>(x->partial.ptr);
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    double* lam_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(x->misc.ptr) + 4096);
+    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lambdas, sizeof(double) * F, cudaMemcpyHostToDevice, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint64_t> key = {5, as_key(mus), as_key(lbary), as_key(v), as_key(w), (uint64_t)n, (uint64_t)nsolve,
+                                 (uint64_t)iters, (uint64_t)opts->flags, (uint64_t)trace, as_key(x->ws.ptr),
+                                 as_key(x->misc.ptr), as_key(partial), as_key(tr)};
+    auto enqueue = [&](cudaStream_t s) -> se2_status {
+        se2_status st = SE2_OK;
+        for (int sv = 0; sv < nsolve; ++sv)
+            SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
+                                         cudaMemcpyDeviceToDevice, s));
+        SE2_CUDA_TRY(launch_log_f64(mu_rep, lmu, FN, s));
+        if (!warm) SE2_CUDA_TRY(launch_fill_f64(v, FN, 0.0, s));
+        SE2_CUDA_TRY(launch_fill_f64(w, FN, 0.0, s));
+        for (int j = 0; j < iters; ++j) {
+            EpiP e1;   // w_i = mu_i / K v_i  (error of the previous v-update fused)
+            e1.op = EPI_DIVIDE;
+            e1.target = lmu;
+            e1.out = w;
+            if (trace && j > 0) {
+                e1.err_a = w;
+                e1.err_mu = mu_rep;
+                e1.err_partial = partial;
+            }
+            st = run_conv_precise(k, v, F, e1, s);
+            if (st != SE2_OK) return st;
+            if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
+            EpiP e2;   // d_i = v_i K w_i
+            e2.op = EPI_MULTIPLY;
+            e2.target = v;
+            e2.out = d;
+            st = run_conv_precise(k, w, F, e2, s);
+            if (st != SE2_OK) return st;
+            SE2_CUDA_TRY(launch_bary_logmean_update_f64(n, nsolve, N, d, lam_dev, lbary, v, s));
+        }
+        if (trace && iters > 0) {
+            EpiP e3;
+            e3.op = EPI_ERRONLY;
+            e3.err_a = w;
+            e3.err_mu = mu_rep;
+            e3.err_partial = partial;
+            st = run_conv_precise(k, v, F, e3, s);
+            if (st != SE2_OK) return st;
+            SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
+        }
+        return SE2_OK;
+    };
+    st = run_graph(k, s, std::move(key), FN <= kGraphMaxElems && !(opts->flags & SE2_NO_GRAPH), enqueue);
+    if (st != SE2_OK) return st;
+    if (trace && iters > 0) {
+        std::vector<double> h((size_t)iters * F);
+        SE2_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, sizeof(double) * iters * F, cudaMemcpyDeviceToHost, s));
+        SE2_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int j = 0; j < iters; ++j)
+            for (int sv = 0; sv < nsolve; ++sv) {
+                double e = 0;
+                for (int i = 0; i < n; ++i) e += lambdas[sv * n + i] * h[(size_t)j * F + sv * n + i];
+                err_trace_host[(size_t)j * nsolve + sv] = e;
+            }
+    }
+    se2_status st2 = ensure(x->misc, 4096 + sizeof(double) * F, x);
+    if (st2 != SE2_OK) return st2;
+    int* cnt = reinterpret_cast<int*>(x->misc.ptr);
+    SE2_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(lbary, (int64_t)nsolve * N, cnt, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(v, FN, cnt, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(w, FN, cnt, s));
+    int h = 0;
+    SE2_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h != 0) {
+        set_error("non-finite values produced by the iteration (" + std::to_string(h) + " entries)");
+        return SE2_ENONFINITE;
+    }
+    return SE2_OK;
 }
 
 se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, const float* mu, int32_t batch,

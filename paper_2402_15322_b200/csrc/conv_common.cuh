@@ -216,4 +216,23 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
     return err;
 }
 
+// K4P's epilogue (fp64 potentials): out = target -+ ly, error of the previous iterate |a_old K b - mu|
+__device__ __forceinline__ float apply_epilogue_precise(const EpiP& e, int64_t idx, double ly) {
+    float err = 0.f;
+    if (e.err_a != nullptr) err = fabsf((float)exp(e.err_a[idx] + ly) - e.err_mu[idx]);
+    double o;
+    switch (e.op) {
+        case EPI_STORE: o = ly; break;
+        case EPI_DIVIDE: {
+            const double t = e.target[idx];
+            o = (t == -(double)INFINITY) ? -(double)INFINITY : t - ly;   // log(0 / y) = -inf
+            break;
+        }
+        case EPI_MULTIPLY: o = e.target[idx] + ly; break;
+        default: return err;   // EPI_ERRONLY
+    }
+    e.out[idx] = o;
+    return err;
+}
+
 }  // namespace se2

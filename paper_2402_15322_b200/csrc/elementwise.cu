@@ -155,6 +155,64 @@ cudaError_t launch_bary_reduce_update(int nranks, const float* const* parts, int
     return cudaGetLastError();
 }
 
+// ---- fp64 state of the precise barycenter (K4P) ----
+__global__ void log_f64_kernel(const float* x, double* y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = x[i];
+        y[i] = v > 0.f ? log((double)v) : -(double)INFINITY;
+    }
+}
+cudaError_t launch_log_f64(const float* x, double* y, int64_t n, cudaStream_t s) {
+    log_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+    count_launch();
+    return cudaGetLastError();
+}
+__global__ void fill_f64_kernel(double* x, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = v;
+}
+cudaError_t launch_fill_f64(double* x, int64_t n, double v, cudaStream_t s) {
+    fill_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, v);
+    count_launch();
+    return cudaGetLastError();
+}
+// lbar = sum_i lambda_i ld_i (lambda_i = 0 skipped, R6); lv_i += lbar - ld_i  -- in fp64
+__global__ void bary_logmean_update_f64_kernel(int n, int nsolve, int64_t N, const double* __restrict__ ld,
+                                               const double* __restrict__ lam, double* __restrict__ lbar,
+                                               double* __restrict__ lv) {
+    const int64_t total = (int64_t)nsolve * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int sv = (int)(t / N);
+        const int64_t x = t - (int64_t)sv * N;
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double l = lam[sv * n + i];
+            if (l != 0.0) acc += l * ld[((int64_t)sv * n + i) * N + x];
+        }
+        lbar[t] = acc;
+        for (int i = 0; i < n; ++i) {
+            const int64_t j = ((int64_t)sv * n + i) * N + x;
+            lv[j] += acc - ld[j];
+        }
+    }
+}
+cudaError_t launch_bary_logmean_update_f64(int n, int nsolve, int64_t N, const double* ld, const double* lam_dev,
+                                           double* lbar, double* lv, cudaStream_t s) {
+    bary_logmean_update_f64_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, ld, lam_dev, lbar, lv);
+    count_launch();
+    return cudaGetLastError();
+}
+__global__ void count_nonfinite_f64_kernel(const double* x, int64_t n, int* count) {
+    int c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += (isnan(x[i]) || (isinf(x[i]) && x[i] > 0.0)) ? 1 : 0;   // -inf is a valid log(0)
+    if (c) atomicAdd(count, c);
+}
+cudaError_t launch_count_nonfinite_f64(const double* x, int64_t n, int* count_dev, cudaStream_t s) {
+    count_nonfinite_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, count_dev);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bary_update_log(int n, int nsolve, int64_t N, float* lv, float* lv_lo, const float* ld,
                                    const float* lbar, cudaStream_t s) {
     bary_update_log_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, lv, lv_lo, ld, lbar);

@@ -94,6 +94,16 @@ struct Epilogue {
     int dn_shift = 0, ny_dn = 0;
 };
 
+// Epilogue of the fp64 log-domain engine (K4P, conv_lse_precise.cu): the same ops in fp64
+struct EpiP {
+    int op = EPI_STORE;
+    const double* target = nullptr;  // [batch][N] log targets
+    double* out = nullptr;
+    const double* err_a = nullptr;   // marginal error |exp(a_old + ly) - mu| (a_old read before out is written)
+    const float* err_mu = nullptr;
+    float* err_partial = nullptr;    // [batch][blocks_per_field]
+};
+
 struct Timing {
     bool on = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // pool
@@ -139,6 +149,8 @@ struct se2_kernel_s {
     void* tc_wcmap = nullptr;
     bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
     unsigned int* guard = nullptr;  // [4] guard counters (Epilogue::guard), zeroed per solve
+    float* L2hi = nullptr;          // K4P: L log2(e) as an exact float pair, Lq layout (built on first use)
+    float* L2lo = nullptr;
     // output window (slab decomposition, se2_kernel_set_window): every conv computes and stores only the
     // output rows [win_lo, win_hi) of each plane; rows outside are input-only halo rows.  Default: all.
     int win_lo = 0, win_hi = 0;
@@ -190,6 +202,12 @@ cudaError_t launch_conv_lse_fast(const se2_kernel_s* k, const float* in, int bat
                                  float* split_scratch, size_t split_floats);
 size_t lse_fast_stats_floats(const se2_kernel_s* k, int batch);
 
+// K4P (conv_lse_precise.cu): exact log-domain conv, fp64 potentials
+cudaError_t launch_conv_lse_precise(const se2_kernel_s* k, const double* in, int batch, const EpiP& epi,
+                                    cudaStream_t s, int* bpf);
+int conv_blocks_per_field_precise(const se2_kernel_s* k);
+cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s);   // L2hi / L2lo on first use
+
 // tabulation (tabulate.cu)
 cudaError_t tabulate(se2_kernel_s* k, cudaStream_t s);
 cudaError_t tabulate_cost(se2_kernel_s* k, cudaStream_t s);
@@ -215,5 +233,11 @@ cudaError_t launch_sum_rows(const float* x, int planes, int ny, int nx, int row0
                             double* scratch, cudaStream_t s);
 cudaError_t launch_scale_rows(float* x, int planes, int ny, int nx, int row0, int rows, double f, cudaStream_t s);
 cudaError_t launch_count_nonfinite(const float* x, int64_t n, int* count_dev, cudaStream_t s);
+// fp64 state of the precise barycenter
+cudaError_t launch_log_f64(const float* x, double* y, int64_t n, cudaStream_t s);
+cudaError_t launch_fill_f64(double* x, int64_t n, double v, cudaStream_t s);
+cudaError_t launch_bary_logmean_update_f64(int n, int nsolve, int64_t N, const double* ld, const double* lam_dev,
+                                           double* lbar, double* lv, cudaStream_t s);
+cudaError_t launch_count_nonfinite_f64(const double* x, int64_t n, int* count_dev, cudaStream_t s);
 
 }  // namespace se2

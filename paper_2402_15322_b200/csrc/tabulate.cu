@@ -17,6 +17,8 @@
 //                                exact path's bounds; an empty segment is -inf)
 #include <math.h>
 
+#include <algorithm>
+
 #include "se2_internal.cuh"
 
 namespace se2 {
@@ -61,6 +63,54 @@ __global__ void tabulate_kernel(double hx, double hy, int nt, int R, double eps,
         if (wv != 0.0f) atomicAdd(&nnz_pair[to * nt + ti], 1);
         if (wv >= 1.17549435e-38f) atomicAdd(&nnz_pair[nt * nt + to * nt + ti], 1);   // fp32 normals
     }
+}
+
+// K4P table: L2 = -rho_b^2/eps log2(e) as an exact float pair (hi = fl(L2), lo = fl(L2 - hi)), Lq layout
+__global__ void tabulate_l2pair_kernel(double hx, double hy, int nt, int R, double eps, double w1, double w2,
+                                       double w3, float* __restrict__ L2hi, float* __restrict__ L2lo) {
+    const int S = 2 * R + 1;
+    const int64_t total = (int64_t)nt * nt * S * S;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int dxi = (int)(idx % S);
+        const int dyi = (int)((idx / S) % S);
+        const int ti = (int)((idx / ((int64_t)S * S)) % nt);
+        const int to = (int)(idx / ((int64_t)S * S * nt));
+        const double two_pi = 6.283185307179586476925286766559;
+        const double ddx = (double)(dxi - R) * hx, ddy = (double)(dyi - R) * hy;
+        const double thi = two_pi * ti / nt;
+        const double ci = cos(thi), si = sin(thi);
+        const double X = ci * ddx + si * ddy, Y = -si * ddx + ci * ddy;   // R_{-theta_i} (dx, dy)
+        int k = ((to - ti) % nt + nt) % nt;
+        if (2 * k >= nt) k -= nt;
+        const double Th = two_pi * k / nt;                                  // wrap(theta_o - theta_i)
+        const double ch = cos(0.5 * Th), sh = sin(0.5 * Th);
+        const double b1 = X * ch + Y * sh, b2 = -X * sh + Y * ch;            // half-angle coordinates
+        const double rho2 = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2 + w3 * w3 * Th * Th;
+        const double l2 = -rho2 / eps * 1.4426950408889634073599246810019;
+        const int64_t o = ((((int64_t)(to >> 2) * nt + ti) * S + dyi) * S + dxi) * 4 + (to & 3);
+        const float hi = (float)l2;
+        L2hi[o] = hi;
+        L2lo[o] = (float)(l2 - (double)hi);
+    }
+}
+
+cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
+    if (k->L2hi != nullptr) return cudaSuccess;
+    const size_t n = (size_t)((k->nt + 3) / 4) * k->nt * k->S * k->S * 4;
+    cudaError_t e = cudaMalloc(&k->L2hi, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&k->L2lo, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemsetAsync(k->L2hi, 0, n * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(k->L2lo, 0, n * sizeof(float), s);
+    if (e != cudaSuccess) return e;
+    const int64_t total = (int64_t)k->nt * k->nt * k->S * k->S;
+    tabulate_l2pair_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, s>>>(
+        k->hx, k->hy, k->nt, k->R, k->eps, k->w1, k->w2, k->w3, k->L2hi, k->L2lo);
+    count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    k->table_bytes += 2 * n * sizeof(float);
+    return e;
 }
 
 // Lth[to][ti] = -w3^2 Theta^2/eps ; LseS[to][ti] = log sum_{dx,dy} exp(Ls(to,ti,dx,dy))  (fp64 sums)

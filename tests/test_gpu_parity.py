@@ -125,6 +125,33 @@ def test_barycenter_parity(case, cuda_device):
     assert trace_err(tr, gold["err"]) <= TOL_TRACE
 
 
+@pytest.mark.parametrize("case", ["c1", "c2m", "c2p", "c2f", "c3p", "c3m", "c3q"])
+def test_barycenter_parity_precise(case, cuda_device):
+    """App. A with fp64 potentials on K4P (se2_barycenter_precise, reading R19) against the oracle at the
+    north star's 1e-4 ELEMENTWISE on gauge-fixed potentials (L18) -- the configs whose log-potentials reach
+    10^2..10^3 nats, where fp32 storage alone is above 1e-4 (DESIGN.md §5 floor)."""
+    from paper_2402_15322_b200 import se2_barycenter_precise
+    pc = S.get_parity_case(case)
+    cfg, d = S.parity_inputs(pc)
+    gold = _golden(case)
+    lams = gold["lambdas"]
+    n, nsolve = len(d["mus"]), lams.shape[0]
+    k = _kernel(cfg, n * nsolve)
+    mus = _dev(np.stack(d["mus"]))
+    v = torch.empty((nsolve, n) + cfg.shape, device="cuda", dtype=torch.float64)
+    w = torch.empty_like(v)
+    lbar, tr = se2_barycenter_precise(k, mus, lams, cfg.iters, lv_state=v, lw_state=w, trace=True)
+    full = pc.full_fields
+    _cmp_pot("log bary", _sel(_host(lbar), gold, full), gold["lbary"].reshape(nsolve, -1))
+    _cmp_meas("bary", np.exp(_sel(_host(lbar), gold, full)), gold["bary_lin"].reshape(nsolve, -1))
+    glv, glw = _sel(_host(v), gold, full), _sel(_host(w), gold, full)
+    rlv, rlw = gold["lv"].reshape(nsolve, n, -1), gold["lw"].reshape(nsolve, n, -1)
+    for s in range(nsolve):
+        e = bary_potential_errs(glv[s], glw[s], rlv[s], rlw[s], lams[s])
+        assert max(e.values()) <= TOL_POT, (s, lams[s], e)
+    assert trace_err(tr, gold["err"]) <= TOL_TRACE
+
+
 @pytest.mark.parametrize("case", ["c4m", "c4p", "c5m", "c4q", "c4m-tc", "c4m-ffma", "c4q-ffma",
                                   "c4w", "c4w-tc", "c4w-ffma", "c4f"])
 def test_jko_parity(case, cuda_device):
