@@ -155,6 +155,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->guard) cudaFree(k->guard);
     if (k->L2hi) cudaFree(k->L2hi);
     if (k->L2lo) cudaFree(k->L2lo);
+    if (k->L2row) cudaFree(k->L2row);
     KernelExtra* x = extra(k);
     if (x) {
         x->clear_graphs();

@@ -38,8 +38,11 @@ struct LsePCfg {
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * S * 4;
     // window hi + lo, filter hi + lo, one buffer (the fp64 staging conversion is done by the threads)
-    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL) * sizeof(float) + 64;
+    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL + 4 * S) * sizeof(float) + 64;
 };
+// pruning margin (log2 units): a term below 2^-64 of every output it could reach is never evaluated;
+// the skipped mass is < S^2 nt 2^-64 < 2^-48 relative
+constexpr float kGap = 64.f;
 
 // a staged -inf (zero mass, zero padding) is the finite sentinel -1e30: TwoSum stays NaN-free and its
 // terms underflow to exactly 0; a pass-A maximum below -1e29 means "no finite term"
@@ -57,13 +60,15 @@ __device__ __forceinline__ void split2(double x, float& hi, float& lo) {
 template <int R>
 __global__ void __launch_bounds__(LsePCfg<R>::NT)
 conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__ L2hi, const float* __restrict__ L2lo,
-                        int nx, int ny, int nt, int tiles_x, int y_lo, int y_hi, EpiP epi) {
+                        const float* __restrict__ L2row, int nx, int ny, int nt, int tiles_x, int y_lo, int y_hi,
+                        EpiP epi) {
     using C = LsePCfg<R>;
     extern __shared__ __align__(16) float smem[];
     float* sWh = smem;
     float* sWl = smem + C::WIN;
     float* sFh = smem + 2 * C::WIN;
     float* sFl = sFh + C::FIL;
+    float* sRow = sFl + C::FIL;   // [S][4] max over each tap row of L2 (pruning bounds)
     __shared__ float sRed[C::NT / 32];
 
     const int tile = blockIdx.x;
@@ -91,7 +96,31 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
 #pragma unroll
         for (int p = 0; p < C::P; ++p) { m[q][p] = NEG_INF; sd[q][p] = 0.0; }
 
-    for (int ti = 0; ti < nt; ++ti) {
+    // valid outputs of this thread (bit 4 q + p)
+    unsigned vmask = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < C::P; ++p)
+            if (4 * qd + q < nt && y0 + lane < y_hi && x0 + wx * C::P + p < nx) vmask |= 1u << (4 * q + p);
+    // pruning floor per output orientation of this lane: min over its valid outputs of (shift - kGap);
+    // -inf while any of them has no finite term yet
+    auto floors = [&](float* lb) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float t = INFINITY;
+#pragma unroll
+            for (int p = 0; p < C::P; ++p)
+                if (vmask & (1u << (4 * q + p))) t = fminf(t, m[q][p]);
+            lb[q] = t - kGap;   // NEG_INF stays NEG_INF
+        }
+    };
+
+    // channels in order of increasing |theta_i - theta_o| around the quad: the dominant ones set the
+    // shifts early, so the pruning bounds below bite on the rest
+    for (int a = 0; a < nt; ++a) {
+        const int off = (a & 1) ? (a + 1) / 2 : -(a / 2);
+        const int ti = (((4 * qd + 1 + off) % nt) + nt) % nt;
         __syncthreads();   // the previous channel's readers are done
         {
             const double* src = vin + (int64_t)ti * nx * ny;
@@ -109,12 +138,33 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                 reinterpret_cast<float4*>(sFh)[i] = reinterpret_cast<const float4*>(fh)[i];
                 reinterpret_cast<float4*>(sFl)[i] = reinterpret_cast<const float4*>(fl)[i];
             }
+            const float* rm = L2row + ((int64_t)qd * nt + ti) * C::S * 4;
+            for (int i = threadIdx.x; i < C::S; i += C::NT)
+                reinterpret_cast<float4*>(sRow)[i] = reinterpret_cast<const float4*>(rm)[i];
         }
         __syncthreads();
         const float* wh = sWh + wx * C::P;
         const float* wl = sWl + wx * C::P;
         const float4* fh4 = reinterpret_cast<const float4*>(sFh);
         const float4* fl4 = reinterpret_cast<const float4*>(sFl);
+        const float4* rw4 = reinterpret_cast<const float4*>(sRow);
+
+        // channel bound of this warp: max of the window columns it reads + the channel's largest L2 (its
+        // centre tap, Ls(0) = 0 >= Ls(d)); a channel below every output's floor is skipped
+        float lb[4];
+        floors(lb);
+        {
+            float wm = kSent;
+            for (int r = lane; r < C::WIN_H; r += 32)
+#pragma unroll
+                for (int c = 0; c < C::RL; ++c) wm = fmaxf(wm, wh[r * C::PITCH + c]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+            const float4 cen = fh4[R * C::S + R];
+            const bool any = __any_sync(0xffffffffu, wm + cen.x >= lb[0] || wm + cen.y >= lb[1] ||
+                                                         wm + cen.z >= lb[2] || wm + cen.w >= lb[3]);
+            if (!any) continue;   // warp-uniform: no term of this channel can reach these outputs
+        }
 
         // pass A: approximate channel maximum (fp32 sums suffice: the shift only has to be near the max)
         float cm[4][C::P];
@@ -126,11 +176,17 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         for (int dy = 0; dy < C::S; ++dy) {
             const float4* rowp = reinterpret_cast<const float4*>(wh + (lane - dy + 2 * R) * C::PITCH);
             float r[C::RL];
+            float rmax = kSent;
 #pragma unroll
             for (int j = 0; j < C::RL / 4; ++j) {
                 const float4 t = rowp[j];
                 r[4 * j + 0] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
+                rmax = fmaxf(fmaxf(rmax, fmaxf(t.x, t.y)), fmaxf(t.z, t.w));
             }
+            const float4 rb = rw4[dy];   // max over the row's taps of L2 (per q)
+            if (!__any_sync(0xffffffffu, rmax + rb.x >= lb[0] || rmax + rb.y >= lb[1] || rmax + rb.z >= lb[2] ||
+                                             rmax + rb.w >= lb[3]))
+                continue;   // no tap of this row can raise any shift of the warp
 #pragma unroll
             for (int dx = 0; dx < C::S; ++dx) {
                 const float4 w = fh4[dy * C::S + dx];
@@ -158,49 +214,57 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                     m[q][p] = mn;
                 }
             }
-        // pass B: sum 2^(t - m) with exact exponents; row sums in fp32, the total in fp64
+        floors(lb);
+        // pass B: sum 2^(t - m) with exact exponents; row sums in fp32, the total in fp64.  A (row,
+        // orientation) whose largest term is below 2^-kGap of every output of the warp is skipped.
 #pragma unroll 1
         for (int dy = 0; dy < C::S; ++dy) {
             const float4* rowh = reinterpret_cast<const float4*>(wh + (lane - dy + 2 * R) * C::PITCH);
             const float4* rowl = reinterpret_cast<const float4*>(wl + (lane - dy + 2 * R) * C::PITCH);
             float rh[C::RL], rl[C::RL];
+            float rmax = kSent;
 #pragma unroll
             for (int j = 0; j < C::RL / 4; ++j) {
                 const float4 t = rowh[j];
                 rh[4 * j + 0] = t.x; rh[4 * j + 1] = t.y; rh[4 * j + 2] = t.z; rh[4 * j + 3] = t.w;
+                rmax = fmaxf(fmaxf(rmax, fmaxf(t.x, t.y)), fmaxf(t.z, t.w));
+            }
+            const float4 rb = rw4[dy];
+            const float rbv[4] = {rb.x, rb.y, rb.z, rb.w};
+            unsigned live = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) live |= __any_sync(0xffffffffu, rmax + rbv[q] >= lb[q]) ? (1u << q) : 0u;
+            if (!live) continue;
+#pragma unroll
+            for (int j = 0; j < C::RL / 4; ++j) {
                 const float4 u = rowl[j];
                 rl[4 * j + 0] = u.x; rl[4 * j + 1] = u.y; rl[4 * j + 2] = u.z; rl[4 * j + 3] = u.w;
             }
-            float rs[4][C::P];
+            const float* frh = reinterpret_cast<const float*>(fh4 + dy * C::S);   // [dx][q]
+            const float* frl = reinterpret_cast<const float*>(fl4 + dy * C::S);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 4; ++q) {
+                if (!((live >> q) & 1u)) continue;
+                float rs[C::P];
 #pragma unroll
-                for (int p = 0; p < C::P; ++p) rs[q][p] = 0.f;
+                for (int p = 0; p < C::P; ++p) rs[p] = 0.f;
 #pragma unroll
-            for (int dx = 0; dx < C::S; ++dx) {
-                const float4 w = fh4[dy * C::S + dx];
-                const float4 wlo = fl4[dy * C::S + dx];
-                const float wv[4] = {w.x, w.y, w.z, w.w};
-                const float wlv[4] = {wlo.x, wlo.y, wlo.z, wlo.w};
+                for (int dx = 0; dx < C::S; ++dx) {
+                    const float bb = frh[4 * dx + q], blo = frl[4 * dx + q];
 #pragma unroll
-                for (int p = 0; p < C::P; ++p) {
-                    const float a = rh[p - dx + 2 * R], alo = rl[p - dx + 2 * R];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float bb = wv[q];
-                        const float s1 = a + bb;                                 // TwoSum(a, bb)
-                        const float bv = s1 - a;
-                        const float e1 = (a - (s1 - bv)) + (bb - bv);
-                        const float u = (s1 - m[q][p]) + (e1 + (alo + wlv[q]));  // s1 - m exact (m integer)
-                        rs[q][p] += ex2_approx(u);                               // -inf -> 0
+                    for (int p = 0; p < C::P; ++p) {
+                        const float av = rh[p - dx + 2 * R];
+                        const float s1 = av + bb;                                   // TwoSum(av, bb)
+                        const float bv = s1 - av;
+                        const float e1 = (av - (s1 - bv)) + (bb - bv);
+                        const float u = (s1 - m[q][p]) + (e1 + (rl[p - dx + 2 * R] + blo));   // s1 - m exact
+                        rs[p] += ex2_approx(u);                                     // sentinel -> 0
                     }
                 }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
 #pragma unroll
                 for (int p = 0; p < C::P; ++p)
-                    if (m[q][p] != NEG_INF) sd[q][p] += (double)rs[q][p];
+                    if (m[q][p] != NEG_INF) sd[q][p] += (double)rs[p];
+            }
         }
     }
 
@@ -240,8 +304,8 @@ static cudaError_t launch_lsep_r(const se2_kernel_s* k, const double* in, int ba
     const int tiles_y = (k->wrows() + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, (k->nt + 3) / 4, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->L2hi, k->L2lo, k->nx, k->ny, k->nt, tiles_x,
-                                                             k->wlo(), k->whi(), epi);
+    conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->L2hi, k->L2lo, k->L2row, k->nx, k->ny, k->nt,
+                                                             tiles_x, k->wlo(), k->whi(), epi);
     count_launch();
     return cudaGetLastError();
 }

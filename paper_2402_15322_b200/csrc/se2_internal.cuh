@@ -151,6 +151,7 @@ struct se2_kernel_s {
     unsigned int* guard = nullptr;  // [4] guard counters (Epilogue::guard), zeroed per solve
     float* L2hi = nullptr;          // K4P: L log2(e) as an exact float pair, Lq layout (built on first use)
     float* L2lo = nullptr;
+    float* L2row = nullptr;         // K4P pruning bounds: [nt/4][nt][S][4] max over each tap row of L2hi
     // output window (slab decomposition, se2_kernel_set_window): every conv computes and stores only the
     // output rows [win_lo, win_hi) of each plane; rows outside are input-only halo rows.  Default: all.
     int win_lo = 0, win_hi = 0;

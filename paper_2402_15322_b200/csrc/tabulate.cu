@@ -95,6 +95,18 @@ __global__ void tabulate_l2pair_kernel(double hx, double hy, int nt, int R, doub
     }
 }
 
+// K4P row bounds: L2row[qd][ti][dy][q] = max over dx of L2hi[qd][ti][dy][dx][q]
+__global__ void tabulate_l2row_kernel(int nt, int S, const float* __restrict__ L2hi, float* __restrict__ L2row) {
+    const int64_t total = (int64_t)((nt + 3) / 4) * nt * S * 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(i & 3);
+        const int64_t row = i >> 2;   // (qd, ti, dy)
+        float m = -INFINITY;
+        for (int dx = 0; dx < S; ++dx) m = fmaxf(m, L2hi[(row * S + dx) * 4 + q]);
+        L2row[i] = m;
+    }
+}
+
 cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
     if (k->L2hi != nullptr) return cudaSuccess;
     const size_t n = (size_t)((k->nt + 3) / 4) * k->nt * k->S * k->S * 4;
@@ -109,7 +121,15 @@ cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
     count_launch();
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    k->table_bytes += 2 * n * sizeof(float);
+    if (e != cudaSuccess) return e;
+    const size_t nr = (size_t)((k->nt + 3) / 4) * k->nt * k->S * 4;
+    e = cudaMalloc(&k->L2row, nr * sizeof(float));
+    if (e != cudaSuccess) return e;
+    tabulate_l2row_kernel<<<(int)std::min<size_t>((nr + 255) / 256, 148 * 32), 256, 0, s>>>(k->nt, k->S, k->L2hi, k->L2row);
+    count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    k->table_bytes += 2 * n * sizeof(float) + nr * sizeof(float);
     return e;
 }
 
