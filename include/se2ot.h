@@ -309,6 +309,12 @@ SE2_API se2_status se2_lse_path_stats(se2_kernel k, int64_t* active_pairs, int64
  * of the warp (K3). */
 SE2_API se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_visited, int32_t reset);
 
+/* Tensor-core linear conv (K10), narrow geometry (nt >= 32; K10): tiles computed since the
+ * last reset, and those among them that took the 32-orientation window because the tile's bound
+ * (taps outside the 16-orientation window <= 2^-30 of every output) did not hold.  Synchronises the
+ * device.  Both counts are 0 for kernels without K10 or with the classic geometry. */
+SE2_API se2_status se2_tc_tile_stats(se2_kernel k, int64_t* tiles, int64_t* wide_tiles, int32_t reset);
+
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)
  * since the last reset (synchronises the events). */

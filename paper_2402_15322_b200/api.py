@@ -105,6 +105,12 @@ class Kernel:
         check(L.load().se2_lse_row_stats(self._h, ctypes.byref(live), ctypes.byref(vis), 1 if reset else 0))
         return dict(live=live.value, visited=vis.value)
 
+    def tc_tile_stats(self, reset: bool = True) -> dict:
+        """K10 narrow geometry: tiles computed / tiles on the wide (32-orientation) window."""
+        t, w = ctypes.c_int64(), ctypes.c_int64()
+        check(L.load().se2_tc_tile_stats(self._h, ctypes.byref(t), ctypes.byref(w), 1 if reset else 0))
+        return dict(tiles=t.value, wide=w.value)
+
     def guard_stats(self, reset: bool = False) -> dict:
         """Division-guard clamps (R9) and porous prox non-convergences since the last solve
         started (se2_guard_stats)."""

@@ -949,6 +949,15 @@ se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_vis
     return SE2_OK;
 }
 
+se2_status se2_tc_tile_stats(se2_kernel k, int64_t* tiles, int64_t* wide_tiles, int32_t reset) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(tiles != nullptr && wide_tiles != nullptr, "null output");
+    DeviceGuard g(k->device);
+    SE2_CUDA_TRY(cudaDeviceSynchronize());
+    SE2_CUDA_TRY(se2::conv_tc_tile_counts(k, tiles, wide_tiles, reset != 0));
+    return SE2_OK;
+}
+
 se2_status se2_timing_enable(se2_kernel k, int32_t on) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     k->timing.on = on != 0;

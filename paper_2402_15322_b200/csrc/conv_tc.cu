@@ -3,7 +3,7 @@
 //
 //   y[b, to, y, x] = sum_ti sum_{dyi, dxi < S} Wl[to, ti, dyi, dxi] * v[b, ti, y + R - dyi, x + R - dxi]
 //
-// Formulation: one CTA owns 8 output rows y0..y0+7 x one block of 16 output
+// Formulation: one CTA owns a tile of kr output rows y0.. x one block of kb output
 // orientations x all nx pixels of those rows.  For every input row yi and every filter column dxi one
 // tcgen05 MMA chain computes
 //
@@ -11,25 +11,34 @@
 //   A[(r, to)][ti] = Wl[to, ti, y0 + r + R - yi, dxi]    (rows with dyi outside the box: 0)
 //   B[x][ti]       = v[ti, yi, x + R - dxi]               (pixels shifted by a descriptor offset)
 //
-// with M = 128 = 8 rows x 16 orientations, N = the row's pixels (<= 256), K = the theta window of the
-// orientation block (32 orientations covering the fp32 band, or all of them when nt <= 32).  Both
-// operands are K-major SWIZZLE_NONE ("interleave") shared-memory tiles:
+// with M = 128 = kr rows x kb orientations, N = the row's pixels (<= 256), K = the theta window.  Two
+// geometries:
+//   * classic (nt = 16): kr = 8, kb = 16, K = all orientations;
+//   * narrow (nt >= 32): kr = 16, kb = 8 orientations to = 8 blk + 4 .. 8 blk + 11, and per tile EITHER
+//     the narrow window ti in [8 blk, 8 blk + 16) (K = 16: every |to - ti| <= 4 kept) when the tile's
+//     bound proves the taps outside it negligible --
+//        wout[blk] * max_{window rows} |v| <= 2^-30 * min_{tile rows, block chunks} v,   v >= 0 on the window
+//     (every output is >= its centre tap W = 1 times v[to, y, x] and the dropped taps sum to <= wout
+//     times the window maximum: relative error <= 2^-30) -- OR the wide window [8 blk - 8, 8 blk + 24)
+//     (K = 32, exact for bands <= 12).  Input-row statistics come from the split kernel.
+// Both operands are K-major SWIZZLE_NONE ("interleave") shared-memory tiles:
 //   * B is a padded input row stored [ti chunk][x'][8 ti] (16 B per pixel), so a pixel shift dxi is
 //     a +16 B start-address change of the descriptor -- no im2col;
-//   * A is stored [dxi][chunk][j = dyi + 7][16 to][8 ti], so the 8 output rows r of one input row yi
+//   * A is stored [dxi][chunk][j = dyi + kr - 1][kb to][8 ti], so the kr output rows r of one input row yi
 //     (dyi = y0 + r + R - yi, consecutive) form one contiguous 2 KB tile per chunk.
 // fp32 accuracy: x = hi + lo with hi = bf16(x), lo = bf16(x - hi) for both operands; the chain adds
 // hi.hi + hi.lo + lo.hi (per-term error <= 3 * 2^-18 relative; simulated on c4m in DESIGN.md).
 //
 // Roles (320 threads): warp 0 lane 0 is the TMA producer (an NA-stage weight ring, one 5-D tensor copy
-// per stage, and a 2-stage ring of split input rows, 8 bulk copies per row); warp 1 lane 0 issues the
+// per stage, and a 2-stage ring of split input rows, one bulk copy per chunk); warp 1 lane 0 issues the
 // MMAs and commits each stage back; warps 2-9 add every input row's TMEM sums into registers (round to
-// nearest; the tensor core's own accumulation truncates) and read the correction accumulator.
+// nearest; the tensor core's own accumulation truncates) and read the correction accumulator; warp 2
+// first decides the window of each of the CTA's tiles.
 //
 // Geometry (chosen per kernel for its max_batch):
-//   * rows mode: one CTA per (rows <= 8 output rows, orientation block, field); the epilogue runs in the
+//   * rows mode: one CTA per (rows <= kr output rows, orientation block, field); the epilogue runs in the
 //     kernel through a shared-memory transpose (coalesced along x);
-//   * balanced mode: 8-row tiles; the tiles' input-row chains are concatenated and split into equal runs
+//   * balanced mode: kr-row tiles; the tiles' input-row chains are concatenated and split into equal runs
 //     over <= 148 CTAs (<= 3 pieces per tile); every piece writes its sums to an L2-resident partial
 //     buffer and tc_pieces_epilogue_kernel adds the pieces in order and applies the fused epilogue.
 #include <cuda_bf16.h>
@@ -44,46 +53,77 @@ namespace se2 {
 
 namespace {
 
-constexpr int kTcRows = 8;     // rows of the MMA M tile (8 rows x 16 orientations = 128)
-constexpr int kTcBlk = 16;     // output orientations per CTA
 constexpr int kTcPadX = 16;    // zero pixels left of x = 0 in the split input rows (>= R)
-constexpr int kTcNA = 6;       // weight-ring stages
-// stages of a row whose correction MMAs are issued before waiting for the previous row's flush (the
-// rest interleave main and corrections per K-step, which keeps consecutive MMAs on different TMEM
+constexpr int kTcNAMax = 8;    // weight-ring stages (allocated); TcGeom::na of them are used
+// The first stage of a chain issues its correction MMAs before waiting for the previous chain's flush
+// (the rest interleave main and corrections per K-step, which keeps consecutive MMAs on different TMEM
 // accumulators: 0.579 -> 0.524 ms at c4; 1 early stage measured best, 0.511 ms, against 0/2/4/6)
-constexpr int kTcEarly = 1;
-// input rows per main-accumulator chain (flushed to registers after each): 2 halves the flush bubbles;
-// truncation bound 2 x S x K/16 = 124 steps of 2^-23 at R 15, inside R18
-constexpr int kTcFlushRows = 2;
+// input rows per main-accumulator chain (flushed to registers after each): 8 / (chunks of the window),
+// i.e. 2 rows at K = 32 and 4 rows at K = 16 -- the truncation bound stays rows x S x K/16 <= 124 steps
+// of 2^-23 at R 15 (inside R18) and the flush bubbles are halved against flushing every row
+constexpr int kTcMaxFlushRows = 4;   // depth of the row-done ring (one barrier per row of a chain)
+// a weight stage is 32 KB: two filter columns of the 4-chunk window or four of a 2-chunk window (the
+// single issuing thread's per-stage work -- barrier wait, descriptors, commit -- is amortised over 12 MMAs)
+constexpr uint32_t kTcAStage = 2u * 8u * 2048u;
+// filter columns per stage (nwa is 2 or 4: no integer division on the single-thread issue path)
+__host__ __device__ constexpr int tc_cols(int nwa) { return nwa == 2 ? 4 : 2; }
+// input rows per main-accumulator chain: 8 / nwl
+__host__ __device__ constexpr int tc_chain_rows(int nwl) { return nwl == 2 ? 4 : 2; }
 constexpr int kTcThreads = 320;   // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: accumulators / epilogue
 constexpr int kTcFlushWarps = 8;
+constexpr int kTcMaxPieces = 4;   // pieces per CTA in the balanced mode (<= 3 by construction)
+constexpr float kTcNarrowEta = 9.313225746154785e-10f;   // 2^-30: relative bound of the narrow window's dropped taps
 
 struct TcGeom {
+    bool nar;    // narrow geometry (16 rows x 8 orientations, per-tile 16- or 32-wide window)
+    int kr, kb;  // rows and orientations of the M tile (kr x kb = 128)
     int npad;    // MMA N: nx rounded up to 16
     int nxp;     // padded row length (pixels) of the split input: npad + 2 * kTcPadX
     int nch;     // theta chunks of 8
-    int nwin;    // chunks in the theta window of one orientation block (2 or 4)
-    int nj;      // dyi + 7 range: S + 14
+    int nwin;    // chunks of the stored theta window of one orientation block (classic: 2 or 4; narrow: 4)
+    int nj;      // dyi + kr - 1 range: S + 2 (kr - 1)
     int nblk;    // orientation blocks
     size_t a_stage, b_stage, smem;
     int tmem_cols;
+    int na;      // weight-ring stages
 };
 
 __host__ __device__ inline int tc_chunk0(int blk, int nch, int nwin) {
     return (nwin == nch) ? 0 : ((2 * blk - 1 + nch) % nch);
 }
+// first chunk of the stored window of block blk: classic as above; narrow: the wide window's first
+// chunk blk - 1 (the narrow window is chunks 1, 2 of it)
+__host__ __device__ inline int tc_win0(bool nar, int blk, int nch, int nwin) {
+    return nar ? (blk - 1 + nch) % nch : tc_chunk0(blk, nch, nwin);
+}
+// output orientation of M-tile orientation tol of block blk
+__host__ __device__ inline int tc_to(bool nar, int blk, int tol, int nt) {
+    return nar ? (8 * blk + 4 + tol) % nt : 16 * blk + tol;
+}
+
+// narrow geometry where it applies (>= 4 theta chunks, so the 32-wide window has distinct chunks, and
+// a band the wide window covers); SE2_TC_NAR=0 keeps the classic geometry (A/B measurements)
+bool tc_use_narrow(const se2_kernel_s* k) {
+    if (k->nt / 8 < 4 || k->band > 12) return false;
+    const char* e = getenv("SE2_TC_NAR");
+    return e == nullptr || atoi(e) != 0;
+}
 
 TcGeom tc_geom(const se2_kernel_s* k) {
     TcGeom g;
+    g.nar = k->tc_nar;   // decided once in conv_tc_prepare
+    g.kr = g.nar ? 16 : 8;
+    g.kb = 128 / g.kr;
     g.npad = (k->nx + 15) / 16 * 16;
     g.nxp = g.npad + 2 * kTcPadX;
     g.nch = k->nt / 8;
-    g.nwin = g.nch <= 4 ? g.nch : 4;
-    g.nj = k->S + 14;
-    g.nblk = k->nt / kTcBlk;
-    g.a_stage = (size_t)2 * g.nwin * kTcRows * kTcBlk * 16;          // hi + lo, 2 KB per chunk
+    g.nwin = g.nar ? 4 : (g.nch <= 4 ? g.nch : 4);
+    g.nj = k->S + 2 * (g.kr - 1);
+    g.nblk = k->nt / g.kb;
+    g.a_stage = kTcAStage;   // hi + lo x (2 columns x 4 chunks | 4 columns x 2 chunks), 2 KB per chunk (kr j x kb to x 16 B)
     g.b_stage = (size_t)2 * g.nwin * g.nxp * 16;                     // hi + lo rows
-    size_t pipe = 2 * g.b_stage + kTcNA * g.a_stage;
+    g.na = getenv("SE2_TC_NA") ? std::max(2, std::min(kTcNAMax, atoi(getenv("SE2_TC_NA")))) : 4;
+    size_t pipe = 2 * g.b_stage + g.na * g.a_stage;
     size_t epi = (size_t)128 * (g.npad + 1) * sizeof(float);         // TMEM -> smem transpose
     g.smem = std::max(pipe, epi) + 1024;                              // + barriers / scratch
     // per accumulator: the npad columns, and every x32 tcgen05.ld of the column-half flush
@@ -111,6 +151,43 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
                  ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+// one filter column of the steady-state chain, as ONE asm block (the compiler wraps every tcgen05 asm
+// statement of a single active lane in an elect loop; one block per column amortises it): per K-step the
+// correction hi.lo into tc, the main hi.hi into tm, the correction lo.hi into tc.  ah / bh are the hi
+// descriptors, alo / blo the hi -> lo descriptor offsets, accm / accc the enable-input flags of the first
+// main / correction MMA.
+__device__ __forceinline__ void tc_mma_col(uint32_t tc, uint32_t tm, uint64_t ah, uint64_t bh, uint64_t alo,
+                                           uint64_t blo, uint32_t idesc, uint32_t accc, uint32_t accm) {
+    asm volatile(
+        "{\n\t.reg .pred pc, pm, pt;\n\t.reg .b64 al, bl;\n\t"
+        "setp.ne.b32 pc, %7, 0;\n\tsetp.ne.b32 pm, %8, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+        "add.s64 bl, %3, %6;\n\tadd.s64 al, %2, %5;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, bl, %4, pc;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %3, %4, pm;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], al, %3, %4, pt;\n\t}"
+        ::"r"(tc), "r"(tm), "l"(ah), "l"(bh), "r"(idesc), "l"(alo), "l"(blo), "r"(accc), "r"(accm));
+}
+// two consecutive filter columns (a 2-column stage of a K = 16 window): the second column's operands are
+// ah + ae (next column's weights) and bh - 1 (the input row shifted by one pixel = 16 B)
+__device__ __forceinline__ void tc_mma_col2(uint32_t tc, uint32_t tm, uint64_t ah, uint64_t bh, uint64_t ae,
+                                            uint64_t alo, uint64_t blo, uint32_t idesc, uint32_t accc, uint32_t accm) {
+    asm volatile(
+        "{\n\t.reg .pred pc, pm, pt;\n\t.reg .b64 al, bl, a2, b2, al2, bl2;\n\t"
+        "setp.ne.b32 pc, %8, 0;\n\tsetp.ne.b32 pm, %9, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+        "add.s64 bl, %3, %7;\n\tadd.s64 al, %2, %6;\n\t"
+        "add.s64 a2, %2, %5;\n\tsub.s64 b2, %3, 1;\n\t"
+        "add.s64 bl2, b2, %7;\n\tadd.s64 al2, a2, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, bl, %4, pc;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %3, %4, pm;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], al, %3, %4, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, bl2, %4, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a2, b2, %4, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], al2, b2, %4, pt;\n\t}"
+        ::"r"(tc), "r"(tm), "l"(ah), "l"(bh), "r"(idesc), "l"(ae), "l"(alo), "l"(blo), "r"(accc), "r"(accm));
+}
+__device__ __forceinline__ void tc_commit_u32(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -118,42 +195,44 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 // bounded wait: a pipeline bug traps (a launch error) instead of hanging the device
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
-    long long spins = 0;
+    uint32_t spins = 0;
     while (!done) {
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-        if (++spins > (1ll << 31)) __trap();
+        if (++spins == (1u << 31)) __trap();
     }
 }
 
 struct TcArgs {
     const __nv_bfloat16* xk;   // split input rows: [hl][batch][ny][nch][nxp][8]
-    const __nv_bfloat16* wk;   // split weights:    [hl][nblk][S][nwin][nj][16][8]
+    const __nv_bfloat16* wk;   // split weights:    [hl][nblk][S][nwin][nj][kb][8]
     size_t xk_hl, wk_hl;       // elements between the hi and lo halves
     int nx, ny, nt, R, S;
     int npad, nxp, nch, nwin, nj;
+    int nar, kr, kb;           // geometry (TcGeom)
+    int na;                    // weight-ring stages
     uint32_t a_stage, b_stage;
     int tmem_cols;
-    int rows_out;              // output rows a CTA owns (<= kTcRows; the M tile's remaining rows are discarded)
+    int rows_out;              // output rows a CTA owns (<= kr; the M tile's remaining rows are discarded)
     int y_lo, y_hi;            // output window (kernel's win_lo / win_hi): rows outside are input-only halos
-    // balanced mode (PIECES): 8-row tiles, CTA c takes chain units [c q, (c + 1) q) of the concatenated
+    // balanced mode (PIECES): kr-row tiles, CTA c takes chain units [c q, (c + 1) q) of the concatenated
     // (tile, input row) list; every piece's sums go to `part` [tile][piece < 3][128][npad]
     int batch, nblk, ngroups, ug, q;
     float* part;
+    // narrow geometry: per (field, input row, chunk) (min v, max |v|) of this launch's input, the weight
+    // mass outside each block's narrow window, and the tile counters (instrumentation)
+    const float2* stats;
+    const float* wout;
+    unsigned long long* cnt;
 };
 
-// chain length (input rows) of 8-row group g, and the units before it within one (field, block)
+// chain length (input rows) of kr-row group g, and the units before it within one (field, block)
 __device__ __forceinline__ int tc_group_len(const TcArgs& a, int g) {
-    const int y0 = a.y_lo + g * kTcRows;
-    return min(a.ny - 1, min(a.y_hi - 1, y0 + kTcRows - 1) + a.R) - max(0, y0 - a.R) + 1;
-}
-__device__ __forceinline__ int tc_group_prefix(const TcArgs& a, int g) {
-    int s = 0;
-    for (int i = 0; i < g; ++i) s += tc_group_len(a, i);
-    return s;
+    const int y0 = a.y_lo + g * a.kr;
+    return min(a.ny - 1, min(a.y_hi - 1, y0 + a.kr - 1) + a.R) - max(0, y0 - a.R) + 1;
 }
 
 struct TcPiece {
@@ -190,7 +269,7 @@ __device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
         if (kk == k) {
             pc.b = grp / a.nblk;
             pc.blk = grp - pc.b * a.nblk;
-            pc.y0 = a.y_lo + g * kTcRows;
+            pc.y0 = a.y_lo + g * a.kr;
             pc.ylo = max(0, pc.y0 - a.R);
             pc.r0 = u - st;
             pc.r1 = r1;
@@ -203,51 +282,106 @@ __device__ __forceinline__ bool tc_piece(const TcArgs& a, int k, TcPiece& pc) {
     return false;
 }
 
-// input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]
+// narrow geometry: may tile (field b, block blk, output rows from y0) use the 16-wide window?  Warp-
+// collective (every lane returns the decision).  Dropped taps of output (to, y, x): ti outside the
+// window, sum <= wout[blk] * max_window |v|; the output is >= its centre tap (W = 1) times v[to, y, x]
+// when v >= 0 on the whole window.  Inputs with NaN / Inf / negative entries take the wide window.
+__device__ bool tc_tile_narrow(const TcArgs& a, int b, int blk, int y0, int rows) {
+    const int lane = threadIdx.x & 31;
+    const float wo = a.wout[blk];
+    const int ylo = max(0, y0 - a.R), yhi = min(a.ny - 1, y0 + rows - 1 + a.R);
+    const int ohi = min(min(a.ny, a.y_hi), y0 + rows) - 1;
+    const int c0 = blk, c1 = (blk + 1) % a.nch;
+    const float2* st = a.stats + (size_t)b * a.ny * a.nch;
+    float wmin = INFINITY, wmax = 0.f, tmin = INFINITY;
+    bool finite = true;
+#pragma unroll 4
+    for (int i = lane; i < (yhi - ylo + 1) * a.nch; i += 32) {
+        const int y = ylo + i / a.nch, c = i % a.nch;
+        const float2 v = __ldg(st + (size_t)y * a.nch + c);
+        finite = finite && isfinite(v.x) && isfinite(v.y);
+        wmin = fminf(wmin, v.x);
+        wmax = fmaxf(wmax, v.y);
+        if (y >= y0 && y <= ohi && (c == c0 || c == c1)) tmin = fminf(tmin, v.x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    if (wo == 0.f) return true;   // nothing outside the narrow window (band <= 4)
+    return finite && wmin >= 0.f && tmin > 0.f && wo * wmax <= kTcNarrowEta * tmin;
+}
+
+// input split: v[b][ti][y][x] (fp32) -> hi/lo bf16 rows [b][y][chunk][x' = x + kTcPadX][8]; one block per
+// (field, row, chunk), one padded pixel per thread (all 8 plane loads in flight); optionally the row's
+// (min v, max |v|) over the 8 planes and the nx real pixels (stats[b][y][chunk])
 __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl,
-                                      int nx, int ny, int nt, int nxp, int batch) {
+                                      int nx, int ny, int nt, int nxp, float2* __restrict__ stats) {
+    __shared__ float sMin[32], sMax[32];
     tc_grid_dep_wait();   // reads the previous kernel's output (launched with PDL)
     const int nch = nt / 8;
-    const int64_t total = (int64_t)batch * ny * nch * nxp;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int xp = (int)(i % nxp);
-        int64_t t = i / nxp;
-        const int c = (int)(t % nch);
-        t /= nch;
-        const int y = (int)(t % ny);
-        const int b = (int)(t / ny);
+    const int64_t row = blockIdx.x;   // (b, y, c)
+    const int c = (int)(row % nch);
+    const int64_t by = row / nch;
+    const int y = (int)(by % ny);
+    const int b = (int)(by / ny);
+    float mn = INFINITY, mx = 0.f;
+    for (int xp = threadIdx.x; xp < nxp; xp += blockDim.x) {
         const int x = xp - kTcPadX;
         __align__(16) __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             float f = 0.f;
-            if (x >= 0 && x < nx) f = v[(((int64_t)b * nt + c * 8 + e) * ny + y) * nx + x];
+            if (x >= 0 && x < nx) {
+                f = v[(((int64_t)b * nt + c * 8 + e) * ny + y) * nx + x];
+                mn = fminf(mn, f);
+                mx = fmaxf(mx, fabsf(f));
+                if (f != f) mn = -INFINITY;   // NaN: never the narrow window
+            }
             const __nv_bfloat16 h = __float2bfloat16_rn(f);
             hi[e] = h;
             lo[e] = __float2bfloat16_rn(f - __bfloat162float(h));
         }
+        const int64_t i = row * nxp + xp;
         reinterpret_cast<uint4*>(xk)[i] = *reinterpret_cast<const uint4*>(hi);
         reinterpret_cast<uint4*>(xk + xk_hl)[i] = *reinterpret_cast<const uint4*>(lo);
     }
+    if (stats == nullptr) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sMin[w] = mn; sMax[w] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < nw; ++i) { mn = fminf(mn, sMin[i]); mx = fmaxf(mx, sMax[i]); }
+        stats[row] = make_float2(mn, mx);
+    }
 }
 
-// weight split: Wl[to][ti][S][SP] (fp32) -> hi/lo [blk][dxi][c][j][to_l][8]
+// weight split: Wl[to][ti][S][SP] (fp32) -> hi/lo [blk][dxi][c][j][to_l < kb][8]
 __global__ void tc_split_weights_kernel(const float* __restrict__ Wl, __nv_bfloat16* __restrict__ wk, size_t wk_hl,
-                                        int nt, int S, int nch, int nwin, int nj, int nblk) {
+                                        int nt, int S, int nch, int nwin, int nj, int nblk, int nar) {
     const int SP = (S + 3) / 4 * 4;
-    const int64_t total = (int64_t)nblk * S * nwin * nj * kTcBlk;
+    const int kb = nar ? 8 : 16, jofs = 128 / kb - 1;
+    const int64_t total = (int64_t)nblk * S * nwin * nj * kb;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int tol = (int)(i % kTcBlk);
-        int64_t t = i / kTcBlk;
+        const int tol = (int)(i % kb);
+        int64_t t = i / kb;
         const int j = (int)(t % nj);
         t /= nj;
         const int c = (int)(t % nwin);
         t /= nwin;
         const int dxi = (int)(t % S);
         const int blk = (int)(t / S);
-        const int to = blk * kTcBlk + tol;
-        const int chunk = (tc_chunk0(blk, nch, nwin) + c) % nch;
-        const int dyi = j - 7;
+        const int to = tc_to(nar != 0, blk, tol, nt);
+        const int chunk = (tc_win0(nar != 0, blk, nch, nwin) + c) % nch;
+        const int dyi = j - jofs;
         __align__(16) __nv_bfloat16 hi[8], lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -263,15 +397,43 @@ __global__ void tc_split_weights_kernel(const float* __restrict__ Wl, __nv_bfloa
     }
 }
 
+// narrow geometry: wout[blk] = max over the block's orientations of the weight mass outside its narrow
+// window (chunks blk, blk + 1), summed in fp64 and rounded up.  One block per orientation block.
+__global__ void tc_wout_kernel(const float* __restrict__ Wl, float* __restrict__ wout, int nt, int S) {
+    __shared__ double sSum[8];
+    const int blk = blockIdx.x, nch = nt / 8, SP = (S + 3) / 4 * 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;   // 8 warps: one output orientation each
+    const int to = tc_to(true, blk, warp, nt);
+    double acc = 0.0;
+    for (int ti = 0; ti < nt; ++ti) {
+        const int c = ti / 8;
+        if (c == blk || c == (blk + 1) % nch) continue;
+        const float* w = Wl + ((int64_t)to * nt + ti) * S * SP;
+        for (int i = lane; i < S * SP; i += 32) acc += (double)w[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sSum[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < 8; ++i) m = fmax(m, sSum[i]);
+        wout[blk] = m == 0.0 ? 0.f : __double2float_ru(m * (1.0 + 1e-6));
+    }
+}
+
 template <bool PIECES>
 __global__ void __launch_bounds__(kTcThreads, 1)
-conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap) {
+conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap wmapn) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char* sB = smem;                                   // [2][hl][nwin][nxp][16 B]
-    unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwin][8 j][16 to][16 B]
-    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNA], emptyA[kTcNA], rowdone[2], flushed, cflushed;
+    unsigned char* sB = smem;                                   // [2][hl][nwl][nxp][16 B]
+    unsigned char* sA = smem + 2 * (size_t)a.b_stage;           // [NA][hl][nwl][kr j][kb to][16 B]
+    __shared__ __align__(8) uint64_t fullB[2], emptyB[2], fullA[kTcNAMax], emptyA[kTcNAMax], rowdone[kTcMaxFlushRows],
+        flushed, cflushed,
+        flagbar;
     __shared__ uint32_t tmem_base;
     __shared__ float sRed[kTcThreads / 32];
+    __shared__ int sNwl[kTcMaxPieces];   // theta chunks of each piece's window (narrow: 2 or 4; classic: nwin)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -282,11 +444,11 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     }
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
-        for (int i = 0; i < kTcNA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
-        mbar_init(&rowdone[0], 1);
-        mbar_init(&rowdone[1], 1);
+        for (int i = 0; i < a.na; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
+        for (int i = 0; i < kTcMaxFlushRows; ++i) mbar_init(&rowdone[i], 1);
         mbar_init(&flushed, kTcFlushWarps);
         mbar_init(&cflushed, kTcFlushWarps);
+        mbar_init(&flagbar, 1);
         mbar_fence_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -300,51 +462,69 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
       if (lane == 0) {
         // ---------------- producer ----------------
         // global input-row counter gr (all pieces of this CTA): B ring stage gr & 1, weight stage (gr S + dxi)
-        auto load_b = [&](int gr, const TcPiece& pc, int yi) {
+        auto load_b = [&](int gr, const TcPiece& pc, int nwl, int yi) {
             const int st = gr & 1;
             if (gr >= 2) tc_wait(&emptyB[st], (uint32_t)(((gr >> 1) - 1) & 1));
-            mbar_expect_tx(&fullB[st], a.b_stage);
-            const int chunk0 = tc_chunk0(pc.blk, a.nch, a.nwin);
+            mbar_expect_tx(&fullB[st], 2u * (uint32_t)nwl * chunk_bytes_b);
+            const int chunk0 = tc_win0(a.nar != 0, pc.blk, a.nch, a.nwin) + ((a.nar && nwl == 2) ? 1 : 0);
             for (int hl = 0; hl < 2; ++hl) {
                 const __nv_bfloat16* row = a.xk + hl * a.xk_hl + ((size_t)pc.b * a.ny + yi) * row_elems;
-                for (int c = 0; c < a.nwin; ++c) {
+                for (int c = 0; c < nwl; ++c) {
                     const int ch = (chunk0 + c) % a.nch;
-                    bulk_load(sB + st * (size_t)a.b_stage + (size_t)(hl * a.nwin + c) * chunk_bytes_b,
+                    bulk_load(sB + st * (size_t)a.b_stage + (size_t)(hl * nwl + c) * chunk_bytes_b,
                               row + (size_t)ch * a.nxp * 8, chunk_bytes_b, &fullB[st]);
                 }
             }
         };
-        const int b_after = min(kTcNA - 1, a.S - 1);
         const uint32_t sA_u = smem_u32(sA), fullA_u = smem_u32(&fullA[0]);
-        const CUtensorMap* wm = &wmap;
+        // weight stage t of piece pc (input row yi, filter columns dxi .. dxi + 8 / nwl - 1): one TMA box
+        // [hl 2][column 8 / nwl][chunk nwl][j kr][kb to x 8 ti] (32 KB)
+        int pst = 0, prnd = 0;   // ring slot and round of the next weight stage (t = prnd * na + pst)
+        auto load_a = [&](int t, const TcPiece& pc, int yi, int dxi, int nwl) {
+            const int st = pst;
+            if (prnd > 0) tc_wait(&emptyA[st], (uint32_t)((prnd - 1) & 1));
+            if (++pst == a.na) { pst = 0; ++prnd; }
+            mbar_expect_tx(&fullA[st], kTcAStage);
+            const int j0 = pc.y0 + a.R - yi + a.kr - 1;
+            const bool n2 = a.nar && nwl == 2;   // the narrow window of the narrow geometry (second map)
+            tma_load_5d(sA_u + (uint32_t)st * a.a_stage, n2 ? (const void*)&wmapn : (const void*)&wmap,
+                        fullA_u + 8u * (uint32_t)st, 0, j0, n2 ? 1 : 0, pc.blk * a.S + dxi, 0);
+        };
+        const int b_after = min((a.na - 1) * tc_cols(a.nwin), a.S - 1);   // filter column that triggers the next row
         TcPiece pc, pn;
+        // PDL: the first weight stages do not depend on the preceding kernels (loaded with the full stored
+        // window, one filter column each: the tile's window is decided from the split kernel's
+        // statistics); the input rows do
+        int t = 0, dpre = 0;   // stages issued, filter columns prefetched
+        if (tc_piece<PIECES>(a, 0, pc))
+            while (dpre < b_after) {
+                load_a(t++, pc, pc.ylo + pc.r0, dpre, a.nwin);
+                dpre += tc_cols(a.nwin);
+            }
+        tc_wait(&flagbar, 0);   // warp 2 has passed the grid-dependency wait and decided every piece's window
+        tc_grid_dep_wait();
         int gr = 0;
-        // PDL: the weight stages do not depend on the preceding kernels, the input rows do (the split
-        // kernel): B(0) is loaded after the first weight stages, behind the grid-dependency wait
-        bool b0 = false;
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
+            const int nwl = sNwl[k];
+            const int nd = tc_cols(nwl);   // filter columns per stage
+            if (k == 0) load_b(0, pc, nwl, pc.ylo + pc.r0);
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 const int yi = pc.ylo + rr;
-                const int j0 = pc.y0 + a.R - yi + 7;
-                for (int dxi = 0; dxi < a.S; ++dxi) {
-                    const int t = gr * a.S + dxi;
-                    const int st = t % kTcNA;
-                    if (t >= kTcNA) tc_wait(&emptyA[st], (uint32_t)(((t / kTcNA) - 1) & 1));
-                    mbar_expect_tx(&fullA[st], a.a_stage);
-                    // one TMA box per stage: [hl 2][chunk nwin][j 8][16 to x 8 ti]
-                    tma_load_5d(sA_u + (uint32_t)st * a.a_stage, wm, fullA_u + 8u * (uint32_t)st, 0, j0, 0,
-                                pc.blk * a.S + dxi, 0);
-                    if (!b0 && dxi == b_after) {
-                        tc_grid_dep_wait();
-                        TcPiece p0;
-                        tc_piece<PIECES>(a, 0, p0);
-                        load_b(0, p0, p0.ylo + p0.r0);
-                        b0 = true;
+                const int d0 = gr == 0 ? dpre : 0;
+                bool nextb = false;   // the next input row's B stage has been requested
+                for (int dxi = d0; dxi < a.S; dxi += nd) {
+                    load_a(t++, pc, yi, dxi, nwl);
+                    // the next input row (this piece's, or the next piece's first) after the stage holding
+                    // filter column b_after (or the row's first stage when the prefetch passed it)
+                    if (!nextb && b_after < dxi + nd) {
+                        nextb = true;
+                        if (rr + 1 < pc.r1) load_b(gr + 1, pc, nwl, yi + 1);
+                        else if (tc_piece<PIECES>(a, k + 1, pn)) load_b(gr + 1, pn, sNwl[k + 1], pn.ylo + pn.r0);
                     }
-                    if (dxi == b_after) {   // the next input row (this piece's, or the next piece's first)
-                        if (rr + 1 < pc.r1) load_b(gr + 1, pc, yi + 1);
-                        else if (tc_piece<PIECES>(a, k + 1, pn)) load_b(gr + 1, pn, pn.ylo + pn.r0);
-                    }
+                }
+                if (!nextb) {   // the prefetch covered the whole first row
+                    if (rr + 1 < pc.r1) load_b(gr + 1, pc, nwl, yi + 1);
+                    else if (tc_piece<PIECES>(a, k + 1, pn)) load_b(gr + 1, pn, sNwl[k + 1], pn.ylo + pn.r0);
                 }
             }
         }
@@ -357,54 +537,46 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
                                ((uint32_t)(128 >> 4) << 24);
         const uint64_t dA0 = tc_desc(smem_u32(sA), 2048, 128);
         const uint64_t dB0 = tc_desc(smem_u32(sB), chunk_bytes_b, 128);
-        const int ksteps = a.nwin / 2;
         const uint32_t tcor = tmem + (uint32_t)(a.tmem_cols / 2);   // correction accumulator (hi.lo + lo.hi)
         uint32_t acc_c = 0;
-        auto issue_corr = [&](int t, int stb, int dxi) {
-            const int st = t % kTcNA;
-            tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t offA = (uint32_t)(st * a.a_stage);
-            const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
+        int nwl = a.nwin;   // the current piece's window (chunks): K = 8 nwl, nwl / 2 K-steps
+        // operand offsets of K-step ks of weight stage st against input-row stage stb, filter column dxi
+        // Per stage the descriptors are formed once (the 14-bit start-address fields never carry: shared
+        // addresses < 256 KB) and stepped per filter column / K-step: the single issuing thread must stay
+        // well ahead of the 128-cycle MMAs.  Stage layout [hl][column e < 4 / nwa][chunk nwa][2 KB].
+        const uint64_t aLo = kTcAStage / 2 / 16, aK = 2 * 2048 / 16, bK = 2 * chunk_bytes_b / 16;
+        int ist = 0, irnd = 0;   // ring slot and round of the next weight stage to consume
+
+        // corrections (hi.lo + lo.hi) of one filter column
+        auto issue_corr = [&](uint64_t dAh, uint64_t dBh, uint64_t bLo, int ksteps) {
             for (int ks = 0; ks < ksteps; ++ks) {
-                const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
-                const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
-                tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);
+                const uint64_t ah = dAh + ks * aK, bh = dBh + ks * bK;
+                tc_mma(tcor, ah, bh + bLo, idesc, acc_c);
                 acc_c = 1;
-                tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);
+                tc_mma(tcor, ah + aLo, bh, idesc, 1);
             }
         };
-        auto issue_main = [&](int t, int stb, int dxi, bool restart) {
-            const int st = t % kTcNA;
-            const uint32_t offA = (uint32_t)(st * a.a_stage);
-            const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
-            for (int ks = 0; ks < ksteps; ++ks) {
-                const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048;
-                const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b;
-                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (!restart || dxi > 0 || ks > 0) ? 1u : 0u);
-            }
-            tc_commit(&emptyA[st]);
+        auto issue_main = [&](uint64_t dAh, uint64_t dBh, int ksteps, uint32_t acc0) {
+            for (int ks = 0; ks < ksteps; ++ks) tc_mma(tmem, dAh + ks * aK, dBh + ks * bK, idesc, ks ? 1u : acc0);
         };
         // steady state: per K-step main (hi.hi), then the two corrections sharing its A / B operand
-        auto issue_both = [&](int t, int stb, int dxi, bool restart) {
-            const int st = t % kTcNA;
-            tc_wait(&fullA[st], (uint32_t)((t / kTcNA) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t offA = (uint32_t)(st * a.a_stage);
-            const uint32_t offB = (uint32_t)(stb * a.b_stage + (kTcPadX + a.R - dxi) * 16);
+        auto issue_both = [&](uint64_t dAh, uint64_t dBh, uint64_t bLo, int ksteps, uint32_t acc0) {
             for (int ks = 0; ks < ksteps; ++ks) {
-                const uint32_t ah = offA + (uint32_t)(2 * ks) * 2048, al = ah + (uint32_t)a.nwin * 2048;
-                const uint32_t bh = offB + (uint32_t)(2 * ks) * chunk_bytes_b, bl = bh + (uint32_t)a.nwin * chunk_bytes_b;
-                tc_mma(tcor, dA0 + (ah >> 4), dB0 + (bl >> 4), idesc, acc_c);              // A_hi shared with
+                tc_mma_col(tcor, tmem, dAh + ks * aK, dBh + ks * bK, aLo, bLo, idesc, acc_c, ks ? 1u : acc0);
                 acc_c = 1;
-                tc_mma(tmem, dA0 + (ah >> 4), dB0 + (bh >> 4), idesc, (!restart || dxi > 0 || ks > 0) ? 1u : 0u);   // <- B_hi
-                tc_mma(tcor, dA0 + (al >> 4), dB0 + (bh >> 4), idesc, 1);                   // shared with
             }
-            tc_commit(&emptyA[st]);
         };
+        const uint32_t emptyA_u = smem_u32(&emptyA[0]);
+        // stages the producer prefetched before the windows were known (the stored window, tc_cols(nwin)
+        // filter columns each; mirrors the producer's prefetch loop)
+        const int b_after = min((a.na - 1) * tc_cols(a.nwin), a.S - 1);
+        const int npre = (b_after + tc_cols(a.nwin) - 1) / tc_cols(a.nwin);
+        tc_wait(&flagbar, 0);
         TcPiece pc;
-        int gr = 0, gs = 0;   // input rows and main-accumulator chains issued so far
+        int gr = 0, gs = 0, t = 0;   // input rows, main-accumulator chains and weight stages issued so far
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
+            nwl = sNwl[k];
+            const int fr = tc_chain_rows(nwl);   // input rows per main-accumulator chain (power of 2)
             if (k > 0) {   // the correction accumulator restarts per piece: the previous piece's was read
                 tc_wait(&cflushed, (uint32_t)((k - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -413,21 +585,50 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 const int stb = gr & 1;
                 tc_wait(&fullB[stb], (uint32_t)((gr >> 1) & 1));
-                // The main accumulator restarts every kTcFlushRows input rows of a piece and the
-                // accumulator warps must first have read the previous chain's sums: the correction MMAs
-                // of the row's first P stages are issued before that wait so the tensor pipe stays busy.
-                const bool restart = (rr - pc.r0) % kTcFlushRows == 0;
-                const int P = (restart && gs > 0) ? min(kTcEarly, a.S) : 0;
-                for (int dxi = 0; dxi < P; ++dxi) issue_corr(gr * a.S + dxi, stb, dxi);
-                if (restart && gs > 0) {
-                    tc_wait(&flushed, (uint32_t)((gs - 1) & 1));
+                // The main accumulator restarts every fr input rows of a piece and the accumulator warps
+                // must first have read the previous chain's sums: the correction MMAs of the row's first
+                // stage are issued before that wait so the tensor pipe stays busy.
+                const bool restart = ((rr - pc.r0) & (fr - 1)) == 0;
+                // chain restart: the corrections of the row's first stage are issued before the wait for
+                // the accumulator warps' flush, its main MMAs after it (0-4 such stages measured alike at c4)
+                bool early = restart && gs > 0;
+                const int ksteps = nwl / 2;
+                const uint64_t bLo = (uint64_t)nwl * chunk_bytes_b / 16;
+                for (int dxi = 0; dxi < a.S; ++t) {
+                    const int st = ist;
+                    tc_wait(&fullA[st], (uint32_t)(irnd & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (++ist == a.na) { ist = 0; ++irnd; }
+                    const int nwa = t < npre ? a.nwin : nwl;                    // chunks loaded into the stage
+                    const int nv = min(tc_cols(nwa), a.S - dxi);               // its filter columns
+                    // a narrow tile on a stage prefetched with the wide window reads the middle chunks
+                    const uint64_t dAh = dA0 + (uint64_t)((st * a.a_stage + (nwa > nwl ? 2048u : 0u)) >> 4);
+                    const uint64_t dBh = dB0 + (uint64_t)((stb * a.b_stage + (kTcPadX + a.R - dxi) * 16) >> 4);
+                    const uint64_t aE = (uint64_t)nwa * 2048 / 16;             // next filter column's weights
+                    const uint32_t first = (!restart || dxi > 0) ? 1u : 0u;     // enable-input of the chain's first main MMA
+                    if (early) {
+                        for (int e = 0; e < nv; ++e) issue_corr(dAh + e * aE, dBh - e, bLo, ksteps);
+                        tc_wait(&flushed, (uint32_t)((gs - 1) & 1));
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        for (int e = 0; e < nv; ++e) issue_main(dAh + e * aE, dBh - e, ksteps, (dxi + e) ? 1u : 0u);
+                        early = false;
+                    } else if (ksteps == 1) {   // K = 16 windows: two filter columns per asm block
+                        int e = 0;
+                        for (; e + 1 < nv; e += 2) {
+                            tc_mma_col2(tcor, tmem, dAh + e * aE, dBh - e, aE, aLo, bLo, idesc, acc_c, e ? 1u : first);
+                            acc_c = 1;
+                        }
+                        if (e < nv) issue_both(dAh + e * aE, dBh - e, bLo, 1, e ? 1u : first);
+                    } else {
+                        for (int e = 0; e < nv; ++e) issue_both(dAh + e * aE, dBh - e, bLo, ksteps, e ? 1u : first);
+                    }
+                    tc_commit_u32(emptyA_u + 8u * (uint32_t)st);
+                    dxi += nv;
                 }
-                for (int dxi = 0; dxi < P; ++dxi) issue_main(gr * a.S + dxi, stb, dxi, restart);
-                for (int dxi = P; dxi < a.S; ++dxi) issue_both(gr * a.S + dxi, stb, dxi, restart);
                 tc_commit(&emptyB[stb]);
-                tc_commit(&rowdone[gr & 1]);   // 2-deep ring: the issuer runs at most one chain (<= 2 rows) ahead
-                if ((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1) ++gs;   // chain end
+                // row-done ring, one barrier per row of a chain: the issuer runs at most one chain ahead
+                tc_commit(&rowdone[gr % kTcMaxFlushRows]);
+                if (((rr - pc.r0) & (fr - 1)) == fr - 1 || rr == pc.r1 - 1) ++gs;   // chain end
             }
         }
       }
@@ -442,7 +643,28 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
     const int half = a.npad / 2;
     TcPiece pc;
     if (warp >= 2) {
-        tc_grid_dep_wait();   // partial / output writes after the preceding kernels (PDL launch)
+        tc_grid_dep_wait();   // statistics, partial / output writes after the preceding kernels (PDL launch)
+        {
+            // the window of every piece (narrow geometry: decided per tile from the split kernel's row
+            // statistics; every piece of a tile takes the same decision): warp 2 + k decides piece k, then
+            // warp 2 releases producer and issuer
+            if (tc_piece<PIECES>(a, warp - 2, pc)) {
+                int nwl = a.nwin;
+                if (a.nar) {
+                    const int rows = PIECES ? a.kr : a.rows_out;
+                    nwl = tc_tile_narrow(a, pc.b, pc.blk, pc.y0, rows) ? 2 : 4;
+                    if (lane == 0 && a.cnt != nullptr && pc.r0 == 0) {
+                        atomicAdd(&a.cnt[0], 1ull);
+                        if (nwl == 4) atomicAdd(&a.cnt[1], 1ull);
+                    }
+                }
+                if (lane == 0) sNwl[warp - 2] = nwl;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kTcFlushWarps * 32) : "memory");   // warps 2-9
+            if (warp == 2 && lane == 0)
+                asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&flagbar)) : "memory");
+        }
+        tc_wait(&flagbar, 0);   // every piece's window (sNwl), hence its chain length
         const int q = warp & 3, h = (warp - 2) >> 2;        // TMEM lane quarter (warp % 4) and column half
         const int m = 32 * q + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * half);
@@ -451,9 +673,10 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+            const int fr = tc_chain_rows(sNwl[k]);   // rows per main-accumulator chain (after flagbar: see below)
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
-                tc_wait(&rowdone[gr & 1], (uint32_t)((gr >> 1) & 1));
-                if (!((rr - pc.r0) % kTcFlushRows == kTcFlushRows - 1 || rr == pc.r1 - 1)) continue;   // mid-chain
+                tc_wait(&rowdone[gr % kTcMaxFlushRows], (uint32_t)((gr / kTcMaxFlushRows) & 1));
+                if (!(((rr - pc.r0) & (fr - 1)) == fr - 1 || rr == pc.r1 - 1)) continue;   // mid-chain
                 __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
@@ -524,8 +747,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
             const int f = warp - 2;
             for (int mm = 0; mm < 128 / kTcFlushWarps; ++mm) {
                 const int m = (128 / kTcFlushWarps) * f + mm;
-                const int r = m / kTcBlk, tol = m % kTcBlk;
-                const int y = pc.y0 + r, to = pc.blk * kTcBlk + tol;
+                const int r = m / a.kb, tol = m % a.kb;
+                const int y = pc.y0 + r, to = tc_to(a.nar != 0, pc.blk, tol, a.nt);
                 if (y >= a.y_hi || r >= a.rows_out) continue;
                 const int64_t rowbase = (int64_t)pc.b * N + ((int64_t)to * a.ny + y) * a.nx;
                 for (int x = lane; x < a.nx; x += 32) err += apply_epilogue<false>(epi, rowbase + x, x, y, T[m * pitch + x]);
@@ -543,13 +766,15 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap)
 }
 
 // balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
-// one block per (8-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
+// one block per (kr-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
 __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
     __shared__ int sNp;
     tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
     const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
-    const int blk = to / kTcBlk, grp = b * a.nblk + blk;
+    // the M-tile orientation of `to`: classic blocks of 16 from 0; narrow blocks of 8 from 4
+    const int u = a.nar ? (to - 4 + a.nt) % a.nt : to;
+    const int blk = u / a.kb, tol = u % a.kb, grp = b * a.nblk + blk;
     if (threadIdx.x < 32) {   // warp 0: the group's unit offset as a strided sum + shuffle reduction
         int pre = 0;
         for (int i = threadIdx.x; i < g; i += 32) pre += tc_group_len(a, i);
@@ -564,27 +789,21 @@ __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilo
     const int np = sNp;
     const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * 3) * 128 * a.npad;
     const int64_t N = (int64_t)a.nx * a.ny * a.nt;
-    // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r and r + 4
+    // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r0 + 4 k
     const int x0 = (threadIdx.x & 63) * 4, r0 = threadIdx.x >> 6;
-    float4 v[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int r = r0 + 4 * k;
-        if (x0 >= a.npad) break;   // narrow rows: no load past the row (npad % 16 == 0, so x0 + 3 < npad)
-        const float4* src = reinterpret_cast<const float4*>(tile + (size_t)(r * kTcBlk + (to % kTcBlk)) * a.npad + x0);
-        v[k] = src[0];
+    float err = 0.f;
+    for (int r = r0; r < a.kr; r += 4) {
+        const int y = a.y_lo + g * a.kr + r;
+        if (x0 >= a.npad || y >= a.y_hi) break;   // narrow rows: no load past the row (npad % 16 == 0)
+        const float4* src = reinterpret_cast<const float4*>(tile + (size_t)(r * a.kb + tol) * a.npad + x0);
+        float4 v = src[0];
         for (int p = 1; p < np; ++p) {
             const float4 w = src[(size_t)p * 32 * a.npad];   // 128 * npad floats = 32 * npad float4
-            v[k].x += w.x; v[k].y += w.y; v[k].z += w.z; v[k].w += w.w;
+            v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
         }
-    }
-    float err = 0.f;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int r = r0 + 4 * k, y = a.y_lo + g * kTcRows + r;
-        if (y >= a.y_hi || x0 >= a.nx) continue;
+        if (x0 >= a.nx) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
-        const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (x0 + j < a.nx) err += apply_epilogue<false>(epi, rowbase + x0 + j, x0 + j, y, vv[j]);
@@ -600,39 +819,44 @@ __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilo
 bool conv_tc_eligible(const se2_kernel_s* k) {
     if (getenv("SE2_NO_TC") != nullptr) return false;
     if (k->nt % 16 != 0 || k->nx > 256 || k->R > kTcPadX) return false;
-    if (k->nt / 8 > 4 && k->band > 8) return false;   // the 32-orientation window must cover the band
+    // the stored window must cover the band: classic 32-wide window (nt > 32) +-8, narrow wide window +-12
+    if (k->nt / 8 > 4 && k->band > (tc_use_narrow(k) ? 12 : 8)) return false;
     return true;
 }
 
-// output rows per CTA: fewer than the M tile's 8 when that fills the SMs in the same number of waves
-// (c4: 7 rows -> 37 x 4 = 148 CTAs, one wave, each chain 37 instead of 38 input rows).  Chosen for the
-// kernel's max_batch so that every launch (and the error-partial layout) uses one geometry.
+// output rows per CTA: fewer than the M tile's kr when that fills the SMs in the same number of waves.
+// Chosen for the kernel's max_batch so that every launch (and the error-partial layout) uses one geometry.
 static int tc_rows_out(const se2_kernel_s* k) {
-    int best = kTcRows;
+    const TcGeom g = tc_geom(k);
+    int best = g.kr;
     double best_cost = 1e300;
-    for (int rows = kTcRows; rows >= 4; --rows) {
-        const double ctas = (double)((k->wrows() + rows - 1) / rows) * (k->nt / kTcBlk) * k->max_batch;
+    for (int rows = g.kr; rows >= g.kr / 2; --rows) {
+        const double ctas = (double)((k->wrows() + rows - 1) / rows) * g.nblk * k->max_batch;
         const double cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
         if (cost < best_cost - 1e-9) { best_cost = cost; best = rows; }
     }
     return best;
 }
 
-// balanced mode geometry (host mirror of tc_group_len / tc_group_prefix)
-static int tc_group_len_h(const se2_kernel_s* k, int g) {
-    const int y0 = k->wlo() + g * kTcRows;
-    return std::min(k->ny - 1, std::min(k->whi() - 1, y0 + kTcRows - 1) + k->R) - std::max(0, y0 - k->R) + 1;
+// balanced mode geometry (host mirror of tc_group_len)
+static int tc_group_len_h(const se2_kernel_s* k, int kr, int g) {
+    const int y0 = k->wlo() + g * kr;
+    return std::min(k->ny - 1, std::min(k->whi() - 1, y0 + kr - 1) + k->R) - std::max(0, y0 - k->R) + 1;
 }
-static int tc_ngroups(const se2_kernel_s* k) { return (k->wrows() + kTcRows - 1) / kTcRows; }
+static int tc_ngroups(const se2_kernel_s* k) {
+    const int kr = tc_geom(k).kr;
+    return (k->wrows() + kr - 1) / kr;
+}
 static void tc_units(const se2_kernel_s* k, int batch, int* ug, int* lmax, long long* U) {
+    const TcGeom gm = tc_geom(k);
     const int ngroups = tc_ngroups(k);
     *ug = 0;
     *lmax = 0;
     for (int g = 0; g < ngroups; ++g) {
-        *ug += tc_group_len_h(k, g);
-        *lmax = std::max(*lmax, tc_group_len_h(k, g));
+        *ug += tc_group_len_h(k, gm.kr, g);
+        *lmax = std::max(*lmax, tc_group_len_h(k, gm.kr, g));
     }
-    *U = (long long)batch * (k->nt / kTcBlk) * (*ug);
+    *U = (long long)batch * gm.nblk * (*ug);
 }
 // units per CTA in the balanced mode: ceil(U / 148), at least half the longest chain (<= 3 pieces per tile)
 static int tc_units_per_cta(const se2_kernel_s* k, int batch) {
@@ -645,18 +869,20 @@ static int tc_units_per_cta(const se2_kernel_s* k, int batch) {
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
     if (k->tc_part != nullptr) return tc_ngroups(k) * k->nt;   // balanced: epilogue blocks
     const int rows = tc_rows_out(k);
-    return (k->wrows() + rows - 1) / rows * (k->nt / kTcBlk);
+    return (k->wrows() + rows - 1) / rows * tc_geom(k).nblk;
 }
 
-// 5-D tensor map over split weights w: one TMA box per pipeline stage ([hl][chunk][8 j][16 to x 8 ti])
-static cudaError_t tc_weight_map(const se2_kernel_s* k, void* w, void** map_out) {
+// 5-D tensor map over split weights w: one TMA box per pipeline stage ([hl][chunk nbox][kr j][kb to x 8 ti])
+static cudaError_t tc_weight_map(const se2_kernel_s* k, void* w, int nbox, void** map_out) {
     const TcGeom g = tc_geom(k);
-    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
+    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * g.kb * 8;
     CUtensorMap* m = new CUtensorMap;
-    const uint64_t dims[5] = {(uint64_t)kTcBlk * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};
-    const uint64_t strides[4] = {(uint64_t)kTcBlk * 8 * 2, (uint64_t)g.nj * kTcBlk * 8 * 2,
-                                 (uint64_t)g.nwin * g.nj * kTcBlk * 8 * 2, (uint64_t)wk_hl * 2};
-    const uint32_t box[5] = {(uint32_t)kTcBlk * 8, (uint32_t)kTcRows, (uint32_t)g.nwin, 1, 2};
+    const uint64_t dims[5] = {(uint64_t)g.kb * 8, (uint64_t)g.nj, (uint64_t)g.nwin, (uint64_t)g.nblk * k->S, 2};
+    const uint64_t strides[4] = {(uint64_t)g.kb * 8 * 2, (uint64_t)g.nj * g.kb * 8 * 2,
+                                 (uint64_t)g.nwin * g.nj * g.kb * 8 * 2, (uint64_t)wk_hl * 2};
+    // 8 / nbox filter columns per box (past the block's last column the box reads the next block's first
+    // columns or zero fill, never used)
+    const uint32_t box[5] = {(uint32_t)g.kb * 8, (uint32_t)g.kr, (uint32_t)nbox, (uint32_t)tc_cols(nbox), 2};
     if (!make_tmap_5d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, dims, strides, box)) {
         delete m;
         return cudaErrorInvalidValue;
@@ -665,19 +891,32 @@ static cudaError_t tc_weight_map(const se2_kernel_s* k, void* w, void** map_out)
     return cudaSuccess;
 }
 
+// split weights + tensor maps (+ the narrow window's outside mass) of one weight table
+static cudaError_t tc_build_weights(se2_kernel_s* k, const float* W, void* wk, void** map, void** mapn, float** wout,
+                                    cudaStream_t s) {
+    const TcGeom g = tc_geom(k);
+    cudaError_t e = tc_weight_map(k, wk, g.nwin, map);
+    if (e == cudaSuccess && g.nar) e = tc_weight_map(k, wk, 2, mapn);
+    if (e != cudaSuccess) return e;
+    tc_split_weights_kernel<<<592, 256, 0, s>>>(W, reinterpret_cast<__nv_bfloat16*>(wk), k->tc_w_hl, k->nt, k->S, g.nch,
+                                                g.nwin, g.nj, g.nblk, g.nar ? 1 : 0);
+    count_launch();
+    if (g.nar) {
+        e = cudaMalloc(wout, g.nblk * sizeof(float));
+        if (e != cudaSuccess) return e;
+        tc_wout_kernel<<<g.nblk, 256, 0, s>>>(W, *wout, k->nt, k->S);
+        count_launch();
+    }
+    return cudaGetLastError();
+}
+
 // K10 weights of the transport-cost table rho^2 exp(-rho^2/eps) (se2_transport_cost, NEXT #2): same
 // layout as the Gibbs weights, built on the first cost evaluation after k->Wcl is tabulated
 cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s) {
     if (k->tc_w == nullptr || k->tc_wc != nullptr || k->Wcl == nullptr) return cudaSuccess;
-    const TcGeom g = tc_geom(k);
     cudaError_t e = cudaMalloc(&k->tc_wc, 2 * k->tc_w_hl * sizeof(__nv_bfloat16));
     if (e != cudaSuccess) return e;
-    e = tc_weight_map(k, k->tc_wc, &k->tc_wcmap);
-    if (e != cudaSuccess) return e;
-    tc_split_weights_kernel<<<592, 256, 0, s>>>(k->Wcl, reinterpret_cast<__nv_bfloat16*>(k->tc_wc), k->tc_w_hl, k->nt,
-                                                k->S, g.nch, g.nwin, g.nj, g.nblk);
-    count_launch();
-    return cudaGetLastError();
+    return tc_build_weights(k, k->Wcl, k->tc_wc, &k->tc_wcmap, &k->tc_wcmapn, &k->tc_woutc, s);
 }
 
 // default-engine and geometry decisions for the kernel's output window (at build, and again when
@@ -689,12 +928,12 @@ cudaError_t conv_tc_decide(se2_kernel_s* k) {
     cudaError_t e = cudaSuccess;
     {
         // cost model at batch 1 (measured on B200, K10): K10 = waves x one CTA's MMA chain
-        // ((8 + 2R) rows x S taps x K/16 steps x 3 passes x N/2 cycles) at ~70% of the tensor floor,
-        // K2 = 2 nnz N flop at ~60 TFLOP/s (0.82 of the FFMA peak)
+        // ((kr + 2R) rows x S taps x K/16 steps x 3 passes x N/2 cycles) at ~70% of the tensor floor,
+        // K2 = 2 nnz N flop at ~60 TFLOP/s (0.82 of the FFMA peak).  Narrow geometry: K = 16 assumed.
         const int rows = tc_rows_out(k);
         const double ctas = (double)((k->wrows() + rows - 1) / rows) * g.nblk;
         const double waves = std::ceil(ctas / 148.0);
-        const double row_cyc = (double)k->S * (g.nwin / 2) * 3 * (g.npad / 2);   // one input row's MMA chain
+        const double row_cyc = (double)k->S * ((g.nar ? 2 : g.nwin) / 2) * 3 * (g.npad / 2);   // one input row's chain
         double t10 = waves * std::min(k->ny, rows + 2 * k->R) * row_cyc / 0.7 / 1.9e9 + 8e-6;
         // the balanced mode (chosen below when it is cheaper): q input rows per SM + its epilogue pass
         t10 = std::min(t10, tc_units_per_cta(k, 1) * row_cyc / 0.7 / 1.9e9 + 20e-6);
@@ -702,7 +941,7 @@ cudaError_t conv_tc_decide(se2_kernel_s* k) {
         k->tc_fast = getenv("SE2_TC_DEFAULT") ? (atoi(getenv("SE2_TC_DEFAULT")) != 0) : (t10 < t2);
     }
     {
-        // balanced mode (8-row tiles split into equal runs of input rows over 148 CTAs + an epilogue
+        // balanced mode (kr-row tiles split into equal runs of input rows over 148 CTAs + an epilogue
         // kernel) when its per-SM chain beats the row-count mode's; decided for max_batch
         int ug, lmax;
         long long U;
@@ -713,8 +952,8 @@ cudaError_t conv_tc_decide(se2_kernel_s* k) {
         const double rows_cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
         const bool want = getenv("SE2_TC_PIECES") ? (atoi(getenv("SE2_TC_PIECES")) != 0) : (q < 0.95 * rows_cost);
         if (want && k->tc_part == nullptr) {
-            // sized for the whole grid: any later output window has at most as many 8-row tiles
-            const size_t tiles = (size_t)k->max_batch * g.nblk * ((k->ny + kTcRows - 1) / kTcRows);
+            // sized for the whole grid: any later output window has at most as many kr-row tiles
+            const size_t tiles = (size_t)k->max_batch * g.nblk * ((k->ny + g.kr - 1) / g.kr);
             e = cudaMalloc(&k->tc_part, tiles * 3 * 128 * g.npad * sizeof(float));
             if (e != cudaSuccess) return e;
         } else if (!want && k->tc_part != nullptr) {
@@ -727,21 +966,22 @@ cudaError_t conv_tc_decide(se2_kernel_s* k) {
 
 cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     if (!conv_tc_eligible(k)) return cudaSuccess;
+    k->tc_nar = tc_use_narrow(k);
     const TcGeom g = tc_geom(k);
-    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * kTcBlk * 8;
+    const size_t wk_hl = (size_t)g.nblk * k->S * g.nwin * g.nj * g.kb * 8;
     const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
     cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_stats, (size_t)k->max_batch * k->ny * g.nch * sizeof(float2));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 2 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
     k->tc_w_hl = wk_hl;
     k->tc_x_hl = xk_hl;
     e = conv_tc_decide(k);
     if (e != cudaSuccess) return e;
-    e = tc_weight_map(k, k->tc_w, &k->tc_wmap);
+    e = tc_build_weights(k, k->Wl, k->tc_w, &k->tc_wmap, &k->tc_wmapn, &k->tc_wout, 0);
     if (e != cudaSuccess) return e;
-    tc_split_weights_kernel<<<592, 256>>>(k->Wl, reinterpret_cast<__nv_bfloat16*>(k->tc_w), wk_hl, k->nt, k->S, g.nch,
-                                          g.nwin, g.nj, g.nblk);
-    count_launch();
     // the attribute is per function: set the maximum once (each launch passes its own size)
     int optin = 0;
     cudaFuncAttributes fa;
@@ -762,10 +1002,31 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
 void conv_tc_release(se2_kernel_s* k) {
     delete reinterpret_cast<CUtensorMap*>(k->tc_wmap);
     delete reinterpret_cast<CUtensorMap*>(k->tc_wcmap);
+    delete reinterpret_cast<CUtensorMap*>(k->tc_wmapn);
+    delete reinterpret_cast<CUtensorMap*>(k->tc_wcmapn);
     if (k->tc_wc) cudaFree(k->tc_wc);
     if (k->tc_part) cudaFree(k->tc_part);
-    k->tc_wmap = k->tc_wcmap = k->tc_wc = nullptr;
+    if (k->tc_wout) cudaFree(k->tc_wout);
+    if (k->tc_woutc) cudaFree(k->tc_woutc);
+    if (k->tc_stats) cudaFree(k->tc_stats);
+    if (k->tc_cnt) cudaFree(k->tc_cnt);
+    k->tc_wmap = k->tc_wcmap = k->tc_wc = k->tc_wmapn = k->tc_wcmapn = nullptr;
     k->tc_part = nullptr;
+    k->tc_wout = k->tc_woutc = nullptr;
+    k->tc_stats = nullptr;
+    k->tc_cnt = nullptr;
+}
+
+cudaError_t conv_tc_tile_counts(const se2_kernel_s* k, int64_t* tiles, int64_t* wide, bool reset) {
+    unsigned long long h[2] = {0, 0};
+    if (k->tc_cnt != nullptr) {
+        cudaError_t e = cudaMemcpy(h, k->tc_cnt, sizeof(h), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && reset) e = cudaMemset(k->tc_cnt, 0, sizeof(h));
+        if (e != cudaSuccess) return e;
+    }
+    *tiles = (int64_t)h[0];
+    *wide = (int64_t)h[1];
+    return cudaSuccess;
 }
 
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
@@ -787,11 +1048,13 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         c.numAttrs = 1;
         return c;
     };
+    float2* stats = g.nar ? reinterpret_cast<float2*>(k->tc_stats) : nullptr;
     {
-        // one (field, row, chunk, pixel) item per thread: all 8 plane loads of every item in flight
-        const long long items = (long long)batch * k->ny * (k->nt / 8) * g.nxp;
-        cudaLaunchConfig_t c = cfg_of(dim3((unsigned)std::min<long long>((items + 255) / 256, 1 << 20)), dim3(256), 0);
-        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, batch);
+        // one block per (field, row, chunk), one padded pixel per thread: all 8 plane loads in flight
+        const long long rows = (long long)batch * k->ny * g.nch;
+        const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
+        cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
+        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
         if (e != cudaSuccess) return e;
     }
     count_launch();
@@ -803,27 +1066,35 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.wk_hl = k->tc_w_hl;
     a.nx = k->nx; a.ny = k->ny; a.nt = k->nt; a.R = k->R; a.S = k->S;
     a.npad = g.npad; a.nxp = g.nxp; a.nch = g.nch; a.nwin = g.nwin; a.nj = g.nj;
+    a.nar = g.nar ? 1 : 0;
+    a.na = g.na;
+    a.kr = g.kr;
+    a.kb = g.kb;
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.tmem_cols = g.tmem_cols;
     a.y_lo = k->wlo();
     a.y_hi = k->whi();
+    a.stats = stats;
+    a.wout = cost ? k->tc_woutc : k->tc_wout;
+    a.cnt = k->tc_cnt;
+    a.nblk = g.nblk;
     const CUtensorMap* wm = reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmap : k->tc_wmap);
+    const CUtensorMap* wmn = g.nar ? reinterpret_cast<const CUtensorMap*>(cost ? k->tc_wcmapn : k->tc_wmapn) : wm;
     if (k->tc_part != nullptr) {
-        // balanced mode: 8-row tiles, equal runs of chain units per CTA, partials + epilogue kernel
+        // balanced mode: kr-row tiles, equal runs of chain units per CTA, partials + epilogue kernel
         long long U;
         int lmax;
         tc_units(k, batch, &a.ug, &lmax, &U);
-        a.rows_out = kTcRows;
+        a.rows_out = g.kr;
         a.batch = batch;
-        a.nblk = g.nblk;
         a.ngroups = tc_ngroups(k);
         a.q = tc_units_per_cta(k, batch);
         a.part = reinterpret_cast<float*>(k->tc_part);
         const int ncta = (int)((U + a.q - 1) / a.q);
         {
             cudaLaunchConfig_t c = cfg_of(dim3(ncta), dim3(kTcThreads), g.smem);
-            cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<true>, a, epi, *wm);
+            cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<true>, a, epi, *wm, *wmn);
             if (e != cudaSuccess) return e;
         }
         count_launch();
@@ -837,12 +1108,16 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         return cudaGetLastError();
     }
     a.rows_out = tc_rows_out(k);
+    a.batch = batch;
+    a.ngroups = 0;
+    a.ug = 0;
+    a.q = 0;
     a.part = nullptr;
     dim3 grid((k->wrows() + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
     {
         cudaLaunchConfig_t c = cfg_of(grid, dim3(kTcThreads), g.smem);
-        cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<false>, a, epi, *wm);
+        cudaError_t e = cudaLaunchKernelEx(&c, conv_tc_kernel<false>, a, epi, *wm, *wmn);
         if (e != cudaSuccess) return e;
     }
     count_launch();

@@ -148,6 +148,15 @@ struct se2_kernel_s {
     void* tc_part = nullptr;      // balanced mode: per-piece partial sums [tiles][3][128][npad] (null: off)
     void* tc_wcmap = nullptr;
     bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
+    // K10 narrow geometry (nt >= 32): 16 rows x 8 orientations per M tile, a 16-orientation K window per
+    // tile when a per-tile bound proves the rest of the band negligible, else the 32-wide window
+    bool tc_nar = false;
+    void* tc_wmapn = nullptr;     // CUtensorMap boxes of the narrow window (Gibbs / cost weights)
+    void* tc_wcmapn = nullptr;
+    float* tc_wout = nullptr;     // [nblk] max over the block's orientations of the weight mass outside the narrow window
+    float* tc_woutc = nullptr;    //   the same for the cost table
+    void* tc_stats = nullptr;     // float2 [max_batch][ny][nt/8]: (min v, max |v|) per input row and theta chunk
+    unsigned long long* tc_cnt = nullptr;   // [2] tiles, tiles on the wide window (instrumentation)
     unsigned int* guard = nullptr;  // [4] guard counters (Epilogue::guard), zeroed per solve
     float* L2hi = nullptr;          // K4P: L log2(e) as an exact float pair, Lq layout (built on first use)
     float* L2lo = nullptr;
@@ -177,6 +186,8 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k);
 cudaError_t conv_tc_decide(se2_kernel_s* k);   // re-run K10's engine / geometry choice (window changes)
 void conv_tc_release(se2_kernel_s* k);
 cudaError_t conv_tc_prepare_cost(se2_kernel_s* k, cudaStream_t s);
+// K10 narrow geometry: tiles launched / tiles that took the wide (32-orientation) window (instrumentation)
+cudaError_t conv_tc_tile_counts(const se2_kernel_s* k, int64_t* tiles, int64_t* wide, bool reset);
 int conv_blocks_per_field_tc(const se2_kernel_s* k);
 cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, const Epilogue& epi, cudaStream_t s,
                            int* bpf);

@@ -76,14 +76,17 @@ TC_GRIDS = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["auto", "rows"])
+@pytest.mark.parametrize("mode", ["auto", "rows", "classic"])
 @pytest.mark.parametrize("case", TC_GRIDS, ids=lambda c: c[0])
 def test_conv_tc_parity(case, mode, cuda_device, monkeypatch):
     """K10 forced on grids it covers, against the fp64 oracle (full fields), at TOL_CONV_TC.  auto: the
-    geometry K10 picks (the balanced mode on these grids: pieces of 8-row tiles over the SMs); rows:
-    the rows-per-CTA mode (SE2_TC_PIECES=0 at kernel build)."""
+    geometry K10 picks (narrow 16-row x 8-orientation tiles for nt >= 32, balanced mode on these grids:
+    pieces of tiles over the SMs); rows: the rows-per-CTA mode (SE2_TC_PIECES=0 at kernel build);
+    classic: the 8-row x 16-orientation geometry with the 32-wide window (SE2_TC_NAR=0)."""
     if mode == "rows":
         monkeypatch.setenv("SE2_TC_PIECES", "0")
+    if mode == "classic":
+        monkeypatch.setenv("SE2_TC_NAR", "0")
     name, nx, ny, nt, eps, w, R = case
     assert _kernel(nx, ny, nt, eps, w, R, 2).has_tensor_cores
     _conv_check(name, nx, ny, nt, eps, w, R, False, batch=2, full=True, extra_flags=L.SE2_LIN_TC)
@@ -152,6 +155,52 @@ def _conv_check(name, nx, ny, nt, eps, w, R, log_domain, batch=2, full=True, lse
         tc = not (extra_flags & L.SE2_LIN_FFMA) and (
             k.uses_tensor_cores or (bool(extra_flags & L.SE2_LIN_TC) and k.has_tensor_cores))
         assert e < (TOL_CONV_TC if tc else TOL_CONV), (name, tc, e)
+
+
+# the c4 kernel (eps 0.003, w (1,3,1), R 15, nt 64: fp32 band +-5) on a ragged reduced window
+NAR_GRID = (60, 45, 64, 0.003, (1.0, 3.0, 1.0), 15)
+
+
+@pytest.mark.parametrize("field", ["smooth", "range80", "zeros", "negative"])
+@pytest.mark.parametrize("mode", ["auto", "rows"])
+def test_conv_tc_narrow_window(field, mode, cuda_device, monkeypatch):
+    """K10's narrow geometry decides per tile between the 16-orientation window (the |to - ti| = 5 taps of
+    the c4 kernel dropped, proven <= 2^-30 of every output from the split kernel's row statistics) and
+    the 32-orientation window.  smooth (log range 20 nats): every tile narrow; range80 (e^U(-40, 40) per
+    entry): the bound fails, tiles go wide; zeros (a few zero rows): the tiles whose outputs may vanish go
+    wide; negative (one negative entry): its window's tiles go wide.  Every case against the fp64 oracle at
+    TOL_CONV_TC (relative, elementwise; absolute against the field's scale for the signed input)."""
+    if mode == "rows":
+        monkeypatch.setenv("SE2_TC_PIECES", "0")
+    from paper_2402_15322_b200 import se2_conv
+    nx, ny, nt, eps, w, R = NAR_GRID
+    batch = 2
+    k = _kernel(nx, ny, nt, eps, w, R, batch)
+    assert k.has_tensor_cores
+    shape = (batch, nt, ny, nx)
+    seed = zlib.crc32(field.encode())
+    v = S.random_positive_field(shape, seed=seed, log_range=80.0 if field == "range80" else 20.0)
+    if field == "zeros":
+        v[0, :, 20:23, :] = 0.0
+        v[1, 5, 40, :] = 0.0
+    if field == "negative":
+        v[1, 30, 10, 7] = -0.5
+    k.tc_tile_stats(reset=True)
+    y = _host(se2_conv(k, _dev(v), extra_flags=L.SE2_LIN_TC))
+    st = k.tc_tile_stats(reset=True)
+    ref = O.conv(O.kernel_table(O.Grid(nx, ny, nt), R, eps, w), v.astype(np.float64))
+    if field == "negative":
+        e = float(np.max(np.abs(y - ref) / np.max(np.abs(ref), axis=(2, 3), keepdims=True)))
+    else:
+        e = float(np.max(np.abs(y - ref) / np.abs(ref)))
+    assert e < TOL_CONV_TC, (field, e, st)
+    assert st["tiles"] > 0, st
+    if field == "smooth":
+        assert st["wide"] == 0, st
+    elif field == "range80":
+        assert st["wide"] > 0, st
+    else:
+        assert 0 < st["wide"] < st["tiles"], st
 
 
 def test_conv_tc_balanced_batch3(cuda_device):

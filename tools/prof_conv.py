@@ -36,5 +36,6 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
 work = 2.0 * cfg.N * a.batch * (st["box_taps"] if a.log else st["nnz_taps"])
-print(f"{a.cfg} {'log' if a.log else 'linear'} batch {a.batch}: {ms:.3f} ms/conv, "
+ts = k.tc_tile_stats() if (not a.log and k.has_tensor_cores) else {}
+print(f"{a.cfg} {'log' if a.log else 'linear'} batch {a.batch}: {ms:.3f} ms/conv, tc tiles {ts}, "
       f"{work / ms / 1e9:.2f} T(flop|tap-op)/s, nnz {st['nnz_taps']} box {st['box_taps']} band {st['theta_band']}")
