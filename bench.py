@@ -40,28 +40,33 @@ WORKLOADS = {
 }
 
 
-def _tc_executed_flop(cfg, R, batch=1):
-    """MMA flops K10 executes per launch (3 BF16 passes over the dense theta window, N = nx rounded up to
-    16): the 'executed' rate next to the algorithmic one.  Mirrors conv_tc.cu's geometry choice: the
-    balanced mode (8-row tiles, chain units spread evenly over 148 CTAs) when its per-SM chain is below
-    0.95 of the row-count mode's, else tc_rows_out's output rows per CTA (max_batch = batch)."""
+def _tc_executed_flop(cfg, R, batch=1, band=5, wide_frac=0.0):
+    """MMA flops K10 executes per launch (3 BF16 passes, N = nx rounded up to 16): the 'executed' rate next
+    to the algorithmic one.  Mirrors conv_tc.cu's geometry choice (tc_geom / conv_tc_decide):
+      * narrow geometry (nt >= 32, band <= 12): 16-row x 8-orientation M tiles, K = 16 (one K-step) on
+        tiles whose bound holds and K = 32 on the rest (wide_frac of the tiles, from se2_tc_tile_stats);
+      * classic (nt = 16): 8-row x 16-orientation tiles, K = all orientations;
+    the balanced mode (tiles' chain units spread evenly over 148 CTAs) when its per-SM chain is below 0.95
+    of the row-count mode's, else tc_rows_out's output rows per CTA (max_batch = batch)."""
     npad = (cfg.nx + 15) // 16 * 16
-    nwin = min(cfg.ntheta // 8, 4)
-    nblk = cfg.ntheta // 16
+    nar = cfg.ntheta // 8 >= 4 and band <= 12
+    kr = 16 if nar else 8
+    nblk = cfg.ntheta // (128 // kr)
     S_ = 2 * R + 1
-    per_row = S_ * (nwin // 2) * 3 * 2.0 * 128 * npad * 16
+    ksteps = (1.0 - wide_frac) * 1 + wide_frac * 2 if nar else min(cfg.ntheta // 8, 4) // 2
+    per_row = S_ * ksteps * 3 * 2.0 * 128 * npad * 16
 
     def chain(y0, rows):
         return min(cfg.ny - 1, y0 + rows - 1 + R) - max(0, y0 - R) + 1
 
-    best, rows_out = None, 8
-    for rows in range(8, 3, -1):
+    best, rows_out = None, kr
+    for rows in range(kr, kr // 2 - 1, -1):
         ctas = -(-cfg.ny // rows) * nblk * batch
         cost = -(-ctas // 148) * min(cfg.ny, rows + 2 * R)
         if best is None or cost < best:
             best, rows_out = cost, rows
-    ug = sum(chain(y0, 8) for y0 in range(0, cfg.ny, 8))
-    lmax = max(chain(y0, 8) for y0 in range(0, cfg.ny, 8))
+    ug = sum(chain(y0, kr) for y0 in range(0, cfg.ny, kr))
+    lmax = max(chain(y0, kr) for y0 in range(0, cfg.ny, kr))
     q = max(-(-batch * nblk * ug // 148), (lmax + 1) // 2)
     if q < 0.95 * best:                      # balanced mode
         return batch * nblk * ug * per_row
@@ -83,7 +88,9 @@ def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, con
             traffic_all = json.load(f)
     if k.uses_tensor_cores:
         peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
-        executed = _tc_executed_flop(cfg, cfg.R) / (conv_avg_ms / 1000.0) / 1e12
+        ts = k.tc_tile_stats(reset=False)
+        tc_wide = ts["wide"] / ts["tiles"] if ts["tiles"] else 0.0
+        executed = _tc_executed_flop(cfg, cfg.R, band=st["theta_band"], wide_frac=tc_wide) / (conv_avg_ms / 1000.0) / 1e12
         return {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 BF16, 3-pass split) + tc_split_input_kernel",
                 "peak": peak, "frac": achieved / peak, "traffic": traffic_all.get(f"{workload}_conv_tc_bytes_per_launch"),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({peak_src}; the kernel runs inside a "
@@ -93,9 +100,11 @@ def _conv_roofline(k, cfg, st, achieved, conv_avg_ms, flop_per_conv, n_conv, con
                 "executed_frac_vs_nominal": executed / (148 * 4096 * 2 * sm_max * 1e6 / 1e12),
                 "executed_frac_note": "executed MMA rate / the BURST bf16 peak (cuBLAS 8192^3 best of 10); "
                                       "executed_frac_vs_nominal: / 148 SM x 4096 BF16 MAC/cycle x 2 x sm_max_mhz",
-                "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the dense 32-orientation window and "
-                                 "the 8 + 2R input rows of each 8-row tile (M tile 128): executed / algorithmic = "
-                                 f"{_tc_executed_flop(cfg, cfg.R) / flop_per_conv:.1f}",
+                "executed_note": "3 BF16 passes (hi.hi + hi.lo + lo.hi) over the 16-orientation window of each "
+                                 "16-row x 8-orientation M tile (32 on tiles whose bound fails) and its 16 + 2R "
+                                 "input rows: executed / algorithmic = "
+                                 f"{_tc_executed_flop(cfg, cfg.R, band=st['theta_band'], wide_frac=tc_wide) / flop_per_conv:.2f}",
+                "tc_tiles_wide_frac": tc_wide,
                 "vs_ffma_roofline": achieved / ffma_peak, **common}
     return {"bound": "alu", "kernel": "conv_linear_kernel<15> (fp32 FFMA)", "peak": ffma_peak,
             "frac": achieved / ffma_peak, "traffic": traffic_all.get(f"{workload}_conv_linear_bytes_per_launch"),

@@ -1,6 +1,7 @@
 """Host-side pin of bench.py's K10 executed-work model (no GPU): the executed MMA flop count per c4
 launch must equal ncu's BF16 UTCHMMA op count of the same launch, recorded in
-profiles/r01_conv_tc_c4.md (sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum)."""
+profiles/r02_conv_tc_c4.md (sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum, narrow
+geometry; r01's classic-geometry count 914 324 717 568 is profiles/r01_conv_tc_c4.md)."""
 import dataclasses
 import os
 import sys
@@ -13,8 +14,12 @@ def test_tc_executed_flop_matches_ncu_count():
     import bench
     import se2_synth as S
     cfg = S.get_config("c4")
-    # balanced mode: 32 eight-row tiles x 4 orientation blocks, chains 23/31/38 x 28/31/23 input rows
-    assert bench._tc_executed_flop(cfg, cfg.R) == 914324717568
+    # narrow geometry, balanced mode: 16 sixteen-row tiles x 8 orientation blocks, chains 31 / 46 x 14 / 31
+    # input rows, every tile on the 16-orientation window (one K-step)
+    assert bench._tc_executed_flop(cfg, cfg.R) == 550779224064
+    # the classic geometry of r01 (8-row x 16-orientation tiles, 32-orientation window): band > 12 is never
+    # the narrow geometry, so the model with band 13 reproduces r01's count on the same grid
+    assert bench._tc_executed_flop(cfg, cfg.R, band=13) == 914324717568
 
 
 def test_tc_executed_flop_modes():
@@ -23,14 +28,17 @@ def test_tc_executed_flop_modes():
     import bench
     import se2_synth as S
     R, S_, npad = 15, 31, 256
-    per_row = S_ * 2 * 3 * 2.0 * 128 * npad * 16
+    per_row = S_ * 1 * 3 * 2.0 * 128 * npad * 16   # narrow geometry, all tiles on the 16-wide window
 
     def chains(ny, rows):
         return [min(ny - 1, y0 + rows - 1 + R) - max(0, y0 - R) + 1 for y0 in range(0, ny, rows)]
 
-    cfg = dataclasses.replace(S.get_config("c4"), ny=128)   # balanced: q = 19 < 0.95 x 34 (4-row mode)
-    assert bench._tc_executed_flop(cfg, R) == 4 * sum(chains(128, 8)) * per_row
-    cfg = S.get_config("c4")                                  # 8 fields: the row-count mode (8 rows) wins
-    assert bench._tc_executed_flop(cfg, R, batch=8) == 8 * 4 * sum(chains(256, 8)) * per_row
-    cfg = dataclasses.replace(S.get_config("c4"), ny=60)    # balanced vs 4-row tiles (34 rows per CTA)
-    assert bench._tc_executed_flop(cfg, R) == 4 * sum(chains(60, 8)) * per_row
+    cfg = dataclasses.replace(S.get_config("c4"), ny=128)   # balanced: q = 23 < 0.95 x 38 (8-row mode)
+    assert bench._tc_executed_flop(cfg, R) == 8 * sum(chains(128, 16)) * per_row
+    cfg = S.get_config("c4")                                  # 8 fields: the row-count mode (16 rows) wins
+    assert bench._tc_executed_flop(cfg, R, batch=8) == 8 * 8 * sum(chains(256, 16)) * per_row
+    cfg = dataclasses.replace(S.get_config("c4"), ny=60)    # balanced vs 8-row tiles (38 rows per CTA)
+    assert bench._tc_executed_flop(cfg, R) == 8 * sum(chains(60, 16)) * per_row
+    # tiles on the 32-wide window (bound failed) execute two K-steps
+    cfg = S.get_config("c4")
+    assert bench._tc_executed_flop(cfg, R, wide_frac=1.0) == 2 * bench._tc_executed_flop(cfg, R)

@@ -20,7 +20,7 @@ g = O.Grid(cfg.nx, cfg.ny, cfg.ntheta)
 Lt = O.log_kernel_table(g, cfg.R, cfg.eps, cfg.w)
 k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1)
 for name in ("lv", "lw"):
-    X = gold[name].reshape((-1,) + g.shape)
+    X = gold[name].reshape((-1,) + g.shape)[:2]
     for i in range(X.shape[0]):
         x64 = X[i]
         x32 = x64.astype(np.float32)
@@ -31,6 +31,7 @@ for name in ("lv", "lw"):
             y = se2_conv(k, torch.from_numpy(x32).cuda(), log_domain=True, extra_flags=fl).cpu().numpy().astype(np.float64)
             e = np.abs(y - ref32in)
             fin = np.isfinite(ref32in)
+            sg = (y - ref32in)[fin]
             print(f"{case} {name}[{i}] range [{x64.min():.0f},{x64.max():.0f}] {eng:8s}: arith err max {e[fin].max():.2e} "
-                  f"mean {e[fin].mean():.2e} | storage-rounding effect max {storage[fin].max():.2e} mean {storage[fin].mean():.2e}",
-                  flush=True)
+                  f"mean {e[fin].mean():.2e} signed mean {sg.mean():+.2e} | storage-rounding effect max "
+                  f"{storage[fin].max():.2e} mean {storage[fin].mean():.2e}", flush=True)
