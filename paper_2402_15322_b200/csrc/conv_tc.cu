@@ -769,41 +769,45 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
 // one block per (kr-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
 __global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
-    __shared__ int sNp;
     tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
     const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
     // the M-tile orientation of `to`: classic blocks of 16 from 0; narrow blocks of 8 from 4
     const int u = a.nar ? (to - 4 + a.nt) % a.nt : to;
     const int blk = u / a.kb, tol = u % a.kb, grp = b * a.nblk + blk;
-    if (threadIdx.x < 32) {   // warp 0: the group's unit offset as a strided sum + shuffle reduction
-        int pre = 0;
-        for (int i = threadIdx.x; i < g; i += 32) pre += tc_group_len(a, i);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-        if (threadIdx.x == 0) {
-            const int st = grp * a.ug + pre, len = tc_group_len(a, g);
-            sNp = (st + len - 1) / a.q - st / a.q + 1;
-        }
-    }
-    __syncthreads();
-    const int np = sNp;
+    // the group's unit offset (every thread: a few integer ops per group, no block barrier) and its pieces
+    int pre = 0;
+    for (int i = 0; i < g; ++i) pre += tc_group_len(a, i);
+    const int st = grp * a.ug + pre, len = tc_group_len(a, g);
+    const int np = (st + len - 1) / a.q - st / a.q + 1;
     const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * 3) * 128 * a.npad;
     const int64_t N = (int64_t)a.nx * a.ny * a.nt;
-    // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r0 + 4 k
+    // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r0 + 4 k.
+    // Every partial load of the thread is issued before the first use (up to 4 rows x 3 pieces in flight).
     const int x0 = (threadIdx.x & 63) * 4, r0 = threadIdx.x >> 6;
-    float err = 0.f;
-    for (int r = r0; r < a.kr; r += 4) {
-        const int y = a.y_lo + g * a.kr + r;
-        if (x0 >= a.npad || y >= a.y_hi) break;   // narrow rows: no load past the row (npad % 16 == 0)
+    constexpr int kMaxR = 4;   // rows per thread: kr / 4 <= 4
+    float4 v[kMaxR];
+#pragma unroll
+    for (int k = 0; k < kMaxR; ++k) {
+        const int r = r0 + 4 * k;
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r >= a.kr || x0 >= a.npad) continue;
         const float4* src = reinterpret_cast<const float4*>(tile + (size_t)(r * a.kb + tol) * a.npad + x0);
-        float4 v = src[0];
-        for (int p = 1; p < np; ++p) {
-            const float4 w = src[(size_t)p * 32 * a.npad];   // 128 * npad floats = 32 * npad float4
-            v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-        }
-        if (x0 >= a.nx) continue;
+        const float4 w0 = src[0];
+        const float4 w1 = np > 1 ? src[(size_t)32 * a.npad] : make_float4(0.f, 0.f, 0.f, 0.f);   // 128 npad floats
+        const float4 w2 = np > 2 ? src[(size_t)64 * a.npad] : make_float4(0.f, 0.f, 0.f, 0.f);   // = 32 npad float4
+        v[k].x = (w0.x + w1.x) + w2.x;   // pieces added in order (as before: ((p0 + p1) + p2))
+        v[k].y = (w0.y + w1.y) + w2.y;
+        v[k].z = (w0.z + w1.z) + w2.z;
+        v[k].w = (w0.w + w1.w) + w2.w;
+    }
+    float err = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxR; ++k) {
+        const int r = r0 + 4 * k;
+        const int y = a.y_lo + g * a.kr + r;
+        if (r >= a.kr || y >= a.y_hi || x0 >= a.nx) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+        const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (x0 + j < a.nx) err += apply_epilogue<false>(epi, rowbase + x0 + j, x0 + j, y, vv[j]);

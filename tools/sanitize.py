@@ -34,12 +34,16 @@ def _f(shape, seed, lo=-3.0, hi=0.0):
 
 
 def k10():
-    for (nx, ny, nt, R, batch, pieces) in [(37, 53, 32, 7, 3, "1"), (37, 53, 32, 7, 1, "0"), (16, 5, 32, 2, 2, "1"),
-                                           (72, 44, 16, 15, 1, "1")]:
+    for (nx, ny, nt, R, batch, pieces, eps) in [(37, 53, 32, 7, 3, "1", 0.01), (37, 53, 32, 7, 1, "0", 0.01),
+                                                (16, 5, 32, 2, 2, "1", 0.01), (72, 44, 16, 15, 1, "1", 0.01),
+                                                (40, 36, 64, 15, 2, "1", 0.003), (40, 36, 64, 15, 1, "0", 0.003)]:
         os.environ["SE2_TC_PIECES"] = pieces
-        k = Kernel(nx, ny, nt, 0.01, (1.0, 3.0, 1.0), R, max_batch=batch)
+        k = Kernel(nx, ny, nt, eps, (1.0, 3.0, 1.0), R, max_batch=batch)
         x = _f((batch, nt, ny, nx), nx + ny)
         se2_conv(k, x, extra_flags=L.SE2_LIN_TC)
+        # narrow geometry (nt >= 32): tiles on the 16-orientation window and, with an e^80 input range,
+        # on the 32-orientation fallback window
+        se2_conv(k, _f((batch, nt, ny, nx), nx + ny + 1, lo=-80.0, hi=0.0), extra_flags=L.SE2_LIN_TC)
         mu = _f((nt, ny, nx), 3)
         mu /= mu.sum()
         a, b, nxt = torch.empty_like(mu), torch.empty_like(mu), torch.empty_like(mu)
@@ -87,6 +91,15 @@ def bary():
     se2_bary_reduce_update(table, 2, N, lv, ld, lbar)
 
 
+def precise():
+    """fp64-potential barycenter (K4P exact log-domain conv + fp64 epilogues)."""
+    from paper_2402_15322_b200 import se2_barycenter_precise
+    k = Kernel(28, 28, 16, 0.02, (1.0, 3.0, 1.0), 5, max_batch=4)
+    mus = torch.stack([_f((16, 28, 28), s) for s in (1, 2)])
+    mus /= mus.sum(dim=(1, 2, 3), keepdim=True)
+    se2_barycenter_precise(k, mus, np.array([[0.3, 0.7], [1.0, 0.0]]), 3, trace=True)
+
+
 def slab():
     """3 slabs of a 48 x 40 x 16 grid on one GPU; each conv's epilogue writes its boundary rows into the
     neighbours' halo rows (peer pointers = plain device pointers here), slab after slab on one stream."""
@@ -124,7 +137,7 @@ def lift():
     se2_project(c, U)
 
 
-ALL = dict(k10=k10, k2=k2, k3=k3, k9=k9, bary=bary, slab=slab, lift=lift)
+ALL = dict(k10=k10, k2=k2, k3=k3, k9=k9, bary=bary, precise=precise, slab=slab, lift=lift)
 
 if __name__ == "__main__":
     names = sys.argv[1:] or ["all"]
