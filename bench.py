@@ -304,6 +304,21 @@ def config_sweep(device: int):
             rec["k3_active_frac"] = ps["active"] / max(ps["visited"], 1)
             rec["k3_ffma_frac_of_active"] = ps["ffma"] / max(ps["active"], 1)
             rec["k3_exact_rows_live_frac"] = rs["live"] / max(rs["visited"], 1)
+        if cfg.problem == "barycenter" and cfg.log_domain:
+            # the fp64-potential engine (K4P): the one whose potentials meet the north star's 1e-4
+            # elementwise (tests/test_gpu_parity.py::test_barycenter_parity_precise; R19)
+            from paper_2402_15322_b200 import se2_barycenter_precise
+            se2_barycenter_precise(k, mus, lams, cfg.iters, trace=True)
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record()
+            se2_barycenter_precise(k, mus, lams, cfg.iters, trace=True)
+            p1.record()
+            torch.cuda.synchronize()
+            pms = p0.elapsed_time(p1)
+            rec["precise_fp64_potentials"] = {"ms": pms, "iters_per_s": cfg.iters / (pms / 1000.0),
+                                              "engine": "K4P exact log-domain conv, fp64 potentials"}
+            rec["engine"] = "K3 (fp32 potentials)"
         out[cfg.name] = rec
         k.close()
     return out
@@ -383,7 +398,7 @@ def next_rows(device: int):
     return out
 
 
-def sharded_barycenter(ws: int, rank: int, local: int, world, iters: int = 100):
+def sharded_barycenter(ws: int, rank: int, local: int, world, iters: int = 500):
     """c3's barycenter (4 inputs, 128x128x32, log domain) through se2_barycenter_dist: the inputs sharded
     over the ranks (NCCL allreduce of the partial weighted log-mean, 2 MB, every iteration) and, at 8
     ranks, each input's grid split into 2 row slabs as well ("sharded one input per GPU pair",
