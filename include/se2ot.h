@@ -376,6 +376,10 @@ SE2_API se2_status se2_project(se2_cake c, const float* U, float* img, int32_t n
 SE2_API se2_status se2_project_signed(se2_cake c, const float* Upos, const float* Uneg, const double* masses_host,
                                       float* img, int32_t nx, int32_t ny, int32_t batch, double* mass_host,
                                       se2_stream stream);
+/* se2_interp_masses -- Step 4 of the image interpolation: the +/- masses of b_t linearly
+ *   interpolated between the two images', m_t = (1 - t) m(f0) + t m(f1), for each t (host arrays:
+ *   masses [2][2] from se2_split_signed of the two images, ts [nts], out [nts][2]).  t in [0, 1]. */
+SE2_API se2_status se2_interp_masses(const double* masses_host, const double* ts_host, int32_t nts, double* out_host);
 SE2_API se2_status se2_lift_field(se2_cake c, const float* angle, const float* mag, float* U, int32_t nx, int32_t ny,
                                   int32_t batch, double* mass_host, se2_stream stream);
 SE2_API se2_status se2_reconstruct_field(se2_cake c, const float* U, float* angle, float* mag, int32_t nx, int32_t ny,

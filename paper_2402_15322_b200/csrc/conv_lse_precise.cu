@@ -37,8 +37,10 @@ struct LsePCfg {
     static constexpr int PITCH = ((P0 / 4) % 2 == 1) ? P0 : P0 + 4;
     static constexpr int WIN = WIN_H * PITCH;
     static constexpr int FIL = S * S * 4;
-    // window hi + lo, filter hi + lo, one buffer (the fp64 staging conversion is done by the threads)
-    static constexpr size_t SMEM = (size_t)(2 * WIN + 2 * FIL + 4 * S) * sizeof(float) + 64;
+    static constexpr int RAW = WIN_H * WIN_W;   // the next channel's fp64 window, dense (cp.async target)
+    // window hi + lo (converted), the raw fp64 window of the next channel, filter hi + lo + row bounds
+    // double-buffered: channel a + 1 loads while channel a computes
+    static constexpr size_t SMEM = (size_t)RAW * sizeof(double) + (size_t)(2 * WIN + 2 * (2 * FIL + 4 * S)) * sizeof(float) + 64;
 };
 // pruning margin (log2 units): a term below 2^-64 of every output it could reach is never evaluated;
 // the skipped mass is < S^2 nt 2^-64 < 2^-48 relative
@@ -64,11 +66,11 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                         EpiP epi) {
     using C = LsePCfg<R>;
     extern __shared__ __align__(16) float smem[];
-    float* sWh = smem;
-    float* sWl = smem + C::WIN;
-    float* sFh = smem + 2 * C::WIN;
-    float* sFl = sFh + C::FIL;
-    float* sRow = sFl + C::FIL;   // [S][4] max over each tap row of L2 (pruning bounds)
+    double* sRaw = reinterpret_cast<double*>(smem);                 // [WIN_H * WIN_W] next channel, fp64
+    float* sWh = smem + 2 * C::RAW;
+    float* sWl = sWh + C::WIN;
+    float* sF0 = sWl + C::WIN;   // 2 buffers of [hi FIL][lo FIL][row S x 4]
+    constexpr int FBUF = 2 * C::FIL + 4 * C::S;
     __shared__ float sRed[C::NT / 32];
 
     const int tile = blockIdx.x;
@@ -118,31 +120,51 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
 
     // channels in order of increasing |theta_i - theta_o| around the quad: the dominant ones set the
     // shifts early, so the pruning bounds below bite on the rest
-    for (int a = 0; a < nt; ++a) {
+    auto chan = [&](int a) {
         const int off = (a & 1) ? (a + 1) / 2 : -(a / 2);
-        const int ti = (((4 * qd + 1 + off) % nt) + nt) % nt;
-        __syncthreads();   // the previous channel's readers are done
-        {
-            const double* src = vin + (int64_t)ti * nx * ny;
-            for (int i = threadIdx.x; i < C::WIN_H * C::WIN_W; i += C::NT) {
-                const int r = i / C::WIN_W, c = i - r * C::WIN_W;
-                const int gy = y0 - R + r, gx = x0 - R + c;
-                float hi = kSent, lo = 0.f;
-                if (gy >= 0 && gy < ny && gx >= 0 && gx < nx) split2(src[(int64_t)gy * nx + gx] * LOG2E, hi, lo);
-                sWh[r * C::PITCH + c] = hi;
-                sWl[r * C::PITCH + c] = lo;
-            }
-            const float* fh = L2hi + ((int64_t)qd * nt + ti) * C::FIL;
-            const float* fl = L2lo + ((int64_t)qd * nt + ti) * C::FIL;
-            for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) {
-                reinterpret_cast<float4*>(sFh)[i] = reinterpret_cast<const float4*>(fh)[i];
-                reinterpret_cast<float4*>(sFl)[i] = reinterpret_cast<const float4*>(fl)[i];
-            }
-            const float* rm = L2row + ((int64_t)qd * nt + ti) * C::S * 4;
-            for (int i = threadIdx.x; i < C::S; i += C::NT)
-                reinterpret_cast<float4*>(sRow)[i] = reinterpret_cast<const float4*>(rm)[i];
+        return (((4 * qd + 1 + off) % nt) + nt) % nt;
+    };
+    // asynchronous staging of channel a: the raw fp64 window (zero padding / -inf as -inf) and the
+    // channel's filter tables into buffer a & 1; the thread that copied an element converts it
+    auto issue = [&](int a) {
+        const int ti = chan(a);
+        const double* src = vin + (int64_t)ti * nx * ny;
+        for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
+            const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+            const int gy = y0 - R + r, gx = x0 - R + c;
+            if (gy >= 0 && gy < ny && gx >= 0 && gx < nx)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sRaw + i)),
+                             "l"(src + (int64_t)gy * nx + gx));
+            else
+                sRaw[i] = -(double)INFINITY;
         }
-        __syncthreads();
+        float* fb = sF0 + (a & 1) * FBUF;
+        const float* fh = L2hi + ((int64_t)qd * nt + ti) * C::FIL;
+        const float* fl = L2lo + ((int64_t)qd * nt + ti) * C::FIL;
+        for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) {
+            cp_async16(fb + 4 * i, fh + 4 * i);
+            cp_async16(fb + C::FIL + 4 * i, fl + 4 * i);
+        }
+        const float* rm = L2row + ((int64_t)qd * nt + ti) * C::S * 4;
+        for (int i = threadIdx.x; i < C::S; i += C::NT) cp_async16(fb + 2 * C::FIL + 4 * i, rm + 4 * i);
+        cp_async_commit();
+    };
+    issue(0);
+    for (int a = 0; a < nt; ++a) {
+        cp_async_wait<0>();
+        __syncthreads();   // channel a's copies visible; the previous channel's readers of sWh / sWl are done
+        for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
+            const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+            float hi, lo;
+            split2(sRaw[i] * LOG2E, hi, lo);
+            sWh[r * C::PITCH + c] = hi;
+            sWl[r * C::PITCH + c] = lo;
+        }
+        __syncthreads();   // sRaw free for the next channel, sWh / sWl complete
+        if (a + 1 < nt) issue(a + 1);
+        const float* sFh = sF0 + (a & 1) * FBUF;
+        const float* sFl = sFh + C::FIL;
+        const float* sRow = sFh + 2 * C::FIL;   // [S][4] max over each tap row of L2 (pruning bounds)
         const float* wh = sWh + wx * C::P;
         const float* wl = sWl + wx * C::P;
         const float4* fh4 = reinterpret_cast<const float4*>(sFh);

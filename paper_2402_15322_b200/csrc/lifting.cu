@@ -611,7 +611,17 @@ SE2_API se2_status se2_project(se2_cake c, const float* U, float* img, int32_t n
     return launch_ok("project");
 }
 
-SE2_API se2_status se2_project_signed(se2_cake c, const float* Upos, const float* Uneg, const double* masses_host,
+SE2_API se2_status se2_interp_masses(const double* masses_host, const double* ts_host, int32_t nts, double* out_host) {
+    SE2_CHECK_ARG(masses_host != nullptr && ts_host != nullptr && out_host != nullptr && nts >= 0, "bad arguments");
+    for (int i = 0; i < nts; ++i) {
+        const double t = ts_host[i];
+        SE2_CHECK_ARG(t >= 0.0 && t <= 1.0, "t must lie in [0, 1]");
+        for (int s = 0; s < 2; ++s) out_host[2 * i + s] = (1.0 - t) * masses_host[s] + t * masses_host[2 + s];
+    }
+    return SE2_OK;
+}
+
+se2_status se2_project_signed(se2_cake c, const float* Upos, const float* Uneg, const double* masses_host,
                                       float* img, int32_t nx, int32_t ny, int32_t batch, double* mass_host,
                                       se2_stream stream) {
     if (check_cake(c) != SE2_OK) return SE2_EINVAL;

@@ -186,6 +186,8 @@ def interpolate_images(k: Kernel, c: Cake, f0: torch.Tensor, f1: torch.Tensor, t
         if log_domain:
             b = se2_exp(b)
         barys.append(b.reshape(len(ts), c.ntheta, ny, nx).contiguous())
-    mt = np.stack([(1 - lam[:, 1]) * m[0, 0] + lam[:, 1] * m[1, 0], (1 - lam[:, 1]) * m[0, 1] + lam[:, 1] * m[1, 1]],
-                  axis=1)
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    tsa = np.ascontiguousarray(ts, dtype=np.float64)
+    mt = np.empty((len(ts), 2), dtype=np.float64)
+    check(L.load().se2_interp_masses(m.ctypes.data, tsa.ctypes.data, len(ts), mt.ctypes.data))
     return se2_project_signed(c, barys[0], barys[1], mt)
