@@ -61,14 +61,14 @@ constexpr int kTcNAMax = 8;    // weight-ring stages (allocated); TcGeom::na of 
 // input rows per main-accumulator chain (flushed to registers after each): 8 / (chunks of the window),
 // i.e. 2 rows at K = 32 and 4 rows at K = 16 -- the truncation bound stays rows x S x K/16 <= 124 steps
 // of 2^-23 at R 15 (inside R18) and the flush bubbles are halved against flushing every row
-constexpr int kTcMaxFlushRows = 4;   // depth of the row-done ring (one barrier per row of a chain)
+constexpr int kTcMaxFlushRows = 16;  // depth of the row-done ring (>= the longest chain: one barrier per row of a chain)
 // a weight stage is 32 KB: two filter columns of the 4-chunk window or four of a 2-chunk window (the
 // single issuing thread's per-stage work -- barrier wait, descriptors, commit -- is amortised over 12 MMAs)
 constexpr uint32_t kTcAStage = 2u * 8u * 2048u;
 // filter columns per stage (nwa is 2 or 4: no integer division on the single-thread issue path)
 __host__ __device__ constexpr int tc_cols(int nwa) { return nwa == 2 ? 4 : 2; }
 // input rows per main-accumulator chain: 8 / nwl
-__host__ __device__ constexpr int tc_chain_rows(int nwl) { return nwl == 2 ? 4 : 2; }
+__host__ __device__ constexpr int tc_chain_rows(int nwl, int chain16) { return nwl == 2 ? chain16 : 2; }
 constexpr int kTcThreads = 320;   // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: accumulators / epilogue
 constexpr int kTcFlushWarps = 8;
 constexpr int kTcMaxPieces = 4;   // pieces per CTA in the balanced mode (<= 3 by construction)
@@ -214,6 +214,7 @@ struct TcArgs {
     int npad, nxp, nch, nwin, nj;
     int nar, kr, kb;           // geometry (TcGeom)
     int na;                    // weight-ring stages
+    int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
     int tmem_cols;
     int rows_out;              // output rows a CTA owns (<= kr; the M tile's remaining rows are discarded)
@@ -576,7 +577,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
         int gr = 0, gs = 0, t = 0;   // input rows, main-accumulator chains and weight stages issued so far
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
             nwl = sNwl[k];
-            const int fr = tc_chain_rows(nwl);   // input rows per main-accumulator chain (power of 2)
+            const int fr = tc_chain_rows(nwl, a.chain16);   // input rows per main-accumulator chain (power of 2)
             if (k > 0) {   // the correction accumulator restarts per piece: the previous piece's was read
                 tc_wait(&cflushed, (uint32_t)((k - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -673,7 +674,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.f;
-            const int fr = tc_chain_rows(sNwl[k]);   // rows per main-accumulator chain (after flagbar: see below)
+            const int fr = tc_chain_rows(sNwl[k], a.chain16);   // rows per main-accumulator chain (after flagbar: see below)
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 tc_wait(&rowdone[gr % kTcMaxFlushRows], (uint32_t)((gr / kTcMaxFlushRows) & 1));
                 if (!(((rr - pc.r0) & (fr - 1)) == fr - 1 || rr == pc.r1 - 1)) continue;   // mid-chain
@@ -1072,6 +1073,11 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.npad = g.npad; a.nxp = g.nxp; a.nch = g.nch; a.nwin = g.nwin; a.nj = g.nj;
     a.nar = g.nar ? 1 : 0;
     a.na = g.na;
+    a.chain16 = 4;   // 4 x S x 1 K-step <= 124 truncation steps at R 15 (R18); SE2_TC_CHAIN16: measurements only
+    if (getenv("SE2_TC_CHAIN16")) {
+        const int c = atoi(getenv("SE2_TC_CHAIN16"));
+        if (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) a.chain16 = c;
+    }
     a.kr = g.kr;
     a.kb = g.kb;
     a.a_stage = (uint32_t)g.a_stage;
