@@ -42,7 +42,7 @@ EXPORTED = [
     "se2_jko_step", "se2_barycenter", "se2_marginal_error", "se2_conv_update", "se2_bary_logmean",
     "se2_bary_update", "se2_sum", "se2_timing_enable", "se2_timing_get", "se2_launch_count",
     "se2_last_error", "se2_abi_version", "se2_lse_path_stats", "se2_sum_rows", "se2_scale_rows",
-    "se2_transport_cost", "se2_lse_row_stats", "se2_tc_tile_stats", "se2_interp_masses",
+    "se2_transport_cost", "se2_lse_row_stats", "se2_tc_tile_stats", "se2_interp_masses", "se2_precise_path_stats",
     "se2_cake_build", "se2_cake_get", "se2_cake_destroy", "se2_lift_image", "se2_split_signed", "se2_project",
     "se2_project_signed", "se2_lift_field", "se2_reconstruct_field", "se2_exp", "se2_log",
     "se2_bary_reduce_update", "se2_conv_update_slab", "se2_guard_stats", "se2_kernel_set_window",
@@ -132,6 +132,7 @@ def load(path: str = LIB_PATH):
         "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_tc_tile_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_interp_masses": [P, P, i32, P],
+        "se2_precise_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_guard_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_kernel_set_window": [P, i32, i32],
         "se2_barycenter_precise": [P, i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],

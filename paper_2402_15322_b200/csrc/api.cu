@@ -156,6 +156,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->L2hi) cudaFree(k->L2hi);
     if (k->L2lo) cudaFree(k->L2lo);
     if (k->L2row) cudaFree(k->L2row);
+    if (k->pstats) cudaFree(k->pstats);
     KernelExtra* x = extra(k);
     if (x) {
         x->clear_graphs();
@@ -946,6 +947,19 @@ se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_vis
     if (rows_live) *rows_live = (int64_t)h[0];
     if (rows_visited) *rows_visited = (int64_t)h[1];
     if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters + 8, 0, sizeof(h)));
+    return SE2_OK;
+}
+
+se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t* channels, int32_t reset) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(ffma_channels != nullptr && channels != nullptr, "null output");
+    DeviceGuard g(k->device);
+    unsigned long long h[2] = {0, 0};
+    SE2_CUDA_TRY(cudaDeviceSynchronize());
+    SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters + 12, sizeof(h), cudaMemcpyDeviceToHost));
+    *ffma_channels = (int64_t)h[0];
+    *channels = (int64_t)h[1];
+    if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters + 12, 0, sizeof(h)));
     return SE2_OK;
 }
 

@@ -18,6 +18,16 @@
 //     an exact power of two (ldexp), and ly = (m + log2 S) ln 2 is formed in fp64.
 // What remains per conv is ex2.approx's ~2^-22 relative error per term: ~1e-7 nats.  Cost per tap and
 // output: 1 MUFU.EX2 + ~11 FP32 ops (K4: 1 + 5).
+//
+// Factored (FFMA) path for channels whose staged window lies within kFfmaRangeP nats of the tile's
+// minimum (K4P): exp(L + lv) = exp(Lth) exp(Ls + 40) exp(lv - M + 40) exp(M - 80) with M the
+// window maximum -- the spatial table Eq = exp(Ls + 40) (fp32, relative rounding only) times
+// v~ = exp(lv - M + 40) computed in fp64 from the fp64 potential and rounded once (relative rounding only),
+// so no term carries an absolute exponent error however large the potentials are.  Per tap one FFMA; tap
+// rows summed in fp32, rows in fp64; the channel's sum S enters the output's (integer shift, fp64 sum) as
+// frexp(S) 2^(floor G) 2^frac(G), G = (M - 80 + Lth) log2 e in fp64 (Lth from its fp64 formula).
+// Validity (range <= 80 nats): every retained product is a normal float >= e^-42, no sum overflows
+// (961 e^80 < 2^127), and the products dropped by underflow are below e^-40 of the output's centre term.
 #include "conv_common.cuh"
 
 namespace se2 {
@@ -49,6 +59,32 @@ constexpr float kGap = 64.f;
 // a staged -inf (zero mass, zero padding) is the finite sentinel -1e30: TwoSum stays NaN-free and its
 // terms underflow to exactly 0; a pass-A maximum below -1e29 means "no finite term"
 constexpr float kSent = -1e30f;
+constexpr double kFfmaRangeP = 80.0;   // natural log units: FFMA path when max(window) - min(tile) <= this
+// compact exact power-of-two scaling / splitting (the libm ldexp / frexp / log2 / exp bodies, inlined per
+// output, made the kernel's code overflow the instruction cache)
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ double ldexp_fast(double x, int e) {   // exact while the result is normal
+    if (e >= -1022 && e <= 1023) return x * pow2i(e);
+    int e1 = e / 2, e2 = e - e1;
+    e1 = max(-1022, min(1023, e1));
+    e2 = max(-1022, min(1023, e2));
+    return (x * pow2i(e1)) * pow2i(e2);
+}
+__device__ __forceinline__ double frexp_pos(double x, int& e) {   // x > 0 normal: x = mant 2^e, mant in [0.5, 1)
+    const long long bits = __double_as_longlong(x);
+    e = (int)((bits >> 52) & 0x7ff) - 1022;
+    return __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1022LL << 52));
+}
+__device__ __noinline__ double log2_once(double x) { return log2(x); }
+__device__ __noinline__ double exp2_once(double x) { return exp2(x); }
+// exp(t) for |t| <~ 200 to ~1.5 ulp of fp32: t = th + tl (fp32 pair), exp(th) (expf) times (1 + tl)
+__device__ __forceinline__ float exp_pair(double t) {
+    if (!(t > -1e300)) return 0.f;   // zero mass / padding (-inf): -inf - -inf would be NaN below
+    const float th = (float)t;
+    const float tl = (float)(t - (double)th);
+    return expf(th) * (1.f + tl);
+}
+
 __device__ __forceinline__ void split2(double x, float& hi, float& lo) {
     if (!(x > -1e300)) {
         hi = kSent;
@@ -59,11 +95,37 @@ __device__ __forceinline__ void split2(double x, float& hi, float& lo) {
     lo = (float)(x - (double)hi);
 }
 
+// channel bounds without staging: per (field, theta, row, 16-column block) the min / max of lv, rounded
+// outward to fp32; one thread per segment (16 consecutive doubles of one row)
+constexpr int kPSegW = 16;
+constexpr int kPMaxNT = 128;                 // channel pruning from these bounds for nt <= 128
+constexpr float kGapNat = 44.3614195558365f;  // kGap log2 units in nats
+__global__ void lsep_stats_kernel(const double* __restrict__ in, int nx, int ny, int nt, int batch,
+                                  float2* __restrict__ st) {
+    const int nxb = (nx + kPSegW - 1) / kPSegW;
+    const int64_t total = (int64_t)batch * nt * ny * nxb;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int xb = (int)(i % nxb);
+        const int64_t row = i / nxb;   // (b, theta, y)
+        const double* src = in + row * nx + xb * kPSegW;
+        double mn = INFINITY, mx = -INFINITY;
+        const int w = min(kPSegW, nx - xb * kPSegW);
+        for (int j = 0; j < w; ++j) {
+            const double v = src[j];
+            mn = fmin(mn, v);
+            mx = fmax(mx, v);
+        }
+        st[i] = make_float2(__double2float_rd(mn), __double2float_ru(mx));
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(LsePCfg<R>::NT)
 conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__ L2hi, const float* __restrict__ L2lo,
-                        const float* __restrict__ L2row, int nx, int ny, int nt, int tiles_x, int y_lo, int y_hi,
-                        EpiP epi) {
+                        const float* __restrict__ L2row, const float* __restrict__ Eq, double w3sq_eps, int nx, int ny,
+                        int nt, int tiles_x, int y_lo, int y_hi, EpiP epi, int ffma_max_a,
+                        unsigned long long* __restrict__ counters, const float2* __restrict__ pst,
+                        const float* __restrict__ Lth, const float* __restrict__ LseS) {
     using C = LsePCfg<R>;
     extern __shared__ __align__(16) float smem[];
     double* sRaw = reinterpret_cast<double*>(smem);                 // [WIN_H * WIN_W] next channel, fp64
@@ -72,6 +134,9 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     float* sF0 = sWl + C::WIN;   // 2 buffers of [hi FIL][lo FIL][row S x 4]
     constexpr int FBUF = 2 * C::FIL + 4 * C::S;
     __shared__ float sRed[C::NT / 32];
+    __shared__ double sWmax[C::NT / 32], sTmin[C::NT / 32];
+    __shared__ float sCM[kPMaxNT], sCMu[kPMaxNT], sPM[C::NT], sPMu[C::NT], sLB[4];
+    __shared__ int sAct[kPMaxNT], sNAct;
 
     const int tile = blockIdx.x;
     const int qd = blockIdx.y;
@@ -120,10 +185,72 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
 
     // channels in order of increasing |theta_i - theta_o| around the quad: the dominant ones set the
     // shifts early, so the pruning bounds below bite on the rest
-    auto chan = [&](int a) {
+    auto chan0 = [&](int a) {
         const int off = (a & 1) ? (a + 1) / 2 : -(a / 2);
         return (((4 * qd + 1 + off) % nt) + nt) % nt;
     };
+    // channel pruning from the row-segment bounds (nt <= kPMaxNT): a channel ti is skipped when its largest
+    // possible total e^{M + Lth + log sum e^Ls} lies more than kGap (log2) below the lower bound
+    // LB(to) = max_j (Lth(to, j) + mu_j) of every output of the tile (centre taps), M the max of lv_ti over
+    // the window, mu_j the min of lv_j over the tile: skipped mass < nt 2^-64 relative (as the per-warp skip)
+    int nact = nt;
+    if (nt <= kPMaxNT) {
+        const int nxb = (nx + kPSegW - 1) / kPSegW, xb0 = x0 / kPSegW;
+        const int parts = C::NT / nt, ti = threadIdx.x % nt, part = threadIdx.x / nt;
+        float M = NEG_INF, mu = INFINITY;
+        if (part < parts) {
+            const float2* sb = pst + (((int64_t)b * nt + ti) * ny) * nxb;
+            const int ra = max(0, y0 - R), rb = min(ny - 1, y0 + C::TY - 1 + R);
+            for (int y = ra + part; y <= rb; y += parts) {
+                const bool own = y >= y0 && y < min(y_hi, y0 + C::TY);
+                for (int xb = max(0, xb0 - 1); xb <= min(nxb - 1, xb0 + 1); ++xb) {
+                    const float2 v = sb[(int64_t)y * nxb + xb];
+                    M = fmaxf(M, v.y);
+                    if (own && xb == xb0) mu = fminf(mu, v.x);
+                }
+            }
+        }
+        sPM[threadIdx.x] = M;
+        sPMu[threadIdx.x] = mu;
+        __syncthreads();
+        if (threadIdx.x < nt) {
+            for (int pp = 1; pp < parts; ++pp) {
+                M = fmaxf(M, sPM[pp * nt + threadIdx.x]);
+                mu = fminf(mu, sPMu[pp * nt + threadIdx.x]);
+            }
+            sCM[threadIdx.x] = M;
+            sCMu[threadIdx.x] = mu;
+        }
+        __syncthreads();
+        if (wx < 4) {   // warp q: LB(to_q)
+            const int to = 4 * qd + wx;
+            float lbv = NEG_INF;
+            if (to < nt)
+                for (int j = lane; j < nt; j += 32) lbv = fmaxf(lbv, Lth[to * nt + j] + sCMu[j]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lbv = fmaxf(lbv, __shfl_xor_sync(0xffffffffu, lbv, o));
+            if (lane == 0) sLB[wx] = lbv;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int n = 0;
+            for (int a = 0; a < nt; ++a) {
+                const int t = chan0(a);
+                const float Mt = sCM[t];
+                bool act = false;
+                if (Mt > NEG_INF && Mt == Mt)
+                    for (int q = 0; q < 4; ++q) {
+                        const int to = 4 * qd + q;
+                        if (to < nt && !(Mt + Lth[to * nt + t] + LseS[to * nt + t] < sLB[q] - kGapNat)) act = true;
+                    }
+                if (act) sAct[n++] = t;
+            }
+            sNAct = n;
+        }
+        __syncthreads();
+        nact = sNAct;
+    }
+    auto chan = [&](int a) { return nt <= kPMaxNT ? sAct[a] : chan0(a); };
     // asynchronous staging of channel a: the raw fp64 window (zero padding / -inf as -inf) and the
     // channel's filter tables into buffer a & 1; the thread that copied an element converts it
     auto issue = [&](int a) {
@@ -149,19 +276,42 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         for (int i = threadIdx.x; i < C::S; i += C::NT) cp_async16(fb + 2 * C::FIL + 4 * i, rm + 4 * i);
         cp_async_commit();
     };
-    issue(0);
-    for (int a = 0; a < nt; ++a) {
+    if (nact > 0) issue(0);
+    for (int a = 0; a < nact; ++a) {
         cp_async_wait<0>();
         __syncthreads();   // channel a's copies visible; the previous channel's readers of sWh / sWl are done
+        double wmax = -(double)INFINITY, tmin = (double)INFINITY;   // window max, tile min (natural)
         for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
             const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+            const double v = sRaw[i];
             float hi, lo;
-            split2(sRaw[i] * LOG2E, hi, lo);
+            split2(v * LOG2E, hi, lo);
             sWh[r * C::PITCH + c] = hi;
             sWl[r * C::PITCH + c] = lo;
+            wmax = fmax(wmax, v);
+            // the tile's own (in-grid) positions: every output of the tile has its centre term there
+            if (r >= R && r < R + C::TY && c >= R && c < R + C::TX && y0 + r - R < y_hi && x0 + c - R < nx)
+                tmin = fmin(tmin, v);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+            tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+        }
+        if (lane == 0) { sWmax[wx] = wmax; sTmin[wx] = tmin; }
+        __syncthreads();
+        wmax = sWmax[0];
+        tmin = sTmin[0];
+#pragma unroll
+        for (int w2 = 1; w2 < C::NT / 32; ++w2) { wmax = fmax(wmax, sWmax[w2]); tmin = fmin(tmin, sTmin[w2]); }
+        const bool ffma = a < ffma_max_a && isfinite(wmax) && isfinite(tmin) && (wmax - tmin <= kFfmaRangeP);
+        if (ffma)   // v~ = exp(lv - M + 40) in fp64, rounded once (zero mass / padding -> 0)
+            for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
+                const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+                sWh[r * C::PITCH + c] = exp_pair(sRaw[i] - wmax + 40.0);   // -inf -> 0
+            }
         __syncthreads();   // sRaw free for the next channel, sWh / sWl complete
-        if (a + 1 < nt) issue(a + 1);
+        if (a + 1 < nact) issue(a + 1);
         const float* sFh = sF0 + (a & 1) * FBUF;
         const float* sFl = sFh + C::FIL;
         const float* sRow = sFh + 2 * C::FIL;   // [S][4] max over each tap row of L2 (pruning bounds)
@@ -170,6 +320,110 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         const float4* fh4 = reinterpret_cast<const float4*>(sFh);
         const float4* fl4 = reinterpret_cast<const float4*>(sFl);
         const float4* rw4 = reinterpret_cast<const float4*>(sRow);
+
+        if (counters != nullptr && threadIdx.x == 0) {
+            atomicAdd(&counters[0], ffma ? 1ull : 0ull);
+            atomicAdd(&counters[1], 1ull);
+        }
+        if (ffma) {
+            // ---------------- factored path: S = sum_d Eq(d) v~(x - d), one FFMA per tap ----------------
+            const int ti = chan(a);
+            float lbf[4];
+            floors(lbf);
+            double Lt[4];
+            bool reach = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int to = 4 * qd + q;
+                int kk = ((to - ti) % nt + nt) % nt;
+                if (2 * kk >= nt) kk -= nt;
+                const double Th = 6.283185307179586476925286766559 * kk / nt;
+                Lt[q] = -w3sq_eps * Th * Th;   // Lth(to, ti), the fp64 formula of tabulate_theta_kernel
+                // largest possible term of the channel: exp(M + Lth) (Ls <= 0)
+                if (to < nt && (float)((wmax + Lt[q]) * LOG2E) >= lbf[q]) reach = true;
+            }
+            if (!__any_sync(0xffffffffu, reach)) continue;   // warp-uniform
+            const float4* eq4 = reinterpret_cast<const float4*>(Eq + ((int64_t)qd * nt + ti) * C::FIL);
+            double accd[4][C::P];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int p = 0; p < C::P; ++p) accd[q][p] = 0.0;
+#pragma unroll 1
+            for (int dy = 0; dy < C::S; ++dy) {
+                const float4* rowp = reinterpret_cast<const float4*>(wh + (lane - dy + 2 * R) * C::PITCH);
+                float r[C::RL];
+#pragma unroll
+                for (int j = 0; j < C::RL / 4; ++j) {
+                    const float4 t = rowp[j];
+                    r[4 * j + 0] = t.x; r[4 * j + 1] = t.y; r[4 * j + 2] = t.z; r[4 * j + 3] = t.w;
+                }
+                float rs[4][C::P];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int p = 0; p < C::P; ++p) rs[q][p] = 0.f;
+                {   // rolled tap loop, 4-wide sliding window of the staged row
+                    const float* rowF = wh + (lane - dy + 2 * R) * C::PITCH;
+                    float x0v = rowF[2 * R], x1v = rowF[2 * R + 1], x2v = rowF[2 * R + 2], x3v = rowF[2 * R + 3];
+#pragma unroll 4
+                    for (int dx = 0; dx < C::S; ++dx) {
+                        const float4 w = __ldg(eq4 + dy * C::S + dx);
+                        const float xs[4] = {x0v, x1v, x2v, x3v};
+#pragma unroll
+                        for (int p = 0; p < C::P; ++p) {
+                            rs[0][p] = fmaf(w.x, xs[p], rs[0][p]);
+                            rs[1][p] = fmaf(w.y, xs[p], rs[1][p]);
+                            rs[2][p] = fmaf(w.z, xs[p], rs[2][p]);
+                            rs[3][p] = fmaf(w.w, xs[p], rs[3][p]);
+                        }
+                        x3v = x2v; x2v = x1v; x1v = x0v;
+                        const int nc = 2 * R - dx - 1;
+                        x0v = nc >= 0 ? rowF[nc] : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int p = 0; p < C::P; ++p) accd[q][p] += (double)rs[q][p];
+            }
+            // fold: the channel's term is accd 2^G, G = (M - 80 + Lth) log2 e; into (m, sd) exactly up to one
+            // fp64 rounding: frexp(accd) = mant 2^ex, c = mant 2^frac(G) in [0.5, 2), value = c 2^(ex + floor G)
+            // 2^frac(G) per orientation: lane q evaluates it once, every lane reads it by shuffle
+            double Fl = 1.0;
+            {
+                const int ql = lane & 3;
+                const double Gl = (wmax - 80.0 + (ql == 0 ? Lt[0] : ql == 1 ? Lt[1] : ql == 2 ? Lt[2] : Lt[3])) * LOG2E;
+                Fl = exp2_once(Gl - floor(Gl));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double G = (wmax - 80.0 + Lt[q]) * LOG2E;
+                const double Gi = floor(G);
+                const double F = __shfl_sync(0xffffffffu, Fl, q);
+#pragma unroll
+                for (int p = 0; p < C::P; ++p) {
+                    const double sa = accd[q][p];
+                    if (!((vmask >> (4 * q + p)) & 1u) || !(sa > 0.0)) continue;
+                    int ex;
+                    const double mant = frexp_pos(sa, ex);
+                    const double cv = mant * F;
+                    const int e = ex + (int)Gi;
+                    const float ef = (float)(e + 1);            // value < 2^(e + 1)
+                    if (m[q][p] == NEG_INF) {
+                        m[q][p] = ef;
+                        sd[q][p] = ldexp_fast(cv, -1);
+                    } else {
+                        if (ef > m[q][p]) {
+                            sd[q][p] = ldexp_fast(sd[q][p], (int)(m[q][p] - ef));
+                            m[q][p] = ef;
+                        }
+                        sd[q][p] += ldexp_fast(cv, e - (int)m[q][p]);
+                    }
+                }
+            }
+            continue;
+        }
 
         // channel bound of this warp: max of the window columns it reads + the channel's largest L2 (its
         // centre tap, Ls(0) = 0 >= Ls(d)); a channel below every output's floor is skipped
@@ -209,16 +463,23 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
             if (!__any_sync(0xffffffffu, rmax + rb.x >= lb[0] || rmax + rb.y >= lb[1] || rmax + rb.z >= lb[2] ||
                                              rmax + rb.w >= lb[3]))
                 continue;   // no tap of this row can raise any shift of the warp
+            {   // rolled tap loop, 4-wide sliding window of the staged row (instruction-cache footprint)
+                const float* rowA = wh + (lane - dy + 2 * R) * C::PITCH;
+                float x0v = rowA[2 * R], x1v = rowA[2 * R + 1], x2v = rowA[2 * R + 2], x3v = rowA[2 * R + 3];
+#pragma unroll 4
+                for (int dx = 0; dx < C::S; ++dx) {
+                    const float4 w = fh4[dy * C::S + dx];
+                    const float xs[4] = {x0v, x1v, x2v, x3v};
 #pragma unroll
-            for (int dx = 0; dx < C::S; ++dx) {
-                const float4 w = fh4[dy * C::S + dx];
-#pragma unroll
-                for (int p = 0; p < C::P; ++p) {
-                    const float xv = r[p - dx + 2 * R];
-                    cm[0][p] = fmaxf(cm[0][p], xv + w.x);
-                    cm[1][p] = fmaxf(cm[1][p], xv + w.y);
-                    cm[2][p] = fmaxf(cm[2][p], xv + w.z);
-                    cm[3][p] = fmaxf(cm[3][p], xv + w.w);
+                    for (int p = 0; p < C::P; ++p) {
+                        cm[0][p] = fmaxf(cm[0][p], xs[p] + w.x);
+                        cm[1][p] = fmaxf(cm[1][p], xs[p] + w.y);
+                        cm[2][p] = fmaxf(cm[2][p], xs[p] + w.z);
+                        cm[3][p] = fmaxf(cm[3][p], xs[p] + w.w);
+                    }
+                    x3v = x2v; x2v = x1v; x1v = x0v;
+                    const int nc = 2 * R - dx - 1;
+                    x0v = nc >= 0 ? rowA[nc] : kSent;
                 }
             }
         }
@@ -232,7 +493,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                 if (m[q][p] == NEG_INF) {
                     m[q][p] = mn;
                 } else if (mn > m[q][p]) {
-                    sd[q][p] = ldexp(sd[q][p], (int)(m[q][p] - mn));
+                    sd[q][p] = ldexp_fast(sd[q][p], (int)(m[q][p] - mn));
                     m[q][p] = mn;
                 }
             }
@@ -243,7 +504,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         for (int dy = 0; dy < C::S; ++dy) {
             const float4* rowh = reinterpret_cast<const float4*>(wh + (lane - dy + 2 * R) * C::PITCH);
             const float4* rowl = reinterpret_cast<const float4*>(wl + (lane - dy + 2 * R) * C::PITCH);
-            float rh[C::RL], rl[C::RL];
+            float rh[C::RL];
             float rmax = kSent;
 #pragma unroll
             for (int j = 0; j < C::RL / 4; ++j) {
@@ -257,35 +518,43 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
 #pragma unroll
             for (int q = 0; q < 4; ++q) live |= __any_sync(0xffffffffu, rmax + rbv[q] >= lb[q]) ? (1u << q) : 0u;
             if (!live) continue;
-#pragma unroll
-            for (int j = 0; j < C::RL / 4; ++j) {
-                const float4 u = rowl[j];
-                rl[4 * j + 0] = u.x; rl[4 * j + 1] = u.y; rl[4 * j + 2] = u.z; rl[4 * j + 3] = u.w;
-            }
+            // per orientation a ROLLED loop over the taps of the row with a 4-wide sliding window of the staged
+            // pair (the unrolled S x 4 x P body overflowed the instruction cache: ncu no_instruction 7 / issue)
+            const float* rowH = wh + (lane - dy + 2 * R) * C::PITCH;
+            const float* rowL = wl + (lane - dy + 2 * R) * C::PITCH;
             const float* frh = reinterpret_cast<const float*>(fh4 + dy * C::S);   // [dx][q]
             const float* frl = reinterpret_cast<const float*>(fl4 + dy * C::S);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (!((live >> q) & 1u)) continue;
-                float rs[C::P];
-#pragma unroll
-                for (int p = 0; p < C::P; ++p) rs[p] = 0.f;
-#pragma unroll
+                const float m0 = m[q][0], m1 = m[q][1], m2 = m[q][2], m3 = m[q][3];
+                float h0 = rowH[2 * R], h1 = rowH[2 * R + 1], h2 = rowH[2 * R + 2], h3 = rowH[2 * R + 3];
+                float l0 = rowL[2 * R], l1 = rowL[2 * R + 1], l2 = rowL[2 * R + 2], l3 = rowL[2 * R + 3];
+                float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
+                auto term = [](float av, float al, float bb, float blo, float mm) {
+                    const float s1 = av + bb;                                   // TwoSum(av, bb)
+                    const float bv = s1 - av;
+                    const float e1 = (av - (s1 - bv)) + (bb - bv);
+                    return ex2_approx((s1 - mm) + (e1 + (al + blo)));           // s1 - m exact; sentinel -> 0
+                };
+#pragma unroll 4
                 for (int dx = 0; dx < C::S; ++dx) {
                     const float bb = frh[4 * dx + q], blo = frl[4 * dx + q];
-#pragma unroll
-                    for (int p = 0; p < C::P; ++p) {
-                        const float av = rh[p - dx + 2 * R];
-                        const float s1 = av + bb;                                   // TwoSum(av, bb)
-                        const float bv = s1 - av;
-                        const float e1 = (av - (s1 - bv)) + (bb - bv);
-                        const float u = (s1 - m[q][p]) + (e1 + (rl[p - dx + 2 * R] + blo));   // s1 - m exact
-                        rs[p] += ex2_approx(u);                                     // sentinel -> 0
-                    }
+                    rs0 += term(h0, l0, bb, blo, m0);
+                    rs1 += term(h1, l1, bb, blo, m1);
+                    rs2 += term(h2, l2, bb, blo, m2);
+                    rs3 += term(h3, l3, bb, blo, m3);
+                    // window of tap dx + 1: staged columns 2R - dx - 1 .. 2R - dx + 2 (p = 0..3)
+                    h3 = h2; h2 = h1; h1 = h0;
+                    l3 = l2; l2 = l1; l1 = l0;
+                    const int nc = 2 * R - dx - 1;
+                    h0 = nc >= 0 ? rowH[nc] : kSent;
+                    l0 = nc >= 0 ? rowL[nc] : 0.f;
                 }
+                const float rsv[4] = {rs0, rs1, rs2, rs3};
 #pragma unroll
                 for (int p = 0; p < C::P; ++p)
-                    if (m[q][p] != NEG_INF) sd[q][p] += (double)rs[p];
+                    if (m[q][p] != NEG_INF) sd[q][p] += (double)rsv[p];
             }
         }
     }
@@ -303,7 +572,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                 if (gx >= nx) continue;
                 const double ly = (m[q][p] == NEG_INF || !(sd[q][p] > 0.0))
                                       ? -(double)INFINITY
-                                      : ((double)m[q][p] + log2(sd[q][p])) * 0.69314718055994530941723212145818;
+                                      : ((double)m[q][p] + log2_once(sd[q][p])) * 0.69314718055994530941723212145818;
                 const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
                 err += apply_epilogue_precise(epi, idx, ly);
             }
@@ -326,8 +595,17 @@ static cudaError_t launch_lsep_r(const se2_kernel_s* k, const double* in, int ba
     const int tiles_y = (k->wrows() + C::TY - 1) / C::TY;
     dim3 grid(tiles_x * tiles_y, (k->nt + 3) / 4, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);
-    conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(in, k->L2hi, k->L2lo, k->L2row, k->nx, k->ny, k->nt,
-                                                             tiles_x, k->wlo(), k->whi(), epi);
+    // channels (in theta-distance order) that may take the factored path; SE2_K4P_EXACT: none (diagnostics)
+    {
+        const int64_t segs = (int64_t)batch * k->nt * k->ny * ((k->nx + kPSegW - 1) / kPSegW);
+        lsep_stats_kernel<<<(int)std::min<int64_t>((segs + 255) / 256, 148 * 16), 256, 0, s>>>(in, k->nx, k->ny, k->nt,
+                                                                                             batch, k->pstats);
+        count_launch();
+    }
+    static const int ffma_max_a = getenv("SE2_K4P_EXACT") ? 0 : (getenv("SE2_K4P_FFMA_A") ? atoi(getenv("SE2_K4P_FFMA_A")) : 1 << 20);
+    conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(
+        in, k->L2hi, k->L2lo, k->L2row, k->Eq, k->w3 * k->w3 / k->eps, k->nx, k->ny, k->nt, tiles_x, k->wlo(), k->whi(),
+        epi, ffma_max_a, reinterpret_cast<unsigned long long*>(k->lse_counters + 12), k->pstats, k->Lth, k->LseS);
     count_launch();
     return cudaGetLastError();
 }

@@ -130,6 +130,8 @@ cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     k->table_bytes += 2 * n * sizeof(float) + nr * sizeof(float);
+    if (e == cudaSuccess)
+        e = cudaMalloc(&k->pstats, (size_t)k->max_batch * k->nt * k->ny * ((k->nx + 15) / 16) * sizeof(float2));
     return e;
 }
 

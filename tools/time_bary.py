@@ -31,5 +31,9 @@ for name in (args or ["c1", "c2", "c3"]):
         call()
         e1.record()
         torch.cuda.synchronize()
-        print(f"{name} {fn.__name__}: {it / (e0.elapsed_time(e1) / 1000.0):.1f} it/s ({it} iterations)", flush=True)
+        extra = ""
+        if fn is se2_barycenter_precise:
+            ps = k.precise_path_stats(reset=True)
+            extra = f", K4P channels on the FFMA path {ps['ffma']}/{ps['channels']}"
+        print(f"{name} {fn.__name__}: {it / (e0.elapsed_time(e1) / 1000.0):.1f} it/s ({it} iterations){extra}", flush=True)
     k.close()
