@@ -157,6 +157,7 @@ void se2_kernel_destroy(se2_kernel k) {
     if (k->L2lo) cudaFree(k->L2lo);
     if (k->L2row) cudaFree(k->L2row);
     if (k->pstats) cudaFree(k->pstats);
+    if (k->psplit) cudaFree(k->psplit);
     KernelExtra* x = extra(k);
     if (x) {
         x->clear_graphs();

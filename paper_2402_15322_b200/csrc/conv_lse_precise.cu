@@ -125,7 +125,8 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                         const float* __restrict__ L2row, const float* __restrict__ Eq, double w3sq_eps, int nx, int ny,
                         int nt, int tiles_x, int y_lo, int y_hi, EpiP epi, int ffma_max_a,
                         unsigned long long* __restrict__ counters, const float2* __restrict__ pst,
-                        const float* __restrict__ Lth, const float* __restrict__ LseS) {
+                        const float* __restrict__ Lth, const float* __restrict__ LseS, int ngroups,
+                        double2* __restrict__ split_out) {
     using C = LsePCfg<R>;
     extern __shared__ __align__(16) float smem[];
     double* sRaw = reinterpret_cast<double*>(smem);                 // [WIN_H * WIN_W] next channel, fp64
@@ -139,7 +140,10 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     __shared__ int sAct[kPMaxNT], sNAct;
 
     const int tile = blockIdx.x;
-    const int qd = blockIdx.y;
+    // theta_i split (small grids): blockIdx.y = qd * ngroups + grp; the CTA takes every ngroups-th channel of
+    // the active list and writes its partial (shift, sum) per output to split_out (combined afterwards)
+    const int qd = blockIdx.y / ngroups;
+    const int grp = blockIdx.y - qd * ngroups;
     const int b = blockIdx.z;
     const int x0 = (tile % tiles_x) * C::TX;
     const int y0 = y_lo + (tile / tiles_x) * C::TY;
@@ -265,7 +269,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
             else
                 sRaw[i] = -(double)INFINITY;
         }
-        float* fb = sF0 + (a & 1) * FBUF;
+        float* fb = sF0 + (((a - grp) / ngroups) & 1) * FBUF;   // this CTA's j-th channel -> buffer j & 1
         const float* fh = L2hi + ((int64_t)qd * nt + ti) * C::FIL;
         const float* fl = L2lo + ((int64_t)qd * nt + ti) * C::FIL;
         for (int i = threadIdx.x; i < C::FIL / 4; i += C::NT) {
@@ -276,8 +280,8 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         for (int i = threadIdx.x; i < C::S; i += C::NT) cp_async16(fb + 2 * C::FIL + 4 * i, rm + 4 * i);
         cp_async_commit();
     };
-    if (nact > 0) issue(0);
-    for (int a = 0; a < nact; ++a) {
+    if (grp < nact) issue(grp);
+    for (int a = grp; a < nact; a += ngroups) {
         cp_async_wait<0>();
         __syncthreads();   // channel a's copies visible; the previous channel's readers of sWh / sWl are done
         double wmax = -(double)INFINITY, tmin = (double)INFINITY;   // window max, tile min (natural)
@@ -311,8 +315,8 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                 sWh[r * C::PITCH + c] = exp_pair(sRaw[i] - wmax + 40.0);   // -inf -> 0
             }
         __syncthreads();   // sRaw free for the next channel, sWh / sWl complete
-        if (a + 1 < nact) issue(a + 1);
-        const float* sFh = sF0 + (a & 1) * FBUF;
+        if (a + ngroups < nact) issue(a + ngroups);
+        const float* sFh = sF0 + (((a - grp) / ngroups) & 1) * FBUF;
         const float* sFl = sFh + C::FIL;
         const float* sRow = sFh + 2 * C::FIL;   // [S][4] max over each tap row of L2 (pruning bounds)
         const float* wh = sWh + wx * C::P;
@@ -574,6 +578,55 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                                       ? -(double)INFINITY
                                       : ((double)m[q][p] + log2_once(sd[q][p])) * 0.69314718055994530941723212145818;
                 const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
+                if (ngroups > 1)
+                    split_out[(int64_t)grp * gridDim.z * N + idx] = make_double2((double)m[q][p], sd[q][p]);
+                else
+                    err += apply_epilogue_precise(epi, idx, ly);
+            }
+        }
+    }
+    if (ngroups == 1 && epi.err_partial != nullptr) {
+        const float t = block_sum<C::NT>(err, sRed);
+        if (threadIdx.x == 0) epi.err_partial[((int64_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// theta_i split: combine the groups' (shift m, fp64 sum) per output exactly (2^(m_g - M) scalings), then the
+// fp64 epilogue; one CTA per (tile, quad, field) with the main kernel's output mapping and error-partial slot
+template <int R>
+__global__ void __launch_bounds__(LsePCfg<R>::NT)
+lsep_split_combine_kernel(const double2* __restrict__ part, int ngroups, int nx, int ny, int nt, int tiles_x, int y_lo,
+                          int y_hi, EpiP epi) {
+    using C = LsePCfg<R>;
+    __shared__ float sRed[C::NT / 32];
+    const int tile = blockIdx.x, qd = blockIdx.y, b = blockIdx.z;
+    const int x0 = (tile % tiles_x) * C::TX, y0 = y_lo + (tile / tiles_x) * C::TY;
+    const int64_t N = (int64_t)nx * ny * nt, GN = (int64_t)gridDim.z * N;
+    const int lane = threadIdx.x & 31, wx = threadIdx.x >> 5;
+    float err = 0.f;
+    const int gy = y0 + lane;
+    if (gy < y_hi) {
+        for (int q = 0; q < 4; ++q) {
+            const int to = 4 * qd + q;
+            if (to >= nt) continue;
+            for (int p = 0; p < C::P; ++p) {
+                const int gx = x0 + wx * C::P + p;
+                if (gx >= nx) continue;
+                const int64_t idx = (int64_t)b * N + ((int64_t)to * ny + gy) * nx + gx;
+                double M = -(double)INFINITY;
+                for (int g = 0; g < ngroups; ++g) {
+                    const double2 v = part[g * GN + idx];
+                    if (v.y > 0.0) M = fmax(M, v.x);
+                }
+                double sum = 0.0;
+                if (M > -(double)INFINITY)
+                    for (int g = 0; g < ngroups; ++g) {
+                        const double2 v = part[g * GN + idx];
+                        if (v.y > 0.0) sum += ldexp_fast(v.y, (int)(v.x - M));
+                    }
+                const double ly = (M == -(double)INFINITY || !(sum > 0.0))
+                                      ? -(double)INFINITY
+                                      : (M + log2_once(sum)) * 0.69314718055994530941723212145818;
                 err += apply_epilogue_precise(epi, idx, ly);
             }
         }
@@ -593,20 +646,57 @@ static cudaError_t launch_lsep_r(const se2_kernel_s* k, const double* in, int ba
     if (e != cudaSuccess) return e;
     const int tiles_x = (k->nx + C::TX - 1) / C::TX;
     const int tiles_y = (k->wrows() + C::TY - 1) / C::TY;
-    dim3 grid(tiles_x * tiles_y, (k->nt + 3) / 4, batch);
-    if (bpf) *bpf = (int)(grid.x * grid.y);
-    // channels (in theta-distance order) that may take the factored path; SE2_K4P_EXACT: none (diagnostics)
+    const int nquad = (k->nt + 3) / 4;
+    if (bpf) *bpf = tiles_x * tiles_y * nquad;
     {
         const int64_t segs = (int64_t)batch * k->nt * k->ny * ((k->nx + kPSegW - 1) / kPSegW);
         lsep_stats_kernel<<<(int)std::min<int64_t>((segs + 255) / 256, 148 * 16), 256, 0, s>>>(in, k->nx, k->ny, k->nt,
                                                                                              batch, k->pstats);
         count_launch();
     }
+    // theta_i split over `groups` CTAs per (tile, quad) when the grid is small: the waves model of K3
+    // (waves(g) / g; <= 8 groups, the scratch, ~16 CTAs per SM)
+    static int slots = 0;
+    if (slots == 0) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_lse_precise_kernel<R>, C::NT, C::SMEM) !=
+                cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        slots = per_sm * nsm;
+        cudaGetLastError();
+    }
+    const int base_ctas = tiles_x * tiles_y * nquad * batch;
+    int gmax = k->nt < 8 ? k->nt : 8;
+    const int gcap = (16 * 148 + base_ctas - 1) / base_ctas;
+    if (gmax > gcap) gmax = gcap;
+    const size_t per_group = (size_t)batch * k->N();
+    if (k->psplit == nullptr || (size_t)gmax * per_group > k->psplit_n) gmax = (int)(k->psplit_n / std::max<size_t>(per_group, 1));
+    if (gmax < 1) gmax = 1;
+    double best = 1e30;
+    for (int g = 1; g <= gmax; ++g) best = fmin(best, (double)(((int64_t)base_ctas * g + slots - 1) / slots) / g);
+    int groups = 1;
+    for (int g = 1; g <= gmax; ++g)   // the largest g within 5% of the best (c2: g 3 / 5 / 6 / 8 measured 1.62k / 1.69k / - / 1.55k it/s)
+        if ((double)(((int64_t)base_ctas * g + slots - 1) / slots) / g <= 1.05 * best) groups = g;
+    static const int force_groups = getenv("SE2_K4P_GROUPS") ? atoi(getenv("SE2_K4P_GROUPS")) : 0;   // tuning
+    if (force_groups > 0) groups = force_groups < gmax ? force_groups : gmax;
+    dim3 grid(tiles_x * tiles_y, nquad * groups, batch);
+    // channels (in theta-distance order) that may take the factored path; SE2_K4P_EXACT: none (diagnostics)
     static const int ffma_max_a = getenv("SE2_K4P_EXACT") ? 0 : (getenv("SE2_K4P_FFMA_A") ? atoi(getenv("SE2_K4P_FFMA_A")) : 1 << 20);
     conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(
         in, k->L2hi, k->L2lo, k->L2row, k->Eq, k->w3 * k->w3 / k->eps, k->nx, k->ny, k->nt, tiles_x, k->wlo(), k->whi(),
-        epi, ffma_max_a, reinterpret_cast<unsigned long long*>(k->lse_counters + 12), k->pstats, k->Lth, k->LseS);
+        epi, ffma_max_a, reinterpret_cast<unsigned long long*>(k->lse_counters + 12), k->pstats, k->Lth, k->LseS, groups,
+        reinterpret_cast<double2*>(k->psplit));
     count_launch();
+    if (groups > 1) {
+        dim3 g2(tiles_x * tiles_y, nquad, batch);
+        lsep_split_combine_kernel<R><<<g2, C::NT, 0, s>>>(reinterpret_cast<const double2*>(k->psplit), groups, k->nx, k->ny,
+                                                          k->nt, tiles_x, k->wlo(), k->whi(), epi);
+        count_launch();
+    }
     return cudaGetLastError();
 }
 

@@ -132,6 +132,14 @@ cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
     k->table_bytes += 2 * n * sizeof(float) + nr * sizeof(float);
     if (e == cudaSuccess)
         e = cudaMalloc(&k->pstats, (size_t)k->max_batch * k->nt * k->ny * ((k->nx + 15) / 16) * sizeof(float2));
+    if (e == cudaSuccess) {   // split partials: up to 8 groups, at most 64 MB
+        size_t n2 = (size_t)8 * k->max_batch * k->N();
+        n2 = std::min<size_t>(n2, ((size_t)64 << 20) / sizeof(double2));
+        if (n2 >= (size_t)2 * k->max_batch * k->N()) {
+            e = cudaMalloc(&k->psplit, n2 * sizeof(double2));
+            k->psplit_n = n2;
+        }
+    }
     return e;
 }
 
