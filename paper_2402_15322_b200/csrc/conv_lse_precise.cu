@@ -135,7 +135,6 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     float* sF0 = sWl + C::WIN;   // 2 buffers of [hi FIL][lo FIL][row S x 4]
     constexpr int FBUF = 2 * C::FIL + 4 * C::S;
     __shared__ float sRed[C::NT / 32];
-    __shared__ double sWmax[C::NT / 32], sTmin[C::NT / 32];
     __shared__ float sCM[kPMaxNT], sCMu[kPMaxNT], sPM[C::NT], sPMu[C::NT], sLB[4];
     __shared__ int sAct[kPMaxNT], sNAct;
 
@@ -284,36 +283,30 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     for (int a = grp; a < nact; a += ngroups) {
         cp_async_wait<0>();
         __syncthreads();   // channel a's copies visible; the previous channel's readers of sWh / sWl are done
-        double wmax = -(double)INFINITY, tmin = (double)INFINITY;   // window max, tile min (natural)
-        for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
-            const int r = i / C::WIN_W, c = i - r * C::WIN_W;
-            const double v = sRaw[i];
-            float hi, lo;
-            split2(v * LOG2E, hi, lo);
-            sWh[r * C::PITCH + c] = hi;
-            sWl[r * C::PITCH + c] = lo;
-            wmax = fmax(wmax, v);
-            // the tile's own (in-grid) positions: every output of the tile has its centre term there
-            if (r >= R && r < R + C::TY && c >= R && c < R + C::TX && y0 + r - R < y_hi && x0 + c - R < nx)
-                tmin = fmin(tmin, v);
+        // path of the channel from the prologue's bounds (no per-element reductions): M >= the window's max,
+        // mu <= the tile's min (fp32 rounded outward), so M - mu >= the true range
+        double wmax = 0.0;
+        bool ffma = false;
+        if (nt <= kPMaxNT) {
+            const int tic = chan(a);
+            const float Mf = sCM[tic], muf = sCMu[tic];
+            ffma = a < ffma_max_a && isfinite(Mf) && isfinite(muf) && ((double)Mf - (double)muf <= kFfmaRangeP);
+            wmax = (double)Mf;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-            tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-        }
-        if (lane == 0) { sWmax[wx] = wmax; sTmin[wx] = tmin; }
-        __syncthreads();
-        wmax = sWmax[0];
-        tmin = sTmin[0];
-#pragma unroll
-        for (int w2 = 1; w2 < C::NT / 32; ++w2) { wmax = fmax(wmax, sWmax[w2]); tmin = fmin(tmin, sTmin[w2]); }
-        const bool ffma = a < ffma_max_a && isfinite(wmax) && isfinite(tmin) && (wmax - tmin <= kFfmaRangeP);
-        if (ffma)   // v~ = exp(lv - M + 40) in fp64, rounded once (zero mass / padding -> 0)
+        if (ffma) {   // v~ = exp(lv - M + 40) from the fp64 potential, rounded once (zero mass / padding -> 0)
             for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
                 const int r = i / C::WIN_W, c = i - r * C::WIN_W;
-                sWh[r * C::PITCH + c] = exp_pair(sRaw[i] - wmax + 40.0);   // -inf -> 0
+                sWh[r * C::PITCH + c] = exp_pair(sRaw[i] - wmax + 40.0);
             }
+        } else {      // the exact path's float pair of lv log2 e
+            for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
+                const int r = i / C::WIN_W, c = i - r * C::WIN_W;
+                float hi, lo;
+                split2(sRaw[i] * LOG2E, hi, lo);
+                sWh[r * C::PITCH + c] = hi;
+                sWl[r * C::PITCH + c] = lo;
+            }
+        }
         __syncthreads();   // sRaw free for the next channel, sWh / sWl complete
         if (a + ngroups < nact) issue(a + ngroups);
         const float* sFh = sF0 + (((a - grp) / ngroups) & 1) * FBUF;
