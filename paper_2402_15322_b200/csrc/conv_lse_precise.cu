@@ -28,6 +28,8 @@
 // frexp(S) 2^(floor G) 2^frac(G), G = (M - 80 + Lth) log2 e in fp64 (Lth from its fp64 formula).
 // Validity (range <= 80 nats): every retained product is a normal float >= e^-42, no sum overflows
 // (961 e^80 < 2^127), and the products dropped by underflow are below e^-40 of the output's centre term.
+#include <type_traits>
+
 #include "conv_common.cuh"
 
 namespace se2 {
@@ -101,21 +103,22 @@ constexpr int kPSegW = 16;
 constexpr int kPMaxNT = 128;                 // channel pruning from these bounds for nt <= 128
 constexpr float kGapNat = 44.3614195558365f;  // kGap log2 units in nats
 __global__ void lsep_stats_kernel(const double* __restrict__ in, int nx, int ny, int nt, int batch,
-                                  float2* __restrict__ st) {
+                                  float4* __restrict__ st) {
     const int nxb = (nx + kPSegW - 1) / kPSegW;
     const int64_t total = (int64_t)batch * nt * ny * nxb;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int xb = (int)(i % nxb);
         const int64_t row = i / nxb;   // (b, theta, y)
         const double* src = in + row * nx + xb * kPSegW;
-        double mn = INFINITY, mx = -INFINITY;
+        double mn = INFINITY, mx = -INFINITY, mnf = INFINITY;
         const int w = min(kPSegW, nx - xb * kPSegW);
         for (int j = 0; j < w; ++j) {
             const double v = src[j];
             mn = fmin(mn, v);
             mx = fmax(mx, v);
+            if (v > -INFINITY) mnf = fmin(mnf, v);
         }
-        st[i] = make_float2(__double2float_rd(mn), __double2float_ru(mx));
+        st[i] = make_float4(__double2float_rd(mn), __double2float_ru(mx), __double2float_rd(mnf), 0.f);
     }
 }
 
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(LsePCfg<R>::NT)
 conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__ L2hi, const float* __restrict__ L2lo,
                         const float* __restrict__ L2row, const float* __restrict__ Eq, double w3sq_eps, int nx, int ny,
                         int nt, int tiles_x, int y_lo, int y_hi, EpiP epi, int ffma_max_a,
-                        unsigned long long* __restrict__ counters, const float2* __restrict__ pst,
+                        unsigned long long* __restrict__ counters, const float4* __restrict__ pst,
                         const float* __restrict__ Lth, const float* __restrict__ LseS, int ngroups,
                         double2* __restrict__ split_out) {
     using C = LsePCfg<R>;
@@ -135,7 +138,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     float* sF0 = sWl + C::WIN;   // 2 buffers of [hi FIL][lo FIL][row S x 4]
     constexpr int FBUF = 2 * C::FIL + 4 * C::S;
     __shared__ float sRed[C::NT / 32];
-    __shared__ float sCM[kPMaxNT], sCMu[kPMaxNT], sPM[C::NT], sPMu[C::NT], sLB[4];
+    __shared__ float sCM[kPMaxNT], sCMu[kPMaxNT], sCMn[kPMaxNT], sPM[C::NT], sPMu[C::NT], sPMn[C::NT], sLB[4];
     __shared__ int sAct[kPMaxNT], sNAct;
 
     const int tile = blockIdx.x;
@@ -200,29 +203,33 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
     if (nt <= kPMaxNT) {
         const int nxb = (nx + kPSegW - 1) / kPSegW, xb0 = x0 / kPSegW;
         const int parts = C::NT / nt, ti = threadIdx.x % nt, part = threadIdx.x / nt;
-        float M = NEG_INF, mu = INFINITY;
+        float M = NEG_INF, mu = INFINITY, mnw = INFINITY;   // window max, tile min, window min of the finite lv
         if (part < parts) {
-            const float2* sb = pst + (((int64_t)b * nt + ti) * ny) * nxb;
+            const float4* sb = pst + (((int64_t)b * nt + ti) * ny) * nxb;
             const int ra = max(0, y0 - R), rb = min(ny - 1, y0 + C::TY - 1 + R);
             for (int y = ra + part; y <= rb; y += parts) {
                 const bool own = y >= y0 && y < min(y_hi, y0 + C::TY);
                 for (int xb = max(0, xb0 - 1); xb <= min(nxb - 1, xb0 + 1); ++xb) {
-                    const float2 v = sb[(int64_t)y * nxb + xb];
+                    const float4 v = sb[(int64_t)y * nxb + xb];
                     M = fmaxf(M, v.y);
+                    mnw = fminf(mnw, v.z);
                     if (own && xb == xb0) mu = fminf(mu, v.x);
                 }
             }
         }
         sPM[threadIdx.x] = M;
         sPMu[threadIdx.x] = mu;
+        sPMn[threadIdx.x] = mnw;
         __syncthreads();
         if (threadIdx.x < nt) {
             for (int pp = 1; pp < parts; ++pp) {
                 M = fmaxf(M, sPM[pp * nt + threadIdx.x]);
                 mu = fminf(mu, sPMu[pp * nt + threadIdx.x]);
+                mnw = fminf(mnw, sPMn[pp * nt + threadIdx.x]);
             }
             sCM[threadIdx.x] = M;
             sCMu[threadIdx.x] = mu;
+            sCMn[threadIdx.x] = mnw;
         }
         __syncthreads();
         if (wx < 4) {   // warp q: LB(to_q)
@@ -285,24 +292,36 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         __syncthreads();   // channel a's copies visible; the previous channel's readers of sWh / sWl are done
         // path of the channel from the prologue's bounds (no per-element reductions): M >= the window's max,
         // mu <= the tile's min (fp32 rounded outward), so M - mu >= the true range
-        double wmax = 0.0;
-        bool ffma = false;
+        double wmax = 0.0, Bd = 0.0;   // Bd: integer base (log2 units) of the exact path's staged values
+        bool ffma = false, gridx = false;
         if (nt <= kPMaxNT) {
             const int tic = chan(a);
-            const float Mf = sCM[tic], muf = sCMu[tic];
+            const float Mf = sCM[tic], muf = sCMu[tic], mnf = sCMn[tic];
             ffma = a < ffma_max_a && isfinite(Mf) && isfinite(muf) && ((double)Mf - (double)muf <= kFfmaRangeP);
             wmax = (double)Mf;
+            if (isfinite(Mf)) {
+                Bd = floor((double)Mf * LOG2E) + 1.0;
+                // staged values x - B in (-2^14, 0] and the table's |L2| < 2^15 on the 2^-8 grid: every sum of
+                // the two (and minus an integer shift) is exact in fp32
+                gridx = isfinite(mnf) && ((double)Mf - (double)mnf) * LOG2E < 16384.0;
+            }
         }
+        const float B = (float)Bd;
         if (ffma) {   // v~ = exp(lv - M + 40) from the fp64 potential, rounded once (zero mass / padding -> 0)
             for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
                 const int r = i / C::WIN_W, c = i - r * C::WIN_W;
                 sWh[r * C::PITCH + c] = exp_pair(sRaw[i] - wmax + 40.0);
             }
-        } else {      // the exact path's float pair of lv log2 e
+        } else {      // the exact path: lv log2 e - B as a pair, hi on the 2^-8 grid (exact in fp32), lo the rest
             for (int i = threadIdx.x; i < C::RAW; i += C::NT) {
                 const int r = i / C::WIN_W, c = i - r * C::WIN_W;
-                float hi, lo;
-                split2(sRaw[i] * LOG2E, hi, lo);
+                const double v = sRaw[i];
+                float hi = kSent, lo = 0.f;
+                if (v > -1e300) {
+                    const double x = v * LOG2E - Bd;
+                    hi = (float)(rint(x * 256.0) / 256.0);
+                    lo = (float)(x - (double)hi);
+                }
                 sWh[r * C::PITCH + c] = hi;
                 sWl[r * C::PITCH + c] = lo;
             }
@@ -426,6 +445,8 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
         // centre tap, Ls(0) = 0 >= Ls(d)); a channel below every output's floor is skipped
         float lb[4];
         floors(lb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lb[q] -= B;   // staged values are relative to B
         {
             float wm = kSent;
             for (int r = lane; r < C::WIN_H; r += 32)
@@ -486,7 +507,7 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
 #pragma unroll
             for (int p = 0; p < C::P; ++p) {
                 if (!(cm[q][p] > -1e29f)) continue;   // only sentinel terms so far
-                const float mn = floorf(cm[q][p]) + 1.f;   // every term t - mn < 1 up to the pass-A rounding
+                const float mn = (float)(floor((double)cm[q][p] + Bd) + 1.0);   // every term t - mn < 1 (absolute)
                 if (m[q][p] == NEG_INF) {
                     m[q][p] = mn;
                 } else if (mn > m[q][p]) {
@@ -495,6 +516,8 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                 }
             }
         floors(lb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lb[q] -= B;
         // pass B: sum 2^(t - m) with exact exponents; row sums in fp32, the total in fp64.  A (row,
         // orientation) whose largest term is below 2^-kGap of every output of the warp is skipped.
 #pragma unroll 1
@@ -521,26 +544,30 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
             const float* rowL = wl + (lane - dy + 2 * R) * C::PITCH;
             const float* frh = reinterpret_cast<const float*>(fh4 + dy * C::S);   // [dx][q]
             const float* frl = reinterpret_cast<const float*>(fl4 + dy * C::S);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!((live >> q) & 1u)) continue;
-                const float m0 = m[q][0], m1 = m[q][1], m2 = m[q][2], m3 = m[q][3];
+            // one orientation's row: exponent (hi + bb) - m + (lo + blo) relative to the base B.  gridx: hi and bb on
+            // the 2^-8 grid within 2^15 -> hi + bb and (hi + bb) - m are exact in fp32 (4 FADD + 1 EX2 per term);
+            // otherwise TwoSum(hi, bb) (10 FADD)
+            auto row_q = [&](auto fast, int q, float mq0, float mq1, float mq2, float mq3, float& rs0, float& rs1,
+                             float& rs2, float& rs3) {
                 float h0 = rowH[2 * R], h1 = rowH[2 * R + 1], h2 = rowH[2 * R + 2], h3 = rowH[2 * R + 3];
                 float l0 = rowL[2 * R], l1 = rowL[2 * R + 1], l2 = rowL[2 * R + 2], l3 = rowL[2 * R + 3];
-                float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
                 auto term = [](float av, float al, float bb, float blo, float mm) {
-                    const float s1 = av + bb;                                   // TwoSum(av, bb)
-                    const float bv = s1 - av;
-                    const float e1 = (av - (s1 - bv)) + (bb - bv);
-                    return ex2_approx((s1 - mm) + (e1 + (al + blo)));           // s1 - m exact; sentinel -> 0
+                    if constexpr (decltype(fast)::value) {
+                        return ex2_approx(((av + bb) - mm) + (al + blo));
+                    } else {
+                        const float s1 = av + bb;                               // TwoSum(av, bb)
+                        const float bv = s1 - av;
+                        const float e1 = (av - (s1 - bv)) + (bb - bv);
+                        return ex2_approx((s1 - mm) + (e1 + (al + blo)));       // s1 - m exact; sentinel -> 0
+                    }
                 };
 #pragma unroll 4
                 for (int dx = 0; dx < C::S; ++dx) {
                     const float bb = frh[4 * dx + q], blo = frl[4 * dx + q];
-                    rs0 += term(h0, l0, bb, blo, m0);
-                    rs1 += term(h1, l1, bb, blo, m1);
-                    rs2 += term(h2, l2, bb, blo, m2);
-                    rs3 += term(h3, l3, bb, blo, m3);
+                    rs0 += term(h0, l0, bb, blo, mq0);
+                    rs1 += term(h1, l1, bb, blo, mq1);
+                    rs2 += term(h2, l2, bb, blo, mq2);
+                    rs3 += term(h3, l3, bb, blo, mq3);
                     // window of tap dx + 1: staged columns 2R - dx - 1 .. 2R - dx + 2 (p = 0..3)
                     h3 = h2; h2 = h1; h1 = h0;
                     l3 = l2; l2 = l1; l1 = l0;
@@ -548,6 +575,17 @@ conv_lse_precise_kernel(const double* __restrict__ in, const float* __restrict__
                     h0 = nc >= 0 ? rowH[nc] : kSent;
                     l0 = nc >= 0 ? rowL[nc] : 0.f;
                 }
+            };
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!((live >> q) & 1u)) continue;
+                // shifts relative to B (integers: exact); NEG_INF stays (sentinel terms underflow to 0)
+                const float m0 = m[q][0] - B, m1 = m[q][1] - B, m2 = m[q][2] - B, m3 = m[q][3] - B;
+                float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
+                if (gridx)
+                    row_q(std::integral_constant<bool, true>(), q, m0, m1, m2, m3, rs0, rs1, rs2, rs3);
+                else
+                    row_q(std::integral_constant<bool, false>(), q, m0, m1, m2, m3, rs0, rs1, rs2, rs3);
                 const float rsv[4] = {rs0, rs1, rs2, rs3};
 #pragma unroll
                 for (int p = 0; p < C::P; ++p)

@@ -161,7 +161,8 @@ struct se2_kernel_s {
     float* L2hi = nullptr;          // K4P: L log2(e) as an exact float pair, Lq layout (built on first use)
     float* L2lo = nullptr;
     float* L2row = nullptr;         // K4P pruning bounds: [nt/4][nt][S][4] max over each tap row of L2hi
-    float2* pstats = nullptr;       // K4P channel bounds: per (field, theta, row, 16-column block) (min lv, max lv)
+    float4* pstats = nullptr;       // K4P channel bounds: per (field, theta, row, 16-column block) (min lv, max lv,
+                                    //   min over the finite lv, -)
     void* psplit = nullptr;         // K4P theta_i split partials: double2 (shift, sum) [groups][max_batch][N]
     size_t psplit_n = 0;            //   capacity in double2
     // output window (slab decomposition, se2_kernel_set_window): every conv computes and stores only the

@@ -65,7 +65,7 @@ __global__ void tabulate_kernel(double hx, double hy, int nt, int R, double eps,
     }
 }
 
-// K4P table: L2 = -rho_b^2/eps log2(e) as an exact float pair (hi = fl(L2), lo = fl(L2 - hi)), Lq layout
+// K4P table: L2 = -rho_b^2/eps log2(e) as a float pair hi + lo (hi on the 2^-8 grid, lo the remainder), Lq layout
 __global__ void tabulate_l2pair_kernel(double hx, double hy, int nt, int R, double eps, double w1, double w2,
                                        double w3, float* __restrict__ L2hi, float* __restrict__ L2lo) {
     const int S = 2 * R + 1;
@@ -89,7 +89,9 @@ __global__ void tabulate_l2pair_kernel(double hx, double hy, int nt, int R, doub
         const double rho2 = w1 * w1 * b1 * b1 + w2 * w2 * b2 * b2 + w3 * w3 * Th * Th;
         const double l2 = -rho2 / eps * 1.4426950408889634073599246810019;
         const int64_t o = ((((int64_t)(to >> 2) * nt + ti) * S + dyi) * S + dxi) * 4 + (to & 3);
-        const float hi = (float)l2;
+        // hi on the 2^-8 grid (exact in fp32 for |l2| < 2^15): K4P adds it to grid-aligned staged potentials
+        // without rounding; lo = the (tiny) remainder
+        const float hi = fabs(l2) < 32768.0 ? (float)(rint(l2 * 256.0) / 256.0) : (float)l2;
         L2hi[o] = hi;
         L2lo[o] = (float)(l2 - (double)hi);
     }
@@ -131,7 +133,7 @@ cudaError_t tabulate_precise(se2_kernel_s* k, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     k->table_bytes += 2 * n * sizeof(float) + nr * sizeof(float);
     if (e == cudaSuccess)
-        e = cudaMalloc(&k->pstats, (size_t)k->max_batch * k->nt * k->ny * ((k->nx + 15) / 16) * sizeof(float2));
+        e = cudaMalloc(&k->pstats, (size_t)k->max_batch * k->nt * k->ny * ((k->nx + 15) / 16) * sizeof(float4));
     if (e == cudaSuccess) {   // split partials: up to 8 groups, at most 64 MB
         size_t n2 = (size_t)8 * k->max_batch * k->N();
         n2 = std::min<size_t>(n2, ((size_t)64 << 20) / sizeof(double2));
