@@ -217,7 +217,14 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
 }
 
 // K4P's epilogue (fp64 potentials): out = target -+ ly, error of the previous iterate |a_old K b - mu|
-__device__ __forceinline__ float apply_epilogue_precise(const EpiP& e, int64_t idx, double ly) {
+// out-of-line copy for kernels that apply the epilogue to many outputs per thread at their end (the log
+// engines): one body instead of one inlined per output keeps the kernel's code small
+template <bool LOG>
+__device__ __noinline__ float apply_epilogue_call(const Epilogue& e, int64_t idx, int ix, int iy, float y) {
+    return apply_epilogue<LOG>(e, idx, ix, iy, y);
+}
+
+static __device__ __noinline__ float apply_epilogue_precise(const EpiP& e, int64_t idx, double ly) {
     float err = 0.f;
     if (e.err_a != nullptr) err = fabsf((float)exp(e.err_a[idx] + ly) - e.err_mu[idx]);
     double o;
