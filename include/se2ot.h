@@ -447,6 +447,17 @@ SE2_API se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32
                                        const double* lambdas, float* bary, float* v_state, float* w_state,
                                        const se2_opts* opts, double* err_trace_host, se2_stream stream);
 
+/* se2_barycenter_precise_dist -- se2_barycenter_precise (fp64 potentials, K4P) with this rank's n inputs
+ *   (mus [n][N] float, lambdas HOST [nsolve][n]: this rank's share of weights that sum to 1 over all `reduce`
+ *   ranks); per iteration one fp64 allreduce of the partial sum_i lambda_i log d_i over `reduce`.  Input
+ *   sharding only: dist->slabs must be NULL and the halos 0 (SE2_EINVAL otherwise).  lbary [nsolve][N]
+ *   (fp64 log barycenter on every rank), lv_state / lw_state [nsolve][n][N] fp64 (nullable).  Trace: the
+ *   lambda-weighted error summed over all ranks' inputs. */
+SE2_API se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve,
+                                               const float* mus, const double* lambdas, double* lbary, double* lv_state,
+                                               double* lw_state, const se2_opts* opts, double* err_trace_host,
+                                               se2_stream stream);
+
 SE2_API const char* se2_last_error(void);
 SE2_API int32_t se2_abi_version(void);
 

@@ -48,6 +48,7 @@ EXPORTED = [
     "se2_bary_reduce_update", "se2_conv_update_slab", "se2_guard_stats", "se2_kernel_set_window",
     "se2_comm_unique_id", "se2_comm_init", "se2_comm_init_loopback", "se2_comm_split", "se2_comm_info",
     "se2_comm_allreduce", "se2_comm_destroy", "se2_jko_step_dist", "se2_barycenter_dist",
+    "se2_barycenter_precise_dist",
     "se2_barycenter_precise", "se2_conv_precise",
 ]
 
@@ -146,6 +147,8 @@ def load(path: str = LIB_PATH):
         "se2_jko_step_dist": [P, ctypes.POINTER(se2_dist), P, P, P, P, ctypes.POINTER(se2_prox),
                               ctypes.POINTER(se2_opts), pd, pd, P],
         "se2_barycenter_dist": [P, ctypes.POINTER(se2_dist), i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],
+        "se2_barycenter_precise_dist": [P, ctypes.POINTER(se2_dist), i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts),
+                                        pd, P],
         "se2_cake_build": [i32, i32, i32, dbl, i32, ctypes.POINTER(P)],
         "se2_cake_get": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), ctypes.POINTER(i32)],
         "se2_lift_image": [P, P, P, i32, i32, i32, P],

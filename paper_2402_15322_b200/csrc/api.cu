@@ -598,31 +598,6 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
 }
 
 // ---- barycenter with fp64 potentials (K4P; the elementwise 1e-4 parity of reading R19) --------------
-static se2_status run_conv_precise(se2_kernel_s* k, const double* in, int batch, const EpiP& epi, cudaStream_t s) {
-    Timing& t = k->timing;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (t.on) {
-        if (t.used == t.events.size()) {
-            cudaEvent_t a, b;
-            SE2_CUDA_TRY(cudaEventCreate(&a));
-            SE2_CUDA_TRY(cudaEventCreate(&b));
-            t.events.push_back({a, b});
-        }
-        e0 = t.events[t.used].first;
-        e1 = t.events[t.used].second;
-        t.used++;
-        SE2_CUDA_TRY(cudaEventRecord(e0, s));
-    }
-    cudaError_t e = launch_conv_lse_precise(k, in, batch, epi, s, nullptr);
-    if (e != cudaSuccess) {
-        set_error(std::string("precise conv launch: ") + cudaGetErrorString(e));
-        return SE2_ECUDA;
-    }
-    t.all_launches++;
-    if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
-    return SE2_OK;
-}
-
 se2_status se2_conv_precise(se2_kernel k, const double* in, double* out, int32_t batch, se2_stream stream) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(in && out && (const void*)in != (const void*)out, "in/out must be distinct non-null device pointers");

@@ -224,6 +224,33 @@ static se2_status reset_guard(se2_kernel_s* k, cudaStream_t s) {
     return SE2_OK;
 }
 
+// one fp64-potential log conv (K4P) with the kernel's optional per-launch timing events
+static se2_status run_conv_precise(se2_kernel_s* k, const double* in, int batch, const EpiP& epi, cudaStream_t s) {
+    Timing& t = k->timing;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (t.on) {
+        if (t.used == t.events.size()) {
+            cudaEvent_t a, b;
+            SE2_CUDA_TRY(cudaEventCreate(&a));
+            SE2_CUDA_TRY(cudaEventCreate(&b));
+            t.events.push_back({a, b});
+        }
+        e0 = t.events[t.used].first;
+        e1 = t.events[t.used].second;
+        t.used++;
+        SE2_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    cudaError_t e = launch_conv_lse_precise(k, in, batch, epi, s, nullptr);
+    if (e != cudaSuccess) {
+        set_error(std::string("precise conv launch: ") + cudaGetErrorString(e));
+        return SE2_ECUDA;
+    }
+    t.all_launches++;
+    if (t.on) SE2_CUDA_TRY(cudaEventRecord(e1, s));
+    return SE2_OK;
+}
+
+
 // End of a solve: count non-finite entries of the outputs (SE2_ENONFINITE) and read the guard counters
 // of the solve: clamped divisions -> warning SE2_WGUARD_HIT (the clamp is counted and reported),
 // porous prox sites without convergence -> warning SE2_WPROX_NOCONV.  Outputs stay valid on warnings.

@@ -840,4 +840,141 @@ se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, in
     return check_finite(k, ps, ns, 3, s);
 }
 
+// App. A with fp64 potentials (K4P, reading R19) and this rank's inputs: per iteration the partial weighted
+// log-mean sum_i lambda_i log d_i (fp64) is all-reduced over `reduce`; row slabs are not supported (the fp64
+// conv has no halo-packing epilogue): dist->slabs must be NULL.
+se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve, const float* mus,
+                                       const double* lambdas, double* lbary, double* lv_state, double* lw_state,
+                                       const se2_opts* opts, double* err_trace_host, se2_stream stream) {
+    if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
+    SE2_CHECK_ARG(dist != nullptr, "dist required (se2_barycenter_precise for one GPU)");
+    SE2_CHECK_ARG(dist->slabs == nullptr && dist->halo_top == 0 && dist->halo_bot == 0,
+                  "fp64-potential barycenter: input sharding only (no row slabs)");
+    SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
+    SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n (inputs on this rank), nsolve >= 1");
+    SE2_CHECK_ARG((int64_t)n * nsolve <= k->max_batch, "n*nsolve exceeds max_batch");
+    SE2_CHECK_ARG(mus && lambdas && lbary, "null pointer");
+    for (int i = 0; i < n * nsolve; ++i)
+        SE2_CHECK_ARG(lambdas[i] >= 0 && isfinite(lambdas[i]), "lambda must be >= 0 (the simplex is over all ranks)");
+    const bool warm = (opts->flags & SE2_WARM_START) != 0;
+    SE2_CHECK_ARG(!warm || lv_state != nullptr, "SE2_WARM_START needs lv_state");
+    DeviceGuard g(k->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    SE2_CUDA_TRY(tabulate_precise(k, s));
+    se2_status st = reset_guard(k, s);
+    if (st != SE2_OK) return st;
+    se2_comm_s* rc = dist->reduce;
+    const bool reduce = rc != nullptr && rc->n > 1;
+    const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
+    const int64_t N = k->N();
+    const int F = n * nsolve;
+    const int64_t FN = (int64_t)F * N;
+    const int iters = opts->iters;
+    KernelExtra* x = extra(k);
+    // workspace: mu_rep (float) [F][N]; lmu, v, w, d (double) [F][N]
+    st = ensure(x->ws, (size_t)FN * (sizeof(float) + 4 * sizeof(double)) + 64, x);
+    if (st != SE2_OK) return st;
+    float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
+    double* lmu = reinterpret_cast<double*>(reinterpret_cast<char*>(x->ws.ptr) + ((FN * sizeof(float) + 63) / 64) * 64);
+    double* v = lv_state ? lv_state : lmu + FN;
+    double* w = lw_state ? lw_state : lmu + 2 * FN;
+    double* d = lmu + 3 * FN;
+    st = ensure(x->misc, 4096 + sizeof(double) * F, x);
+    if (st != SE2_OK) return st;
+    const int bpf = conv_blocks_per_field_precise(k);
+    if (trace) {
+        st = ensure(x->partial, (size_t)F * bpf * sizeof(float), x);
+        if (st != SE2_OK) return st;
+        st = ensure(x->trace, (size_t)std::max(iters, 1) * F * sizeof(double), x);
+        if (st != SE2_OK) return st;
+    }
+    float* partial = reinterpret_cast<float*>(x->partial.ptr);
+    double* tr = reinterpret_cast<double*>(x->trace.ptr);
+    double* lam_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(x->misc.ptr) + 4096);
+    SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lambdas, sizeof(double) * F, cudaMemcpyHostToDevice, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint64_t> key = {6, as_key(mus), as_key(lbary), as_key(v), as_key(w), (uint64_t)n, (uint64_t)nsolve,
+                                 (uint64_t)iters, (uint64_t)opts->flags, (uint64_t)trace, as_key(x->ws.ptr),
+                                 as_key(x->misc.ptr), as_key(partial), as_key(tr)};
+    auto enqueue = [&](cudaStream_t s) -> se2_status {
+        se2_status st = SE2_OK;
+        for (int sv = 0; sv < nsolve; ++sv)
+            SE2_CUDA_TRY(cudaMemcpyAsync(mu_rep + (int64_t)sv * n * N, mus, sizeof(float) * n * N,
+                                         cudaMemcpyDeviceToDevice, s));
+        SE2_CUDA_TRY(launch_log_f64(mu_rep, lmu, FN, s));
+        if (!warm) SE2_CUDA_TRY(launch_fill_f64(v, FN, 0.0, s));
+        SE2_CUDA_TRY(launch_fill_f64(w, FN, 0.0, s));
+        for (int j = 0; j < iters; ++j) {
+            EpiP e1;   // w_i = mu_i / K v_i  (error of the previous v-update fused)
+            e1.op = EPI_DIVIDE;
+            e1.target = lmu;
+            e1.out = w;
+            if (trace && j > 0) {
+                e1.err_a = w;
+                e1.err_mu = mu_rep;
+                e1.err_partial = partial;
+            }
+            st = run_conv_precise(k, v, F, e1, s);
+            if (st != SE2_OK) return st;
+            if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
+            EpiP e2;   // d_i = v_i K w_i
+            e2.op = EPI_MULTIPLY;
+            e2.target = v;
+            e2.out = d;
+            st = run_conv_precise(k, w, F, e2, s);
+            if (st != SE2_OK) return st;
+            if (!reduce) {
+                SE2_CUDA_TRY(launch_bary_logmean_update_f64(n, nsolve, N, d, lam_dev, lbary, v, s));
+            } else {   // this rank's partial sum_i lambda_i log d_i, summed over the input ranks in fp64
+                SE2_CUDA_TRY(launch_bary_logmean_f64(n, nsolve, N, d, lam_dev, lbary, s));
+                st = rc->allreduce(lbary, (int64_t)nsolve * N, true, s);
+                if (st != SE2_OK) return st;
+                SE2_CUDA_TRY(launch_bary_update_f64(n, nsolve, N, d, lbary, v, s));
+            }
+        }
+        if (trace && iters > 0) {
+            EpiP e3;
+            e3.op = EPI_ERRONLY;
+            e3.err_a = w;
+            e3.err_mu = mu_rep;
+            e3.err_partial = partial;
+            st = run_conv_precise(k, v, F, e3, s);
+            if (st != SE2_OK) return st;
+            SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(iters - 1) * F, s));
+        }
+        return SE2_OK;
+    };
+    const bool graph = FN <= kGraphMaxElems && !(opts->flags & SE2_NO_GRAPH) && !any_multi(dist);
+    st = run_graph(k, s, std::move(key), graph, enqueue);
+    if (st != SE2_OK) return st;
+    if (trace && iters > 0) {
+        std::vector<double> h((size_t)iters * F), e((size_t)iters * nsolve, 0.0);
+        SE2_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, sizeof(double) * iters * F, cudaMemcpyDeviceToHost, s));
+        SE2_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int j = 0; j < iters; ++j)
+            for (int sv = 0; sv < nsolve; ++sv)
+                for (int i = 0; i < n; ++i) e[(size_t)j * nsolve + sv] += lambdas[sv * n + i] * h[(size_t)j * F + sv * n + i];
+        SE2_CUDA_TRY(cudaMemcpyAsync(tr, e.data(), sizeof(double) * e.size(), cudaMemcpyHostToDevice, s));
+        if (rc) {
+            st = rc->allreduce(tr, (int64_t)e.size(), true, s);
+            if (st != SE2_OK) return st;
+        }
+        SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * e.size(), cudaMemcpyDeviceToHost, s));
+        SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    int* cnt = reinterpret_cast<int*>(x->misc.ptr);
+    SE2_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(lbary, (int64_t)nsolve * N, cnt, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(v, FN, cnt, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(w, FN, cnt, s));
+    int h = 0;
+    SE2_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h != 0) {
+        set_error("non-finite values produced by the iteration (" + std::to_string(h) + " entries)");
+        return SE2_ENONFINITE;
+    }
+    return SE2_OK;
+}
+
 }  // extern "C"

@@ -201,6 +201,42 @@ cudaError_t launch_bary_logmean_update_f64(int n, int nsolve, int64_t N, const d
     count_launch();
     return cudaGetLastError();
 }
+// the distributed fp64 barycenter: this rank's partial sum_i lambda_i ld_i (all-reduced over the input ranks
+// by the caller), then lv_i += lbar - ld_i
+__global__ void bary_logmean_f64_kernel(int n, int nsolve, int64_t N, const double* __restrict__ ld,
+                                        const double* __restrict__ lam, double* __restrict__ lbar) {
+    const int64_t total = (int64_t)nsolve * N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int sv = (int)(t / N);
+        const int64_t x = t - (int64_t)sv * N;
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double l = lam[sv * n + i];
+            if (l != 0.0) acc += l * ld[((int64_t)sv * n + i) * N + x];
+        }
+        lbar[t] = acc;
+    }
+}
+cudaError_t launch_bary_logmean_f64(int n, int nsolve, int64_t N, const double* ld, const double* lam_dev,
+                                    double* lbar, cudaStream_t s) {
+    bary_logmean_f64_kernel<<<grid_for((int64_t)nsolve * N, 256), 256, 0, s>>>(n, nsolve, N, ld, lam_dev, lbar);
+    count_launch();
+    return cudaGetLastError();
+}
+__global__ void bary_update_f64_kernel(int n, int nsolve, int64_t N, const double* __restrict__ ld,
+                                       const double* __restrict__ lbar, double* __restrict__ lv) {
+    const int64_t total = (int64_t)nsolve * n * N;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = j / N, x = j - f * N;
+        lv[j] += lbar[(f / n) * N + x] - ld[j];
+    }
+}
+cudaError_t launch_bary_update_f64(int n, int nsolve, int64_t N, const double* ld, const double* lbar, double* lv,
+                                   cudaStream_t s) {
+    bary_update_f64_kernel<<<grid_for((int64_t)nsolve * n * N, 256), 256, 0, s>>>(n, nsolve, N, ld, lbar, lv);
+    count_launch();
+    return cudaGetLastError();
+}
 __global__ void count_nonfinite_f64_kernel(const double* x, int64_t n, int* count) {
     int c = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

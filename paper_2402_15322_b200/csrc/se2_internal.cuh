@@ -255,5 +255,9 @@ cudaError_t launch_fill_f64(double* x, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_bary_logmean_update_f64(int n, int nsolve, int64_t N, const double* ld, const double* lam_dev,
                                            double* lbar, double* lv, cudaStream_t s);
 cudaError_t launch_count_nonfinite_f64(const double* x, int64_t n, int* count_dev, cudaStream_t s);
+cudaError_t launch_bary_logmean_f64(int n, int nsolve, int64_t N, const double* ld, const double* lam_dev,
+                                    double* lbar, cudaStream_t s);
+cudaError_t launch_bary_update_f64(int n, int nsolve, int64_t N, const double* ld, const double* lbar, double* lv,
+                                   cudaStream_t s);
 
 }  // namespace se2

@@ -171,3 +171,33 @@ def se2_barycenter_dist(k: Kernel, d: Dist, mus: torch.Tensor, lambdas, iters: i
                                        tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None,
                                        _stream(mus.device)))
     return bary, (tr[:iters] if trace else None)
+
+
+def se2_barycenter_precise_dist(k: Kernel, d: Dist, mus: torch.Tensor, lambdas, iters: int,
+                                lbary: Optional[torch.Tensor] = None, lv_state: Optional[torch.Tensor] = None,
+                                lw_state: Optional[torch.Tensor] = None, trace: bool = False,
+                                warm_start: bool = False, no_graph: bool = False):
+    """App. A with fp64 potentials (K4P, reading R19) and this rank's inputs mus [n][N] (float32), weights
+    lambdas [nsolve][n] (a share of weights that sum to 1 over the `reduce` ranks); input sharding only.
+    Returns (log mu [nsolve][N] float64 on every rank, trace [iters][nsolve] or None)."""
+    from .api import _check_field64
+    _check_field(mus, k, "mus")
+    n = mus.numel() // k.N
+    lam = np.ascontiguousarray(np.atleast_2d(np.asarray(lambdas, dtype=np.float64)))
+    if lam.shape[1] != n:
+        raise ValueError(f"lambdas must be [nsolve][{n}]")
+    nsolve = lam.shape[0]
+    if lbary is None:
+        lbary = torch.empty((nsolve, k.ntheta, k.ny, k.nx), device=mus.device, dtype=torch.float64)
+    _check_field64(lbary, k, "lbary", nsolve)
+    for name, t in (("lv_state", lv_state), ("lw_state", lw_state)):
+        if t is not None:
+            _check_field64(t, k, name, nsolve * n)
+    opts = L.se2_opts(int(iters), _flags(True, trace, warm=warm_start, no_graph=no_graph))
+    tr = np.zeros((max(iters, 1), nsolve), dtype=np.float64) if trace else None
+    check(L.load().se2_barycenter_precise_dist(k.handle, ctypes.byref(d.s), n, nsolve, _ptr(mus),
+                                               lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _ptr(lbary),
+                                               _ptr(lv_state), _ptr(lw_state), ctypes.byref(opts),
+                                               tr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if trace else None,
+                                               _stream(mus.device)))
+    return lbary, (tr[:iters] if trace else None)
