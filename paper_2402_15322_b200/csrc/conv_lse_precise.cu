@@ -712,11 +712,12 @@ static cudaError_t launch_lsep_r(const se2_kernel_s* k, const double* in, int ba
     int groups = 1;
     for (int g = 1; g <= gmax; ++g)   // the largest g within 5% of the best (c2: g 3 / 5 / 6 / 8 measured 1.62k / 1.69k / - / 1.55k it/s)
         if ((double)(((int64_t)base_ctas * g + slots - 1) / slots) / g <= 1.05 * best) groups = g;
-    static const int force_groups = getenv("SE2_K4P_GROUPS") ? atoi(getenv("SE2_K4P_GROUPS")) : 0;   // tuning
+    const char* fg = getenv("SE2_K4P_GROUPS");   // tuning / tests (read per launch)
+    const int force_groups = fg ? atoi(fg) : 0;
     if (force_groups > 0) groups = force_groups < gmax ? force_groups : gmax;
     dim3 grid(tiles_x * tiles_y, nquad * groups, batch);
     // channels (in theta-distance order) that may take the factored path; SE2_K4P_EXACT: none (diagnostics)
-    static const int ffma_max_a = getenv("SE2_K4P_EXACT") ? 0 : (getenv("SE2_K4P_FFMA_A") ? atoi(getenv("SE2_K4P_FFMA_A")) : 1 << 20);
+    const int ffma_max_a = getenv("SE2_K4P_EXACT") ? 0 : (getenv("SE2_K4P_FFMA_A") ? atoi(getenv("SE2_K4P_FFMA_A")) : 1 << 20);
     conv_lse_precise_kernel<R><<<grid, C::NT, C::SMEM, s>>>(
         in, k->L2hi, k->L2lo, k->L2row, k->Eq, k->w3 * k->w3 / k->eps, k->nx, k->ny, k->nt, tiles_x, k->wlo(), k->whi(),
         epi, ffma_max_a, reinterpret_cast<unsigned long long*>(k->lse_counters + 12), k->pstats, k->Lth, k->LseS, groups,

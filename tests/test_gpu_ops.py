@@ -414,11 +414,12 @@ def test_transport_cost(grid, log_domain, cuda_device):
 
 @pytest.mark.parametrize("case", CFG_GRIDS[:4] + [g for g in ODD_GRIDS if g[0] in ("ragged", "nt6", "r15", "r0", "wide")],
                          ids=lambda c: c[0])
-@pytest.mark.parametrize("span", [20.0, 2000.0])
+@pytest.mark.parametrize("span", [20.0, 2000.0, 30000.0])
 def test_conv_precise(case, span, cuda_device):
     """K4P (fp64 potentials, exact exponents): elementwise ABSOLUTE error <= 2e-6 nats against the fp64 oracle
     on the same fp64 input -- even for 2000-nat fields, where every fp32 engine is limited to ~1e-4
-    (lse_abs_tol).  -inf entries (zero mass) included."""
+    (lse_abs_tol).  -inf entries (zero mass) included.  span 20: the factored FFMA path; 2000: the exact path
+    with grid-aligned exponents; 30000 (windows beyond 2^14 log2 units): its TwoSum form."""
     from paper_2402_15322_b200 import se2_conv_precise
     name, nx, ny, nt, eps, w, R = case
     k = _kernel(nx, ny, nt, eps, w, R, 2)
@@ -431,3 +432,29 @@ def test_conv_precise(case, span, cuda_device):
     assert np.array_equal(np.isfinite(y), fin)
     d = np.abs(y[fin] - ref[fin])
     assert d.max() <= 2e-6 * np.maximum(1.0, np.abs(ref[fin]) / 1000.0).max(), (name, d.max())
+
+
+@pytest.mark.parametrize("mode", ["groups1", "groups3", "groups8", "exact-only"])
+@pytest.mark.parametrize("span", [20.0, 400.0])
+def test_conv_precise_modes(mode, span, cuda_device, monkeypatch):
+    """K4P's theta_i split (SE2_K4P_GROUPS: partial (shift, fp64 sum) per output, exact combine) and the
+    per-tap path alone (SE2_K4P_EXACT: no factored channels) against the fp64 oracle on c1's grid with a
+    batch of 3 fields: the same 2e-6-nat bound whichever way the channels are dealt."""
+    from paper_2402_15322_b200 import se2_conv_precise
+    if mode == "exact-only":
+        monkeypatch.setenv("SE2_K4P_EXACT", "1")
+    else:
+        monkeypatch.setenv("SE2_K4P_GROUPS", mode[len("groups"):])
+    nx, ny, nt, eps, w, R = 28, 28, 16, 0.02, (1.0, 3.0, 1.0), 5
+    k = _kernel(nx, ny, nt, eps, w, R, 3)
+    rng = np.random.default_rng(zlib.crc32((mode + str(span)).encode()))
+    # a smooth potential (planes per orientation) plus noise: window ranges below and above the 80-nat
+    # factored-path limit depending on span
+    yy, xx = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    v = np.stack([np.stack([span * (0.01 * (xx * np.cos(t) + yy * np.sin(t))) + rng.uniform(-span / 20, span / 20,
+                                                                                         (ny, nx))
+                            for t in np.linspace(0, 2 * np.pi, nt, endpoint=False)]) for _ in range(3)])
+    y = _host(se2_conv_precise(k, torch.from_numpy(v).cuda()))
+    ref = O.lse_conv(O.log_kernel_table(O.Grid(nx, ny, nt), R, eps, w), v)
+    d = np.abs(y - ref)
+    assert d.max() <= 2e-6 * max(1.0, np.abs(ref).max() / 1000.0), (mode, span, d.max())
