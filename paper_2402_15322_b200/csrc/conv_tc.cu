@@ -768,7 +768,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
 
 // balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
 // one block per (kr-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
-__global__ void __launch_bounds__(256) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
+__global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
     tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
     const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
@@ -1054,15 +1054,16 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         return c;
     };
     float2* stats = g.nar ? reinterpret_cast<float2*>(k->tc_stats) : nullptr;
-    {
+    static const bool skip_split = getenv("SE2_TC_DIAG_SKIP_SPLIT") != nullptr;   // timing diagnostics only
+    if (!skip_split) {
         // one block per (field, row, chunk), one padded pixel per thread: all 8 plane loads in flight
         const long long rows = (long long)batch * k->ny * g.nch;
         const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
         cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
         cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
         if (e != cudaSuccess) return e;
+        count_launch();
     }
-    count_launch();
     TcArgs a;
     a.xk = xk;
     const bool cost = epi.table != nullptr;   // the transport-cost table (launch only when tc_wc exists)
@@ -1108,12 +1109,13 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
             if (e != cudaSuccess) return e;
         }
         count_launch();
-        {
+        static const bool skip_epi = getenv("SE2_TC_DIAG_SKIP_EPI") != nullptr;   // timing diagnostics only
+        if (!skip_epi) {
             cudaLaunchConfig_t c = cfg_of(dim3(a.ngroups, k->nt, batch), dim3(256), 0);
             cudaError_t e = cudaLaunchKernelEx(&c, tc_pieces_epilogue_kernel, a, epi);
             if (e != cudaSuccess) return e;
+            count_launch();
         }
-        count_launch();
         if (bpf) *bpf = a.ngroups * k->nt;
         return cudaGetLastError();
     }
