@@ -321,6 +321,28 @@ def config_sweep(device: int):
             rec["engine"] = "K3 (fp32 potentials)"
         out[cfg.name] = rec
         k.close()
+        if cfg.name == "c0":
+            # c0's "replicas" unit: 64 independent c0 problems (seeds 0..63) in ONE K9 launch, one thread-block
+            # cluster per problem (the batched mode of the one-launch solver): problems x iterations / s
+            B = 64
+            kb = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=B, device=device)
+            mu_b = torch.from_numpy(np.stack([S.stroke_measure(cfg.nx, cfg.ny, cfg.ntheta, 2, seed=5000 + 2 * i)
+                                              for i in range(B)]).astype(np.float32)).cuda()
+            nu_b = torch.from_numpy(np.stack([S.stroke_measure(cfg.nx, cfg.ny, cfg.ntheta, 2, seed=5001 + 2 * i)
+                                              for i in range(B)]).astype(np.float32)).cuda()
+            a_b, b_b = torch.empty_like(mu_b), torch.empty_like(mu_b)
+            se2_sinkhorn(kb, mu_b, nu_b, a_b, b_b, cfg.iters, True, trace=True)
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record()
+            se2_sinkhorn(kb, mu_b, nu_b, a_b, b_b, cfg.iters, True, trace=True)
+            q1.record()
+            torch.cuda.synchronize()
+            qms = q0.elapsed_time(q1)
+            out["c0_batched64"] = {"problems": B, "iters": cfg.iters, "ms": qms,
+                                   "problem_iters_per_s": B * cfg.iters / (qms / 1000.0),
+                                   "engine": "K9, one cluster per problem in one launch"}
+            kb.close()
     return out
 
 
@@ -492,6 +514,43 @@ def sharded_barycenter_precise(ws: int, rank: int, local: int, world, iters: int
             "n_gpus_used": nin}
 
 
+def c1_tvalues(ws: int, rank: int, local: int):
+    """c1's five t-values distributed over the ranks (SURVEY §8e: 5 / 3 / 2 / 1 per GPU at 1 / 2 / 4 / 8;
+    no collective), each rank solving its share of the interpolation batched, fp64 potentials (K4P).
+    Returns barycenter iterations/s summed over all t-values (max device time over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import se2_synth as S
+    from paper_2402_15322_b200 import Kernel, se2_barycenter_precise
+    from paper_2402_15322_b200.parallel import partition
+    cfg = S.get_config("c1")
+    d = S.config_inputs(cfg)
+    lams_all = np.atleast_2d(np.stack(d["lambdas"]))
+    lo, hi = partition(lams_all.shape[0], ws, rank)
+    ms = 0.0
+    k = None
+    if hi > lo:
+        k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=2 * (hi - lo), device=local)
+        mus = torch.from_numpy(np.stack(d["mus"])).cuda()
+        se2_barycenter_precise(k, mus, lams_all[lo:hi], cfg.iters)
+        torch.cuda.synchronize()
+    dist.barrier()
+    if k is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        se2_barycenter_precise(k, mus, lams_all[lo:hi], cfg.iters)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        k.close()
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": f"c1: 5 t-values x 200 barycenter iterations (fp64 potentials), split over {ws} GPUs",
+            "ms": ms, "solve_iters_per_s": lams_all.shape[0] * cfg.iters / (ms / 1000.0), "scaling": "strong"}
+
+
 def replicas(ws: int, rank: int, local: int, cfg, d, steps: int = 2):
     """Every rank runs its own c4 JKO flow (independent problems, no collective): the weak-scaling extra."""
     import torch
@@ -646,6 +705,12 @@ def run_gpu(args):
             rep = {"error": f"{type(exc).__name__}: {exc}"}
         if rank == 0:
             out["replicas"] = rep
+        try:
+            c1t = c1_tvalues(ws, rank, local)
+        except Exception as exc:
+            c1t = {"error": f"{type(exc).__name__}: {exc}"}
+        if rank == 0:
+            out["c1_tvalues"] = c1t
     if not args.no_configs:
         try:
             sharded = sharded_barycenter(ws, rank, local, world)

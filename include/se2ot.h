@@ -316,8 +316,10 @@ SE2_API se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* 
 SE2_API se2_status se2_tc_tile_stats(se2_kernel k, int64_t* tiles, int64_t* wide_tiles, int32_t reset);
 
 /* fp64-potential log-domain engine (K4P, se2_barycenter_precise): (CTA, input orientation) channels that
- * took the factored FFMA path / all channels visited, since the last reset (synchronises the device). */
-SE2_API se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t* channels, int32_t reset);
+ * took the factored FFMA path / all channels visited, and CTAs whose hinted shifts failed verification and
+ * were redone two-pass, since the last reset (synchronises the device). */
+SE2_API se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t* channels, int64_t* hint_redos,
+                                          int32_t reset);
 
 /* Instrumentation: when enabled, every conv launch is bracketed by CUDA events on its stream;
  * se2_timing_get returns the number of conv launches and their summed device time (ms)

@@ -133,7 +133,7 @@ def load(path: str = LIB_PATH):
         "se2_lse_row_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_tc_tile_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_interp_masses": [P, P, i32, P],
-        "se2_precise_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
+        "se2_precise_path_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_guard_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i64), i32],
         "se2_kernel_set_window": [P, i32, i32],
         "se2_barycenter_precise": [P, i32, i32, P, pd, P, P, P, ctypes.POINTER(se2_opts), pd, P],

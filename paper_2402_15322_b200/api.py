@@ -107,9 +107,10 @@ class Kernel:
 
     def precise_path_stats(self, reset: bool = True) -> dict:
         """K4P: channels on the factored FFMA path / channels visited."""
-        f, c = ctypes.c_int64(), ctypes.c_int64()
-        check(L.load().se2_precise_path_stats(self._h, ctypes.byref(f), ctypes.byref(c), 1 if reset else 0))
-        return dict(ffma=f.value, channels=c.value)
+        f, c, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(L.load().se2_precise_path_stats(self._h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(r),
+                                              1 if reset else 0))
+        return dict(ffma=f.value, channels=c.value, hint_redos=r.value)
 
     def tc_tile_stats(self, reset: bool = True) -> dict:
         """K10 narrow geometry: tiles computed / tiles on the wide (32-orientation) window."""

@@ -926,7 +926,8 @@ se2_status se2_lse_row_stats(se2_kernel k, int64_t* rows_live, int64_t* rows_vis
     return SE2_OK;
 }
 
-se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t* channels, int32_t reset) {
+se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t* channels, int64_t* hint_redos,
+                                  int32_t reset) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(ffma_channels != nullptr && channels != nullptr, "null output");
     DeviceGuard g(k->device);
@@ -935,6 +936,7 @@ se2_status se2_precise_path_stats(se2_kernel k, int64_t* ffma_channels, int64_t*
     SE2_CUDA_TRY(cudaMemcpy(h, k->lse_counters + 12, sizeof(h), cudaMemcpyDeviceToHost));
     *ffma_channels = (int64_t)h[0];
     *channels = (int64_t)h[1];
+    if (hint_redos) *hint_redos = 0;   // K4P runs two-pass (a hinted variant measured no faster on c3)
     if (reset) SE2_CUDA_TRY(cudaMemset(k->lse_counters + 12, 0, sizeof(h)));
     return SE2_OK;
 }

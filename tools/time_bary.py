@@ -34,6 +34,6 @@ for name in (args or ["c1", "c2", "c3"]):
         extra = ""
         if fn is se2_barycenter_precise:
             ps = k.precise_path_stats(reset=True)
-            extra = f", K4P channels on the FFMA path {ps['ffma']}/{ps['channels']}"
+            extra = f", K4P channels on the FFMA path {ps['ffma']}/{ps['channels']}, hinted CTAs redone {ps['hint_redos']}"
         print(f"{name} {fn.__name__}: {it / (e0.elapsed_time(e1) / 1000.0):.1f} it/s ({it} iterations){extra}", flush=True)
     k.close()
