@@ -207,8 +207,9 @@ SE2_API se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const
 
 /* ------------------------------------------------------------------------------------------
  * se2_barycenter_precise -- App. A in the log domain with the potentials held in fp64 and every
- *   conv on K4P (exact per-tap log-sum-exp with exact exponents: TwoSum of float pairs, integer shifts,
- *   fp64 row-sum accumulation; ~1e-7 nats per conv): the engine of the north star's elementwise 1e-4
+ *   conv on K4P (channels within 80 nats on a factored FFMA path whose terms carry only relative rounding;
+ *   the rest per tap with exponents exact in fp32 (grid-aligned float pairs, integer shifts); fp64
+ *   accumulation; ~1e-7 nats per conv): the engine of the north star's elementwise 1e-4
  *   parity on potentials of 10^2..10^3 nats (reading R19, SURVEY ledger L16).  Same arguments as
  *   se2_barycenter with fp64 outputs: lbary [nsolve][N] = log mu, lv_state / lw_state (nullable)
  *   [nsolve][n][N] = log v_i / log w_i (with SE2_WARM_START lv_state is also the initial log v_i).
