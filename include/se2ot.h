@@ -452,10 +452,11 @@ SE2_API se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32
 
 /* se2_barycenter_precise_dist -- se2_barycenter_precise (fp64 potentials, K4P) with this rank's n inputs
  *   (mus [n][N] float, lambdas HOST [nsolve][n]: this rank's share of weights that sum to 1 over all `reduce`
- *   ranks); per iteration one fp64 allreduce of the partial sum_i lambda_i log d_i over `reduce`.  Input
- *   sharding only: dist->slabs must be NULL and the halos 0 (SE2_EINVAL otherwise).  lbary [nsolve][N]
- *   (fp64 log barycenter on every rank), lv_state / lw_state [nsolve][n][N] fp64 (nullable).  Trace: the
- *   lambda-weighted error summed over all ranks' inputs. */
+ *   ranks); per iteration one fp64 allreduce of the partial sum_i lambda_i log d_i over `reduce` and, with
+ *   `slabs`, exchanges of the fp64 w_i / v_i boundary rows (R rows toward each neighbour; the kernel is built on
+ *   the local grid as for se2_barycenter_dist).  lbary [nsolve][N_local] (fp64 log barycenter; its owned rows
+ *   on every rank of the slab), lv_state / lw_state [nsolve][n][N_local] fp64 (nullable).  Trace: the
+ *   lambda-weighted error summed over all ranks' inputs and slabs. */
 SE2_API se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve,
                                                const float* mus, const double* lambdas, double* lbary, double* lv_state,
                                                double* lw_state, const se2_opts* opts, double* err_trace_host,

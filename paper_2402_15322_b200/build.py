@@ -43,9 +43,13 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     objs = []
     procs = []
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "se2ot.h")]
+    t_hdr = max(os.path.getmtime(h) for h in hdrs)
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), t_hdr)):
+            continue   # object newer than its source and every header
         cmd = [NVCC, *NVCC_FLAGS, *inc, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -412,21 +412,23 @@ void set_pack(Epilogue& e, const se2_kernel_s* k, const Slab& sl, const se2_comm
 // neighbours' boundary rows -> the halo rows of x ([planes][ny][nx]).  The send buffers hold x's first /
 // last R owned rows: packed by the producing conv's epilogue (set_pack), or here when pack is set (fields
 // written by elementwise kernels)
+// (row_words: 4-byte words per grid row -- nx for float fields, 2 nx for fp64 fields moved as word pairs)
 se2_status exchange(se2_kernel_s* k, const Slab& sl, se2_comm_s* c, float* x, int planes, float* bufs, cudaStream_t s,
-                    bool pack = false) {
+                    bool pack = false, int row_words = 0) {
     if (!sl.on) return SE2_OK;
-    const int64_t cnt = (int64_t)planes * k->R * k->nx;
+    const int nxw = row_words > 0 ? row_words : k->nx;
+    const int64_t cnt = (int64_t)planes * k->R * nxw;
     float* send_up = bufs;
     float* send_dn = bufs + cnt;
     float* recv_up = bufs + 2 * cnt;
     float* recv_dn = bufs + 3 * cnt;
     if (pack) {
         if (c->r > 0) {
-            pack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, k->nx, sl.lo, k->R, send_up);
+            pack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, nxw, sl.lo, k->R, send_up);
             count_launch();
         }
         if (c->r + 1 < c->n) {
-            pack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, k->nx, sl.hi - k->R, k->R, send_dn);
+            pack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, nxw, sl.hi - k->R, k->R, send_dn);
             count_launch();
         }
         SE2_CUDA_TRY(cudaGetLastError());
@@ -434,11 +436,11 @@ se2_status exchange(se2_kernel_s* k, const Slab& sl, se2_comm_s* c, float* x, in
     se2_status st = c->neighbours(send_up, recv_up, send_dn, recv_dn, cnt, s);
     if (st != SE2_OK) return st;
     if (sl.top > 0) {
-        unpack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, k->nx, 0, sl.top, recv_up);
+        unpack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, nxw, 0, sl.top, recv_up);
         count_launch();
     }
     if (sl.bot > 0) {
-        unpack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, k->nx, sl.hi, sl.bot, recv_dn);
+        unpack_rows_kernel<<<grid_of(cnt), 256, 0, s>>>(x, planes, k->ny, nxw, sl.hi, sl.bot, recv_dn);
         count_launch();
     }
     SE2_CUDA_TRY(cudaGetLastError());
@@ -841,15 +843,14 @@ se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, in
 }
 
 // App. A with fp64 potentials (K4P, reading R19) and this rank's inputs: per iteration the partial weighted
-// log-mean sum_i lambda_i log d_i (fp64) is all-reduced over `reduce`; row slabs are not supported (the fp64
-// conv has no halo-packing epilogue): dist->slabs must be NULL.
+// log-mean sum_i lambda_i log d_i (fp64) is all-reduced over `reduce` and, with row slabs, the fp64 w_i / v_i
+// boundary rows are exchanged with the neighbour slabs (packed by a row-copy kernel: the fp64 epilogue has no
+// packing stores) -- c3's 8-GPU "one input per GPU pair" layout on the 1e-4 engine.
 se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve, const float* mus,
                                        const double* lambdas, double* lbary, double* lv_state, double* lw_state,
                                        const se2_opts* opts, double* err_trace_host, se2_stream stream) {
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(dist != nullptr, "dist required (se2_barycenter_precise for one GPU)");
-    SE2_CHECK_ARG(dist->slabs == nullptr && dist->halo_top == 0 && dist->halo_bot == 0,
-                  "fp64-potential barycenter: input sharding only (no row slabs)");
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
     SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n (inputs on this rank), nsolve >= 1");
     SE2_CHECK_ARG((int64_t)n * nsolve <= k->max_batch, "n*nsolve exceeds max_batch");
@@ -861,8 +862,12 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
     DeviceGuard g(k->device);
     cudaStream_t s = (cudaStream_t)stream;
     SE2_CUDA_TRY(tabulate_precise(k, s));
-    se2_status st = reset_guard(k, s);
+    Slab sl;
+    se2_status st = slab_of(k, dist, &sl);
     if (st != SE2_OK) return st;
+    st = reset_guard(k, s);
+    if (st != SE2_OK) return st;
+    se2_comm_s* sc = dist->slabs;
     se2_comm_s* rc = dist->reduce;
     const bool reduce = rc != nullptr && rc->n > 1;
     const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
@@ -871,14 +876,19 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
     const int64_t FN = (int64_t)F * N;
     const int iters = opts->iters;
     KernelExtra* x = extra(k);
-    // workspace: mu_rep (float) [F][N]; lmu, v, w, d (double) [F][N]
-    st = ensure(x->ws, (size_t)FN * (sizeof(float) + 4 * sizeof(double)) + 64, x);
+    // workspace: mu_rep (float) [F][N]; lmu, v, w, d (double) [F][N]; 4 halo buffers of fp64 rows
+    const int64_t cnt = sl.on ? (int64_t)F * k->nt * k->R * 2 * k->nx : 0;   // 4-byte words per buffer
+    st = ensure(x->ws, (size_t)FN * (sizeof(float) + 4 * sizeof(double)) + 64 + (size_t)4 * cnt * sizeof(float), x);
     if (st != SE2_OK) return st;
     float* mu_rep = reinterpret_cast<float*>(x->ws.ptr);
     double* lmu = reinterpret_cast<double*>(reinterpret_cast<char*>(x->ws.ptr) + ((FN * sizeof(float) + 63) / 64) * 64);
     double* v = lv_state ? lv_state : lmu + FN;
     double* w = lw_state ? lw_state : lmu + 2 * FN;
     double* d = lmu + 3 * FN;
+    float* bufs = reinterpret_cast<float*>(lmu + 4 * FN);
+    auto xchg = [&](double* f, cudaStream_t s) {   // f's halo rows <- the neighbours' boundary rows (fp64)
+        return exchange(k, sl, sc, reinterpret_cast<float*>(f), F * k->nt, bufs, s, true, 2 * k->nx);
+    };
     st = ensure(x->misc, 4096 + sizeof(double) * F, x);
     if (st != SE2_OK) return st;
     const int bpf = conv_blocks_per_field_precise(k);
@@ -895,7 +905,7 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
     std::vector<uint64_t> key = {6, as_key(mus), as_key(lbary), as_key(v), as_key(w), (uint64_t)n, (uint64_t)nsolve,
                                  (uint64_t)iters, (uint64_t)opts->flags, (uint64_t)trace, as_key(x->ws.ptr),
-                                 as_key(x->misc.ptr), as_key(partial), as_key(tr)};
+                                 as_key(x->misc.ptr), as_key(partial), as_key(tr), (uint64_t)sl.lo, (uint64_t)sl.hi};
     auto enqueue = [&](cudaStream_t s) -> se2_status {
         se2_status st = SE2_OK;
         for (int sv = 0; sv < nsolve; ++sv)
@@ -904,6 +914,11 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
         SE2_CUDA_TRY(launch_log_f64(mu_rep, lmu, FN, s));
         if (!warm) SE2_CUDA_TRY(launch_fill_f64(v, FN, 0.0, s));
         SE2_CUDA_TRY(launch_fill_f64(w, FN, 0.0, s));
+        if (sl.on) SE2_CUDA_TRY(launch_fill_f64(d, FN, 0.0, s));   // halo rows of d are never written
+        if (warm) {   // the caller's v_i may lack current halo rows
+            st = xchg(v, s);
+            if (st != SE2_OK) return st;
+        }
         for (int j = 0; j < iters; ++j) {
             EpiP e1;   // w_i = mu_i / K v_i  (error of the previous v-update fused)
             e1.op = EPI_DIVIDE;
@@ -917,6 +932,8 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
             st = run_conv_precise(k, v, F, e1, s);
             if (st != SE2_OK) return st;
             if (trace && j > 0) SE2_CUDA_TRY(launch_reduce_partials(partial, F, bpf, tr + (int64_t)(j - 1) * F, s));
+            st = xchg(w, s);
+            if (st != SE2_OK) return st;
             EpiP e2;   // d_i = v_i K w_i
             e2.op = EPI_MULTIPLY;
             e2.target = v;
@@ -931,6 +948,8 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
                 if (st != SE2_OK) return st;
                 SE2_CUDA_TRY(launch_bary_update_f64(n, nsolve, N, d, lbary, v, s));
             }
+            st = xchg(v, s);   // v's halo rows for the next K v
+            if (st != SE2_OK) return st;
         }
         if (trace && iters > 0) {
             EpiP e3;
@@ -955,6 +974,10 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
             for (int sv = 0; sv < nsolve; ++sv)
                 for (int i = 0; i < n; ++i) e[(size_t)j * nsolve + sv] += lambdas[sv * n + i] * h[(size_t)j * F + sv * n + i];
         SE2_CUDA_TRY(cudaMemcpyAsync(tr, e.data(), sizeof(double) * e.size(), cudaMemcpyHostToDevice, s));
+        if (sc) {
+            st = sc->allreduce(tr, (int64_t)e.size(), true, s);
+            if (st != SE2_OK) return st;
+        }
         if (rc) {
             st = rc->allreduce(tr, (int64_t)e.size(), true, s);
             if (st != SE2_OK) return st;
@@ -962,13 +985,13 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
         SE2_CUDA_TRY(cudaMemcpyAsync(err_trace_host, tr, sizeof(double) * e.size(), cudaMemcpyDeviceToHost, s));
         SE2_CUDA_TRY(cudaStreamSynchronize(s));
     }
-    int* cnt = reinterpret_cast<int*>(x->misc.ptr);
-    SE2_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), s));
-    SE2_CUDA_TRY(launch_count_nonfinite_f64(lbary, (int64_t)nsolve * N, cnt, s));
-    SE2_CUDA_TRY(launch_count_nonfinite_f64(v, FN, cnt, s));
-    SE2_CUDA_TRY(launch_count_nonfinite_f64(w, FN, cnt, s));
+    int* nbad = reinterpret_cast<int*>(x->misc.ptr);
+    SE2_CUDA_TRY(cudaMemsetAsync(nbad, 0, sizeof(int), s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(lbary, (int64_t)nsolve * N, nbad, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(v, FN, nbad, s));
+    SE2_CUDA_TRY(launch_count_nonfinite_f64(w, FN, nbad, s));
     int h = 0;
-    SE2_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SE2_CUDA_TRY(cudaMemcpyAsync(&h, nbad, sizeof(int), cudaMemcpyDeviceToHost, s));
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
     if (h != 0) {
         set_error("non-finite values produced by the iteration (" + std::to_string(h) + " entries)");

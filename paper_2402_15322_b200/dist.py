@@ -178,8 +178,9 @@ def se2_barycenter_precise_dist(k: Kernel, d: Dist, mus: torch.Tensor, lambdas, 
                                 lw_state: Optional[torch.Tensor] = None, trace: bool = False,
                                 warm_start: bool = False, no_graph: bool = False):
     """App. A with fp64 potentials (K4P, reading R19) and this rank's inputs mus [n][N] (float32), weights
-    lambdas [nsolve][n] (a share of weights that sum to 1 over the `reduce` ranks); input sharding only.
-    Returns (log mu [nsolve][N] float64 on every rank, trace [iters][nsolve] or None)."""
+    lambdas [nsolve][n] (a share of weights that sum to 1 over the `reduce` ranks) and, with `d.slabs`, this
+    rank's row slab of every input (fp64 halo exchanges of w_i / v_i).  Returns (log mu [nsolve][N_local]
+    float64, trace [iters][nsolve] or None)."""
     from .api import _check_field64
     _check_field(mus, k, "mus")
     n = mus.numel() // k.N

@@ -189,13 +189,13 @@ def test_barycenter_precise_dist_one_rank_is_precise(cuda_device):
     assert torch.equal(b1, b2) and np.array_equal(t1, t2)
 
 
-@pytest.mark.parametrize("nranks", [2, 4])
-def test_barycenter_precise_dist_loopback(nranks, cuda_device):
-    """The fp64-potential barycenter with the 4 inputs of a c3-like problem sharded over 2 / 4 ranks (fp64
-    allreduce of the weighted log-mean per iteration) against the fp64 oracle at the north star's 1e-4
-    ELEMENTWISE on gauge-fixed potentials, 120 iterations."""
-    from paper_2402_15322_b200 import Kernel
-    from paper_2402_15322_b200.dist import Comm, Dist, se2_barycenter_precise_dist
+@pytest.mark.parametrize("layout", ["inputs2", "inputs4", "slabs2", "inputs2xslabs2", "slabs3"])
+def test_barycenter_precise_dist_loopback(layout, cuda_device):
+    """The fp64-potential barycenter with the 4 inputs of a c3-like problem sharded over ranks (fp64
+    allreduce of the weighted log-mean per iteration) and/or every input's grid split into row slabs (fp64
+    halo exchanges of w_i / v_i; inputs2xslabs2 is c3's 8-GPU 'one input per GPU pair' layout at 4 ranks)
+    against the fp64 oracle at the north star's 1e-4 ELEMENTWISE on gauge-fixed potentials, 120 iterations."""
+    from paper_2402_15322_b200.dist import Comm, Dist, local_rows, se2_barycenter_precise_dist, slab_kernel
     nx, ny, nt, R, eps, w = 36, 40, 16, 6, 0.01, (1.0, 3.0, 1.0)
     g = O.Grid(nx, ny, nt)
     mus = [S.stroke_measure(nx, ny, nt, 3, seed=300 + i, sigma_px=1.5).astype(np.float64) for i in range(4)]
@@ -203,29 +203,37 @@ def test_barycenter_precise_dist_loopback(nranks, cuda_device):
     iters = 120
     ref = O.barycenter(O.kernel_table(g, R, eps, w), O.log_kernel_table(g, R, eps, w), mus, lam, iters,
                        log_domain=True, trace=True)
-    world = Comm.loopback(nranks)
-    per = 4 // nranks
+    nin = {"inputs2": 2, "inputs4": 4, "slabs2": 1, "inputs2xslabs2": 2, "slabs3": 1}[layout]
+    nsl = {"slabs2": 2, "inputs2xslabs2": 2, "slabs3": 3}.get(layout, 1)
+    world = Comm.loopback(nin * nsl)
+    per = 4 // nin
 
     def rank(r):
-        k = Kernel(nx, ny, nt, eps, w, R, max_batch=per)
-        sel = list(range(r * per, (r + 1) * per))
-        m = _dev(np.stack([mus[i] for i in sel]))
-        v = torch.empty((1, per, nt, ny, nx), device="cuda", dtype=torch.float64)
+        ii, si = r // nsl, r % nsl                                    # input group, slab
+        reduce = world[r].split(si, ii) if nin > 1 else None          # ranks with the same slab
+        slabs = world[r].split(1000 + ii, si) if nsl > 1 else None    # ranks with the same inputs
+        k, row0, rows, top, bot = slab_kernel(nx, ny, nt, eps, w, R, nsl, si, max_batch=per)
+        sel = list(range(ii * per, (ii + 1) * per))
+        m = _dev(np.stack([local_rows(mus[i], row0, rows, top, bot) for i in sel]))
+        v = torch.empty((1, per) + tuple(m.shape[1:]), device="cuda", dtype=torch.float64)
         wst = torch.empty_like(v)
-        lb, tr = se2_barycenter_precise_dist(k, Dist(reduce=world[r]), m, lam[sel][None], iters, lv_state=v,
-                                             lw_state=wst, trace=True)
-        return sel, _host(lb)[0], _host(v)[0], _host(wst)[0], tr
+        lb, tr = se2_barycenter_precise_dist(k, Dist(reduce=reduce, slabs=slabs, halo_top=top, halo_bot=bot), m,
+                                             lam[sel][None], iters, lv_state=v, lw_state=wst, trace=True)
+        return (row0, rows, sel, _host(lb)[0][:, top:top + rows], _host(v)[0][:, :, top:top + rows],
+                _host(wst)[0][:, :, top:top + rows], tr)
 
-    res = _run_ranks(nranks, rank)
+    res = _run_ranks(nin * nsl, rank)
+    lbar = np.zeros(g.shape)
     lv = np.zeros((4,) + g.shape)
     lw = np.zeros((4,) + g.shape)
-    for sel, lb, v, wv, tr in res:
-        assert potential_err(lb, ref["lbary"]) <= 1e-4
-        assert measure_err(np.exp(lb), ref["bary"]) <= 1e-4
+    for row0, rows, sel, lb, v, wv, tr in res:
+        lbar[:, row0:row0 + rows] = lb                # identical on every input rank of the slab
         assert trace_err(tr[:, 0], ref["err"]) <= 1.0
         for j, i in enumerate(sel):
-            lv[i] = v[j]
-            lw[i] = wv[j]
+            lv[i][:, row0:row0 + rows] = v[j]
+            lw[i][:, row0:row0 + rows] = wv[j]
+    assert potential_err(lbar, ref["lbary"]) <= 1e-4
+    assert measure_err(np.exp(lbar), ref["bary"]) <= 1e-4
     e = bary_potential_errs(lv, lw, ref["lv"], ref["lw"], lam)
     assert max(e.values()) <= 1e-4, e
 
