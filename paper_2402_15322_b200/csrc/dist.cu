@@ -216,6 +216,12 @@ struct LoopWorld {
     int arrived = 0;
     uint64_t gen = 0;
     std::map<std::pair<uint64_t, int>, std::shared_ptr<LoopWorld>> subs;   // (split sequence, color)
+    // events of destroyed member comms: a slower rank may still be enqueueing a wait on an event of a rank
+    // that already returned from the call and destroyed its communicator, so they live as long as the world
+    std::vector<cudaEvent_t> retired;
+    ~LoopWorld() {
+        for (auto e : retired) cudaEventDestroy(e);
+    }
 
     std::vector<Rec> gather(int r, const Rec& rec) {
         std::unique_lock<std::mutex> lk(mu);
@@ -244,7 +250,12 @@ struct LoopComm final : se2_comm_s {
     void** table = nullptr;   // device pointer table (n entries)
     LoopComm() { capturable = false; }
     ~LoopComm() override {
-        for (auto e : evs) cudaEventDestroy(e);
+        if (w) {
+            std::lock_guard<std::mutex> lk(w->mu);
+            w->retired.insert(w->retired.end(), evs.begin(), evs.end());
+        } else {
+            for (auto e : evs) cudaEventDestroy(e);
+        }
         if (scratch) cudaFree(scratch);
         if (table) cudaFree(table);
     }
