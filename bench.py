@@ -743,6 +743,52 @@ def run_gpu(args):
     return 0
 
 
+def write_manifest(path, args, cfg, inputs, out):
+    """Run manifest (SURVEY §5 "metrics / logging"): one JSON line per bench run with the config, the input
+    seeds and the SHA-256 of every seeded input array and of the library that ran, the GPU, the SM clock
+    samples of the timed region and the headline numbers.  Appended, never read back by the bench."""
+    import dataclasses
+    import hashlib
+    import platform
+
+    import torch
+
+    import paper_2402_15322_b200 as pkg
+    from paper_2402_15322_b200 import _lib
+
+    def sha(b):
+        return hashlib.sha256(b).hexdigest()
+
+    ci = int(cfg.name[1:])
+    lib = os.path.join(os.path.dirname(os.path.abspath(pkg.__file__)), "libse2ot.so")
+    prop = torch.cuda.get_device_properties(torch.cuda.current_device())
+    man = {
+        "time_utc": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+        "argv": sys.argv[1:],
+        "config": dataclasses.asdict(cfg),
+        "seeds": {f"mu[{i}]": 1000 * ci + i for i in range(len(inputs["mus"]))},
+        "input_sha256": {f"mu[{i}]": sha(np.ascontiguousarray(m, dtype=np.float32).tobytes())
+                         for i, m in enumerate(inputs["mus"])},
+        "libse2ot_sha256": sha(open(lib, "rb").read()),
+        "abi_version": int(_lib.load().se2_abi_version()),
+        "gpu": {"name": prop.name, "sms": prop.multi_processor_count, "cc": f"{prop.major}.{prop.minor}",
+                "memory_gb": round(prop.total_memory / 2 ** 30, 1)},
+        "host": {"cores": os.cpu_count(), "machine": platform.machine()},
+        "torch": torch.__version__, "cuda": torch.version.cuda,
+        "clocks": out.get("clocks"),
+        "value": out.get("value"), "unit": out.get("unit"), "n_gpus": out.get("n_gpus"),
+        "ms_per_step": out.get("ms_per_step"), "e2e": out.get("e2e"),
+        "roofline_frac": (out.get("roofline") or {}).get("frac"),
+        "gpu_launches": out.get("gpu_launches"),
+        "configs_iters_per_s": {n: c.get("iters_per_s") for n, c in (out.get("configs") or {}).items()
+                                if isinstance(c, dict) and "iters_per_s" in c},
+    }
+    d = os.path.dirname(os.path.abspath(path))
+    os.makedirs(d, exist_ok=True)
+    with open(path, "a") as f:
+        f.write(json.dumps(man) + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -752,6 +798,9 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (c0..c4 solves)")
+    ap.add_argument("--manifest", default=os.environ.get("SE2_MANIFEST", ""),
+                    help="append a run manifest (config, seeds, input / library SHA-256, GPU, clocks, results) "
+                         "as one JSON line to this file")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -355,6 +355,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
     float* hint1 = hints ? reinterpret_cast<float*>(x->ws.ptr) + 2 * BN : nullptr;   // K b
     float* hint2 = hints ? hint1 + BN : nullptr;                                      // K a
     for (int l = 0; l < iters; ++l) {
+        NvtxRange nvtx_iter("se2 iteration", l);
         // a = mu / K b   (error of the previous iterate fused: sum |a_old K b - mu|)
         Epilogue e1;
         e1.op = EPI_DIVIDE;
@@ -408,6 +409,7 @@ static se2_status sinkhorn_impl(se2_kernel_s* k, const float* mu, const float* n
 
 se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a, float* b, int32_t batch,
                         const se2_prox* prox, const se2_opts* opts, double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_sinkhorn");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required, iters >= 0");
     SE2_CHECK_ARG(mu && a && b && a != b, "mu, a, b must be non-null distinct device pointers");
@@ -430,6 +432,7 @@ se2_status se2_sinkhorn(se2_kernel k, const float* mu, const float* nu, float* a
 
 se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* a, float* b, const se2_prox* prox,
                         const se2_opts* opts, double* mass_host, double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_jko_step");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 1, "opts required, iters >= 1");
     SE2_CHECK_ARG(prox != nullptr && prox->tau >= 0 &&
@@ -460,6 +463,7 @@ se2_status se2_jko_step(se2_kernel k, const float* mu_k, float* mu_next, float* 
 se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* mus, const double* lambdas,
                           float* bary, float* v_state, float* w_state, const se2_opts* opts,
                           double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_barycenter");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
     SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n, nsolve >= 1");
@@ -535,6 +539,7 @@ se2_status se2_barycenter(se2_kernel k, int32_t n, int32_t nsolve, const float* 
         SE2_CUDA_TRY(launch_fill(v_lo, FN, 0.f, s));
         SE2_CUDA_TRY(launch_fill(w, FN, LOG ? 0.f : 1.f, s));
         for (int j = 0; j < iters; ++j) {
+            NvtxRange nvtx_iter("se2 iteration", j);
             // w_i = mu_i / K v_i   (fused: error of the previous v-update, sum |w_i K v_i - mu_i|)
             Epilogue e1;
             e1.op = EPI_DIVIDE;
@@ -614,6 +619,7 @@ se2_status se2_conv_precise(se2_kernel k, const double* in, double* out, int32_t
 se2_status se2_barycenter_precise(se2_kernel k, int32_t n, int32_t nsolve, const float* mus, const double* lambdas,
                                   double* lbary, double* lv_state, double* lw_state, const se2_opts* opts,
                                   double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_barycenter_precise");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
     SE2_CHECK_ARG(n >= 1 && nsolve >= 1, "n, nsolve >= 1");
@@ -674,6 +680,7 @@ se2_status se2_barycenter_precise(se2_kernel k, int32_t n, int32_t nsolve, const
         if (!warm) SE2_CUDA_TRY(launch_fill_f64(v, FN, 0.0, s));
         SE2_CUDA_TRY(launch_fill_f64(w, FN, 0.0, s));
         for (int j = 0; j < iters; ++j) {
+            NvtxRange nvtx_iter("se2 iteration", j);
             EpiP e1;   // w_i = mu_i / K v_i  (error of the previous v-update fused)
             e1.op = EPI_DIVIDE;
             e1.target = lmu;
@@ -738,6 +745,7 @@ se2_status se2_barycenter_precise(se2_kernel k, int32_t n, int32_t nsolve, const
 
 se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, const float* mu, int32_t batch,
                               uint32_t flags, double* err_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_marginal_error");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(a && b && mu && err_host, "null pointer");
     SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");
@@ -766,6 +774,7 @@ se2_status se2_marginal_error(se2_kernel k, const float* a, const float* b, cons
 
 se2_status se2_transport_cost(se2_kernel k, const float* a, const float* b, int32_t batch, uint32_t flags,
                               double* cost_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_transport_cost");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(a && b && cost_host, "null pointer");
     SE2_CHECK_ARG(batch >= 1 && batch <= k->max_batch, "batch out of range [1, max_batch]");

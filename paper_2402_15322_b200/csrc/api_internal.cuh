@@ -4,15 +4,46 @@
 #pragma once
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX 3 (resolves the tool's injection library with dlopen)
+
 #include "se2_internal.cuh"
 
 extern "C" int64_t se2_launch_count(void);
+
+// NVTX ranges (SURVEY §5 "tracing"): one per C-ABI solve, per scaling iteration and per conv, pushed only
+// when the process runs with SE2_NVTX=1 (read once) so the default hot loops do no extra host work.
+inline bool se2_nvtx_on() {
+    static const bool on = [] {
+        const char* e = getenv("SE2_NVTX");
+        return e && e[0] && e[0] != '0';
+    }();
+    return on;
+}
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const char* name) : on(se2_nvtx_on()) {
+        if (on) nvtxRangePushA(name);
+    }
+    NvtxRange(const char* name, int index) : on(se2_nvtx_on()) {
+        if (on) {
+            char buf[64];
+            snprintf(buf, sizeof buf, "%s %d", name, index);
+            nvtxRangePushA(buf);
+        }
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace se2;
 
@@ -83,6 +114,7 @@ static se2_status ensure(Workspace& w, size_t bytes, KernelExtra* owner = nullpt
 static se2_status run_conv(se2_kernel_s* k, const float* in, int batch, uint32_t flags, const Epilogue& epi_in,
                            cudaStream_t s, int* bpf) {
     const bool log_domain = (flags & SE2_LOG_DOMAIN) != 0;
+    NvtxRange nvtx_conv(log_domain ? "se2 conv (log domain)" : "se2 conv (linear)");
     Epilogue epi = epi_in;
     epi.guard = k->guard;   // every conv epilogue counts its guarded divisions / prox failures
     if (k->win_hi > 0 && epi.slab_hi == 0) {   // output window: rows outside are input-only halo rows
@@ -226,6 +258,7 @@ static se2_status reset_guard(se2_kernel_s* k, cudaStream_t s) {
 
 // one fp64-potential log conv (K4P) with the kernel's optional per-launch timing events
 static se2_status run_conv_precise(se2_kernel_s* k, const double* in, int batch, const EpiP& epi, cudaStream_t s) {
+    NvtxRange nvtx_conv("se2 conv (log domain, fp64 potentials)");
     Timing& t = k->timing;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (t.on) {

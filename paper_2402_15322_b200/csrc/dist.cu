@@ -566,6 +566,7 @@ se2_status se2_comm_allreduce(se2_comm c, void* buf, int64_t count, int32_t f64,
 se2_status se2_jko_step_dist(se2_kernel k, const se2_dist* dist, const float* mu_k, float* mu_next, float* a, float* b,
                              const se2_prox* prox, const se2_opts* opts, double* mass_host, double* err_trace_host,
                              se2_stream stream) {
+    NvtxRange nvtx_call("se2_jko_step_dist");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(dist != nullptr, "dist required (se2_jko_step for one GPU)");
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 1, "opts required, iters >= 1");
@@ -624,6 +625,7 @@ se2_status se2_jko_step_dist(se2_kernel k, const se2_dist* dist, const float* mu
         SE2_CUDA_TRY(launch_fill(b, N, LOG ? 0.f : 1.f, s));
         if (sl.on) SE2_CUDA_TRY(launch_fill(mu_next, N, 0.f, s));   // its halo rows are never written
         for (int l = 0; l < iters; ++l) {
+            NvtxRange nvtx_iter("se2 iteration", l);
             Epilogue e1;   // a = mu / K b, owned rows; error of the previous iterate fused
             e1.op = EPI_DIVIDE;
             e1.target = tmu;
@@ -700,6 +702,7 @@ se2_status se2_jko_step_dist(se2_kernel k, const se2_dist* dist, const float* mu
 se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve, const float* mus,
                                const double* lambdas, float* bary, float* v_state, float* w_state, const se2_opts* opts,
                                double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_barycenter_dist");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(dist != nullptr, "dist required (se2_barycenter for one GPU)");
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
@@ -776,6 +779,7 @@ se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, in
             if (st != SE2_OK) return st;
         }
         for (int j = 0; j < iters; ++j) {
+            NvtxRange nvtx_iter("se2 iteration", j);
             Epilogue e1;   // w_i = mu_i / K v_i
             e1.op = EPI_DIVIDE;
             e1.target = lmu_rep;
@@ -860,6 +864,7 @@ se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, in
 se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32_t n, int32_t nsolve, const float* mus,
                                        const double* lambdas, double* lbary, double* lv_state, double* lw_state,
                                        const se2_opts* opts, double* err_trace_host, se2_stream stream) {
+    NvtxRange nvtx_call("se2_barycenter_precise_dist");
     if (check_kernel(k) != SE2_OK) return SE2_EINVAL;
     SE2_CHECK_ARG(dist != nullptr, "dist required (se2_barycenter_precise for one GPU)");
     SE2_CHECK_ARG(opts != nullptr && opts->iters >= 0, "opts required");
@@ -931,6 +936,7 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
             if (st != SE2_OK) return st;
         }
         for (int j = 0; j < iters; ++j) {
+            NvtxRange nvtx_iter("se2 iteration", j);
             EpiP e1;   // w_i = mu_i / K v_i  (error of the previous v-update fused)
             e1.op = EPI_DIVIDE;
             e1.target = lmu;

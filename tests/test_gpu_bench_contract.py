@@ -20,8 +20,9 @@ def _run(args):
     return json.loads(lines[0])
 
 
-def test_bench_line_contract(cuda_device):
-    d = _run(["--steps", "1", "--warmup", "3", "--no-configs", "--no-cpu-baseline"])
+def test_bench_line_contract(cuda_device, tmp_path):
+    man = tmp_path / "manifest.jsonl"
+    d = _run(["--steps", "1", "--warmup", "3", "--no-configs", "--no-cpu-baseline", "--manifest", str(man)])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
                 "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert key in d, key
@@ -33,6 +34,11 @@ def test_bench_line_contract(cuda_device):
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # the run manifest: one JSON line with the seeded inputs' and the library's SHA-256 and the same numbers
+    (m,) = [json.loads(l) for l in man.read_text().splitlines()]
+    assert m["value"] == d["value"] and m["config"]["name"] == "c4" and m["seeds"] == {"mu[0]": 4000}
+    assert len(m["input_sha256"]["mu[0]"]) == 64 and len(m["libse2ot_sha256"]) == 64
+    assert m["gpu"]["sms"] > 0 and m["clocks"]["sm_mhz"] == d["clocks"]["sm_mhz"]
 
 
 def test_bench_reference_arm_contract(cuda_device):
