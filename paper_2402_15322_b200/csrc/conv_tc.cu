@@ -138,6 +138,15 @@ TcGeom tc_geom(const se2_kernel_s* k) {
 // writes are visible (a no-op for a normally launched kernel)
 __device__ __forceinline__ void tc_grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// One lane of a converged warp, chosen with elect.sync: ptxas then knows a single thread runs the role's
+// code and emits bare UTCHMMA / UTMALDG / UTCBAR instructions; under `lane == 0` it wraps every one of
+// them in its own ELECT / branch loop (6 SASS per MMA on the issue path).
+__device__ __forceinline__ bool tc_elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    return e != 0;
+}
+
 __device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
@@ -170,12 +179,13 @@ __device__ __forceinline__ void tc_mma_col(uint32_t tc, uint32_t tm, uint64_t ah
 // two consecutive filter columns (a 2-column stage of a K = 16 window): the second column's operands are
 // ah + ae (next column's weights) and bh - 1 (the input row shifted by one pixel = 16 B)
 __device__ __forceinline__ void tc_mma_col2(uint32_t tc, uint32_t tm, uint64_t ah, uint64_t bh, uint64_t ae,
-                                            uint64_t alo, uint64_t blo, uint32_t idesc, uint32_t accc, uint32_t accm) {
+                                            uint64_t alo, uint64_t blo, uint32_t idesc, uint32_t accc, uint32_t accm,
+                                            uint64_t bstep) {
     asm volatile(
         "{\n\t.reg .pred pc, pm, pt;\n\t.reg .b64 al, bl, a2, b2, al2, bl2;\n\t"
         "setp.ne.b32 pc, %8, 0;\n\tsetp.ne.b32 pm, %9, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
         "add.s64 bl, %3, %7;\n\tadd.s64 al, %2, %6;\n\t"
-        "add.s64 a2, %2, %5;\n\tsub.s64 b2, %3, 1;\n\t"
+        "add.s64 a2, %2, %5;\n\tsub.s64 b2, %3, %10;\n\t"
         "add.s64 bl2, b2, %7;\n\tadd.s64 al2, a2, %6;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, bl, %4, pc;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %3, %4, pm;\n\t"
@@ -183,7 +193,7 @@ __device__ __forceinline__ void tc_mma_col2(uint32_t tc, uint32_t tm, uint64_t a
         "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, bl2, %4, pt;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%1], a2, b2, %4, pt;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], al2, b2, %4, pt;\n\t}"
-        ::"r"(tc), "r"(tm), "l"(ah), "l"(bh), "r"(idesc), "l"(ae), "l"(alo), "l"(blo), "r"(accc), "r"(accm));
+        ::"r"(tc), "r"(tm), "l"(ah), "l"(bh), "r"(idesc), "l"(ae), "l"(alo), "l"(blo), "r"(accc), "r"(accm), "l"(bstep));
 }
 __device__ __forceinline__ void tc_commit_u32(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -216,6 +226,8 @@ struct TcArgs {
     int na;                    // weight-ring stages
     int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
+    int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N
+    uint32_t a_tx;             // bytes one weight-stage TMA box delivers (kTcAStage; halved by a timing diagnostic)
     int tmem_cols;
     int rows_out;              // output rows a CTA owns (<= kr; the M tile's remaining rows are discarded)
     int y_lo, y_hi;            // output window (kernel's win_lo / win_hi): rows outside are input-only halos
@@ -460,7 +472,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
     const size_t row_elems = (size_t)a.nch * a.nxp * 8;               // one (b, y) row of the split input
     const uint32_t chunk_bytes_b = (uint32_t)a.nxp * 16;
     if (warp == 0) {
-      if (lane == 0) {
+      if (tc_elect_one()) {
         // ---------------- producer ----------------
         // global input-row counter gr (all pieces of this CTA): B ring stage gr & 1, weight stage (gr S + dxi)
         auto load_b = [&](int gr, const TcPiece& pc, int nwl, int yi) {
@@ -485,7 +497,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             const int st = pst;
             if (prnd > 0) tc_wait(&emptyA[st], (uint32_t)((prnd - 1) & 1));
             if (++pst == a.na) { pst = 0; ++prnd; }
-            mbar_expect_tx(&fullA[st], kTcAStage);
+            mbar_expect_tx(&fullA[st], a.a_tx);
             const int j0 = pc.y0 + a.R - yi + a.kr - 1;
             const bool n2 = a.nar && nwl == 2;   // the narrow window of the narrow geometry (second map)
             tma_load_5d(sA_u + (uint32_t)st * a.a_stage, n2 ? (const void*)&wmapn : (const void*)&wmap,
@@ -532,9 +544,9 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
       }
       __syncwarp();
     } else if (warp == 1) {
-      if (lane == 0) {
+      if (tc_elect_one()) {
         // ---------------- MMA issuer ----------------
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(a.npad >> 3) << 17) |
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(((a.diag & 2) ? a.npad / 2 : a.npad) >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
         const uint64_t dA0 = tc_desc(smem_u32(sA), 2048, 128);
         const uint64_t dB0 = tc_desc(smem_u32(sB), chunk_bytes_b, 128);
@@ -547,6 +559,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
         // well ahead of the 128-cycle MMAs.  Stage layout [hl][column e < 4 / nwa][chunk nwa][2 KB].
         const uint64_t aLo = kTcAStage / 2 / 16, aK = 2 * 2048 / 16, bK = 2 * chunk_bytes_b / 16;
         int ist = 0, irnd = 0;   // ring slot and round of the next weight stage to consume
+        const uint64_t bstep = (a.diag & 1) ? 0 : 1;   // descriptor step of one pixel (16 B)
 
         // corrections (hi.lo + lo.hi) of one filter column
         auto issue_corr = [&](uint64_t dAh, uint64_t dBh, uint64_t bLo, int ksteps) {
@@ -604,24 +617,24 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
                     const int nv = min(tc_cols(nwa), a.S - dxi);               // its filter columns
                     // a narrow tile on a stage prefetched with the wide window reads the middle chunks
                     const uint64_t dAh = dA0 + (uint64_t)((st * a.a_stage + (nwa > nwl ? 2048u : 0u)) >> 4);
-                    const uint64_t dBh = dB0 + (uint64_t)((stb * a.b_stage + (kTcPadX + a.R - dxi) * 16) >> 4);
+                    const uint64_t dBh = dB0 + (uint64_t)((stb * a.b_stage + (bstep ? kTcPadX + a.R - dxi : kTcPadX) * 16) >> 4);
                     const uint64_t aE = (uint64_t)nwa * 2048 / 16;             // next filter column's weights
                     const uint32_t first = (!restart || dxi > 0) ? 1u : 0u;     // enable-input of the chain's first main MMA
                     if (early) {
-                        for (int e = 0; e < nv; ++e) issue_corr(dAh + e * aE, dBh - e, bLo, ksteps);
+                        for (int e = 0; e < nv; ++e) issue_corr(dAh + e * aE, dBh - e * bstep, bLo, ksteps);
                         tc_wait(&flushed, (uint32_t)((gs - 1) & 1));
                         asm volatile("tcgen05.fence::after_thread_sync;");
-                        for (int e = 0; e < nv; ++e) issue_main(dAh + e * aE, dBh - e, ksteps, (dxi + e) ? 1u : 0u);
+                        for (int e = 0; e < nv; ++e) issue_main(dAh + e * aE, dBh - e * bstep, ksteps, (dxi + e) ? 1u : 0u);
                         early = false;
                     } else if (ksteps == 1) {   // K = 16 windows: two filter columns per asm block
                         int e = 0;
                         for (; e + 1 < nv; e += 2) {
-                            tc_mma_col2(tcor, tmem, dAh + e * aE, dBh - e, aE, aLo, bLo, idesc, acc_c, e ? 1u : first);
+                            tc_mma_col2(tcor, tmem, dAh + e * aE, dBh - e * bstep, aE, aLo, bLo, idesc, acc_c, e ? 1u : first, bstep);
                             acc_c = 1;
                         }
-                        if (e < nv) issue_both(dAh + e * aE, dBh - e, bLo, 1, e ? 1u : first);
+                        if (e < nv) issue_both(dAh + e * aE, dBh - e * bstep, bLo, 1, e ? 1u : first);
                     } else {
-                        for (int e = 0; e < nv; ++e) issue_both(dAh + e * aE, dBh - e, bLo, ksteps, e ? 1u : first);
+                        for (int e = 0; e < nv; ++e) issue_both(dAh + e * aE, dBh - e * bstep, bLo, ksteps, e ? 1u : first);
                     }
                     tc_commit_u32(emptyA_u + 8u * (uint32_t)st);
                     dxi += nv;
@@ -887,7 +900,10 @@ static cudaError_t tc_weight_map(const se2_kernel_s* k, void* w, int nbox, void*
                                  (uint64_t)g.nwin * g.nj * g.kb * 8 * 2, (uint64_t)wk_hl * 2};
     // 8 / nbox filter columns per box (past the block's last column the box reads the next block's first
     // columns or zero fill, never used)
-    const uint32_t box[5] = {(uint32_t)g.kb * 8, (uint32_t)g.kr, (uint32_t)nbox, (uint32_t)tc_cols(nbox), 2};
+    // SE2_TC_DIAG_HALFW (timing diagnostic, wrong results): half the weight rows per stage -- does the weight
+    // stream (L2 -> shared memory, 2.7 KB per MMA) cost MMA time?
+    static const bool halfw = getenv("SE2_TC_DIAG_HALFW") != nullptr;
+    const uint32_t box[5] = {(uint32_t)g.kb * 8, (uint32_t)(halfw ? g.kr / 2 : g.kr), (uint32_t)nbox, (uint32_t)tc_cols(nbox), 2};
     if (!make_tmap_5d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w, dims, strides, box)) {
         delete m;
         return cudaErrorInvalidValue;
@@ -1083,6 +1099,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.kb = g.kb;
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
+    a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0);
+    a.a_tx = getenv("SE2_TC_DIAG_HALFW") ? kTcAStage / 2 : kTcAStage;
     a.tmem_cols = g.tmem_cols;
     a.y_lo = k->wlo();
     a.y_hi = k->whi();
