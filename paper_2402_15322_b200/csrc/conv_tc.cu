@@ -226,7 +226,7 @@ struct TcArgs {
     int na;                    // weight-ring stages
     int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
-    int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N
+    int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N, bit 2 = no weight loads after the first ring fill
     uint32_t a_tx;             // bytes one weight-stage TMA box delivers (kTcAStage; halved by a timing diagnostic)
     int tmem_cols;
     int rows_out;              // output rows a CTA owns (<= kr; the M tile's remaining rows are discarded)
@@ -497,6 +497,10 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             const int st = pst;
             if (prnd > 0) tc_wait(&emptyA[st], (uint32_t)((prnd - 1) & 1));
             if (++pst == a.na) { pst = 0; ++prnd; }
+            if ((a.diag & 4) && t >= a.na) {   // timing diagnostic: no weight traffic after the first ring fill
+                mbar_expect_tx(&fullA[st], 0);
+                return;
+            }
             mbar_expect_tx(&fullA[st], a.a_tx);
             const int j0 = pc.y0 + a.R - yi + a.kr - 1;
             const bool n2 = a.nar && nwl == 2;   // the narrow window of the narrow geometry (second map)
@@ -586,19 +590,26 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
         const int b_after = min((a.na - 1) * tc_cols(a.nwin), a.S - 1);
         const int npre = (b_after + tc_cols(a.nwin) - 1) / tc_cols(a.nwin);
         tc_wait(&flagbar, 0);
+        // SE2_TC_DIAG_PROF: cycles the issuer spends in total and waiting on its barriers (cnt[2..6])
+        const bool prof = (a.diag & 8) != 0 && a.cnt != nullptr;
+        long long pt0 = prof ? clock64() : 0, pwA = 0, pwB = 0, pwF = 0, ptmp = 0;
         TcPiece pc;
         int gr = 0, gs = 0, t = 0;   // input rows, main-accumulator chains and weight stages issued so far
         for (int k = 0; tc_piece<PIECES>(a, k, pc); ++k) {
             nwl = sNwl[k];
             const int fr = tc_chain_rows(nwl, a.chain16);   // input rows per main-accumulator chain (power of 2)
             if (k > 0) {   // the correction accumulator restarts per piece: the previous piece's was read
+                if (prof) ptmp = clock64();
                 tc_wait(&cflushed, (uint32_t)((k - 1) & 1));
+                if (prof) pwF += clock64() - ptmp;
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 acc_c = 0;
             }
             for (int rr = pc.r0; rr < pc.r1; ++rr, ++gr) {
                 const int stb = gr & 1;
+                if (prof) ptmp = clock64();
                 tc_wait(&fullB[stb], (uint32_t)((gr >> 1) & 1));
+                if (prof) pwB += clock64() - ptmp;
                 // The main accumulator restarts every fr input rows of a piece and the accumulator warps
                 // must first have read the previous chain's sums: the correction MMAs of the row's first
                 // stage are issued before that wait so the tensor pipe stays busy.
@@ -610,7 +621,9 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
                 const uint64_t bLo = (uint64_t)nwl * chunk_bytes_b / 16;
                 for (int dxi = 0; dxi < a.S; ++t) {
                     const int st = ist;
+                    if (prof) ptmp = clock64();
                     tc_wait(&fullA[st], (uint32_t)(irnd & 1));
+                    if (prof) pwA += clock64() - ptmp;
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     if (++ist == a.na) { ist = 0; ++irnd; }
                     const int nwa = t < npre ? a.nwin : nwl;                    // chunks loaded into the stage
@@ -622,7 +635,9 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
                     const uint32_t first = (!restart || dxi > 0) ? 1u : 0u;     // enable-input of the chain's first main MMA
                     if (early) {
                         for (int e = 0; e < nv; ++e) issue_corr(dAh + e * aE, dBh - e * bstep, bLo, ksteps);
+                        if (prof) ptmp = clock64();
                         tc_wait(&flushed, (uint32_t)((gs - 1) & 1));
+                        if (prof) pwF += clock64() - ptmp;
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         for (int e = 0; e < nv; ++e) issue_main(dAh + e * aE, dBh - e * bstep, ksteps, (dxi + e) ? 1u : 0u);
                         early = false;
@@ -644,6 +659,13 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
                 tc_commit(&rowdone[gr % kTcMaxFlushRows]);
                 if (((rr - pc.r0) & (fr - 1)) == fr - 1 || rr == pc.r1 - 1) ++gs;   // chain end
             }
+        }
+        if (prof) {
+            atomicAdd(&a.cnt[2], (unsigned long long)(clock64() - pt0));
+            atomicAdd(&a.cnt[3], (unsigned long long)pwA);
+            atomicAdd(&a.cnt[4], (unsigned long long)pwB);
+            atomicAdd(&a.cnt[5], (unsigned long long)pwF);
+            atomicAdd(&a.cnt[6], 1ull);
         }
       }
       __syncwarp();
@@ -994,8 +1016,8 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_stats, (size_t)k->max_batch * k->ny * g.nch * sizeof(float2));
-    if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
     k->tc_w_hl = wk_hl;
     k->tc_x_hl = xk_hl;
@@ -1039,12 +1061,15 @@ void conv_tc_release(se2_kernel_s* k) {
 }
 
 cudaError_t conv_tc_tile_counts(const se2_kernel_s* k, int64_t* tiles, int64_t* wide, bool reset) {
-    unsigned long long h[2] = {0, 0};
+    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (k->tc_cnt != nullptr) {
         cudaError_t e = cudaMemcpy(h, k->tc_cnt, sizeof(h), cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && reset) e = cudaMemset(k->tc_cnt, 0, sizeof(h));
         if (e != cudaSuccess) return e;
     }
+    if (getenv("SE2_TC_DIAG_PROF") && h[6] > 0)   // issuer cycle profile (timing diagnostic), mean per CTA
+        fprintf(stderr, "K10 issuer per CTA: %.0f cycles in its loop; waiting on weights %.0f, input rows %.0f, flushes %.0f (%llu CTAs)\n",
+                (double)h[2] / h[6], (double)h[3] / h[6], (double)h[4] / h[6], (double)h[5] / h[6], h[6]);
     *tiles = (int64_t)h[0];
     *wide = (int64_t)h[1];
     return cudaSuccess;
@@ -1099,7 +1124,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.kb = g.kb;
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
-    a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0);
+    a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0) |
+             (getenv("SE2_TC_DIAG_NOWLOAD") ? 4 : 0) | (getenv("SE2_TC_DIAG_PROF") ? 8 : 0);
     a.a_tx = getenv("SE2_TC_DIAG_HALFW") ? kTcAStage / 2 : kTcAStage;
     a.tmem_cols = g.tmem_cols;
     a.y_lo = k->wlo();
