@@ -216,6 +216,13 @@ class SlabJKO:
         self.p2p = exchange == "p2p"
         if exchange not in ("nccl", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
+        if self.world > 1 and R > 0:
+            # a slab thinner than the halo would send rows it does not own (x[:, R:2R] reaches into its own
+            # bottom halo): every rank must own at least R rows
+            rows_all = [None] * self.world
+            dist.all_gather_object(rows_all, int(rows), group=group)
+            if min(rows_all) < R:
+                raise ValueError(f"slab decomposition needs >= R = {R} rows per rank, got {rows_all}")
         if self.p2p:
             self._setup_p2p()
         else:

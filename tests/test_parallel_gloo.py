@@ -188,6 +188,36 @@ def test_slab_jko_gloo():
     assert rel < 1e-10 and dmass < 1e-12, (rel, dmass)
 
 
+def _thin_slab_worker(rank, world, port, q):
+    """4 ranks on 6 rows with R = 2: ranks own 2, 2, 1, 1 rows -- thinner than the halo, rejected on every rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny, nt, R = 8, 6, 4, 2
+        g = O.Grid(nx, ny, nt)
+        T = O.kernel_table(g, R, 0.05, (1, 3, 1))
+        mu = np.full(g.shape, 1.0 / (nx * ny * nt))
+        r0, r1 = partition(ny, world, rank)
+        ops = OracleOps(T, None, False, eps=0.05, global_ny=ny, nx=nx)
+        try:
+            SlabJKO(ops, torch.from_numpy(mu[:, r0:r1].copy()), R, prox=(0.02, r0 - R))
+            msg = "accepted"
+        except ValueError as e:
+            msg = str(e)
+        msgs = [None] * world
+        dist.all_gather_object(msgs, msg)
+        if rank == 0:
+            q.put(msgs)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_jko_rejects_slabs_thinner_than_the_halo_gloo():
+    msgs = _run(_thin_slab_worker, world=4)
+    assert all("rows per rank" in m for m in msgs), msgs
+
+
 def _empty_rank_worker(rank, world, port, q):
     """3 ranks, 2 inputs: rank 2 owns none and still takes part in the allreduce."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
