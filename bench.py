@@ -740,6 +740,11 @@ def run_gpu(args):
             out["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": threads, "kind": "oracle",
                                    "sample": desc + " (a PROJECTION of one inner iteration from that timed sample)"}
         print(json.dumps(out), flush=True)
+        if args.manifest:
+            try:
+                write_manifest(args.manifest, args, cfg, d, out)
+            except Exception as exc:  # the manifest is a log: it never fails the bench line
+                print(f"manifest not written: {type(exc).__name__}: {exc}", file=sys.stderr)
     return 0
 
 

@@ -406,7 +406,8 @@ SE2_API se2_status se2_log(const float* x, float* y, int64_t n, se2_stream strea
  *   torch.distributed).  NCCL is resolved at run time (dlopen libnccl.so.2; the build torch loaded is
  *   reused).  Errors: SE2_ENCCL (no NCCL).
  * se2_comm_init -- communicator of nranks ranks on `device` (ncclCommInitRank; nranks = 1 needs no id
- *   and no NCCL).  se2_comm_init_loopback -- nranks communicators in ONE process on one device (out
+ *   and no NCCL -- given an id it still builds a one-rank NCCL communicator and the solvers run their
+ *   collectives on it: the NCCL transport on one GPU).  se2_comm_init_loopback -- nranks communicators in ONE process on one device (out
  *   [nranks]), each to be driven by its own host thread: the exchanges are device copies / reductions
  *   ordered by CUDA events and host rendezvous (no kernel waits on another rank's kernel) -- the test
  *   transport of the multi-rank logic on one GPU.

@@ -142,6 +142,9 @@ __global__ void sum_ranks_kernel(const T* const* __restrict__ in, int n, int64_t
 struct se2_comm_s {
     int n = 1, r = 0, device = 0;
     bool capturable = true;   // the exchanges can be recorded into a CUDA graph
+    // the solvers run their collectives on this communicator: more than one rank, or a one-rank NCCL
+    // communicator built from a unique id (the NCCL transport exercised on one GPU)
+    bool live = false;
     virtual ~se2_comm_s() {}
     // in-place sum over the ranks (f64: doubles, else floats), identical result on every rank
     virtual se2_status allreduce(void* buf, int64_t count, bool f64, cudaStream_t s) = 0;
@@ -160,7 +163,7 @@ struct NcclComm final : se2_comm_s {
         if (c && nccl().loaded) nccl().CommDestroy(c);
     }
     se2_status allreduce(void* buf, int64_t count, bool f64, cudaStream_t s) override {
-        if (n == 1 || count == 0) return SE2_OK;
+        if (c == nullptr || count == 0) return SE2_OK;
         SE2_NCCL_TRY(nccl().AllReduce(buf, buf, (size_t)count, f64 ? ncclFloat64 : ncclFloat32, ncclSum, c, s));
         return SE2_OK;
     }
@@ -195,6 +198,7 @@ struct NcclComm final : se2_comm_s {
         m->n = cnt;
         m->r = me;
         m->device = device;
+        m->live = true;
         *out = m;
         return SE2_OK;
     }
@@ -345,6 +349,7 @@ struct LoopComm final : se2_comm_s {
         std::sort(members.begin(), members.end());
         auto* m = new LoopComm();
         m->n = (int)members.size();
+        m->live = m->n > 1;
         for (int i = 0; i < m->n; ++i)
             if (members[i].second == r) m->r = i;
         m->device = device;
@@ -459,10 +464,10 @@ se2_status exchange(se2_kernel_s* k, const Slab& sl, se2_comm_s* c, float* x, in
 }
 
 bool any_multi(const se2_dist* d) {
-    return (d->slabs && d->slabs->n > 1) || (d->reduce && d->reduce->n > 1);
+    return (d->slabs && d->slabs->n > 1) || (d->reduce && d->reduce->live);
 }
 bool all_capturable(const se2_dist* d) {
-    return (!d->slabs || d->slabs->n == 1 || d->slabs->capturable) && (!d->reduce || d->reduce->n == 1 || d->reduce->capturable);
+    return (!d->slabs || d->slabs->n == 1 || d->slabs->capturable) && (!d->reduce || !d->reduce->live || d->reduce->capturable);
 }
 
 }  // namespace
@@ -493,8 +498,8 @@ se2_status se2_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_
     c->n = nranks;
     c->r = rank;
     c->device = device;
-    if (nranks > 1) {
-        SE2_CHECK_ARG(id != nullptr, "null unique id");
+    SE2_CHECK_ARG(nranks == 1 || id != nullptr, "null unique id");
+    if (id != nullptr) {   // nranks = 1 with an id: a real one-rank NCCL communicator
         Nccl& n = nccl();
         if (!n.loaded) {
             delete c;
@@ -510,6 +515,7 @@ se2_status se2_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_
             set_error(std::string("ncclCommInitRank: ") + n.GetErrorString(r));
             return SE2_ENCCL;
         }
+        c->live = true;
     }
     *out = c;
     return SE2_OK;
@@ -522,6 +528,7 @@ se2_status se2_comm_init_loopback(int32_t nranks, int32_t device, se2_comm* out)
     for (int r = 0; r < nranks; ++r) {
         auto* c = new LoopComm();
         c->n = nranks;
+        c->live = nranks > 1;
         c->r = r;
         c->device = device;
         c->w = w;
@@ -533,7 +540,7 @@ se2_status se2_comm_init_loopback(int32_t nranks, int32_t device, se2_comm* out)
 se2_status se2_comm_split(se2_comm parent, int32_t color, int32_t key, se2_comm* out) {
     SE2_CHECK_ARG(parent != nullptr && out != nullptr && color >= 0, "bad arguments");
     *out = nullptr;
-    if (parent->n == 1) {
+    if (parent->n == 1 && !parent->live) {
         auto* c = new NcclComm();   // a single rank: no transport needed
         c->device = parent->device;
         *out = c;
@@ -760,7 +767,7 @@ se2_status se2_barycenter_dist(se2_kernel k, const se2_dist* dist, int32_t n, in
     for (int i = 0; i < F; ++i) lamf[i] = (float)lambdas[i];
     SE2_CUDA_TRY(cudaMemcpyAsync(lam_dev, lamf.data(), sizeof(float) * F, cudaMemcpyHostToDevice, s));
     SE2_CUDA_TRY(cudaStreamSynchronize(s));
-    const bool reduce = rc != nullptr && rc->n > 1;
+    const bool reduce = rc != nullptr && rc->live;
     std::vector<uint64_t> key = {4, as_key(mus), as_key(bary), as_key(v), as_key(w), (uint64_t)n, (uint64_t)nsolve,
                                  (uint64_t)iters, (uint64_t)opts->flags, (uint64_t)trace, as_key(x->ws.ptr),
                                  as_key(x->misc.ptr), as_key(partial), as_key(tr), (uint64_t)sl.lo, (uint64_t)sl.hi};
@@ -885,7 +892,7 @@ se2_status se2_barycenter_precise_dist(se2_kernel k, const se2_dist* dist, int32
     if (st != SE2_OK) return st;
     se2_comm_s* sc = dist->slabs;
     se2_comm_s* rc = dist->reduce;
-    const bool reduce = rc != nullptr && rc->n > 1;
+    const bool reduce = rc != nullptr && rc->live;
     const bool trace = (opts->flags & SE2_TRACE_ERR) != 0 && err_trace_host != nullptr;
     const int64_t N = k->N();
     const int F = n * nsolve;

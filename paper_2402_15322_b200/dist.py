@@ -58,6 +58,16 @@ class Comm:
         return cls(h)
 
     @classmethod
+    def nccl_one_rank(cls, device: int = 0) -> "Comm":
+        """A REAL one-rank NCCL communicator (unique id + ncclCommInitRank): the solvers run their collectives
+        on it, so the NCCL transport can be exercised on one GPU."""
+        buf = ctypes.create_string_buffer(128)
+        check(L.load().se2_comm_unique_id(buf))
+        h = ctypes.c_void_p()
+        check(L.load().se2_comm_init(bytes(buf.raw), 1, 0, int(device), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
     def loopback(cls, nranks: int, device: int = 0) -> List["Comm"]:
         arr = (ctypes.c_void_p * nranks)()
         check(L.load().se2_comm_init_loopback(int(nranks), int(device), arr))

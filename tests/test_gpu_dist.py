@@ -263,3 +263,45 @@ def test_conv_output_window(engine, cuda_device):
         assert np.max(np.abs(got[:, :, lo:hi] - ref[:, :, lo:hi])) < 1e-4
     else:
         assert np.max(np.abs(got[:, :, lo:hi] / ref[:, :, lo:hi] - 1)) < 3e-5
+
+
+def test_nccl_transport_one_rank(cuda_device):
+    """The NCCL transport itself on one GPU: a REAL one-rank NCCL communicator (ncclGetUniqueId +
+    ncclCommInitRank through the dlopen'ed entry points), its allreduce (fp32 / fp64: a one-rank sum is the
+    identity), ncclCommSplit, and the sharded barycenter solvers running their per-iteration log-mean
+    allreduce on it -- inside the CUDA graph of a small solve too.  The multi-rank exchange logic is the
+    loopback tests'; this pins the NCCL calls (symbols, datatypes, stream, in-place buffers, capture)."""
+    from paper_2402_15322_b200 import Kernel, se2_barycenter, se2_barycenter_precise
+    from paper_2402_15322_b200.dist import Comm, Dist, se2_barycenter_dist, se2_barycenter_precise_dist
+    comm = Comm.nccl_one_rank(0)
+    assert (comm.nranks, comm.rank) == (1, 0)
+    x32 = torch.arange(100003, dtype=torch.float32, device="cuda") * 0.25
+    x64 = torch.arange(4099, dtype=torch.float64, device="cuda") / 3.0
+    r32, r64 = x32.clone(), x64.clone()
+    comm.allreduce_(x32)
+    comm.allreduce_(x64)
+    torch.cuda.synchronize()
+    assert torch.equal(x32, r32) and torch.equal(x64, r64)
+    sub = comm.split(0, 0)
+    assert (sub.nranks, sub.rank) == (1, 0)
+    sub.allreduce_(x32)
+    torch.cuda.synchronize()
+    assert torch.equal(x32, r32)
+    pc = S.get_parity_case("c1")
+    cfg, d = S.parity_inputs(pc)
+    lams = np.stack(d["lambdas"])
+    k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=10)
+    mus = _dev(np.stack(d["mus"]))
+    # the allreduce path sums partial log-means and then updates (two kernels) where the one-rank path fuses
+    # them: equal up to fp32 rounding of the log-mean, not bit for bit
+    b1, t1 = se2_barycenter(k, mus, lams, 30, True, trace=True)
+    b2, t2 = se2_barycenter_dist(k, Dist(reduce=sub), mus, lams, 30, trace=True)
+    assert measure_err(np.exp(_host(b2)), np.exp(_host(b1))) < 2e-3   # the fp32 potentials' rounding floor (R19)
+    assert trace_err(t2, t1) < 1.0
+    p1, u1 = se2_barycenter_precise(k, mus, lams, 30, trace=True)
+    p2, u2 = se2_barycenter_precise_dist(k, Dist(reduce=comm), mus, lams, 30, trace=True)
+    assert potential_err(_host(p2), _host(p1)) < 1e-6
+    assert trace_err(u2, u1) < 1.0
+    k.close()
+    sub.close()
+    comm.close()
