@@ -226,6 +226,7 @@ struct TcArgs {
     int na;                    // weight-ring stages
     int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
+    int epi_vec;               // pieces epilogue: 4 outputs per thread with 16-byte loads / stores (tc_epilogue4)
     int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N, bit 2 = no weight loads after the first ring fill
     uint32_t a_tx;             // bytes one weight-stage TMA box delivers (kTcAStage; halved by a timing diagnostic)
     int tmem_cols;
@@ -375,6 +376,63 @@ __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16
         for (int i = 1; i < nw; ++i) { mn = fminf(mn, sMin[i]); mx = fmaxf(mx, sMax[i]); }
         stats[row] = make_float2(mn, mx);
     }
+}
+
+// The same split for rows whose pitch allows 16-byte loads (nx % 4 == 0): one block per (field, row, chunk),
+// one thread per 4 consecutive real pixels -- 8 plane loads of 16 bytes, 4 + 4 stores of 16 bytes; the padding
+// pixels are never written (zero since allocation).  ~4x fewer instructions per element than the scalar
+// kernel, which made that one issue-bound (ncu: issue active 74%, L2 22%).  Bit-identical outputs.
+__global__ void __launch_bounds__(64)
+tc_split_input4_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl, int nx, int ny, int nt,
+                       int nxp, float2* __restrict__ stats) {
+    __shared__ float sMin[2], sMax[2];
+    tc_grid_dep_wait();   // reads the previous kernel's output (launched with PDL)
+    const int nch = nt / 8;
+    const int64_t row = blockIdx.x;   // (b, y, c)
+    const int c = (int)(row % nch);
+    const int64_t by = row / nch;
+    const int y = (int)(by % ny);
+    const int b = (int)(by / ny);
+    const int64_t plane = (int64_t)ny * nx;
+    const float* src = v + (((int64_t)b * nt + c * 8) * ny + y) * nx;
+    float mn = INFINITY, mx = 0.f;
+    for (int x = 4 * threadIdx.x; x < nx; x += 4 * blockDim.x) {
+        float4 f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = *reinterpret_cast<const float4*>(src + e * plane + x);
+        __align__(16) __nv_bfloat16 hi[4][8], lo[4][8];
+        float nanacc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float fe[4] = {f[e].x, f[e].y, f[e].z, f[e].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                mn = fminf(mn, fe[j]);
+                mx = fmaxf(mx, fabsf(fe[j]));
+                nanacc += fe[j] * 0.f;   // NaN (or Inf) anywhere -> NaN
+                const __nv_bfloat16 h = __float2bfloat16_rn(fe[j]);
+                hi[j][e] = h;
+                lo[j][e] = __float2bfloat16_rn(fe[j] - __bfloat162float(h));
+            }
+        }
+        if (nanacc != nanacc) mn = -INFINITY;   // NaN / Inf: never the narrow window
+        const int64_t i = row * nxp + kTcPadX + x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            reinterpret_cast<uint4*>(xk)[i + j] = *reinterpret_cast<const uint4*>(hi[j]);
+            reinterpret_cast<uint4*>(xk + xk_hl)[i + j] = *reinterpret_cast<const uint4*>(lo[j]);
+        }
+    }
+    if (stats == nullptr) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sMin[w] = mn; sMax[w] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) stats[row] = make_float2(fminf(sMin[0], sMin[1]), fmaxf(sMax[0], sMax[1]));
 }
 
 // weight split: Wl[to][ti][S][SP] (fp32) -> hi/lo [blk][dxi][c][j][to_l < kb][8]
@@ -801,6 +859,54 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
 }
 
+// apply_epilogue<false> (conv_common.cuh) for 4 consecutive outputs of one row with 16-byte loads / stores: the
+// same expressions per output and the same order of the error sum, for the ops of the linear solvers (store,
+// divide, multiply, entropic prox) without peer halos.  The scalar form cost ~69 instructions per output and
+// made the pieces epilogue issue-bound (ncu: issue active 62%, L2 32%).
+__device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int ix, int iy, const float (&y)[4],
+                                             float& err) {
+    if (e.err_a != nullptr) {
+        const float4 ao = *reinterpret_cast<const float4*>(e.err_a + idx);
+        const float4 mu = *reinterpret_cast<const float4*>(e.err_mu + idx);
+        err += fabsf(ao.x * y[0] - mu.x);
+        err += fabsf(ao.y * y[1] - mu.y);
+        err += fabsf(ao.z * y[2] - mu.z);
+        err += fabsf(ao.w * y[3] - mu.w);
+    }
+    float o[4];
+    if (e.op == EPI_STORE) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = y[j];
+    } else if (e.op == EPI_PROX) {
+        const float dyp = ((float)iy + 0.5f - e.cy) * e.hy;
+        float s[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float dxp = ((float)(ix + j) + 0.5f - e.cx) * e.hx;
+            const float V = dxp * dxp + dyp * dyp;
+            if (y[j] < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
+            const float z = fmaxf(y[j], kDivFloor);
+            o[j] = exp2f(-e.prox_p * log2f(z) - e.prox_q * V * kLog2e);
+            s[j] = o[j] * z;
+        }
+        if (e.out2 != nullptr) *reinterpret_cast<float4*>(e.out2 + idx) = make_float4(s[0], s[1], s[2], s[3]);
+    } else {
+        const float4 t4 = *reinterpret_cast<const float4*>(e.target + idx);
+        const float t[4] = {t4.x, t4.y, t4.z, t4.w};
+        if (e.op == EPI_DIVIDE) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (y[j] < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
+                o[j] = t[j] / fmaxf(y[j], kDivFloor);
+            }
+        } else {   // EPI_MULTIPLY
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = t[j] * y[j];
+        }
+    }
+    *reinterpret_cast<float4*>(e.out + idx) = make_float4(o[0], o[1], o[2], o[3]);
+}
+
 // balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
 // one block per (kr-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
 __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
@@ -844,6 +950,10 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
         if (r >= a.kr || y >= a.y_hi || x0 >= a.nx) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
         const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+        if (a.epi_vec) {   // nx % 4 == 0, 16-byte aligned fields, a vector op, no peer halos (uniform per launch)
+            tc_epilogue4(epi, rowbase + x0, x0, y, vv, err);
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (x0 + j < a.nx) err += apply_epilogue<false>(epi, rowbase + x0 + j, x0 + j, y, vv[j]);
@@ -1015,6 +1125,9 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
     cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
+    // the padding pixels (x' < kTcPadX, x' >= kTcPadX + nx) are zero: written here once, the 4-pixel split
+    // kernel writes only the real pixels
+    if (e == cudaSuccess) e = cudaMemset(k->tc_x, 0, 2 * xk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_stats, (size_t)k->max_batch * k->ny * g.nch * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 8 * sizeof(unsigned long long));
@@ -1099,9 +1212,16 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     if (!skip_split) {
         // one block per (field, row, chunk), one padded pixel per thread: all 8 plane loads in flight
         const long long rows = (long long)batch * k->ny * g.nch;
-        const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
-        cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
-        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
+        static const bool scalar_split = getenv("SE2_TC_SPLIT1") != nullptr;   // A/B measurements
+        cudaError_t e;
+        if (k->nx % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 && !scalar_split) {
+            cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(64), 0);
+            e = cudaLaunchKernelEx(&c, tc_split_input4_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
+        } else {
+            const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
+            cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
+            e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
+        }
         if (e != cudaSuccess) return e;
         count_launch();
     }
@@ -1124,6 +1244,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.kb = g.kb;
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
+    a.epi_vec = 0;
     a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0) |
              (getenv("SE2_TC_DIAG_NOWLOAD") ? 4 : 0) | (getenv("SE2_TC_DIAG_PROF") ? 8 : 0);
     a.a_tx = getenv("SE2_TC_DIAG_HALFW") ? kTcAStage / 2 : kTcAStage;
@@ -1153,6 +1274,13 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
             if (e != cudaSuccess) return e;
         }
         count_launch();
+        static const bool scalar_epi = getenv("SE2_TC_EPI1") != nullptr;   // A/B measurements
+        auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        const bool vec_op = epi.op == EPI_STORE || epi.op == EPI_DIVIDE || epi.op == EPI_MULTIPLY ||
+                            (epi.op == EPI_PROX && epi.prox_kind != 2);
+        a.epi_vec = (!scalar_epi && vec_op && k->nx % 4 == 0 && epi.halo_up == nullptr && epi.halo_dn == nullptr &&
+                     al16(epi.out) && al16(epi.out2) && al16(epi.target) && al16(epi.err_a) && al16(epi.err_mu))
+                        ? 1 : 0;
         static const bool skip_epi = getenv("SE2_TC_DIAG_SKIP_EPI") != nullptr;   // timing diagnostics only
         if (!skip_epi) {
             cudaLaunchConfig_t c = cfg_of(dim3(a.ngroups, k->nt, batch), dim3(256), 0);
