@@ -378,63 +378,6 @@ __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16
     }
 }
 
-// The same split for rows whose pitch allows 16-byte loads (nx % 4 == 0): one block per (field, row, chunk),
-// one thread per 4 consecutive real pixels -- 8 plane loads of 16 bytes, 4 + 4 stores of 16 bytes; the padding
-// pixels are never written (zero since allocation).  ~4x fewer instructions per element than the scalar
-// kernel, which made that one issue-bound (ncu: issue active 74%, L2 22%).  Bit-identical outputs.
-__global__ void __launch_bounds__(64)
-tc_split_input4_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl, int nx, int ny, int nt,
-                       int nxp, float2* __restrict__ stats) {
-    __shared__ float sMin[2], sMax[2];
-    tc_grid_dep_wait();   // reads the previous kernel's output (launched with PDL)
-    const int nch = nt / 8;
-    const int64_t row = blockIdx.x;   // (b, y, c)
-    const int c = (int)(row % nch);
-    const int64_t by = row / nch;
-    const int y = (int)(by % ny);
-    const int b = (int)(by / ny);
-    const int64_t plane = (int64_t)ny * nx;
-    const float* src = v + (((int64_t)b * nt + c * 8) * ny + y) * nx;
-    float mn = INFINITY, mx = 0.f;
-    for (int x = 4 * threadIdx.x; x < nx; x += 4 * blockDim.x) {
-        float4 f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = *reinterpret_cast<const float4*>(src + e * plane + x);
-        __align__(16) __nv_bfloat16 hi[4][8], lo[4][8];
-        float nanacc = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const float fe[4] = {f[e].x, f[e].y, f[e].z, f[e].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                mn = fminf(mn, fe[j]);
-                mx = fmaxf(mx, fabsf(fe[j]));
-                nanacc += fe[j] * 0.f;   // NaN (or Inf) anywhere -> NaN
-                const __nv_bfloat16 h = __float2bfloat16_rn(fe[j]);
-                hi[j][e] = h;
-                lo[j][e] = __float2bfloat16_rn(fe[j] - __bfloat162float(h));
-            }
-        }
-        if (nanacc != nanacc) mn = -INFINITY;   // NaN / Inf: never the narrow window
-        const int64_t i = row * nxp + kTcPadX + x;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            reinterpret_cast<uint4*>(xk)[i + j] = *reinterpret_cast<const uint4*>(hi[j]);
-            reinterpret_cast<uint4*>(xk + xk_hl)[i + j] = *reinterpret_cast<const uint4*>(lo[j]);
-        }
-    }
-    if (stats == nullptr) return;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { sMin[w] = mn; sMax[w] = mx; }
-    __syncthreads();
-    if (threadIdx.x == 0) stats[row] = make_float2(fminf(sMin[0], sMin[1]), fmaxf(sMax[0], sMax[1]));
-}
-
 // weight split: Wl[to][ti][S][SP] (fp32) -> hi/lo [blk][dxi][c][j][to_l < kb][8]
 __global__ void tc_split_weights_kernel(const float* __restrict__ Wl, __nv_bfloat16* __restrict__ wk, size_t wk_hl,
                                         int nt, int S, int nch, int nwin, int nj, int nblk, int nar) {
@@ -1125,9 +1068,6 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     const size_t xk_hl = (size_t)k->max_batch * k->ny * g.nch * g.nxp * 8;
     cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
-    // the padding pixels (x' < kTcPadX, x' >= kTcPadX + nx) are zero: written here once, the 4-pixel split
-    // kernel writes only the real pixels
-    if (e == cudaSuccess) e = cudaMemset(k->tc_x, 0, 2 * xk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_stats, (size_t)k->max_batch * k->ny * g.nch * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 8 * sizeof(unsigned long long));
@@ -1212,16 +1152,11 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     if (!skip_split) {
         // one block per (field, row, chunk), one padded pixel per thread: all 8 plane loads in flight
         const long long rows = (long long)batch * k->ny * g.nch;
-        static const bool scalar_split = getenv("SE2_TC_SPLIT1") != nullptr;   // A/B measurements
-        cudaError_t e;
-        if (k->nx % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 && !scalar_split) {
-            cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(64), 0);
-            e = cudaLaunchKernelEx(&c, tc_split_input4_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
-        } else {
-            const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
-            cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
-            e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
-        }
+        // (a 4-pixels-per-thread form with 16-byte plane loads measured no faster, 11.9 vs 11.2 us: each of its
+        // store instructions half-fills 32 sectors; this form's stores are fully coalesced)
+        const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
+        cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
+        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
         if (e != cudaSuccess) return e;
         count_launch();
     }
