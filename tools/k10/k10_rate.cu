@@ -1,11 +1,18 @@
 // K10 rate probe (not on the product path): the measured cycles per tcgen05 BF16 MMA of K10's shape and
-// operand layout -- M = 128, N = 256 (or argv N), K = 16, both operands K-major SWIZZLE_NONE from shared
-// memory, A a 2 KB-per-chunk weight tile (SBO 128, LBO 2048), B a padded input row [chunk][x'][8 ti]
-// (SBO 128, LBO = row chunk bytes) read at a pixel-shifted start -- issued by one thread on every SM at
-// once, with no barrier waits in the loop.  This is the per-MMA floor K10's chain can reach.
+// operand layout -- M = 128, N = 256, K = 16, both operands K-major SWIZZLE_NONE from shared memory, A a
+// 2 KB-per-chunk weight tile (SBO 128, LBO 2048), B a padded input row [chunk][x'][8 ti] (SBO 128, LBO =
+// row chunk bytes) read at a pixel-shifted start -- issued by one thread on every SM at once, in K10's
+// column-pair order (corr, main, corr, corr, main, corr into two accumulators).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o k10_rate tools/k10/k10_rate.cu && ./k10_rate
-// modes: 0 = K10's column pair block (corr, main, corr, corr, main, corr: two accumulators)
-//        1 = every MMA into ONE accumulator         2 = alternate two accumulators MMA by MMA
+// Measured on B200 (gpurun_out/r02bf, r02bp-br; profiles/r02_conv_tc_c4.md):
+//   * 128.0 cycles per MMA on 1 SM and on all 148 at once (2.19 PFLOP/s, ~1.81 GHz under that load), with or
+//     without the pixel shift, into one or two accumulators; 64.0 at N = 128; a tcgen05.commit every 6 / 12 /
+//     24 MMAs costs nothing;
+//   * the tensor pipe queues about ONE MMA beyond the running one: an issuer pause of D cycles every 12 MMAs
+//     (the `idle` sweep below) costs D - ~70 cycles of pipe time (D = 128 -> 133.6 cycles per MMA, 256 -> 143.4,
+//     512 -> 162.9, 1024 -> 208.4).  The issuing thread cannot run ahead, so every gap between two of its
+//     UTCHMMAs beyond ~70 cycles is lost -- K10's stage and row boundaries are that loss (its loop keeps the
+//     pipe ~90% busy).
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
@@ -24,10 +31,10 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(a), "l"(b), "r"(idesc));
 }
 
-__global__ void __launch_bounds__(128, 1) k10_rate(int n, int nmma, int mode, int shift, long long* cycles) {
+__global__ void __launch_bounds__(128, 1) k10_rate(int n, int nmma, int mode, int shift, int commit_every, int delay, long long* cycles) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) uint64_t mbar;
+    __shared__ __align__(8) uint64_t mbar, mbar2;
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t a_bytes = 32768, chunk_b = 288 * 16, b_bytes = 4 * chunk_b;   // A: hi/lo x 4 col x 2 chunk x 2 KB; B: hi/lo x 2 chunks
     for (uint32_t i = tid; i < (a_bytes + b_bytes) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u + i;
@@ -37,6 +44,7 @@ __global__ void __launch_bounds__(128, 1) k10_rate(int n, int nmma, int mode, in
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(smem_u32(&mbar2)));   // never completes
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;");
@@ -54,15 +62,25 @@ __global__ void __launch_bounds__(128, 1) k10_rate(int n, int nmma, int mode, in
         for (int i = 0; i < nmma; i += 6) {
             const int e = (i / 6) & 1;   // the stage's column pair
             const uint64_t a1 = dA + e * 2 * aE, b1 = dB - (shift ? (i / 6) % 30 : 0), a2 = a1 + aE, b2 = b1 - (shift ? 1 : 0);
-            if (mode == 0) {
+            if ((mode & 3) == 0) {
                 mma(tc, a1, b1 + bLo, idesc); mma(tm, a1, b1, idesc); mma(tc, a1 + aLo, b1, idesc);
                 mma(tc, a2, b2 + bLo, idesc); mma(tm, a2, b2, idesc); mma(tc, a2 + aLo, b2, idesc);
-            } else if (mode == 1) {
+            } else if ((mode & 3) == 1) {
                 mma(tm, a1, b1 + bLo, idesc); mma(tm, a1, b1, idesc); mma(tm, a1 + aLo, b1, idesc);
                 mma(tm, a2, b2 + bLo, idesc); mma(tm, a2, b2, idesc); mma(tm, a2 + aLo, b2, idesc);
             } else {
                 mma(tc, a1, b1 + bLo, idesc); mma(tm, a1, b1, idesc); mma(tc, a1 + aLo, b1, idesc);
                 mma(tm, a2, b2 + bLo, idesc); mma(tc, a2, b2, idesc); mma(tm, a2 + aLo, b2, idesc);
+            }
+            // K10 commits every weight stage (12 MMAs) back to the producer: does a commit cost pipe time?
+            if (commit_every && ((i / 6 + 1) % commit_every) == 0) {
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar2)));
+                // queue-depth probe: the issuer idles `delay` cycles at every stage boundary; the delay the
+                // tensor pipe's instruction queue hides shows how far ahead the issuer can be
+                if (delay > 0) {
+                    const long long t = clock64();
+                    while (clock64() - t < delay) {}
+                }
             }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
@@ -83,15 +101,17 @@ int main(int argc, char** argv) {
     cudaMalloc(&dc, 148 * 8);
     const size_t smem = 32768 + 4 * 288 * 16 + 1024;
     cudaFuncSetAttribute(k10_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int n : {256, 128, 64})
-        for (int mode = 0; mode < 3; ++mode)
-            for (int shift = 0; shift < 2; ++shift)
+    for (int n : {256})
+        for (int mode : {0})
+            for (int shift = 1; shift < 2; ++shift)
+              for (int commit_every : {2})   // a stage boundary every 12 MMAs
+              for (int delay : {0, 64, 128, 192, 256, 384, 512, 768, 1024})
                 for (int grid : {1, 148}) {
                     cudaEvent_t e0, e1;
                     cudaEventCreate(&e0); cudaEventCreate(&e1);
-                    k10_rate<<<grid, 128, smem>>>(n, nmma, mode, shift, dc);   // warm-up
+                    k10_rate<<<grid, 128, smem>>>(n, nmma, mode, shift, commit_every, delay, dc);   // warm-up
                     cudaEventRecord(e0);
-                    k10_rate<<<grid, 128, smem>>>(n, nmma, mode, shift, dc);
+                    k10_rate<<<grid, 128, smem>>>(n, nmma, mode, shift, commit_every, delay, dc);
                     cudaEventRecord(e1);
                     cudaError_t e = cudaDeviceSynchronize();
                     if (e != cudaSuccess) { printf("CUDA error: %s\n", cudaGetErrorString(e)); return 1; }
@@ -101,8 +121,8 @@ int main(int argc, char** argv) {
                     for (int i = 0; i < grid; ++i) mx = c[i] > mx ? c[i] : mx;
                     float ms;
                     cudaEventElapsedTime(&ms, e0, e1);
-                    printf("N %3d mode %d shift %d grid %3d: %.1f cycles per MMA (max over CTAs), kernel %.3f ms -> %.0f TFLOP/s\n",
-                           n, mode, shift, grid, (double)mx / nmma, ms, 2.0 * 128 * n * 16 * nmma * grid / (ms * 1e-3) / 1e12);
+                    printf("N %3d mode %d shift %d boundary every %d column pairs, idle %4d cycles, grid %3d: %.1f cycles per MMA (max over CTAs), kernel %.3f ms -> %.0f TFLOP/s\n",
+                           n, mode, shift, commit_every, delay, grid, (double)mx / nmma, ms, 2.0 * 128 * n * 16 * nmma * grid / (ms * 1e-3) / 1e12);
                 }
     return 0;
 }
