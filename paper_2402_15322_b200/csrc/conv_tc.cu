@@ -894,6 +894,8 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
         const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
         if (a.epi_vec) {   // nx % 4 == 0, 16-byte aligned fields, a vector op, no peer halos (uniform per launch)
+            // (a slab epilogue on a kernel without an output window: rows outside the slab are a neighbour's)
+            if (epi.slab_hi > 0 && (y < epi.slab_lo || y >= epi.slab_hi)) continue;
             tc_epilogue4(epi, rowbase + x0, x0, y, vv, err);
             continue;
         }
