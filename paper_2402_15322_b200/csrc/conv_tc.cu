@@ -39,7 +39,7 @@
 //   * rows mode: one CTA per (rows <= kr output rows, orientation block, field); the epilogue runs in the
 //     kernel through a shared-memory transpose (coalesced along x);
 //   * balanced mode: kr-row tiles; the tiles' input-row chains are concatenated and split into equal runs
-//     over <= 148 CTAs (<= 3 pieces per tile); every piece writes its sums to an L2-resident partial
+//     over <= 148 CTAs (<= 3 pieces per tile on whole grids, up to 12 on thin row slabs); every piece writes its sums to an L2-resident partial
 //     buffer and tc_pieces_epilogue_kernel adds the pieces in order and applies the fused epilogue.
 #include <cuda_bf16.h>
 
@@ -233,8 +233,9 @@ struct TcArgs {
     int rows_out;              // output rows a CTA owns (<= kr; the M tile's remaining rows are discarded)
     int y_lo, y_hi;            // output window (kernel's win_lo / win_hi): rows outside are input-only halos
     // balanced mode (PIECES): kr-row tiles, CTA c takes chain units [c q, (c + 1) q) of the concatenated
-    // (tile, input row) list; every piece's sums go to `part` [tile][piece < 3][128][npad]
+    // (tile, input row) list; every piece's sums go to `part` [tile][piece < pt][128][npad]
     int batch, nblk, ngroups, ug, q;
+    int pt;                    // piece slots per tile in `part`: ceil(longest chain / q) + 1 (3 on the whole c4 grid)
     float* part;
     // narrow geometry: per (field, input row, chunk) (min v, max |v|) of this launch's input, the weight
     // mass outside each block's narrow window, and the tile counters (instrumentation)
@@ -740,7 +741,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             }
             // the correction accumulator (complete with the piece's last row commit)
             const uint32_t tc2 = tl + (uint32_t)(a.tmem_cols / 2);
-            float* prow = PIECES ? a.part + ((size_t)pc.tile * 3 + pc.p) * 128 * a.npad + (size_t)m * a.npad + h * half
+            float* prow = PIECES ? a.part + ((size_t)pc.tile * a.pt + pc.p) * 128 * a.npad + (size_t)m * a.npad + h * half
                                  : nullptr;
 #pragma unroll
             for (int c = 0; c < 128; c += 32) {
@@ -864,7 +865,7 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
     for (int i = 0; i < g; ++i) pre += tc_group_len(a, i);
     const int st = grp * a.ug + pre, len = tc_group_len(a, g);
     const int np = (st + len - 1) / a.q - st / a.q + 1;
-    const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * 3) * 128 * a.npad;
+    const float* tile = a.part + ((size_t)(grp * a.ngroups + g) * a.pt) * 128 * a.npad;
     const int64_t N = (int64_t)a.nx * a.ny * a.nt;
     // 256 threads: 4 consecutive x per thread (float4 partial loads; npad % 16 == 0), rows r0 + 4 k.
     // Every partial load of the thread is issued before the first use (up to 4 rows x 3 pieces in flight).
@@ -884,6 +885,10 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
         v[k].y = (w0.y + w1.y) + w2.y;
         v[k].z = (w0.z + w1.z) + w2.z;
         v[k].w = (w0.w + w1.w) + w2.w;
+        for (int p = 3; p < np; ++p) {   // thin output windows (row slabs): short runs, up to kTcTilePieces per tile
+            const float4 w = src[(size_t)p * 32 * a.npad];
+            v[k].x += w.x; v[k].y += w.y; v[k].z += w.z; v[k].w += w.w;
+        }
     }
     float err = 0.f;
 #pragma unroll
@@ -953,12 +958,23 @@ static void tc_units(const se2_kernel_s* k, int batch, int* ug, int* lmax, long 
     }
     *U = (long long)batch * gm.nblk * (*ug);
 }
-// units per CTA in the balanced mode: ceil(U / 148), at least half the longest chain (<= 3 pieces per tile)
+// units per CTA in the balanced mode: ceil(U / 148), and long enough that a tile has at most kTcTilePieces
+// pieces.  On the whole c4 grid that is 39 of a 46-row chain (<= 3 pieces per tile); on a thin output window
+// (one of 8 row slabs: 16 tiles) the runs go down to 5 rows so that all 148 SMs still take part.
+constexpr int kTcTilePieces = 12;
 static int tc_units_per_cta(const se2_kernel_s* k, int batch) {
     int ug, lmax;
     long long U;
     tc_units(k, batch, &ug, &lmax, &U);
-    return (int)std::max<long long>((U + 147) / 148, (lmax + 1) / 2);
+    return (int)std::max<long long>((U + 147) / 148, (lmax + kTcTilePieces - 2) / (kTcTilePieces - 1));
+}
+// piece slots per tile of a launch: a chain of lmax rows cut into runs of q touches at most this many CTAs
+static int tc_tile_pieces(const se2_kernel_s* k, int batch) {
+    int ug, lmax;
+    long long U;
+    tc_units(k, batch, &ug, &lmax, &U);
+    const int q = tc_units_per_cta(k, batch);
+    return std::max(3, (lmax + q - 1) / q + 1);
 }
 
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
@@ -1049,14 +1065,23 @@ cudaError_t conv_tc_decide(se2_kernel_s* k) {
         const double ctas = (double)((k->wrows() + rows - 1) / rows) * g.nblk * k->max_batch;
         const double rows_cost = std::ceil(ctas / 148.0) * std::min(k->ny, rows + 2 * k->R);
         const bool want = getenv("SE2_TC_PIECES") ? (atoi(getenv("SE2_TC_PIECES")) != 0) : (q < 0.95 * rows_cost);
-        if (want && k->tc_part == nullptr) {
-            // sized for the whole grid: any later output window has at most as many kr-row tiles
-            const size_t tiles = (size_t)k->max_batch * g.nblk * ((k->ny + g.kr - 1) / g.kr);
-            e = cudaMalloc(&k->tc_part, tiles * 3 * 128 * g.npad * sizeof(float));
-            if (e != cudaSuccess) return e;
-        } else if (!want && k->tc_part != nullptr) {
+        if (want) {
+            // tiles x piece slots of the current output window, for every batch size a launch may use
+            size_t need = 0;
+            for (int b = 1; b <= k->max_batch; ++b)
+                need = std::max(need, (size_t)b * g.nblk * tc_ngroups(k) * tc_tile_pieces(k, b));
+            need *= (size_t)128 * g.npad * sizeof(float);
+            if (k->tc_part == nullptr || need > k->tc_part_bytes) {
+                if (k->tc_part != nullptr) cudaFree(k->tc_part);
+                k->tc_part = nullptr;
+                e = cudaMalloc(&k->tc_part, need);
+                if (e != cudaSuccess) return e;
+                k->tc_part_bytes = need;
+            }
+        } else if (k->tc_part != nullptr) {
             cudaFree(k->tc_part);
             k->tc_part = nullptr;
+            k->tc_part_bytes = 0;
         }
     }
     return e;
@@ -1203,6 +1228,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         a.batch = batch;
         a.ngroups = tc_ngroups(k);
         a.q = tc_units_per_cta(k, batch);
+        a.pt = tc_tile_pieces(k, batch);
         a.part = reinterpret_cast<float*>(k->tc_part);
         const int ncta = (int)((U + a.q - 1) / a.q);
         {
@@ -1233,6 +1259,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.ngroups = 0;
     a.ug = 0;
     a.q = 0;
+    a.pt = 0;
     a.part = nullptr;
     dim3 grid((k->wrows() + a.rows_out - 1) / a.rows_out, g.nblk, batch);
     if (bpf) *bpf = (int)(grid.x * grid.y);

@@ -145,7 +145,8 @@ struct se2_kernel_s {
     size_t tc_w_hl = 0, tc_x_hl = 0;
     void* tc_wmap = nullptr;      // CUtensorMap (5-D) over tc_w: one TMA per weight stage
     void* tc_wc = nullptr;        // the same for the transport-cost table Wcl (built with it)
-    void* tc_part = nullptr;      // balanced mode: per-piece partial sums [tiles][3][128][npad] (null: off)
+    void* tc_part = nullptr;      // balanced mode: per-piece partial sums [tiles][pieces per tile][128][npad] (null: off)
+    size_t tc_part_bytes = 0;
     void* tc_wcmap = nullptr;
     bool tc_fast = false;         // cost model: K10 beats K2 on this grid (default engine)
     // K10 narrow geometry (nt >= 32): 16 rows x 8 orientations per M tile, a 16-orientation K window per

@@ -114,6 +114,51 @@ def test_jko_dist_slabs_loopback(nslabs, engine, cuda_device):
     assert measure_err(out, ref["mus"][2]) <= 1e-4
 
 
+@pytest.mark.parametrize("nslabs", [2, 8])
+def test_jko_dist_slabs_headline_geometry(nslabs, cuda_device):
+    """The north star's c4 split at the HEADLINE geometry and length: the full 256x256x64 grid (R 15, eps 0.003),
+    JKO step 0 with all 200 inner iterations, rows split into 2 / 8 slabs (8: the 8-GPU layout, 32 owned rows +
+    15-row halos) over the loopback transport, default engine (K10 on every slab), against the whole-grid fp64
+    oracle's golden c4f (sampled entries of mu_1 and both potentials, the mass, the 200-entry error trace)."""
+    import os
+    from paper_2402_15322_b200 import make_prox
+    from paper_2402_15322_b200.dist import Comm, Dist, local_rows, se2_jko_step_dist, slab_kernel
+    from gpu_util import potential_err
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4f.npz")
+    if not os.path.exists(path):
+        pytest.skip("golden c4f.npz not generated: run tests/golden/make_golden.py c4f")
+    gold = dict(np.load(path))
+    pc = S.get_parity_case("c4f")
+    cfg, d = S.parity_inputs(pc)
+    mu0 = d["mus"][0]
+    comms = Comm.loopback(nslabs)
+
+    def rank(r):
+        k, row0, rows, top, bot = slab_kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, nslabs, r)
+        assert k.uses_tensor_cores
+        prox = make_prox(k, cfg.tau, global_ny=cfg.ny, row_offset=row0 - top)
+        dd = Dist(slabs=comms[r], halo_top=top, halo_bot=bot)
+        mu = _dev(local_rows(mu0, row0, rows, top, bot))
+        nxt, a, b = torch.empty_like(mu), torch.empty_like(mu), torch.empty_like(mu)
+        m, tr = se2_jko_step_dist(k, dd, mu, nxt, a, b, cfg.iters, prox, False, trace=True)
+        own = slice(top, top + rows)
+        res = (row0, rows, _host(nxt)[:, own], _host(a)[:, own], _host(b)[:, own], m, tr)
+        k.close()
+        return res
+
+    res = _run_ranks(nslabs, rank)
+    shape = (cfg.ntheta, cfg.ny, cfg.nx)
+    mu1, a, b = np.zeros(shape), np.zeros(shape), np.zeros(shape)
+    for row0, rows, o_mu, o_a, o_b, m, tr in res:
+        mu1[:, row0:row0 + rows], a[:, row0:row0 + rows], b[:, row0:row0 + rows] = o_mu, o_a, o_b
+        assert abs(m - gold["masses"][0]) <= 1e-4 * abs(gold["masses"][0])     # every rank sees the global mass
+        assert trace_err(tr, gold["err"][0]) <= 1.0
+    idx = gold["sample_idx"]
+    assert measure_err(mu1.reshape(-1)[idx], gold["mus"][1].reshape(-1)) <= 1e-4
+    assert potential_err(np.log(a.reshape(-1)[idx]), np.log(gold["a"].reshape(-1))) <= 1e-4
+    assert potential_err(np.log(b.reshape(-1)[idx]), np.log(gold["b"].reshape(-1))) <= 1e-4
+
+
 def test_barycenter_dist_one_rank_is_barycenter(cuda_device):
     from paper_2402_15322_b200 import Kernel, se2_barycenter
     from paper_2402_15322_b200.dist import Dist, se2_barycenter_dist
