@@ -805,7 +805,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
 
 // apply_epilogue<false> (conv_common.cuh) for 4 consecutive outputs of one row with 16-byte loads / stores: the
 // same expressions per output and the same order of the error sum, for the ops of the linear solvers (store,
-// divide, multiply, entropic prox) without peer halos.  The scalar form cost ~69 instructions per output and
+// divide, multiply, entropic prox), boundary rows to the peer halos / send buffers included.  The scalar form cost ~69 instructions per output and
 // made the pieces epilogue issue-bound (ncu: issue active 62%, L2 32%).
 __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int ix, int iy, const float (&y)[4],
                                              float& err) {
@@ -848,7 +848,15 @@ __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int
             for (int j = 0; j < 4; ++j) o[j] = t[j] * y[j];
         }
     }
-    *reinterpret_cast<float4*>(e.out + idx) = make_float4(o[0], o[1], o[2], o[3]);
+    const float4 o4 = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(e.out + idx) = o4;
+    if (e.slab_hi > 0) {   // boundary rows into the neighbours' halo rows / the send buffers (as apply_epilogue)
+        const int64_t plane = idx / ((int64_t)e.ny_self * e.nx_self);
+        if (e.halo_up != nullptr && iy < e.slab_lo + e.slab_halo)
+            *reinterpret_cast<float4*>(e.halo_up + (plane * e.ny_up + iy + e.up_shift) * e.nx_self + ix) = o4;
+        if (e.halo_dn != nullptr && iy >= e.slab_hi - e.slab_halo)
+            *reinterpret_cast<float4*>(e.halo_dn + (plane * e.ny_dn + iy - e.dn_shift) * e.nx_self + ix) = o4;
+    }
 }
 
 // balanced mode: sum each output's piece partials (1-3, in piece order) and apply the fused epilogue;
@@ -898,7 +906,7 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
         if (r >= a.kr || y >= a.y_hi || x0 >= a.nx) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
         const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-        if (a.epi_vec) {   // nx % 4 == 0, 16-byte aligned fields, a vector op, no peer halos (uniform per launch)
+        if (a.epi_vec) {   // nx % 4 == 0, 16-byte aligned fields and halo buffers, a vector op (uniform per launch)
             // (a slab epilogue on a kernel without an output window: rows outside the slab are a neighbour's)
             if (epi.slab_hi > 0 && (y < epi.slab_lo || y >= epi.slab_hi)) continue;
             tc_epilogue4(epi, rowbase + x0, x0, y, vv, err);
@@ -1241,7 +1249,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
         const bool vec_op = epi.op == EPI_STORE || epi.op == EPI_DIVIDE || epi.op == EPI_MULTIPLY ||
                             (epi.op == EPI_PROX && epi.prox_kind != 2);
-        a.epi_vec = (!scalar_epi && vec_op && k->nx % 4 == 0 && epi.halo_up == nullptr && epi.halo_dn == nullptr &&
+        a.epi_vec = (!scalar_epi && vec_op && k->nx % 4 == 0 && al16(epi.halo_up) && al16(epi.halo_dn) &&
                      al16(epi.out) && al16(epi.out2) && al16(epi.target) && al16(epi.err_a) && al16(epi.err_mu))
                         ? 1 : 0;
         static const bool skip_epi = getenv("SE2_TC_DIAG_SKIP_EPI") != nullptr;   // timing diagnostics only
