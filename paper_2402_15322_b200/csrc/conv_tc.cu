@@ -226,6 +226,7 @@ struct TcArgs {
     int na;                    // weight-ring stages
     int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
+    int epi_split;             // pieces epilogue: blocks per (row group, orientation)
     int epi_vec;               // pieces epilogue: 4 outputs per thread with 16-byte loads / stores (tc_epilogue4)
     int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N, bit 2 = no weight loads after the first ring fill
     uint32_t a_tx;             // bytes one weight-stage TMA box delivers (kTcAStage; halved by a timing diagnostic)
@@ -864,7 +865,7 @@ __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int
 __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
     tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
-    const int g = blockIdx.x, to = blockIdx.y, b = blockIdx.z;
+    const int g = blockIdx.x / a.epi_split, kpart = blockIdx.x % a.epi_split, to = blockIdx.y, b = blockIdx.z;
     // the M-tile orientation of `to`: classic blocks of 16 from 0; narrow blocks of 8 from 4
     const int u = a.nar ? (to - 4 + a.nt) % a.nt : to;
     const int blk = u / a.kb, tol = u % a.kb, grp = b * a.nblk + blk;
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
     for (int k = 0; k < kMaxR; ++k) {
         const int r = r0 + 4 * k;
         v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r >= a.kr || x0 >= a.npad) continue;
+        if (r >= a.kr || x0 >= a.npad || (a.epi_split > 1 && k != kpart)) continue;
         const float4* src = reinterpret_cast<const float4*>(tile + (size_t)(r * a.kb + tol) * a.npad + x0);
         const float4 w0 = src[0];
         const float4 w1 = np > 1 ? src[(size_t)32 * a.npad] : make_float4(0.f, 0.f, 0.f, 0.f);   // 128 npad floats
@@ -903,7 +904,7 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
     for (int k = 0; k < kMaxR; ++k) {
         const int r = r0 + 4 * k;
         const int y = a.y_lo + g * a.kr + r;
-        if (r >= a.kr || y >= a.y_hi || x0 >= a.nx) continue;
+        if (r >= a.kr || y >= a.y_hi || x0 >= a.nx || (a.epi_split > 1 && k != kpart)) continue;
         const int64_t rowbase = (int64_t)b * N + ((int64_t)to * a.ny + y) * a.nx;
         const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
         if (a.epi_vec) {   // nx % 4 == 0, 16-byte aligned fields and halo buffers, a vector op (uniform per launch)
@@ -918,7 +919,7 @@ __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Ep
     }
     if (epi.err_partial != nullptr) {
         const float t = block_sum<256>(err, sRed);
-        if (threadIdx.x == 0) epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + (int64_t)to * gridDim.x + g] = t;
+        if (threadIdx.x == 0) epi.err_partial[(int64_t)b * (gridDim.x * gridDim.y) + (int64_t)to * gridDim.x + blockIdx.x] = t;
     }
 }
 
@@ -985,8 +986,12 @@ static int tc_tile_pieces(const se2_kernel_s* k, int batch) {
     return std::max(3, (lmax + q - 1) / q + 1);
 }
 
+// pieces epilogue: blocks per (kr-row group, orientation) -- 4 (one of the thread rows r0 + 4 k each) when the
+// grid would otherwise leave most SMs without a block (thin output windows: 128 blocks on one of 8 c4 slabs)
+static int tc_epi_split(const se2_kernel_s* k) { return tc_ngroups(k) * k->nt < 2 * 148 ? 4 : 1; }
+
 int conv_blocks_per_field_tc(const se2_kernel_s* k) {
-    if (k->tc_part != nullptr) return tc_ngroups(k) * k->nt;   // balanced: epilogue blocks
+    if (k->tc_part != nullptr) return tc_ngroups(k) * tc_epi_split(k) * k->nt;   // balanced: epilogue blocks
     const int rows = tc_rows_out(k);
     return (k->wrows() + rows - 1) / rows * tc_geom(k).nblk;
 }
@@ -1215,6 +1220,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.epi_vec = 0;
+    a.epi_split = tc_epi_split(k);
     a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0) |
              (getenv("SE2_TC_DIAG_NOWLOAD") ? 4 : 0) | (getenv("SE2_TC_DIAG_PROF") ? 8 : 0);
     a.a_tx = getenv("SE2_TC_DIAG_HALFW") ? kTcAStage / 2 : kTcAStage;
@@ -1254,12 +1260,12 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
                         ? 1 : 0;
         static const bool skip_epi = getenv("SE2_TC_DIAG_SKIP_EPI") != nullptr;   // timing diagnostics only
         if (!skip_epi) {
-            cudaLaunchConfig_t c = cfg_of(dim3(a.ngroups, k->nt, batch), dim3(256), 0);
+            cudaLaunchConfig_t c = cfg_of(dim3(a.ngroups * a.epi_split, k->nt, batch), dim3(256), 0);
             cudaError_t e = cudaLaunchKernelEx(&c, tc_pieces_epilogue_kernel, a, epi);
             if (e != cudaSuccess) return e;
             count_launch();
         }
-        if (bpf) *bpf = a.ngroups * k->nt;
+        if (bpf) *bpf = a.ngroups * a.epi_split * k->nt;
         return cudaGetLastError();
     }
     a.rows_out = tc_rows_out(k);
