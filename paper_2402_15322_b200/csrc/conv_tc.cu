@@ -137,6 +137,10 @@ TcGeom tc_geom(const se2_kernel_s* k) {
 // programmatic dependent launch: block until the preceding kernel in the stream has completed and its
 // writes are visible (a no-op for a normally launched kernel)
 __device__ __forceinline__ void tc_grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ... and its counterpart (SE2_TC_PDL_EARLY=1, an experiment): at the top of each K10 kernel, so that once every
+// block of this grid has started the next kernel's blocks may take the SM resources that free up and run to
+// their griddepcontrol.wait.  Measured no gain (c4 conv 0.338 vs 0.335 ms): off by default.
+__device__ __forceinline__ void tc_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // One lane of a converged warp, chosen with elect.sync: ptxas then knows a single thread runs the role's
 // code and emits bare UTCHMMA / UTMALDG / UTCBAR instructions; under `lane == 0` it wraps every one of
@@ -226,6 +230,7 @@ struct TcArgs {
     int na;                    // weight-ring stages
     int chain16;               // input rows per main-accumulator chain at K = 16 (power of 2, <= kTcMaxFlushRows)
     uint32_t a_stage, b_stage;
+    int pdl_early;             // griddepcontrol.launch_dependents at the top of the kernels (SE2_TC_PDL_EARLY=1; off by default)
     int epi_split;             // pieces epilogue: blocks per (row group, orientation)
     int epi_vec;               // pieces epilogue: 4 outputs per thread with 16-byte loads / stores (tc_epilogue4)
     int diag;                  // timing diagnostics (wrong results): bit 0 = no pixel shift of the B descriptor, bit 1 = MMAs of half the N, bit 2 = no weight loads after the first ring fill
@@ -335,8 +340,9 @@ __device__ bool tc_tile_narrow(const TcArgs& a, int b, int blk, int y0, int rows
 // (field, row, chunk), one padded pixel per thread (all 8 plane loads in flight); optionally the row's
 // (min v, max |v|) over the 8 planes and the nx real pixels (stats[b][y][chunk])
 __global__ void tc_split_input_kernel(const float* __restrict__ v, __nv_bfloat16* __restrict__ xk, size_t xk_hl,
-                                      int nx, int ny, int nt, int nxp, float2* __restrict__ stats) {
+                                      int nx, int ny, int nt, int nxp, float2* __restrict__ stats, int pdl_early) {
     __shared__ float sMin[32], sMax[32];
+    if (pdl_early) tc_launch_dependents();
     tc_grid_dep_wait();   // reads the previous kernel's output (launched with PDL)
     const int nch = nt / 8;
     const int64_t row = blockIdx.x;   // (b, y, c)
@@ -452,6 +458,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
     __shared__ int sNwl[kTcMaxPieces];   // theta chunks of each piece's window (narrow: 2 or 4; classic: nwin)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (a.pdl_early) tc_launch_dependents();
+    const long long t_entry = (a.diag & 8) ? clock64() : 0;   // SE2_TC_DIAG_PROF
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -669,6 +677,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             atomicAdd(&a.cnt[4], (unsigned long long)pwB);
             atomicAdd(&a.cnt[5], (unsigned long long)pwF);
             atomicAdd(&a.cnt[6], 1ull);
+            atomicAdd(&a.cnt[7], (unsigned long long)(pt0 - t_entry));   // kernel entry -> the issuer's loop
         }
       }
       __syncwarp();
@@ -777,6 +786,8 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&cflushed)) : "memory");
         }
+        if ((a.diag & 8) && a.cnt != nullptr && warp == 2 && lane == 0)   // kernel entry -> the last piece's sums stored
+            atomicAdd(&a.cnt[8], (unsigned long long)(clock64() - t_entry));
     }
     if (!PIECES) {
         __syncthreads();   // T complete (every warp reaches this; the role warps have finished their loops)
@@ -864,6 +875,7 @@ __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int
 // one block per (kr-row group, orientation, field) -- one tile row block -- threads along x (coalesced)
 __global__ void __launch_bounds__(256, 4) tc_pieces_epilogue_kernel(TcArgs a, Epilogue epi) {
     __shared__ float sRed[32];
+    if (a.pdl_early) tc_launch_dependents();
     tc_grid_dep_wait();   // the partials of the MMA kernel (PDL launch)
     const int g = blockIdx.x / a.epi_split, kpart = blockIdx.x % a.epi_split, to = blockIdx.y, b = blockIdx.z;
     // the M-tile orientation of `to`: classic blocks of 16 from 0; narrow blocks of 8 from 4
@@ -1109,8 +1121,8 @@ cudaError_t conv_tc_prepare(se2_kernel_s* k) {
     cudaError_t e = cudaMalloc(&k->tc_w, 2 * wk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_x, 2 * xk_hl * sizeof(__nv_bfloat16));
     if (e == cudaSuccess) e = cudaMalloc(&k->tc_stats, (size_t)k->max_batch * k->ny * g.nch * sizeof(float2));
-    if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 8 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&k->tc_cnt, 10 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(k->tc_cnt, 0, 10 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
     k->tc_w_hl = wk_hl;
     k->tc_x_hl = xk_hl;
@@ -1154,7 +1166,7 @@ void conv_tc_release(se2_kernel_s* k) {
 }
 
 cudaError_t conv_tc_tile_counts(const se2_kernel_s* k, int64_t* tiles, int64_t* wide, bool reset) {
-    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long h[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (k->tc_cnt != nullptr) {
         cudaError_t e = cudaMemcpy(h, k->tc_cnt, sizeof(h), cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && reset) e = cudaMemset(k->tc_cnt, 0, sizeof(h));
@@ -1163,6 +1175,9 @@ cudaError_t conv_tc_tile_counts(const se2_kernel_s* k, int64_t* tiles, int64_t* 
     if (getenv("SE2_TC_DIAG_PROF") && h[6] > 0)   // issuer cycle profile (timing diagnostic), mean per CTA
         fprintf(stderr, "K10 issuer per CTA: %.0f cycles in its loop; waiting on weights %.0f, input rows %.0f, flushes %.0f (%llu CTAs)\n",
                 (double)h[2] / h[6], (double)h[3] / h[6], (double)h[4] / h[6], (double)h[5] / h[6], h[6]);
+    if (getenv("SE2_TC_DIAG_PROF") && h[6] > 0)
+        fprintf(stderr, "K10 per CTA: %.0f cycles from kernel entry to the issuer's loop, %.0f to the last piece's sums stored\n",
+                (double)h[7] / h[6], (double)h[8] / h[6]);
     *tiles = (int64_t)h[0];
     *wide = (int64_t)h[1];
     return cudaSuccess;
@@ -1188,6 +1203,8 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         return c;
     };
     float2* stats = g.nar ? reinterpret_cast<float2*>(k->tc_stats) : nullptr;
+    // (measured: 0.338 vs 0.335 ms per c4 conv with the early trigger, so it is off by default)
+    static const int pdl_early = getenv("SE2_TC_PDL_EARLY") ? 1 : 0;
     static const bool skip_split = getenv("SE2_TC_DIAG_SKIP_SPLIT") != nullptr;   // timing diagnostics only
     if (!skip_split) {
         // one block per (field, row, chunk), one padded pixel per thread: all 8 plane loads in flight
@@ -1196,7 +1213,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         // store instructions half-fills 32 sectors; this form's stores are fully coalesced)
         const int threads = std::min(1024, (g.nxp + 31) / 32 * 32);
         cudaLaunchConfig_t c = cfg_of(dim3((unsigned)rows), dim3(threads), 0);
-        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats);
+        cudaError_t e = cudaLaunchKernelEx(&c, tc_split_input_kernel, in, xk, k->tc_x_hl, k->nx, k->ny, k->nt, g.nxp, stats, pdl_early);
         if (e != cudaSuccess) return e;
         count_launch();
     }
@@ -1220,6 +1237,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
     a.a_stage = (uint32_t)g.a_stage;
     a.b_stage = (uint32_t)g.b_stage;
     a.epi_vec = 0;
+    a.pdl_early = pdl_early;
     a.epi_split = tc_epi_split(k);
     a.diag = (getenv("SE2_TC_DIAG_NOSHIFT") ? 1 : 0) | (getenv("SE2_TC_DIAG_HALFN") ? 2 : 0) |
              (getenv("SE2_TC_DIAG_NOWLOAD") ? 4 : 0) | (getenv("SE2_TC_DIAG_PROF") ? 8 : 0);
