@@ -222,7 +222,9 @@ static uint64_t as_key(double v) {
     memcpy(&u, &v, sizeof(u));
     return u;
 }
-constexpr int64_t kGraphMaxElems = (int64_t)1 << 21;   // batch * N at or below which solves use graphs
+// batch * N at or below which solves use graphs (2^21; SE2_GRAPH_MAX_LOG2 overrides it for measurements: the c4
+// JKO step as one graph of 1 200 kernel nodes measured no faster than its direct launches)
+static const int64_t kGraphMaxElems = (int64_t)1 << (getenv("SE2_GRAPH_MAX_LOG2") ? atoi(getenv("SE2_GRAPH_MAX_LOG2")) : 21);
 
 static se2_status check_kernel(se2_kernel k) {
     if (!k) {
