@@ -107,3 +107,30 @@ def test_barycenter_warm_start_resume(log_domain, cuda_device):
         assert np.max(np.abs(_host(v1) - _host(v2))) < 1e-4
     else:
         assert torch.equal(bary1, bary2) and torch.equal(v1, v2) and torch.equal(w1, w2)
+
+
+def test_nvtx_ranges_do_not_change_results(cuda_device):
+    """SE2_NVTX=1 (NVTX ranges per solve / iteration / conv, read once per process) in a fresh process: the same
+    small Sinkhorn solve gives bit-identical scalings with and without the ranges."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import hashlib, torch, numpy as np, se2_synth as S\n"
+        "from paper_2402_15322_b200 import Kernel, se2_sinkhorn\n"
+        "cfg = S.get_config('c0'); d = S.config_inputs(cfg)\n"
+        "k = Kernel(cfg.nx, cfg.ny, cfg.ntheta, cfg.eps, cfg.w, cfg.R, max_batch=1)\n"
+        "mu, nu = (torch.from_numpy(m).cuda() for m in d['mus'][:2])\n"
+        "a, b = torch.empty_like(mu), torch.empty_like(mu)\n"
+        "se2_sinkhorn(k, mu, nu, a, b, 12, log_domain=True, trace=True, persistent=False, no_graph=True)\n"
+        "torch.cuda.synchronize()\n"
+        "print(hashlib.sha256(a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes()).hexdigest())\n")
+    outs = []
+    for nvtx in ("0", "1"):
+        env = dict(os.environ, SE2_NVTX=nvtx, PYTHONPATH=root)
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1] and len(outs[0]) == 64
