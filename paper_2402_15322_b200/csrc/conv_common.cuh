@@ -128,6 +128,32 @@ __device__ __forceinline__ float block_sum(float v, float* red /* >= NT/32 float
     return t;
 }
 
+// Porous-medium prox: u = log s solves g(u) = c e^{(m-1) u} + u - log z = 0, g convex and
+// increasing.  Bracket: g(lz) > 0, and at lo = min(lz - 50, (ln 50 - ln c)/(m-1)) both c e^{(m-1) lo} <= 50 and
+// lo - lz <= -50, so g(lo) <= 0.  Newton from lz, falling back to bisection of the bracket whenever a step
+// leaves it or fails to halve it (safeguarded Newton); c e^{...} is evaluated as exp(ln c + (m-1) u) with the
+// exponent capped at 88 (no overflow far above the root).  Returns u; *conv = false when 64 steps did not converge.
+__device__ __forceinline__ float porous_prox_u(float lz, float lnc, float m1, bool* conv) {
+    float lo = fminf(lz - 50.f, (3.9120230054f - lnc) / m1), hi = lz;
+    float u = lz, dold = hi - lo;
+    *conv = false;
+    for (int it = 0; it < 64; ++it) {
+        const float ex = expf(fminf(lnc + m1 * u, 88.f));
+        const float g = ex + u - lz;
+        if (g > 0.f) hi = u; else lo = u;
+        const float dg = m1 * ex + 1.f;
+        float un = u - g / dg;
+        if (!(un > lo && un < hi) || fabsf(2.f * g) > fabsf(dold * dg)) un = 0.5f * (lo + hi);
+        dold = un - u;
+        u = un;
+        if (fabsf(dold) <= 1e-7f * (1.f + fabsf(u)) || hi - lo <= 1e-7f * (1.f + fabsf(u))) {
+            *conv = true;
+            break;
+        }
+    }
+    return u;
+}
+
 // Apply the fused epilogue to one conv output.  y_lin: linear-domain value (linear engine),
 // or ly (natural log) in the log engine.  Returns the marginal-error contribution.
 template <bool LOG>
@@ -160,31 +186,12 @@ __device__ __forceinline__ float apply_epilogue(const Epilogue& e, int64_t idx, 
         case EPI_MULTIPLY: o = LOG ? (e.target[idx] + y) : (e.target[idx] * y); break;
         case EPI_PROX: {
             if (e.prox_kind == 2) {
-                // porous medium: u = log s solves g(u) = c e^{(m-1) u} + u - log z = 0, g convex
-                // and increasing.  Bracket: g(lz) > 0, and at lo = min(lz - 50, (ln 50 - ln c)/(m-1)) both
-                // c e^{(m-1) lo} <= 50 and lo - lz <= -50, so g(lo) <= 0.  Newton from lz, falling back to
-                // bisection of the bracket whenever a step leaves it or fails to halve it (safeguarded
-                // Newton); c e^{...} is evaluated as exp(ln c + (m-1) u) with the exponent capped at 88
-                // (no overflow far above the root).  Sites not converged in 64 steps are counted.
+                // porous medium: safeguarded Newton on u = log s (porous_prox_u); sites not converged
+                // in 64 steps are counted
                 if (!LOG && y < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
                 const float lz = LOG ? y : logf(fmaxf(y, kDivFloor));
-                float lo = fminf(lz - 50.f, (3.9120230054f - e.prox_lnc) / e.prox_m1), hi = lz;
-                float u = lz, dold = hi - lo;
-                bool conv = false;
-                for (int it = 0; it < 64; ++it) {
-                    const float ex = expf(fminf(e.prox_lnc + e.prox_m1 * u, 88.f));
-                    const float g = ex + u - lz;
-                    if (g > 0.f) hi = u; else lo = u;
-                    const float dg = e.prox_m1 * ex + 1.f;
-                    float un = u - g / dg;
-                    if (!(un > lo && un < hi) || fabsf(2.f * g) > fabsf(dold * dg)) un = 0.5f * (lo + hi);
-                    dold = un - u;
-                    u = un;
-                    if (fabsf(dold) <= 1e-7f * (1.f + fabsf(u)) || hi - lo <= 1e-7f * (1.f + fabsf(u))) {
-                        conv = true;
-                        break;
-                    }
-                }
+                bool conv;
+                const float u = porous_prox_u(lz, e.prox_lnc, e.prox_m1, &conv);
                 if (!conv && e.guard != nullptr) atomicAdd(&e.guard[1], 1u);
                 o = LOG ? (u - lz) : expf(u - lz);
                 if (e.out2 != nullptr) e.out2[idx] = expf(u);

@@ -817,7 +817,7 @@ conv_tc_kernel(TcArgs a, Epilogue epi, const __grid_constant__ CUtensorMap wmap,
 
 // apply_epilogue<false> (conv_common.cuh) for 4 consecutive outputs of one row with 16-byte loads / stores: the
 // same expressions per output and the same order of the error sum, for the ops of the linear solvers (store,
-// divide, multiply, entropic prox), boundary rows to the peer halos / send buffers included.  The scalar form cost ~69 instructions per output and
+// divide, multiply, entropic and porous prox), boundary rows to the peer halos / send buffers included.  The scalar form cost ~69 instructions per output and
 // made the pieces epilogue issue-bound (ncu: issue active 62%, L2 32%).
 __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int ix, int iy, const float (&y)[4],
                                              float& err) {
@@ -833,6 +833,19 @@ __device__ __forceinline__ void tc_epilogue4(const Epilogue& e, int64_t idx, int
     if (e.op == EPI_STORE) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) o[j] = y[j];
+    } else if (e.op == EPI_PROX && e.prox_kind == 2) {   // porous medium: safeguarded Newton per output
+        float s[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (y[j] < kDivFloor && e.guard != nullptr) atomicAdd(&e.guard[0], 1u);
+            const float lz = logf(fmaxf(y[j], kDivFloor));
+            bool conv;
+            const float u = porous_prox_u(lz, e.prox_lnc, e.prox_m1, &conv);
+            if (!conv && e.guard != nullptr) atomicAdd(&e.guard[1], 1u);
+            o[j] = expf(u - lz);
+            s[j] = expf(u);
+        }
+        if (e.out2 != nullptr) *reinterpret_cast<float4*>(e.out2 + idx) = make_float4(s[0], s[1], s[2], s[3]);
     } else if (e.op == EPI_PROX) {
         const float dyp = ((float)iy + 0.5f - e.cy) * e.hy;
         float s[4];
@@ -1271,8 +1284,7 @@ cudaError_t launch_conv_tc(const se2_kernel_s* k, const float* in, int batch, co
         count_launch();
         static const bool scalar_epi = getenv("SE2_TC_EPI1") != nullptr;   // A/B measurements
         auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-        const bool vec_op = epi.op == EPI_STORE || epi.op == EPI_DIVIDE || epi.op == EPI_MULTIPLY ||
-                            (epi.op == EPI_PROX && epi.prox_kind != 2);
+        const bool vec_op = epi.op == EPI_STORE || epi.op == EPI_DIVIDE || epi.op == EPI_MULTIPLY || epi.op == EPI_PROX;
         a.epi_vec = (!scalar_epi && vec_op && k->nx % 4 == 0 && al16(epi.halo_up) && al16(epi.halo_dn) &&
                      al16(epi.out) && al16(epi.out2) && al16(epi.target) && al16(epi.err_a) && al16(epi.err_mu))
                         ? 1 : 0;
