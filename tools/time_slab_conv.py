@@ -30,4 +30,6 @@ for nslabs in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
         out.append(f"{name} {e0.elapsed_time(e1) / 20 * 1e3:.1f} us")
     print(f"c4 slab {nslabs // 2} of {nslabs}: rows {rows} (+{top}+{bot} halo), uses_tensor_cores {k.uses_tensor_cores}: "
           + ", ".join(out), flush=True)
+    if os.environ.get("SE2_TC_DIAG_PROF"):
+        k.tc_tile_stats()   # prints the issuer's cycle counters (stderr)
     k.close()
